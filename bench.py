@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse-embedding hot path (BASELINE.json metric).
+
+Metric: unique-ID lookups+updates per second (one step = dedup -> table
+find-or-insert -> jagged gather -> segment-reduce + Adagrad update of one
+batch), whole job over all ranks.  Default workload = BASELINE config 1:
+one dynamic table, dim 64, 2^20 keys pre-populated, batch 1024 jagged
+sequences (lognormal, mean 128, max 4096), Zipf(1.1) ids, Adagrad.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/librsref.so, compiled from /root/reference sources; else the C
+restatement) on the host cores, same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C1 = dict(workload="config1: 1 dynamic table dim 64, 2^20 keys, batch 1024 seqs (mean 128, max 4096, sigma 1.0), "
+                   "Zipf 1.1, dedup+lookup+Adagrad", dim=64, vocab=1 << 20, seqs=1024, mean=128.0, max_len=4096,
+          sigma=1.0, zipf=1.1, seed=1, capacity=1 << 22)
+TAG1 = np.uint64(1 << 62)
+L2_FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, index=0):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {getattr(N, k, 0): k for k in (
+            "nvmlClocksEventReasonGpuIdle", "nvmlClocksEventReasonSwPowerCap", "nvmlClocksEventReasonHwSlowdown",
+            "nvmlClocksEventReasonHwThermalSlowdown", "nvmlClocksEventReasonSwThermalSlowdown",
+            "nvmlClocksEventReasonHwPowerBrakeSlowdown", "nvmlClocksEventReasonApplicationsClocksSetting",
+            "nvmlClocksEventReasonSyncBoost")}
+        short = {"nvmlClocksEventReasonSwPowerCap": "sw_power_cap", "nvmlClocksEventReasonHwSlowdown": "hw_slowdown",
+                 "nvmlClocksEventReasonHwThermalSlowdown": "hw_thermal_slowdown",
+                 "nvmlClocksEventReasonSwThermalSlowdown": "sw_thermal_slowdown",
+                 "nvmlClocksEventReasonHwPowerBrakeSlowdown": "hw_power_brake",
+                 "nvmlClocksEventReasonApplicationsClocksSetting": "applications_clocks",
+                 "nvmlClocksEventReasonSyncBoost": "sync_boost", "nvmlClocksEventReasonGpuIdle": "gpu_idle"}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if bit and r & bit and name in short:
+                        self.reasons.add(short[name])
+            except Exception:
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.N:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.N:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"})}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_12663_b200 as P
+    from paper_2505_12663_b200 import workload as W
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dim, vocab = cfg["dim"], cfg["vocab"]
+
+    # table: 2^20 keys pre-populated with pseudo_sparse_grad(k, 0) rows (bench_main.cpp:105-108)
+    table = P.EmbedTable(P.TableConfig(capacity=cfg["capacity"], embedding_dim=dim, optimizer="adagrad",
+                                       chunk_rows=1 << 16, initial_rows=vocab + (1 << 20)))
+    raw = torch.arange(vocab, dtype=torch.int64, device="cuda")
+    init = W.pseudo_grads(raw, 0, dim)
+    table.insert(raw + int(TAG1), init)
+    del init
+    # distinct batches (weak scaling: each rank its own seed stream)
+    nb = max(1, min(args.steps + args.warmup, 6))
+    batches = []
+    for b in range(nb):
+        lengths, ids = W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"],
+                                  cfg["sigma"], cfg["zipf"], [vocab])
+        batches.append((lengths, ids))
+    max_t = max(len(i) for _, i in batches)
+    step = P.SparseStep(table, max_t, P.AdagradParams(lr=0.01, eps=1e-8))
+    dev = []
+    for b, (lengths, ids) in enumerate(batches):
+        d_ids = P.as_keys(ids)
+        d_g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim)
+        dev.append((d_ids, d_g, torch.empty((len(ids), dim), device="cuda")))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    lib = P.lib()
+
+    def one(b):
+        d_ids, d_g, out = dev[b % nb]
+        step.step(d_ids, d_g, out)
+
+    for w in range(args.warmup):
+        one(w)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- device-timed steps (inputs resident in HBM, L2 flushed between steps)
+    times, uniq, toks = [], 0, 0
+    launches0 = lib.rs_kernel_launches()
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            one(args.warmup + k)
+            e.record(stream)
+            e.synchronize()
+            times.append(s.elapsed_time(e))
+            uniq += _n_unique(step)
+            toks += dev[(args.warmup + k) % nb][0].numel()
+    launches = lib.rs_kernel_launches() - launches0
+    t_sum = sum(times) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_sum], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        uu = torch.tensor([uniq, toks], dtype=torch.float64, device="cuda")
+        dist.all_reduce(uu)
+        t_job, uniq_job, toks_job = tt.item(), uu[0].item(), uu[1].item()
+    else:
+        t_job, uniq_job, toks_job = t_sum, uniq, toks
+    value = uniq_job / t_job
+
+    # ---- per-kernel shares (separate pass with phase events, same inputs)
+    phases = phase_times(step, dev, nb, args, flush, P)
+
+    # ---- end to end through the public API with HOST buffers
+    e2e = e2e_pass(args, cfg, batches, step, P, W, rank)
+
+    # ---- roofline of the dominant kernel (segment-reduce + Adagrad)
+    hbm, how = peaks()
+    D = dim
+    T_avg, U_avg = toks / args.steps, uniq / args.steps
+    algo = {
+        "reduce_update": 4 * D * T_avg + 16 * D * U_avg,
+        "gather": 4 * D * T_avg + 4 * D * U_avg,
+        "dedup": 12 * T_avg + 8 * U_avg,
+        "table": 16 * U_avg,
+    }
+    dom = "reduce_update"
+    ach = algo[dom] / (phases[dom] / 1e3) / 1e9 if phases.get(dom) else None
+    step_bytes = 12 * T_avg + 24 * U_avg + 8 * D * T_avg + 20 * D * U_avg
+    res = {
+        "metric": "unique-ID lookups+updates/sec",
+        "value": value,
+        "unit": "unique-ids/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": t_job / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 rows, f64 optimizer math, u64 ids",
+        "data": "synthetic: the reference's generator (mt19937_64, truncated lognormal lengths, Zipf 1.1 ids), "
+                "pseudo_sparse_grad gradients",
+        "config": {"workload": cfg["workload"], "tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg,
+                   "embedding_dim": D, "table_keys": vocab, "optimizer": "adagrad",
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed (512 MiB write) between timed steps"},
+        "tokens_per_s": toks_job / t_job,
+        "step_hbm_gbs": step_bytes * world / (t_job / args.steps) / 1e9,
+        "step_roofline_frac": step_bytes / (t_job / args.steps) / 1e9 / hbm,
+        "kernel_ms": phases,
+        "roofline": {"bound": "hbm", "kernel": "k_reduce_update (segment-reduce + Adagrad)",
+                     "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if ach else None,
+                     "traffic": None, "peak_source": how,
+                     "algorithmic_bytes_per_launch": algo[dom]},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, batches, budget_s=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _n_unique(step):
+    import ctypes
+
+    import paper_2505_12663_b200 as P
+    n = ctypes.c_uint64()
+    P._lib.check(P.lib().rs_workspace_n_unique(step.ws.handle, ctypes.byref(n)), "n_unique")
+    return n.value
+
+
+def phase_times(step, dev, nb, args, flush, P):
+    """Average device time per kernel group, CUDA events on the launching stream
+    (forward: dedup+table+gather measured by splitting forward/backward)."""
+    import torch
+    stream = torch.cuda.current_stream()
+    acc = {"forward": 0.0, "reduce_update": 0.0}
+    reps = max(3, min(args.steps, 10))
+    for k in range(reps):
+        d_ids, d_g, out = dev[k % nb]
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        step.forward(d_ids, out)
+        ev[1].record(stream)
+        step.backward(d_g)
+        ev[2].record(stream)
+        ev[2].synchronize()
+        acc["forward"] += ev[0].elapsed_time(ev[1])
+        acc["reduce_update"] += ev[1].elapsed_time(ev[2])
+    res = {k: v / reps for k, v in acc.items()}
+    # gather alone: re-run the forward's last kernel shape via lookup of the same rows
+    return res
+
+
+def e2e_pass(args, cfg, batches, step, P, W, rank):
+    """Same metric through the public API with host buffers: H2D of ids+grads from
+    pinned memory, the step, D2H of the gathered embeddings -- all in the timed region."""
+    import torch
+    dim = cfg["dim"]
+    stream = torch.cuda.current_stream()
+    host = []
+    for b, (lengths, ids) in enumerate(batches):
+        h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
+        g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim).cpu().pin_memory()
+        h_out = torch.empty((len(ids), dim), dtype=torch.float32).pin_memory()
+        host.append((h_ids, g, h_out))
+    max_t = max(h[0].numel() for h in host)
+    d_ids = torch.empty(max_t, dtype=torch.int64, device="cuda")
+    d_g = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
+    d_out = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
+    times, uniq, h2d, d2h = [], 0, 0, 0
+    n = max(3, min(args.steps, 10))
+    for k in range(n + 2):
+        h_ids, g, h_out = host[k % len(host)]
+        T = h_ids.numel()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        d_ids[:T].copy_(h_ids, non_blocking=True)
+        d_g[:T].copy_(g, non_blocking=True)
+        step.step(d_ids[:T], d_g[:T], d_out[:T])
+        h_out.copy_(d_out[:T], non_blocking=True)
+        e.record(stream)
+        e.synchronize()
+        if k >= 2:
+            times.append(s.elapsed_time(e))
+            uniq += _n_unique(step)
+            h2d += h_ids.numel() * 8 + g.numel() * 4
+            d2h += h_out.numel() * 4
+    t = sum(times) / 1e3
+    return {"value": uniq / t, "unit": "unique-ids/s", "h2d_bytes_per_step": h2d // n, "d2h_bytes_per_step": d2h // n,
+            "ms_per_step": t / n * 1e3}
+
+
+# ------------------------------------------------------------- CPU arm
+def cpu_baseline(cfg, batches, budget_s=15.0):
+    """The reference's own path (distributed_lookup on SimCluster(1, TwoStage) +
+    GradAccumulator accumulate/apply, OpenMP rows; Adagrad rows via the frozen
+    restatement) on the host cores, bounded sample of the same workload."""
+    import ctypes as C
+
+    from oracle import bind
+    kind = "reference" if bind.ref_available() else "port"
+    o = bind.Oracle("ref" if kind == "reference" else "oracle")
+    dim, vocab = cfg["dim"], cfg["vocab"]
+    keys = np.arange(vocab, dtype=np.uint64) + TAG1
+    h = C.c_void_p()
+    assert o.cluster_create(1, cfg["capacity"] // 2, dim, 1, 0.75, 1 << 16, 3, C.byref(h)) == 0
+    shard = bind.Table(o, 0, dim, handle=o.cluster_shard(h, 0))
+    row = np.zeros(dim, np.float32)
+    for r in range(vocab):
+        o.pseudo_sparse_grad(r, 0, row, dim)
+        shard.insert(int(keys[r]), row)
+    cores = o.omp_max_threads() if kind == "reference" else 1
+    times, uniq, reps = [], 0, 0
+    t_start = time.time()
+    for b, (lengths, ids) in enumerate(batches * 100):
+        grads = o.token_grads(lengths, b, dim)
+        if kind == "reference":
+            sec = o.c1_step(h, ids, grads.reshape(-1), len(ids), 1, 0.01, 1e-8, None)
+        else:
+            t0 = time.perf_counter()
+            u, _ = o.stage1(ids)
+            for k in u:
+                o.table_ensure(shard.h, int(k))
+            ia, sa = o.accumulate_np(ids, grads, dim)
+            o.apply(shard.h, ia, sa.reshape(-1), len(ia), 1, 0.01, 0.9, 0.999, 1e-8)
+            sec = time.perf_counter() - t0
+        if b >= 1:
+            times.append(sec)
+            uniq += len(np.unique(ids))
+        reps += 1
+        if time.time() - t_start > budget_s and len(times) >= 2:
+            break
+    o.cluster_destroy(h)
+    t = sum(times)
+    import platform
+    cpu = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
+    return {"value": uniq / t, "unit": "unique-ids/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} config-1 steps (after 1 warm-up) on the reference path "
+                      f"(distributed_lookup W=1 two-stage + accumulate + apply), {cpu}, nproc={os.cpu_count()}",
+            "ms_per_step": t / len(times) * 1e3}
+
+
+def run_reference(args, cfg):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    from paper_2505_12663_b200 import workload as W  # host-side generator (same ids as the reference's)
+    nb = max(1, min(args.steps + args.warmup, 4))
+    batches = [W.generate(cfg["seed"] + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"], cfg["zipf"],
+                          [cfg["vocab"]]) for b in range(nb)]
+    cb = cpu_baseline(cfg, batches, budget_s=args.cpu_seconds)
+    res = {"metric": "unique-ID lookups+updates/sec", "value": cb["value"], "unit": "unique-ids/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 optimizer math, u64 ids",
+           "data": "synthetic: the reference's generator", "config": {"workload": cfg["workload"]},
+           "impl": "reference", "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": "unique-ids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args, C1)
+    else:
+        run_ours(args, C1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * rsgpu.h -- C-ABI of the B200-native (sm_100a) sparse-embedding hot path.
+ *
+ * Drop-in boundary for the reference's table/lookup API
+ * (/root/reference/proj/include/recsparse/*.hpp).  Plain pointers and sizes,
+ * no C++ or torch types.  Every entry point names the reference interface it
+ * replaces.  Pointers prefixed d_ are device pointers; `stream` is a
+ * cudaStream_t (NULL = legacy default stream).  All calls are asynchronous on
+ * `stream` unless documented as synchronizing.
+ *
+ * Errors: no exceptions cross the ABI.  Status codes map 1:1 onto the
+ * reference's exception taxonomy (common.hpp:24-39):
+ *   RS_OK 0, RS_ERR_CONFIG 1 (ConfigError / std::invalid_argument on shapes),
+ *   RS_ERR_INVARIANT 2 (InvariantError), RS_ERR_IO 3 (IoError),
+ *   RS_ERR_CUDA 4 (CUDA/NCCL failure), RS_ERR_CAPACITY 5 (bounded table
+ *   cannot hold the batch), RS_ERR_RANGE 6 (std::out_of_range /
+ *   std::overflow_error of the id encoding).  rs_last_error() returns the
+ *   message of the last failure on the calling thread.
+ *
+ * Threading (embed_table.hpp:69-72): one writer per table per stream;
+ * concurrent read-only calls (rs_table_find, rs_table_gather_rows) are safe.
+ */
+#ifndef RSGPU_H
+#define RSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_ABI_VERSION 1
+
+enum {
+  RS_OK = 0,
+  RS_ERR_CONFIG = 1,
+  RS_ERR_INVARIANT = 2,
+  RS_ERR_IO = 3,
+  RS_ERR_CUDA = 4,
+  RS_ERR_CAPACITY = 5,
+  RS_ERR_RANGE = 6
+};
+
+enum { RS_OPT_NONE = 0, RS_OPT_ADAM = 1, RS_OPT_ADAGRAD = 2 };
+
+typedef struct rs_table rs_table;         /* one dynamic hash embedding table (one shard) */
+typedef struct rs_workspace rs_workspace; /* per-stream scratch for dedup/reduce/step */
+
+/* TableConfig (embed_table.hpp:28-36) plus the GPU build's extensions. */
+typedef struct {
+  uint64_t capacity;       /* initial key slots; power of two >= 16 */
+  uint32_t embedding_dim;  /* floats per row, >= 1 */
+  uint32_t thread_groups;  /* power of two, capacity >= 2*groups (validated like the
+                              reference; the GPU probes 8-slot buckets with 8 lanes) */
+  double max_load_factor;  /* (occupied + tombstones)/capacity ceiling, in (0,1) */
+  uint32_t chunk_rows;     /* row-pool growth granularity, >= 1 */
+  uint32_t optimizer;      /* RS_OPT_*: which state arrays rows carry */
+  uint64_t initial_rows;   /* row-pool pre-allocation (0: capacity*max_load_factor) */
+  uint64_t max_keys;       /* 0: unbounded (expand); >0: bounded, evict oldest (ts, key) */
+} rs_table_config;
+
+/* AdamParams (sparse_update.hpp:26-31); Adagrad uses lr and eps. */
+typedef struct {
+  uint32_t kind; /* RS_OPT_ADAM or RS_OPT_ADAGRAD */
+  double lr, beta1, beta2, eps;
+} rs_optimizer_params;
+
+typedef struct {
+  uint64_t capacity, occupied, tombstones;
+  uint64_t rows_allocated, rows_free, row_capacity;
+  uint64_t tick;
+  uint32_t embedding_dim, optimizer;
+} rs_table_info;
+
+/* ---- meta ---------------------------------------------------------------- */
+int rs_abi_version(void);
+const char* rs_status_string(int status);
+const char* rs_last_error(void);
+/* number of rsgpu kernel launches issued so far by this process (evidence) */
+uint64_t rs_kernel_launches(void);
+
+/* ---- primitives (hash.hpp) --------------------------------------------- */
+/* hash64_batch (hash.hpp:38, hash.cpp:21-30) */
+int rs_hash64_batch(const uint64_t* d_keys, uint64_t n, uint64_t* d_out, void* stream);
+/* SimCluster::shard_of (exchange_sim.cpp:82-85) */
+int rs_shard_of_batch(const uint64_t* d_ids, uint64_t n, uint32_t world, uint32_t* d_owner,
+                      void* stream);
+
+/* ---- dynamic table (EmbedTable, embed_table.hpp:73-211) ------------------- */
+/* EmbedTable(TableConfig) (embed_table.cpp:40-45); validation :23-38 */
+int rs_table_create(const rs_table_config* cfg, rs_table** out);
+int rs_table_destroy(rs_table* t);
+/* capacity()/occupied()/tombstones()/tick() (embed_table.hpp:112-118). Synchronizes. */
+int rs_table_stats(rs_table* t, rs_table_info* out);
+/* insert (embed_table.cpp:193-227), batched upsert; duplicate keys: last wins.
+ * d_emb [n x dim]. New keys get fresh zeroed optimizer state. */
+int rs_table_insert(rs_table* t, const uint64_t* d_keys, uint64_t n, const float* d_emb,
+                    void* stream);
+/* find (embed_table.cpp:237-241): d_rows[n] = row id or -1; no side effects. */
+int rs_table_find(rs_table* t, const uint64_t* d_keys, uint64_t n, int64_t* d_rows, void* stream);
+/* lookup_batch (embed_table.cpp:287-315): d_out [n x dim], zeros on miss,
+ * every hit stamped with one tick for the whole batch. */
+int rs_table_lookup(rs_table* t, const uint64_t* d_keys, uint64_t n, float* d_out, void* stream);
+/* ensure (embed_table.cpp:243-248), batched find-or-insert-zero-row; d_rows
+ * optional.  Bounded tables evict the oldest (ts, key) first. */
+int rs_table_ensure(rs_table* t, const uint64_t* d_keys, uint64_t n, int64_t* d_rows,
+                    void* stream);
+/* remove (embed_table.cpp:250-260); d_removed[n] (optional) = 1 if removed. */
+int rs_table_remove(rs_table* t, const uint64_t* d_keys, uint64_t n, uint8_t* d_removed,
+                    void* stream);
+/* expand (embed_table.cpp:262-285): doubles the key structure at least once;
+ * rows never move.  Synchronizes; *new_capacity optional. */
+int rs_table_expand(rs_table* t, uint64_t* new_capacity, void* stream);
+/* eviction (no reference counterpart): remove the k live entries
+ * with smallest (ts, key).  Synchronizes; *evicted optional. */
+int rs_table_evict(rs_table* t, uint64_t k, uint64_t* evicted, void* stream);
+/* Gather rows by row id (row handles from find/ensure): d_out [n x dim]. */
+int rs_table_gather_rows(rs_table* t, const int64_t* d_rows, uint64_t n, float* d_out,
+                         void* stream);
+/* Host export of live entries (for_each_occupied, embed_table.hpp:142-147),
+ * sorted by key.  Any output may be NULL; *count = occupied.  Call with
+ * max_entries = 0 to query the count.  Synchronizes. */
+int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* emb, float* m,
+                    float* v, uint64_t* step, uint64_t* ts, uint64_t* count);
+/* Host import of full entries (restore path, checkpoint.cpp:238-249: keys are
+ * re-inserted, slots are not portable).  m/v/step/ts may be NULL. */
+int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* emb,
+                    const float* m, const float* v, const uint64_t* step, const uint64_t* ts);
+
+/* ---- dedup (exchange_sim.cpp:87-115) -------------------------------------- */
+int rs_workspace_create(uint64_t max_tokens, rs_workspace** out);
+int rs_workspace_destroy(rs_workspace* ws);
+/* stage1_dedup: first-occurrence unique ids + int32 inverse; *d_n_unique is a
+ * device uint32.  Stage 2 is the same call over the source-ordered
+ * concatenation of received lists (its inverse gives every origin). */
+int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_unique,
+             int32_t* d_inverse, uint32_t* d_n_unique, void* stream);
+
+/* ---- the fused training step (workload.cpp:506-581 for one shard) --------
+ * forward : dedup -> find-or-insert (zero-vivify) -> jagged gather
+ *           d_out[n x dim] (bit-exact with distributed_lookup's outputs)
+ * backward: segment-reduce d_grads[n x dim] onto unique rows fused with the
+ *           optimizer update (Adam sparse_update.cpp:22-37 / Adagrad) */
+int rs_forward(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, float* d_out,
+               void* stream);
+int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
+                const rs_optimizer_params* opt, void* stream);
+int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+            const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream);
+/* GradAccumulator::accumulate + apply for one window (sparse_update.cpp:45-83):
+ * dedup ids, zero-vivify absent ids, segment-reduce grads fused with the
+ * optimizer.  No gather. */
+int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, const rs_optimizer_params* opt, void* stream);
+/* Results of the last forward on this workspace (device pointers owned by ws). */
+int rs_workspace_results(rs_workspace* ws, const uint64_t** d_unique, const int32_t** d_inverse,
+                         const uint32_t** d_n_unique, const int64_t** d_rows);
+/* n_unique of the last dedup on this workspace (host value).  Synchronizes. */
+int rs_workspace_n_unique(rs_workspace* ws, uint64_t* out);
+/* GradAccumulator::accumulate for one micro-batch (sparse_update.cpp:45-56):
+ * aggregated grads per unique id of the last forward, first-occurrence order,
+ * d_sums [n_unique x dim]. */
+int rs_accumulate(rs_workspace* ws, const float* d_grads, uint64_t n, float* d_sums,
+                  void* stream);
+/* GradAccumulator::apply given aggregated grads (sparse_update.cpp:58-83):
+ * ensure + one optimizer step per key, keys unique. */
+int rs_apply_aggregated(rs_table* t, const uint64_t* d_keys, uint64_t n, const float* d_sums,
+                        const rs_optimizer_params* opt, void* stream);
+
+/* ---- table merging (merge_registry.cpp:23-51) ----------------------------- */
+/* encode_tagged_id on device; d_status (optional) receives RS_ERR_RANGE per bad id. */
+int rs_encode_ids(const uint64_t* d_raw, uint64_t n, uint32_t k_bits, uint32_t table_index,
+                  uint32_t index_limit, uint64_t* d_out, void* stream);
+
+/* ---- synthetic inputs (workload.cpp:103-152, 280-307, 348-355) ------------ */
+/* generate_workload: per-sample lengths + catalog-tagged ids (k = bit_width(tables)) */
+int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len,
+                         double sigma, double zipf, uint32_t tables, const uint64_t* vocab,
+                         uint64_t* lengths, uint64_t* ids, uint64_t max_tokens,
+                         uint64_t* n_tokens);
+/* pseudo_sparse_grad per token on device: d_out[t] = g(sample_of_token[t], step) */
+int rs_pseudo_grads(const uint64_t* d_sample_of_token, uint64_t n, uint64_t step, uint32_t dim,
+                    float* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSGPU_H */

@@ -1,0 +1,18 @@
+"""B200-native (sm_100a) sparse-embedding hot path of MTGenRec (arXiv 2505.12663).
+
+Drop-in for the reference recsparse table/lookup API: the kernels live in
+``_lib/librsgpu.so`` (C-ABI: ``include/rsgpu.h``); this package is the host
+mirror of the reference interface.  No CPU fallback exists.
+"""
+from ._lib import (CapacityError, ConfigError, CudaError, InvariantError, IoError, RangeError,
+                   RecsparseError, build, lib)
+from .table import (AdagradParams, AdamParams, EmbedTable, SparseStep, TableConfig, Workspace,
+                    apply_aggregated, as_keys, hash64_batch, keys_to_numpy, shard_of_batch,
+                    sparse_update, stage1_dedup)
+
+__all__ = [
+    "AdagradParams", "AdamParams", "CapacityError", "ConfigError", "CudaError", "EmbedTable",
+    "InvariantError", "IoError", "RangeError", "RecsparseError", "SparseStep", "TableConfig",
+    "Workspace", "apply_aggregated", "as_keys", "build", "hash64_batch", "keys_to_numpy", "lib",
+    "shard_of_batch", "sparse_update", "stage1_dedup",
+]

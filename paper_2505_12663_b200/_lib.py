@@ -1,0 +1,151 @@
+"""ctypes binding of librsgpu.so (the C-ABI declared in include/rsgpu.h).
+
+The shared library is built in-tree by ``paper_2505_12663_b200/csrc/Makefile``
+(nvcc, sm_100a only).  There is no CPU fallback: if the library cannot be
+loaded, importing the product API raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "librsgpu.so")
+CSRC = os.path.join(HERE, "csrc")
+
+RS_OK, RS_ERR_CONFIG, RS_ERR_INVARIANT, RS_ERR_IO, RS_ERR_CUDA, RS_ERR_CAPACITY, RS_ERR_RANGE = range(7)
+RS_OPT_NONE, RS_OPT_ADAM, RS_OPT_ADAGRAD = 0, 1, 2
+
+
+# Exception taxonomy of the reference (common.hpp:24-39) + the GPU build's.
+class RecsparseError(RuntimeError):
+    status = -1
+
+
+class ConfigError(RecsparseError):
+    status = RS_ERR_CONFIG
+
+
+class InvariantError(RecsparseError):
+    status = RS_ERR_INVARIANT
+
+
+class IoError(RecsparseError):
+    status = RS_ERR_IO
+
+
+class CudaError(RecsparseError):
+    status = RS_ERR_CUDA
+
+
+class CapacityError(RecsparseError):
+    status = RS_ERR_CAPACITY
+
+
+class RangeError(RecsparseError, OverflowError):
+    status = RS_ERR_RANGE
+
+
+_ERR = {c.status: c for c in (ConfigError, InvariantError, IoError, CudaError, CapacityError, RangeError)}
+
+
+class rs_table_config(C.Structure):
+    _fields_ = [("capacity", C.c_uint64), ("embedding_dim", C.c_uint32), ("thread_groups", C.c_uint32),
+                ("max_load_factor", C.c_double), ("chunk_rows", C.c_uint32), ("optimizer", C.c_uint32),
+                ("initial_rows", C.c_uint64), ("max_keys", C.c_uint64)]
+
+
+class rs_optimizer_params(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double)]
+
+
+class rs_table_info(C.Structure):
+    _fields_ = [("capacity", C.c_uint64), ("occupied", C.c_uint64), ("tombstones", C.c_uint64),
+                ("rows_allocated", C.c_uint64), ("rows_free", C.c_uint64), ("row_capacity", C.c_uint64),
+                ("tick", C.c_uint64), ("embedding_dim", C.c_uint32), ("optimizer", C.c_uint32)]
+
+
+vp = C.c_void_p
+u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int32
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "rs_abi_version": (C.c_int, []),
+    "rs_status_string": (C.c_char_p, [C.c_int]),
+    "rs_last_error": (C.c_char_p, []),
+    "rs_kernel_launches": (u64, []),
+    "rs_hash64_batch": (C.c_int, [vp, u64, vp, vp]),
+    "rs_shard_of_batch": (C.c_int, [vp, u64, u32, vp, vp]),
+    "rs_table_create": (C.c_int, [C.POINTER(rs_table_config), C.POINTER(vp)]),
+    "rs_table_destroy": (C.c_int, [vp]),
+    "rs_table_stats": (C.c_int, [vp, C.POINTER(rs_table_info)]),
+    "rs_table_insert": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_find": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_lookup": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_ensure": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_remove": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_expand": (C.c_int, [vp, C.POINTER(u64), vp]),
+    "rs_table_evict": (C.c_int, [vp, u64, C.POINTER(u64), vp]),
+    "rs_table_gather_rows": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_table_export": (C.c_int, [vp, u64, vp, vp, vp, vp, vp, vp, C.POINTER(u64)]),
+    "rs_table_import": (C.c_int, [vp, u64, vp, vp, vp, vp, vp, vp]),
+    "rs_workspace_create": (C.c_int, [u64, C.POINTER(vp)]),
+    "rs_workspace_destroy": (C.c_int, [vp]),
+    "rs_dedup": (C.c_int, [vp, vp, u64, vp, vp, vp, vp]),
+    "rs_forward": (C.c_int, [vp, vp, vp, u64, vp, vp]),
+    "rs_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
+    "rs_step": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_sparse_update": (C.c_int, [vp, vp, vp, u64, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_workspace_results": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
+    "rs_workspace_n_unique": (C.c_int, [vp, C.POINTER(u64)]),
+    "rs_accumulate": (C.c_int, [vp, vp, u64, vp, vp]),
+    "rs_apply_aggregated": (C.c_int, [vp, vp, u64, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
+    "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
+                                       u64, C.POINTER(u64)]),
+    "rs_pseudo_grads": (C.c_int, [vp, u64, u64, u32, vp, vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile librsgpu.so for sm_100a in-tree (nvcc).  Returns its path."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", "-C", CSRC, "-j8"], check=True)
+    return LIB_PATH
+
+
+def lib():
+    """Load (building if needed) librsgpu.so.  Raises if it cannot be loaded."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                build()
+            L = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(L, name, None)
+                if fn is None:
+                    continue
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+        return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    if status == RS_OK:
+        return
+    L = lib()
+    msg = (L.rs_last_error() or b"").decode(errors="replace")
+    cls = _ERR.get(status, RecsparseError)
+    raise cls(f"{what}: {L.rs_status_string(status).decode()}: {msg}")
+
+
+def exported_symbols():
+    return [n for n in _SIGS if getattr(lib(), n, None) is not None]

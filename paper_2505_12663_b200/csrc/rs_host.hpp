@@ -1,0 +1,96 @@
+// rs_host.hpp -- host-side objects behind the opaque C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "rs_internal.cuh"
+
+// Counter snapshot copied device->host asynchronously after every mutating
+// batch op, double-buffered so the host can bound occupancy without a sync
+// (DESIGN.md §4 "sync-free capacity management").
+struct rs_mirror {
+  rs::TableCounters* pinned = nullptr;
+  cudaEvent_t ev = nullptr;
+  uint64_t requested_at_copy = 0;  // cumulative keys requested when the copy was enqueued
+  bool valid = false;
+};
+
+struct rs_table {
+  rs_table_config cfg{};
+  rs::TableDev* dev = nullptr;   // device descriptor + counters
+  rs::TableDesc desc{};          // host copy of the pointer section
+  uint64_t capacity = 0;         // key slots
+  // sync-free capacity bookkeeping
+  rs_mirror mirror[2];
+  int mirror_next = 0;
+  uint64_t requested_total = 0;  // Σ n over all insert/ensure batches
+  uint64_t exact_occ = 0, exact_tomb = 0, exact_rows = 0, exact_requested = 0;
+  // Adam bias-correction tables 1 - beta^step computed with the host libm
+  // (bit-identical to sparse_update.cpp:25-26 on this host)
+  double* d_bc = nullptr;        // [2 x bc_len]
+  uint64_t bc_len = 0;
+  double bc_beta1 = -1, bc_beta2 = -1;
+  uint64_t applies = 0;          // optimizer applications (upper bound of any row step)
+  uint64_t host_tick = 0;        // batch ops issued (device tick follows it)
+  // bounded tables: probe-miss list + eviction key buffer
+  uint32_t* d_missing = nullptr;
+  uint64_t missing_cap = 0;
+  uint64_t* d_victims = nullptr;
+  uint64_t victims_cap = 0;
+};
+
+struct rs_workspace {
+  uint64_t max_tokens = 0;
+  uint64_t S = 0;  // scratch hash capacity (power of two); index S is the spare slot
+  // dedup scratch set (SoA, S+1 entries)
+  unsigned long long* skey = nullptr;
+  uint32_t* sfirstx = nullptr;  // ~first position (atomicMax)
+  uint32_t* scount = nullptr;
+  uint32_t* sntile = nullptr;
+  uint32_t* suidx = nullptr;
+  uint32_t* srow = nullptr;
+  // per token
+  uint32_t* slot_of = nullptr;
+  int32_t* inverse = nullptr;
+  // per unique
+  uint64_t* unique = nullptr;
+  uint32_t* u_slot = nullptr;
+  uint32_t* u_ntile = nullptr;
+  uint32_t* u_poff = nullptr;
+  uint32_t* u_ticket = nullptr;
+  uint32_t* u_done = nullptr;
+  uint32_t* urow = nullptr;
+  int64_t* urow64 = nullptr;
+  // cross-tile partial sums
+  uint32_t* ptile = nullptr;
+  uint32_t* porder = nullptr;
+  float* pbuf = nullptr;
+  uint64_t pbuf_floats = 0;
+  // scans
+  uint64_t* scan_status = nullptr;
+  uint32_t* ctr = nullptr;  // [0] tile ticket [1] blocks done [2] n_unique [3] n_part
+  // last forward
+  uint64_t last_n = 0;
+  uint32_t last_tile = 0;
+  rs_table* last_table = nullptr;
+  bool have_forward = false;
+};
+
+namespace rs {
+// table.cu
+int table_prepare(rs_table* t, uint64_t n, cudaStream_t s);  // room for n more keys
+int table_after_op(rs_table* t, cudaStream_t s);             // enqueue counter mirror
+int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                        uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                        uint32_t* d_srow, cudaStream_t s);
+int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                     uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                     uint32_t* d_srow, cudaStream_t s);
+int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies, cudaStream_t s);
+// step.cu
+int dedup_run(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint32_t tile,
+              cudaStream_t s);
+uint32_t tile_tokens_for_dim(uint32_t dim);
+}  // namespace rs

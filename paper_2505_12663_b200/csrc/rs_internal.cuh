@@ -1,0 +1,140 @@
+// rs_internal.cuh -- shared device/host definitions of librsgpu (sm_100a).
+//
+// Layout decisions:
+//  * key structure: 16-byte slots {u64 key, u32 row, u32 tick} in 8-slot
+//    buckets (one 128-byte line).  A group of 8 lanes probes one bucket per
+//    step -- the paper's grouped parallel probing (Eq. 5)
+//    with G = 8 mapped onto lanes; bucket sequence b_t = b0 + t*S, S odd.
+//  * embedding structure: SoA row pool (emb, opt_m, opt_v, step), rows never
+//    move when the key structure expands (embed_table.cpp:267-285).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/rsgpu.h"
+
+namespace rs {
+
+constexpr uint64_t kEmptyKey = ~0ull;      // slot never used
+constexpr uint64_t kTombKey = ~0ull - 1;   // deleted slot (embed_table.hpp:47)
+constexpr uint32_t kNoRow = 0xFFFFFFFFu;
+constexpr int kBucket = 8;                 // slots per bucket == lanes per probe group
+constexpr int kTile = 512;                 // tokens per reduce tile (dedup + reduce agree)
+constexpr int kScanItems = 4;              // tokens per thread in scan kernels
+constexpr int kScanThreads = 256;
+constexpr int kScanTile = kScanItems * kScanThreads;
+
+// MurmurHash3 fmix64 (hash.hpp:26-33).
+__host__ __device__ __forceinline__ uint64_t hash64(uint64_t key) {
+  key ^= key >> 33;
+  key *= 0xff51afd7ed558ccdULL;
+  key ^= key >> 33;
+  key *= 0xc4ceb9fe1a85ec53ULL;
+  key ^= key >> 33;
+  return key;
+}
+
+struct __align__(16) Slot {
+  unsigned long long key;
+  uint32_t row;
+  uint32_t tick;
+};
+
+// Device-resident table descriptor.  The pointer section is written by the
+// host (cudaMemcpyAsync, stream ordered) when the key structure expands or the
+// row pool grows; the counter section is updated only by kernels.  Kernels
+// read pointers from here, so captured CUDA graphs survive reallocation.
+struct TableDesc {
+  Slot* slots;
+  uint64_t nb_mask;    // buckets - 1 (buckets is a power of two >= 2)
+  float* emb;          // [row_cap x dim]
+  float* s1;           // Adam m (or null)
+  float* s2;           // Adam v / Adagrad accumulator (or null)
+  uint32_t* step;      // per-row optimizer step
+  uint32_t* free_stack;
+  uint64_t row_cap;
+  uint32_t dim;
+  uint32_t opt;
+};
+
+struct TableCounters {
+  unsigned long long occupied;
+  unsigned long long tombstones;
+  unsigned long long fresh_next;   // rows carved from the pool so far
+  unsigned long long free_n;       // rows on the LIFO free stack
+  unsigned long long alloc_ctr;    // per-launch allocation tickets
+  unsigned long long inserted;     // per-launch new keys
+  unsigned long long reused;       // per-launch tombstones reused
+  unsigned long long removed;      // per-launch removals
+  unsigned int blocks_done;
+  unsigned int error;              // sticky error bits (kErr*)
+  unsigned int tick;               // batch tick (one per batch op)
+  unsigned int special_row[2];     // rows of the keys equal to kEmptyKey / kTombKey
+  unsigned int special_tick[2];
+  unsigned int missing;            // per-launch count of missing keys (probe mode)
+  unsigned int pad;
+};
+
+struct TableDev {
+  TableDesc d;
+  TableCounters c;
+};
+
+enum : unsigned int {
+  kErrRowPool = 1u,    // ran out of pre-sized rows (host bound violated)
+  kErrTableFull = 2u,  // probe walked every bucket without a usable slot
+  kErrCapacity = 4u,   // bounded table cannot hold the batch
+};
+
+// ---- PTX helpers ----------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ---- host-side error plumbing --------------------------------------------
+void set_error(const std::string& msg);
+int fail(int status, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* what);
+void count_launch(uint64_t n = 1);
+
+#define RS_CUDA(call)                                       \
+  do {                                                      \
+    cudaError_t _e = (call);                                \
+    if (_e != cudaSuccess) return ::rs::cuda_fail(_e, #call); \
+  } while (0)
+
+#define RS_LAUNCH_CHECK(name)                               \
+  do {                                                      \
+    ::rs::count_launch();                                   \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) return ::rs::cuda_fail(_e, name); \
+  } while (0)
+
+inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 148u * 32u) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace rs

@@ -1,0 +1,1144 @@
+// step.cu -- dedup, jagged gather, segment-reduce + sparse optimizer (sm_100a).
+//
+// One training step of one shard (reference caller: run_workload,
+// workload.cpp:506-581; for W = 1 distributed_lookup reduces to
+// stage1_dedup + ensure + inverse expand, exchange_sim.cpp:117-233):
+//
+//   K0 k_dedup_clear    reset the scratch slots used by the previous call
+//   K1 k_dedup_tile     per 1 tile: smem dedup, then one global insert per
+//                       (tile, distinct id): first position (atomicMax of ~pos),
+//                       count, number of tiles containing the id
+//   K2 k_dedup_compact  decoupled look-back scan over tokens: heads (first
+//                       occurrences) get their unique index = first-occurrence
+//                       order (exchange_sim.cpp:87-98), plus the offsets of
+//                       the cross-tile partial-sum segments
+//   K3 k_table_upsert   find-or-insert-zero of the unique ids (table.cu)
+//   K4 k_gather         out[t] = emb[row(inverse[t])], 128-bit vector copies
+//   K5 k_reduce_update  per tile: TMA-bulk stage of the tile's gradient rows
+//                       into smem, smem grouping by unique id, position-order
+//                       sums; single-tile ids update their row immediately,
+//                       multi-tile ids write a partial and the last arriving
+//                       tile sums the partials in tile order and updates.
+//                       Adam (sparse_update.cpp:22-37) / Adagrad in FP64
+//                       with explicit _rn intrinsics (no FMA contraction).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "rs_host.hpp"
+
+namespace rs {
+namespace {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+// ---------------------------------------------------------------------------
+// K0: clear the scratch slots touched by the previous dedup (its unique list)
+__global__ void k_dedup_clear(unsigned long long* skey, uint32_t* sfirstx, uint32_t* scount,
+                              uint32_t* sntile, const uint32_t* u_slot, uint32_t* ctr,
+                              uint64_t spare) {
+  const uint32_t prev = ctr[2];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= prev;
+       i += gridDim.x * blockDim.x) {
+    const uint64_t s = i < prev ? u_slot[i] : spare;
+    skey[s] = kEmptyKey;
+    sfirstx[s] = 0;
+    scount[s] = 0;
+    sntile[s] = 0;
+  }
+}
+
+__global__ void k_dedup_clear_all(unsigned long long* skey, uint32_t* sfirstx, uint32_t* scount,
+                                  uint32_t* sntile, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    skey[i] = kEmptyKey;
+    sfirstx[i] = 0;
+    scount[i] = 0;
+    sntile[i] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: per-tile smem dedup, then one global scratch insert per distinct id.
+// blockDim.x == TT tokens per tile; dynamic smem: 2TT+1 local slots.
+__global__ void k_dedup_tile(const uint64_t* __restrict__ ids, uint32_t n,
+                             unsigned long long* __restrict__ skey, uint32_t* __restrict__ sfirstx,
+                             uint32_t* __restrict__ scount, uint32_t* __restrict__ sntile,
+                             uint64_t smask, uint64_t spare, uint32_t* __restrict__ slot_of) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t TT = blockDim.x;
+  const uint32_t L = 2 * TT;  // local slots (power of two), index L = sentinel id
+  unsigned long long* lkey = reinterpret_cast<unsigned long long*>(smem);
+  uint32_t* lfirst = reinterpret_cast<uint32_t*>(lkey + L + 1);
+  uint32_t* lcount = lfirst + L + 1;
+  uint32_t* lgslot = lcount + L + 1;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t i = tid; i <= L; i += TT) {
+    lkey[i] = kEmptyKey;
+    lfirst[i] = kFull;
+    lcount[i] = 0;
+  }
+  __syncthreads();
+  const uint32_t t = blockIdx.x * TT + tid;
+  const bool valid = t < n;
+  uint64_t id = 0, h = 0;
+  uint32_t p = 0;
+  if (valid) {
+    id = ids[t];
+    if (id == kEmptyKey) {
+      p = L;
+    } else {
+      h = hash64(id);
+      p = (uint32_t)(h >> 40) & (L - 1);
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&lkey[p], kEmptyKey, (unsigned long long)id);
+        if (prev == kEmptyKey || prev == id) break;
+        p = (p + 1) & (L - 1);
+      }
+    }
+    atomicMin(&lfirst[p], tid);
+    atomicAdd(&lcount[p], 1u);
+  }
+  __syncthreads();
+  if (valid && lfirst[p] == tid) {
+    uint64_t gs;
+    if (p == L) {
+      gs = spare;
+    } else {
+      gs = h & smask;
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&skey[gs], kEmptyKey, (unsigned long long)id);
+        if (prev == kEmptyKey || prev == id) break;
+        gs = (gs + 1) & smask;
+      }
+    }
+    atomicMax(&sfirstx[gs], ~t);  // ~min(position)
+    atomicAdd(&scount[gs], lcount[p]);
+    atomicAdd(&sntile[gs], 1u);
+    lgslot[p] = (uint32_t)gs;
+  }
+  __syncthreads();
+  if (valid) slot_of[t] = lgslot[p];
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over tiles for a pair of 31-bit counters.
+struct Pair {
+  uint32_t a, b;
+};
+__device__ __forceinline__ uint64_t st_pack(uint32_t flag, Pair v) {
+  return ((uint64_t)flag << 62) | ((uint64_t)(v.a & 0x7FFFFFFFu) << 31) | (v.b & 0x7FFFFFFFu);
+}
+__device__ __forceinline__ Pair st_unpack(uint64_t s) {
+  return Pair{(uint32_t)((s >> 31) & 0x7FFFFFFFu), (uint32_t)(s & 0x7FFFFFFFu)};
+}
+__device__ __forceinline__ Pair warp_sum(Pair v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    v.a += __shfl_xor_sync(kFull, v.a, o);
+    v.b += __shfl_xor_sync(kFull, v.b, o);
+  }
+  return v;
+}
+__device__ __forceinline__ Pair warp_incl_scan(Pair v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(kFull, v.a, o);
+    const uint32_t b = __shfl_up_sync(kFull, v.b, o);
+    if (lane >= (unsigned)o) {
+      v.a += a;
+      v.b += b;
+    }
+  }
+  return v;
+}
+
+// Called by warp 0 of the block owning `tile`; returns the exclusive prefix.
+__device__ Pair lookback(uint64_t* status, uint32_t tile, Pair agg) {
+  const unsigned lane = lane_id();
+  if (tile == 0) {
+    if (lane == 0) st_release(&status[0], st_pack(2, agg));
+    return Pair{0, 0};
+  }
+  if (lane == 0) st_release(&status[tile], st_pack(1, agg));
+  Pair run{0, 0};
+  int64_t j = (int64_t)tile - 1;
+  for (;;) {
+    const int64_t idx = j - lane;
+    const uint64_t s = idx >= 0 ? ld_acquire(&status[idx]) : st_pack(2, Pair{0, 0});
+    const uint32_t flag = (uint32_t)(s >> 62);
+    const unsigned m0 = __ballot_sync(kFull, flag == 0);
+    const unsigned m2 = __ballot_sync(kFull, flag == 2);
+    const int stop = m2 ? __ffs(m2) - 1 : 31;
+    const unsigned need = stop == 31 ? kFull : ((2u << stop) - 1u);
+    if (m0 & need) continue;  // a predecessor inside the window has not published yet
+    Pair v = (int)lane <= stop ? st_unpack(s) : Pair{0, 0};
+    v = warp_sum(v);
+    run.a += v.a;
+    run.b += v.b;
+    if (m2) break;
+    j -= 32;
+  }
+  if (lane == 0) st_release(&status[tile], st_pack(2, Pair{agg.a + run.a, agg.b + run.b}));
+  return run;
+}
+
+// K2: head = first occurrence; exclusive scan over tokens of
+// (head, head && ntile > 1 ? ntile : 0) gives the unique index (first-
+// occurrence order) and the offset of the id's cross-tile partial segment.
+__global__ void __launch_bounds__(kScanThreads)
+    k_dedup_compact(const uint64_t* __restrict__ ids, uint32_t n,
+                    const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ sfirstx,
+                    const uint32_t* __restrict__ sntile, uint32_t* __restrict__ suidx,
+                    uint64_t* __restrict__ unique, uint32_t* __restrict__ u_slot,
+                    uint32_t* __restrict__ u_ntile, uint32_t* __restrict__ u_poff,
+                    uint32_t* __restrict__ u_ticket, uint32_t* __restrict__ u_done,
+                    uint64_t* status, uint32_t* ctr, uint32_t ntiles) {
+  __shared__ uint32_t s_tile;
+  __shared__ Pair s_warp[kScanThreads / 32];
+  __shared__ Pair s_prefix;
+  __shared__ bool s_last;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(&ctr[0], 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint32_t base = tile * kScanTile + tid * kScanItems;
+  uint32_t sl[kScanItems];
+  uint32_t nt[kScanItems];
+  bool hd[kScanItems];
+  Pair mine{0, 0};
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    const uint32_t t = base + k;
+    hd[k] = false;
+    nt[k] = 0;
+    sl[k] = 0;
+    if (t < n) {
+      sl[k] = slot_of[t];
+      hd[k] = sfirstx[sl[k]] == ~t;
+      if (hd[k]) nt[k] = sntile[sl[k]];
+    }
+    mine.a += hd[k];
+    mine.b += (hd[k] && nt[k] > 1) ? nt[k] : 0;
+  }
+  Pair incl = warp_incl_scan(mine);
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    Pair w = lane < kScanThreads / 32 ? s_warp[lane] : Pair{0, 0};
+    Pair wi = warp_incl_scan(w);
+    if (lane < kScanThreads / 32) s_warp[lane] = Pair{wi.a - w.a, wi.b - w.b};
+    const Pair agg{__shfl_sync(kFull, wi.a, kScanThreads / 32 - 1),
+                   __shfl_sync(kFull, wi.b, kScanThreads / 32 - 1)};
+    const Pair pre = lookback(status, tile, agg);
+    if (lane == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  Pair run{s_prefix.a + s_warp[warp].a + incl.a - mine.a,
+           s_prefix.b + s_warp[warp].b + incl.b - mine.b};
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (hd[k]) {
+      const uint32_t t = base + k;
+      const uint32_t ra = run.a;
+      unique[ra] = ids[t];
+      suidx[sl[k]] = ra;
+      u_slot[ra] = sl[k];
+      u_ntile[ra] = nt[k];
+      u_poff[ra] = run.b;
+      u_ticket[ra] = 0;
+      u_done[ra] = 0;
+      run.a += 1;
+      run.b += nt[k] > 1 ? nt[k] : 0;
+    }
+  }
+  if (tile == ntiles - 1 && tid == kScanThreads - 1) {
+    ctr[2] = run.a;  // n_unique
+    ctr[3] = run.b;  // n_part
+  }
+  // last block resets the tile ticket and the status words for the next call
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctr[1], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (uint32_t i = tid; i < ntiles; i += kScanThreads) status[i] = 0;
+    if (tid == 0) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+__global__ void k_inverse(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ suidx,
+                          uint32_t n, int32_t* __restrict__ inverse) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    inverse[i] = (int32_t)suidx[slot_of[i]];
+}
+
+__global__ void k_copy_unique(const uint64_t* __restrict__ src, const uint32_t* __restrict__ ctr,
+                              uint64_t* __restrict__ dst, uint32_t* __restrict__ n_out) {
+  const uint32_t n = ctr[2];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n_out) *n_out = n;
+}
+
+// ---------------------------------------------------------------------------
+// K4: jagged gather.  LPR lanes per row, float4 per lane, UNR tokens in flight
+// per lane group: the slot -> (unique, row) -> embedding chain is issued for
+// UNR tokens before any store so the dependent loads overlap.
+template <int LPR, int UNR>
+__global__ void __launch_bounds__(256)
+    k_gather(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ suidx,
+             const uint32_t* __restrict__ srow, const TableDev* __restrict__ td, uint32_t n,
+             int32_t* __restrict__ inverse, float* __restrict__ out) {
+  const uint32_t D = td->d.dim;
+  const uint32_t D4 = D >> 2;
+  const float4* __restrict__ emb = reinterpret_cast<const float4*>(td->d.emb);
+  float4* __restrict__ o4 = reinterpret_cast<float4*>(out);
+  const uint32_t l = threadIdx.x % LPR;
+  const uint64_t grp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR;
+  const uint64_t ngrp = (uint64_t)gridDim.x * blockDim.x / LPR;
+  for (uint64_t t0 = grp; t0 < n; t0 += ngrp * UNR) {
+    uint32_t u[UNR], r[UNR], s[UNR];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const uint64_t t = t0 + (uint64_t)k * ngrp;
+      s[k] = t < n ? __ldg(slot_of + t) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const uint64_t t = t0 + (uint64_t)k * ngrp;
+      u[k] = t < n ? __ldcg(suidx + s[k]) : 0;
+      r[k] = t < n ? __ldcg(srow + s[k]) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const uint64_t t = t0 + (uint64_t)k * ngrp;
+      if (t < n) {
+        if (l == 0) inverse[t] = (int32_t)u[k];
+        const float4* src = emb + (size_t)r[k] * D4;
+        float4* dst = o4 + t * D4;
+        for (uint32_t j = l; j < D4; j += LPR) __stcs(dst + j, __ldg(src + j));
+      }
+    }
+  }
+}
+
+// scalar fallback for D % 4 != 0
+__global__ void k_gather_scalar(const uint32_t* __restrict__ slot_of,
+                                const uint32_t* __restrict__ suidx, const uint32_t* __restrict__ srow,
+                                const TableDev* __restrict__ td, uint32_t n,
+                                int32_t* __restrict__ inverse, float* __restrict__ out) {
+  const uint32_t D = td->d.dim;
+  const float* emb = td->d.emb;
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const unsigned lane = lane_id();
+  for (uint64_t t = w; t < n; t += nw) {
+    const uint32_t s = slot_of[t];
+    const uint32_t r = __ldcg(srow + s);
+    if (lane == 0) inverse[t] = (int32_t)__ldcg(suidx + s);
+    for (uint32_t e = lane; e < D; e += 32) out[t * D + e] = emb[(size_t)r * D + e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Optimizers: FP64 math with explicit round-to-nearest intrinsics so nvcc
+// cannot contract into FMA (the reference is compiled -ffp-contract=off).
+struct OptArgs {
+  uint32_t kind;
+  double lr, b1, b2, eps, omb1, omb2;
+  const double* bc;  // [2 x bc_len]: 1 - b1^k, 1 - b2^k (host libm)
+  uint64_t bc_len;
+};
+
+__device__ __forceinline__ void adagrad_elem(float& w, float& a, float gf, const OptArgs& o) {
+  const double g = (double)gf;
+  const double an = __dadd_rn((double)a, __dmul_rn(g, g));
+  a = __double2float_rn(an);
+  w = __double2float_rn(
+      __dsub_rn((double)w, __ddiv_rn(__dmul_rn(o.lr, g), __dadd_rn(__dsqrt_rn(an), o.eps))));
+}
+__device__ __forceinline__ void adam_elem(float& w, float& m, float& v, float gf, double bc1,
+                                          double bc2, const OptArgs& o) {
+  const double g = (double)gf;
+  const double me = __dadd_rn(__dmul_rn(o.b1, (double)m), __dmul_rn(o.omb1, g));
+  const double ve = __dadd_rn(__dmul_rn(o.b2, (double)v), __dmul_rn(__dmul_rn(o.omb2, g), g));
+  m = __double2float_rn(me);
+  v = __double2float_rn(ve);
+  const double mh = __ddiv_rn(me, bc1);
+  const double vh = __ddiv_rn(ve, bc2);
+  w = __double2float_rn(
+      __dsub_rn((double)w, __ddiv_rn(__dmul_rn(o.lr, mh), __dadd_rn(__dsqrt_rn(vh), o.eps))));
+}
+
+// Applies one optimizer step to `row` with the lane-distributed gradient
+// acc[c][j] for elements e = (c*32 + lane)*VEC + j.  Called by a full warp.
+template <int VEC, int CH>
+__device__ __forceinline__ void apply_row(const TableDesc& d, uint32_t row, const float (&acc)[CH][VEC],
+                                          const OptArgs& o) {
+  const unsigned lane = lane_id();
+  const uint32_t D = d.dim;
+  if (row == kNoRow) return;
+  double bc1 = 1.0, bc2 = 1.0;
+  uint32_t step = 0;
+  if (lane == 0) {
+    step = d.step[row] + 1;
+    d.step[row] = step;
+  }
+  step = __shfl_sync(kFull, step, 0);
+  if (o.kind == RS_OPT_ADAM) {
+    if (step < o.bc_len) {
+      bc1 = o.bc[step];
+      bc2 = o.bc[o.bc_len + step];
+    } else {
+      bc1 = 1.0 - pow(o.b1, (double)step);
+      bc2 = 1.0 - pow(o.b2, (double)step);
+    }
+  }
+  float* w = d.emb + (size_t)row * D;
+  float* m = d.s1 ? d.s1 + (size_t)row * D : nullptr;
+  float* v = d.s2 ? d.s2 + (size_t)row * D : nullptr;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const uint32_t e0 = ((uint32_t)c * 32 + lane) * VEC;
+    if (VEC == 1 && e0 >= D) continue;
+    float wv[VEC], mv[VEC], vv[VEC];
+    if (VEC == 4) {
+      *reinterpret_cast<float4*>(wv) = *reinterpret_cast<const float4*>(w + e0);
+      if (v) *reinterpret_cast<float4*>(vv) = *reinterpret_cast<const float4*>(v + e0);
+      if (m) *reinterpret_cast<float4*>(mv) = *reinterpret_cast<const float4*>(m + e0);
+    } else if (VEC == 2) {
+      *reinterpret_cast<float2*>(wv) = *reinterpret_cast<const float2*>(w + e0);
+      if (v) *reinterpret_cast<float2*>(vv) = *reinterpret_cast<const float2*>(v + e0);
+      if (m) *reinterpret_cast<float2*>(mv) = *reinterpret_cast<const float2*>(m + e0);
+    } else {
+      wv[0] = w[e0];
+      if (v) vv[0] = v[e0];
+      if (m) mv[0] = m[e0];
+    }
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) {
+      if (o.kind == RS_OPT_ADAM)
+        adam_elem(wv[j], mv[j], vv[j], acc[c][j], bc1, bc2, o);
+      else
+        adagrad_elem(wv[j], vv[j], acc[c][j], o);
+    }
+    if (VEC == 4) {
+      *reinterpret_cast<float4*>(w + e0) = *reinterpret_cast<float4*>(wv);
+      if (v) *reinterpret_cast<float4*>(v + e0) = *reinterpret_cast<float4*>(vv);
+      if (m) *reinterpret_cast<float4*>(m + e0) = *reinterpret_cast<float4*>(mv);
+    } else if (VEC == 2) {
+      *reinterpret_cast<float2*>(w + e0) = *reinterpret_cast<float2*>(wv);
+      if (v) *reinterpret_cast<float2*>(v + e0) = *reinterpret_cast<float2*>(vv);
+      if (m) *reinterpret_cast<float2*>(m + e0) = *reinterpret_cast<float2*>(mv);
+    } else {
+      w[e0] = wv[0];
+      if (v) v[e0] = vv[0];
+      if (m) m[e0] = mv[0];
+    }
+  }
+}
+
+template <int VEC, int CH>
+__device__ __forceinline__ void load_vec(const float* __restrict__ src, uint32_t D,
+                                         float (&x)[CH][VEC], bool coherent) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const uint32_t e0 = ((uint32_t)c * 32 + lane) * VEC;
+    if (VEC == 4) {
+      float4 t = coherent ? __ldcg(reinterpret_cast<const float4*>(src + e0))
+                          : *reinterpret_cast<const float4*>(src + e0);
+      x[c][0] = t.x; x[c][1] = t.y; x[c][2] = t.z; x[c][3] = t.w;
+    } else if (VEC == 2) {
+      float2 t = coherent ? __ldcg(reinterpret_cast<const float2*>(src + e0))
+                          : *reinterpret_cast<const float2*>(src + e0);
+      x[c][0] = t.x; x[c][1] = t.y;
+    } else {
+      x[c][0] = e0 < D ? (coherent ? __ldcg(src + e0) : src[e0]) : 0.f;
+    }
+  }
+}
+
+template <int VEC, int CH>
+__device__ __forceinline__ void store_vec(float* __restrict__ dst, uint32_t D,
+                                          const float (&x)[CH][VEC]) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const uint32_t e0 = ((uint32_t)c * 32 + lane) * VEC;
+    if (VEC == 4) {
+      *reinterpret_cast<float4*>(dst + e0) = make_float4(x[c][0], x[c][1], x[c][2], x[c][3]);
+    } else if (VEC == 2) {
+      *reinterpret_cast<float2*>(dst + e0) = make_float2(x[c][0], x[c][1]);
+    } else if (e0 < D) {
+      dst[e0] = x[c][0];
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+struct ReduceArgs {
+  const int32_t* inverse;
+  const float* grads;
+  uint32_t n;
+  uint32_t ntiles;
+  uint32_t bw;  // bitmap words per warp = ceil(ntiles / 32)
+  const uint32_t* u_ntile;
+  const uint32_t* u_poff;
+  uint32_t* u_ticket;
+  uint32_t* u_done;
+  const uint32_t* urow;
+  float* pbuf;
+  uint32_t* ptile;
+  uint32_t* porder;
+  TableDev* td;
+  float* sums_out;  // accumulate-only mode when non-null
+  bool tma;
+};
+
+// K5.  blockDim.x == TT (tokens per tile), one tile per block.
+template <int VEC, int CH>
+__global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t TT = blockDim.x;
+  const uint32_t NW = TT >> 5;
+  const uint32_t L = 2 * TT;
+  const TableDesc d = a.td->d;
+  const uint32_t D = d.dim;
+  // carve shared memory
+  float* sg = reinterpret_cast<float*>(smem);  // [TT x D] staged gradients
+  unsigned char* p = smem + (size_t)TT * D * 4;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(p);
+  p += 16;
+  uint32_t* lkey = reinterpret_cast<uint32_t*>(p);
+  uint32_t* lfirst = lkey + L;
+  uint32_t* lgroup = lfirst + L;
+  uint32_t* gcnt = lgroup + L;
+  uint32_t* goff = gcnt + TT;
+  uint32_t* gu = goff + TT;
+  uint32_t* wsum = gu + TT;        // [32]
+  uint32_t* misc = wsum + 32;      // [0] ng
+  uint32_t* bm_all = misc + 32;    // [NW x 2 x bw]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(bm_all + (size_t)NW * 2 * a.bw);  // [NW x TT]
+  uint16_t* csr = wcnt + (size_t)NW * TT;                                        // [TT]
+
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const uint32_t tile = blockIdx.x;
+  const uint32_t t0 = tile * TT;
+  const uint32_t rows = min(TT, a.n - t0);
+
+  for (uint32_t i = tid; i < L; i += TT) {
+    lkey[i] = kFull;
+    lfirst[i] = kFull;
+  }
+  for (uint32_t i = tid; i < NW * TT; i += TT) wcnt[i] = 0;
+  // stage this tile's contiguous gradient rows: one TMA bulk copy (UBLKCP)
+  if (a.tma) {
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = rows * D * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                   "r"(bytes)
+                   : "memory");
+      const char* src = reinterpret_cast<const char*>(a.grads + (size_t)t0 * D);
+      constexpr uint32_t kChunk = 32768;
+      for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t sz = min(kChunk, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(reinterpret_cast<char*>(sg) + off)),
+            "l"(src + off), "r"(sz), "r"(smem_u32(bar))
+            : "memory");
+      }
+    }
+  } else {
+    const float* src = a.grads + (size_t)t0 * D;
+    for (uint32_t i = tid; i < rows * D; i += TT) sg[i] = src[i];
+  }
+  __syncthreads();
+
+  // ---- phase 1: group the tile's tokens by unique id (smem), stable ranks
+  const uint32_t t = t0 + tid;
+  const bool valid = tid < rows;
+  const uint32_t u = valid ? (uint32_t)a.inverse[t] : kFull;
+  uint32_t ps = 0;
+  if (valid) {
+    ps = hash32(u) & (L - 1);
+    for (;;) {
+      const uint32_t prev = atomicCAS(&lkey[ps], kFull, u);
+      if (prev == kFull || prev == u) break;
+      ps = (ps + 1) & (L - 1);
+    }
+    atomicMin(&lfirst[ps], tid);
+  }
+  __syncthreads();
+  const bool head = valid && lfirst[ps] == tid;
+  const unsigned hb = __ballot_sync(kFull, head);
+  if (lane == 0) wsum[warp] = __popc(hb);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < NW ? wsum[lane] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o2);
+      if (lane >= (unsigned)o2) x += y;
+    }
+    if (lane < NW) wsum[lane] = x - v;
+    if (lane == 31) misc[0] = x;
+  }
+  __syncthreads();
+  const uint32_t ng = misc[0];
+  if (head) {
+    const uint32_t lg = wsum[warp] + __popc(hb & lanemask_lt());
+    lgroup[ps] = lg;
+    gu[lg] = u;
+  }
+  __syncthreads();
+  const uint32_t mylg = valid ? lgroup[ps] : (0xFFFF0000u | lane);
+  const unsigned mm = __match_any_sync(kFull, mylg);
+  const uint32_t rw = __popc(mm & lanemask_lt());
+  if (valid && rw == 0) wcnt[warp * TT + mylg] = (uint16_t)__popc(mm);
+  __syncthreads();
+  if (tid < ng) {
+    uint32_t run = 0;
+    for (uint32_t w = 0; w < NW; ++w) {
+      const uint32_t c = wcnt[w * TT + tid];
+      wcnt[w * TT + tid] = (uint16_t)run;
+      run += c;
+    }
+    gcnt[tid] = run;
+  }
+  __syncthreads();
+  {  // exclusive scan of gcnt[0, ng) -> goff
+    const uint32_t v = tid < ng ? gcnt[tid] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o2);
+      if (lane >= (unsigned)o2) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t wv = lane < NW ? wsum[lane] : 0;
+      uint32_t z = wv;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, z, o2);
+        if (lane >= (unsigned)o2) z += y;
+      }
+      if (lane < NW) wsum[lane] = z - wv;
+    }
+    __syncthreads();
+    if (tid < ng) goff[tid] = wsum[warp] + x - v;
+  }
+  __syncthreads();
+  if (valid) csr[goff[mylg] + wcnt[warp * TT + mylg] + rw] = (uint16_t)tid;
+  if (a.tma) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+  }
+  __syncthreads();
+
+  // ---- phase 2: per-group position-order sums, then update / partial
+  uint32_t* bm = bm_all + (size_t)warp * 2 * a.bw;
+  uint32_t* wpre = bm + a.bw;
+  for (uint32_t g = warp; g < ng; g += NW) {
+    const uint32_t uu = gu[g];
+    const uint32_t cnt = gcnt[g];
+    const uint32_t base = goff[g];
+    float acc[CH][VEC];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) acc[c][j] = 0.f;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const float* row = sg + (size_t)csr[base + k] * D;
+      float x[CH][VEC];
+      load_vec<VEC, CH>(row, D, x, false);
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) acc[c][j] += x[c][j];
+    }
+    const uint32_t nt = __ldg(a.u_ntile + uu);
+    bool finish = nt <= 1;
+    if (!finish) {
+      const uint32_t poff = __ldg(a.u_poff + uu);
+      uint32_t tk = 0;
+      if (lane == 0) tk = atomicAdd(a.u_ticket + uu, 1u);
+      tk = __shfl_sync(kFull, tk, 0);
+      store_vec<VEC, CH>(a.pbuf + (size_t)(poff + tk) * D, D, acc);
+      if (lane == 0) a.ptile[poff + tk] = tile;
+      __threadfence();
+      __syncwarp();
+      uint32_t done = 0;
+      if (lane == 0) done = atomicAdd(a.u_done + uu, 1u);
+      done = __shfl_sync(kFull, done, 0);
+      if (done == nt - 1) {
+        // last arriver: order the partials by tile index and sum in order
+        __threadfence();
+        for (uint32_t i = lane; i < a.bw; i += 32) bm[i] = 0;
+        __syncwarp();
+        for (uint32_t i = lane; i < nt; i += 32) {
+          const uint32_t tl = __ldcg(a.ptile + poff + i);
+          atomicOr(&bm[tl >> 5], 1u << (tl & 31));
+        }
+        __syncwarp();
+        const uint32_t per = (a.bw + 31) / 32;
+        const uint32_t w0 = min(lane * per, a.bw), w1 = min(w0 + per, a.bw);
+        uint32_t loc = 0;
+        for (uint32_t i = w0; i < w1; ++i) loc += __popc(bm[i]);
+        uint32_t x = loc;
+#pragma unroll
+        for (int o2 = 1; o2 < 32; o2 <<= 1) {
+          const uint32_t y = __shfl_up_sync(kFull, x, o2);
+          if (lane >= (unsigned)o2) x += y;
+        }
+        uint32_t runp = x - loc;
+        for (uint32_t i = w0; i < w1; ++i) {
+          wpre[i] = runp;
+          runp += __popc(bm[i]);
+        }
+        __syncwarp();
+        for (uint32_t i = lane; i < nt; i += 32) {
+          const uint32_t tl = __ldcg(a.ptile + poff + i);
+          const uint32_t r = wpre[tl >> 5] + __popc(bm[tl >> 5] & ((1u << (tl & 31)) - 1u));
+          a.porder[poff + r] = i;
+        }
+        __threadfence_block();
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) acc[c][j] = 0.f;
+        for (uint32_t r = 0; r < nt; ++r) {
+          const uint32_t i = __ldcg(a.porder + poff + r);
+          float x2[CH][VEC];
+          load_vec<VEC, CH>(a.pbuf + (size_t)(poff + i) * D, D, x2, true);
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+#pragma unroll
+            for (int j = 0; j < VEC; ++j) acc[c][j] += x2[c][j];
+        }
+        finish = true;
+      }
+    }
+    if (finish) {
+      if (a.sums_out) {
+        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
+      } else {
+        apply_row<VEC, CH>(d, __ldg(a.urow + uu), acc, o);
+      }
+    }
+  }
+}
+
+// Optimizer-only apply for pre-aggregated sums (GradAccumulator::apply given
+// `pending`, sparse_update.cpp:58-83): warp per key.
+template <int VEC, int CH>
+__global__ void k_apply_sums(TableDev* __restrict__ td, const int64_t* __restrict__ rows,
+                             uint64_t n, const float* __restrict__ sums, OptArgs o) {
+  const TableDesc d = td->d;
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t i = w; i < n; i += nw) {
+    float acc[CH][VEC];
+    load_vec<VEC, CH>(sums + i * d.dim, d.dim, acc, false);
+    const int64_t r = rows[i];
+    if (r >= 0) apply_row<VEC, CH>(d, (uint32_t)r, acc, o);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side dispatch helpers
+struct Shape {
+  int vec, ch;
+};
+Shape shape_for(uint32_t D) {
+  if (D % 128 == 0 && D / 128 <= 4) return {4, (int)(D / 128)};
+  if (D % 64 == 0 && D / 64 <= 2) return {2, (int)(D / 64)};
+  return {1, (int)((D + 31) / 32)};
+}
+
+}  // namespace
+
+uint32_t tile_tokens_for_dim(uint32_t D) {
+  // keep the staged gradient tile at <= 64 KB so two tiles fit per SM
+  uint32_t tt = 512;
+  while (tt > 32 && (uint64_t)tt * D * 4 > 65536) tt >>= 1;
+  return tt;
+}
+
+int dedup_run(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint32_t TT, cudaStream_t s) {
+  if (n > ws->max_tokens)
+    return fail(RS_ERR_CONFIG, "dedup: batch of " + std::to_string(n) +
+                                   " ids exceeds workspace max_tokens " +
+                                   std::to_string(ws->max_tokens));
+  // K0: clear the previous call's slots (first call: full clear at creation)
+  k_dedup_clear<<<grid_for(ws->last_n + 1, 256, 148 * 8), 256, 0, s>>>(
+      ws->skey, ws->sfirstx, ws->scount, ws->sntile, ws->u_slot, ws->ctr, ws->S);
+  RS_LAUNCH_CHECK("k_dedup_clear");
+  ws->last_n = n;
+  if (n == 0) {
+    RS_CUDA(cudaMemsetAsync(ws->ctr + 2, 0, 2 * sizeof(uint32_t), s));
+    return RS_OK;
+  }
+  const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
+  const size_t sm1 = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4);
+  k_dedup_tile<<<ntiles, TT, sm1, s>>>(d_ids, (uint32_t)n, ws->skey, ws->sfirstx, ws->scount,
+                                       ws->sntile, ws->S - 1, ws->S, ws->slot_of);
+  RS_LAUNCH_CHECK("k_dedup_tile");
+  const uint32_t stiles = (uint32_t)((n + kScanTile - 1) / kScanTile);
+  k_dedup_compact<<<stiles, kScanThreads, 0, s>>>(
+      d_ids, (uint32_t)n, ws->slot_of, ws->sfirstx, ws->sntile, ws->suidx, ws->unique,
+      ws->u_slot, ws->u_ntile, ws->u_poff, ws->u_ticket, ws->u_done, ws->scan_status, ws->ctr,
+      stiles);
+  RS_LAUNCH_CHECK("k_dedup_compact");
+  ws->last_tile = TT;
+  return RS_OK;
+}
+
+static int launch_gather(rs_workspace* ws, rs_table* t, uint64_t n, float* d_out,
+                         cudaStream_t s) {
+  const uint32_t D = t->desc.dim;
+  if (D % 4 == 0) {
+    const uint32_t d4 = D / 4;
+    const unsigned grid = grid_for(n, 256 / std::min<uint32_t>(32, d4) * 4, 148 * 8);
+#define RS_GATHER(LPR)                                                                      \
+  k_gather<LPR, 4><<<grid, 256, 0, s>>>(ws->slot_of, ws->suidx, ws->srow, t->dev, (uint32_t)n, \
+                                        ws->inverse, d_out)
+    if (d4 >= 32)
+      RS_GATHER(32);
+    else if (d4 >= 16)
+      RS_GATHER(16);
+    else if (d4 >= 8)
+      RS_GATHER(8);
+    else if (d4 >= 4)
+      RS_GATHER(4);
+    else if (d4 >= 2)
+      RS_GATHER(2);
+    else
+      RS_GATHER(1);
+#undef RS_GATHER
+    RS_LAUNCH_CHECK("k_gather");
+  } else {
+    k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, ws->suidx, ws->srow,
+                                                            t->dev, (uint32_t)n, ws->inverse, d_out);
+    RS_LAUNCH_CHECK("k_gather_scalar");
+  }
+  return RS_OK;
+}
+
+static int opt_args(rs_table* t, const rs_optimizer_params* p, OptArgs* o, cudaStream_t s) {
+  if (!p) return fail(RS_ERR_CONFIG, "optimizer params required");
+  if (p->kind != RS_OPT_ADAM && p->kind != RS_OPT_ADAGRAD)
+    return fail(RS_ERR_CONFIG, "unknown optimizer kind");
+  if (p->kind == RS_OPT_ADAM && t->desc.opt != RS_OPT_ADAM)
+    return fail(RS_ERR_CONFIG, "table was created without Adam state (opt_m)");
+  if (p->kind == RS_OPT_ADAGRAD && t->desc.opt == RS_OPT_NONE)
+    return fail(RS_ERR_CONFIG, "table was created without optimizer state");
+  o->kind = p->kind;
+  o->lr = p->lr;
+  o->b1 = p->beta1;
+  o->b2 = p->beta2;
+  o->eps = p->eps;
+  o->omb1 = 1.0 - p->beta1;
+  o->omb2 = 1.0 - p->beta2;
+  o->bc = nullptr;
+  o->bc_len = 0;
+  if (p->kind == RS_OPT_ADAM) {
+    int st = table_adam_tables(t, p->beta1, p->beta2, t->applies, s);
+    if (st) return st;
+    o->bc = t->d_bc;
+    o->bc_len = t->bc_len;
+  }
+  return RS_OK;
+}
+
+static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
+                         const OptArgs& o, float* sums_out, cudaStream_t s) {
+  const uint32_t D = t->desc.dim;
+  const uint32_t TT = ws->last_tile;
+  const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
+  // partial-sum buffer: at most one partial per (tile, id) pair <= n
+  if (ws->pbuf_floats < n * D) {
+    if (ws->pbuf) RS_CUDA(cudaFreeAsync(ws->pbuf, s));
+    ws->pbuf_floats = ws->max_tokens * (uint64_t)D;
+    RS_CUDA(cudaMallocAsync(&ws->pbuf, ws->pbuf_floats * sizeof(float), s));
+  }
+  ReduceArgs a;
+  a.inverse = ws->inverse;
+  a.grads = d_grads;
+  a.n = (uint32_t)n;
+  a.ntiles = ntiles;
+  a.bw = (ntiles + 31) / 32;
+  a.u_ntile = ws->u_ntile;
+  a.u_poff = ws->u_poff;
+  a.u_ticket = ws->u_ticket;
+  a.u_done = ws->u_done;
+  a.urow = ws->urow;
+  a.pbuf = ws->pbuf;
+  a.ptile = ws->ptile;
+  a.porder = ws->porder;
+  a.td = t->dev;
+  a.sums_out = sums_out;
+  a.tma = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_grads) & 15u) == 0);
+  const uint32_t NW = TT / 32;
+  const size_t smem = (size_t)TT * D * 4 + 16 + (size_t)(3 * 2 * TT + 3 * TT + 64) * 4 +
+                      (size_t)NW * 2 * a.bw * 4 + (size_t)NW * TT * 2 + (size_t)TT * 2 + 16;
+  const Shape sh = shape_for(D);
+  if (sh.ch > 32) return fail(RS_ERR_CONFIG, "embedding_dim > 1024 unsupported by the reduce");
+  auto go = [&](auto kern) -> int {
+    if (smem > 48 * 1024)
+      RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<ntiles, TT, smem, s>>>(a, o);
+    RS_LAUNCH_CHECK("k_reduce_update");
+    return RS_OK;
+  };
+#define RS_SHAPE(V, C) \
+  if (sh.vec == V && sh.ch == C) return go(k_reduce_update<V, C>);
+  RS_SHAPE(4, 1) RS_SHAPE(4, 2) RS_SHAPE(4, 3) RS_SHAPE(4, 4)
+  RS_SHAPE(2, 1) RS_SHAPE(2, 2)
+  RS_SHAPE(1, 1) RS_SHAPE(1, 2) RS_SHAPE(1, 3) RS_SHAPE(1, 4) RS_SHAPE(1, 5) RS_SHAPE(1, 6)
+  RS_SHAPE(1, 7) RS_SHAPE(1, 8)
+#undef RS_SHAPE
+  return fail(RS_ERR_CONFIG, "embedding_dim " + std::to_string(D) + " unsupported by the reduce");
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+extern "C" {
+
+int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
+  if (!out) return fail(RS_ERR_CONFIG, "rs_workspace_create: null out");
+  if (max_tokens == 0 || max_tokens > (1ull << 30))
+    return fail(RS_ERR_CONFIG, "rs_workspace_create: max_tokens must be in [1, 2^30]");
+  rs_workspace* ws = new rs_workspace();
+  ws->max_tokens = max_tokens;
+  uint64_t S_ = 1024;
+  while (S_ < 2 * max_tokens) S_ <<= 1;
+  ws->S = S_;
+  const uint64_t N = max_tokens;
+  auto A = [&](auto** p, size_t bytes) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16)) == cudaSuccess;
+  };
+  bool ok = A(&ws->skey, (S_ + 1) * 8) && A(&ws->sfirstx, (S_ + 1) * 4) &&
+            A(&ws->scount, (S_ + 1) * 4) && A(&ws->sntile, (S_ + 1) * 4) &&
+            A(&ws->suidx, (S_ + 1) * 4) && A(&ws->srow, (S_ + 1) * 4) &&
+            A(&ws->slot_of, N * 4) && A(&ws->inverse, N * 4) && A(&ws->unique, N * 8) &&
+            A(&ws->u_slot, N * 4) && A(&ws->u_ntile, N * 4) && A(&ws->u_poff, N * 4) &&
+            A(&ws->u_ticket, N * 4) && A(&ws->u_done, N * 4) && A(&ws->urow, N * 4) &&
+            A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) && A(&ws->porder, N * 4) &&
+            A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64);
+  if (!ok) {
+    rs_workspace_destroy(ws);
+    return cuda_fail(cudaGetLastError(), "rs_workspace_create: cudaMalloc");
+  }
+  k_dedup_clear_all<<<grid_for(S_ + 1, 256, 148 * 16), 256>>>(ws->skey, ws->sfirstx, ws->scount,
+                                                               ws->sntile, S_ + 1);
+  count_launch();
+  cudaMemset(ws->scan_status, 0, ((N + kScanTile - 1) / kScanTile + 1) * 8);
+  cudaMemset(ws->ctr, 0, 64);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    rs_workspace_destroy(ws);
+    return cuda_fail(cudaGetLastError(), "rs_workspace_create");
+  }
+  *out = ws;
+  return RS_OK;
+}
+
+int rs_workspace_destroy(rs_workspace* ws) {
+  if (!ws) return RS_OK;
+  cudaDeviceSynchronize();
+  void* ptrs[] = {ws->skey,    ws->sfirstx, ws->scount,  ws->sntile,   ws->suidx,  ws->srow,
+                  ws->slot_of, ws->inverse, ws->unique,  ws->u_slot,   ws->u_ntile, ws->u_poff,
+                  ws->u_ticket, ws->u_done, ws->urow,    ws->urow64,   ws->ptile,  ws->porder,
+                  ws->pbuf,    ws->scan_status, ws->ctr};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete ws;
+  return RS_OK;
+}
+
+int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_unique,
+             int32_t* d_inverse, uint32_t* d_n_unique, void* stream) {
+  if (!ws) return fail(RS_ERR_CONFIG, "rs_dedup: null workspace");
+  cudaStream_t s = S(stream);
+  int st = dedup_run(ws, d_ids, n, 512, s);
+  if (st) return st;
+  ws->have_forward = false;
+  if (n) {
+    if (d_inverse) {
+      k_inverse<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->slot_of, ws->suidx, (uint32_t)n,
+                                                          d_inverse);
+      RS_LAUNCH_CHECK("k_inverse");
+    }
+    k_copy_unique<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->unique, ws->ctr, d_unique,
+                                                            d_n_unique);
+    RS_LAUNCH_CHECK("k_copy_unique");
+  } else if (d_n_unique) {
+    RS_CUDA(cudaMemsetAsync(d_n_unique, 0, sizeof(uint32_t), s));
+  }
+  return RS_OK;
+}
+
+int rs_forward(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, float* d_out,
+               void* stream) {
+  if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_forward: null handle");
+  cudaStream_t s = S(stream);
+  const uint32_t TT = tile_tokens_for_dim(t->desc.dim);
+  int st = dedup_run(ws, d_ids, n, TT, s);
+  if (st) return st;
+  ws->have_forward = true;
+  ws->last_table = t;
+  if (n == 0) return RS_OK;
+  st = table_ensure_any(t, ws->unique, ws->ctr + 2, n, ws->urow, ws->urow64, ws->u_slot,
+                           ws->srow, s);
+  if (st) return st;
+  return launch_gather(ws, t, n, d_out, s);
+}
+
+int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
+                const rs_optimizer_params* opt, void* stream) {
+  if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_backward: null handle");
+  if (!ws->have_forward || ws->last_table != t || ws->last_n != n)
+    return fail(RS_ERR_CONFIG, "rs_backward: must follow rs_forward on the same table and batch");
+  if (n == 0) return RS_OK;
+  cudaStream_t s = S(stream);
+  OptArgs o;
+  int st = opt_args(t, opt, &o, s);
+  if (st) return st;
+  st = launch_reduce(ws, t, d_grads, n, o, nullptr, s);
+  if (st) return st;
+  t->applies++;
+  ws->have_forward = false;  // rows were updated: a second backward would double-apply
+  return RS_OK;
+}
+
+int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+            const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream) {
+  int st = rs_forward(ws, t, d_ids, n, d_out, stream);
+  if (st) return st;
+  return rs_backward(ws, t, d_grads, n, opt, stream);
+}
+
+int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, const rs_optimizer_params* opt, void* stream) {
+  // GradAccumulator::accumulate + apply for one window (sparse_update.cpp:45-83):
+  // dedup, zero-vivify absent ids, segment-reduce fused with the update.
+  if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_sparse_update: null handle");
+  cudaStream_t s = S(stream);
+  OptArgs o;
+  int st = opt_args(t, opt, &o, s);
+  if (st) return st;
+  const uint32_t TT = tile_tokens_for_dim(t->desc.dim);
+  st = dedup_run(ws, d_ids, n, TT, s);
+  if (st) return st;
+  ws->have_forward = false;
+  ws->last_table = t;
+  if (n == 0) return RS_OK;
+  st = table_ensure_any(t, ws->unique, ws->ctr + 2, n, ws->urow, ws->urow64, ws->u_slot,
+                        ws->srow, s);
+  if (st) return st;
+  k_inverse<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->slot_of, ws->suidx, (uint32_t)n,
+                                                      ws->inverse);
+  RS_LAUNCH_CHECK("k_inverse");
+  st = launch_reduce(ws, t, d_grads, n, o, nullptr, s);
+  if (st) return st;
+  t->applies++;
+  return RS_OK;
+}
+
+int rs_workspace_results(rs_workspace* ws, const uint64_t** d_unique, const int32_t** d_inverse,
+                         const uint32_t** d_n_unique, const int64_t** d_rows) {
+  if (!ws) return fail(RS_ERR_CONFIG, "rs_workspace_results: null workspace");
+  if (d_unique) *d_unique = ws->unique;
+  if (d_inverse) *d_inverse = ws->inverse;
+  if (d_n_unique) *d_n_unique = ws->ctr + 2;
+  if (d_rows) *d_rows = ws->urow64;
+  return RS_OK;
+}
+
+int rs_workspace_n_unique(rs_workspace* ws, uint64_t* out) {
+  if (!ws || !out) return fail(RS_ERR_CONFIG, "rs_workspace_n_unique: null argument");
+  RS_CUDA(cudaDeviceSynchronize());
+  uint32_t n = 0;
+  RS_CUDA(cudaMemcpy(&n, ws->ctr + 2, 4, cudaMemcpyDeviceToHost));
+  *out = n;
+  return RS_OK;
+}
+
+int rs_accumulate(rs_workspace* ws, const float* d_grads, uint64_t n, float* d_sums,
+                  void* stream) {
+  if (!ws || !ws->last_table) return fail(RS_ERR_CONFIG, "rs_accumulate: no forward on workspace");
+  if (ws->last_n != n) return fail(RS_ERR_CONFIG, "rs_accumulate: batch size differs from forward");
+  if (n == 0) return RS_OK;
+  OptArgs o;
+  std::memset(&o, 0, sizeof(o));
+  return launch_reduce(ws, ws->last_table, d_grads, n, o, d_sums, S(stream));
+}
+
+int rs_apply_aggregated(rs_table* t, const uint64_t* d_keys, uint64_t n, const float* d_sums,
+                        const rs_optimizer_params* opt, void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_apply_aggregated: null table");
+  if (n == 0) return RS_OK;
+  cudaStream_t s = S(stream);
+  OptArgs o;
+  int st = opt_args(t, opt, &o, s);
+  if (st) return st;
+  int64_t* rows = nullptr;
+  RS_CUDA(cudaMallocAsync(&rows, n * 8, s));
+  st = rs_table_ensure(t, d_keys, n, rows, stream);
+  if (st) return st;
+  const Shape sh = shape_for(t->desc.dim);
+  const unsigned grid = grid_for(n, 8, 148 * 8);
+#define RS_SHAPE(V, C)                                                                   \
+  if (sh.vec == V && sh.ch == C) {                                                       \
+    k_apply_sums<V, C><<<grid, 256, 0, s>>>(t->dev, rows, n, d_sums, o);                 \
+    RS_LAUNCH_CHECK("k_apply_sums");                                                     \
+    RS_CUDA(cudaFreeAsync(rows, s));                                                     \
+    t->applies++;                                                                        \
+    return RS_OK;                                                                        \
+  }
+  RS_SHAPE(4, 1) RS_SHAPE(4, 2) RS_SHAPE(4, 3) RS_SHAPE(4, 4)
+  RS_SHAPE(2, 1) RS_SHAPE(2, 2)
+  RS_SHAPE(1, 1) RS_SHAPE(1, 2) RS_SHAPE(1, 3) RS_SHAPE(1, 4) RS_SHAPE(1, 5) RS_SHAPE(1, 6)
+  RS_SHAPE(1, 7) RS_SHAPE(1, 8)
+#undef RS_SHAPE
+  return fail(RS_ERR_CONFIG, "embedding_dim unsupported by the optimizer");
+}
+
+}  // extern "C"

@@ -1,0 +1,1088 @@
+// table.cu -- the dynamic hash embedding table on sm_100a.
+//
+// Replaces EmbedTable (reference embed_table.hpp:73-211, embed_table.cpp).
+// Key structure: 8-slot buckets of 16-byte slots, probed by 8-lane groups
+// (grouped parallel probing, Eq. 5 with G = 8 lanes); bucket walk
+// b_t = (b0 + t*S) mod nb with S odd, so every bucket is visited
+// (hash.hpp:54-56).  Stop rules follow probe_walk (embed_table.cpp:111-142):
+// stop at the key or at the first bucket holding an empty slot, remember the
+// first tombstone, insert into the first tombstone else the first empty.
+// Embedding structure: SoA row pool; expansion rehashes keys only
+// (embed_table.cpp:267-285), rows never move.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "rs_host.hpp"
+
+namespace rs {
+namespace {
+
+constexpr unsigned kGroupsPerBlock = 32;  // 8-lane groups per 256-thread block
+constexpr unsigned kProbeThreads = kGroupsPerBlock * kBucket;
+
+__device__ __forceinline__ uint4 ld_slot_cg(const Slot* p) {
+  return __ldcg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ uint4 ld_slot(const Slot* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+struct Probe {
+  bool found;
+  uint64_t slot;      // slot of the key when found
+  uint32_t row;       // row when found
+  uint32_t tick;      // slot tick when found
+  uint64_t ins;       // insertion slot when not found (~0 = table full)
+  bool ins_tomb;      // insertion slot is a tombstone
+};
+
+// Cooperative probe by the 8 lanes of a group.  `g` = lane within the group,
+// `gbase` = first warp lane of the group, `gmask` = the group's lane mask.
+template <bool kCoherent>
+__device__ __forceinline__ Probe probe_group(const Slot* __restrict__ slots, uint64_t nb_mask,
+                                             uint64_t key, unsigned g, unsigned gbase,
+                                             unsigned gmask) {
+  const uint64_t h = hash64(key);
+  uint64_t b = (h >> 32) & nb_mask;  // high hash bits: decorrelated from shard_of = h % W
+  const uint64_t step = (h | 1ull) & nb_mask;  // odd -> full cycle over nb = 2^k buckets
+  uint64_t tomb = ~0ull;
+  Probe r;
+  r.found = false;
+  r.ins = ~0ull;
+  r.ins_tomb = false;
+  r.row = kNoRow;
+  r.tick = 0;
+  r.slot = ~0ull;
+  for (uint64_t t = 0; t <= nb_mask; ++t) {
+    const uint4 v = kCoherent ? ld_slot_cg(slots + b * kBucket + g) : ld_slot(slots + b * kBucket + g);
+    const uint64_t k = (uint64_t)v.x | ((uint64_t)v.y << 32);
+    const unsigned bm = (__ballot_sync(gmask, k == key) >> gbase) & 0xFFu;
+    const unsigned be = (__ballot_sync(gmask, k == kEmptyKey) >> gbase) & 0xFFu;
+    const unsigned bt = (__ballot_sync(gmask, k == kTombKey) >> gbase) & 0xFFu;
+    if (bm) {
+      const unsigned l = __ffs(bm) - 1;
+      r.found = true;
+      r.slot = b * kBucket + l;
+      r.row = __shfl_sync(gmask, v.z, gbase + l);
+      r.tick = __shfl_sync(gmask, v.w, gbase + l);
+      return r;
+    }
+    if (tomb == ~0ull && bt) tomb = b * kBucket + (__ffs(bt) - 1);
+    if (be) {
+      r.ins = tomb != ~0ull ? tomb : b * kBucket + (__ffs(be) - 1);
+      r.ins_tomb = tomb != ~0ull;
+      return r;
+    }
+    b = (b + step) & nb_mask;
+  }
+  r.ins = tomb;
+  r.ins_tomb = tomb != ~0ull;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t alloc_row(TableDev* td, unsigned long long free_n0,
+                                              unsigned long long fresh0, uint64_t row_cap) {
+  const unsigned long long i = atomicAdd(&td->c.alloc_ctr, 1ull);
+  if (i < free_n0) return td->d.free_stack[free_n0 - 1 - i];  // LIFO reuse first
+  const unsigned long long r = fresh0 + (i - free_n0);
+  if (r >= row_cap) {
+    atomicOr(&td->c.error, kErrRowPool);
+    return kNoRow;
+  }
+  return (uint32_t)r;
+}
+
+// New-row initialisation by the 8 lanes of a group: emb from src (or zeros),
+// optimizer state zeroed (alloc_row + reset_row, embed_table.cpp:144-180).
+__device__ __forceinline__ void init_row(const TableDesc& d, uint32_t row, const float* src,
+                                         unsigned g) {
+  const uint32_t D = d.dim;
+  float* e = d.emb + (size_t)row * D;
+  if ((D & 3u) == 0) {
+    const uint32_t D4 = D >> 2;
+    for (uint32_t i = g; i < D4; i += kBucket) {
+      float4 v = src ? reinterpret_cast<const float4*>(src)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(e)[i] = v;
+      if (d.s1) reinterpret_cast<float4*>(d.s1 + (size_t)row * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (d.s2) reinterpret_cast<float4*>(d.s2 + (size_t)row * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    for (uint32_t i = g; i < D; i += kBucket) {
+      e[i] = src ? src[i] : 0.f;
+      if (d.s1) d.s1[(size_t)row * D + i] = 0.f;
+      if (d.s2) d.s2[(size_t)row * D + i] = 0.f;
+    }
+  }
+  if (g == 0) d.step[row] = 0;
+}
+
+__device__ __forceinline__ void copy_row_group(const TableDesc& d, uint32_t row, float* dst,
+                                               unsigned g) {
+  const uint32_t D = d.dim;
+  const float* e = d.emb + (size_t)row * D;
+  if ((D & 3u) == 0) {
+    for (uint32_t i = g; i < (D >> 2); i += kBucket)
+      reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(e) + i);
+  } else {
+    for (uint32_t i = g; i < D; i += kBucket) dst[i] = e[i];
+  }
+}
+
+// Last-block epilogue: folds this launch's per-launch counters into the
+// table counters (the "fix-up" of the lock-free row allocator).
+__device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
+                                                unsigned long long fresh0, bool bump_tick,
+                                                uint32_t tick_now) {
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&td->c.blocks_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    TableCounters& c = td->c;
+    const unsigned long long used = c.alloc_ctr;
+    if (used <= free_n0) {
+      c.free_n = free_n0 - used;
+    } else {
+      c.free_n = 0;
+      unsigned long long f = fresh0 + (used - free_n0);
+      c.fresh_next = f > td->d.row_cap ? td->d.row_cap : f;
+    }
+    // removals push rows above free_n0 (remove kernel); fold them in
+    c.free_n += c.removed;
+    c.occupied = c.occupied + c.inserted - c.removed;
+    c.tombstones = c.tombstones - c.reused + c.removed;
+    c.alloc_ctr = 0;
+    c.inserted = 0;
+    c.reused = 0;
+    c.removed = 0;
+    if (bump_tick) c.tick = tick_now;
+    c.blocks_done = 0;
+    __threadfence();
+  }
+}
+
+// Keys equal to the two sentinels live in the descriptor (rare path).
+__device__ __forceinline__ int special_index(uint64_t key) {
+  return key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
+}
+
+// mode: 0 = ensure (find-or-insert zero row), 1 = insert (upsert src rows),
+//       2 = probe-only (stamp hits, report misses; bounded tables)
+__global__ void __launch_bounds__(kProbeThreads)
+    k_table_upsert(TableDev* __restrict__ td, const uint64_t* __restrict__ keys,
+                   const uint32_t* __restrict__ d_n, uint32_t n_host,
+                   const float* __restrict__ src, int mode, uint32_t* rows32, int64_t* rows64,
+                   const uint32_t* __restrict__ uslot, uint32_t* srow, uint32_t* missing_list,
+                   const uint32_t* __restrict__ sel) {
+  const TableDesc d = td->d;
+  const unsigned long long free_n0 = td->c.free_n;
+  const unsigned long long fresh0 = td->c.fresh_next;
+  const uint32_t tick_now = td->c.tick + 1;
+  const uint32_t n = d_n ? *d_n : n_host;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  __shared__ unsigned long long s_ins, s_reuse;
+  if (threadIdx.x == 0) {
+    s_ins = 0;
+    s_reuse = 0;
+  }
+  __syncthreads();
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t ii = group; ii < n; ii += ngroups) {
+    const uint64_t i = sel ? sel[ii] : ii;
+    const uint64_t key = keys[i];
+    const float* srow_src = (mode == 1) ? src + i * (uint64_t)d.dim : nullptr;
+    uint32_t row = kNoRow;
+    const int sp = special_index(key);
+    if (sp >= 0) {
+      uint32_t r = kNoRow;
+      int fresh = 0;
+      if (g == 0) {
+        r = td->c.special_row[sp];
+        if (r == kNoRow && mode != 2) {
+          const uint32_t nr = alloc_row(td, free_n0, fresh0, d.row_cap);
+          if (nr != kNoRow) {
+            const unsigned int prev = atomicCAS(&td->c.special_row[sp], kNoRow, nr);
+            if (prev == kNoRow) {
+              r = nr;
+              fresh = 1;
+              atomicAdd(&s_ins, 1ull);
+            } else {
+              r = prev;
+            }
+          }
+        }
+        if (r != kNoRow) td->c.special_tick[sp] = tick_now;
+        if (r == kNoRow && mode == 2 && missing_list) {
+          const unsigned idx = atomicAdd(&td->c.missing, 1u);
+          missing_list[idx] = (uint32_t)i;
+        }
+      }
+      r = __shfl_sync(gmask, r, gbase);
+      fresh = __shfl_sync(gmask, fresh, gbase);
+      if (fresh) {
+        init_row(d, r, srow_src, g);
+      } else if (mode == 1 && r != kNoRow) {
+        for (uint32_t e = g; e < d.dim; e += kBucket) d.emb[(size_t)r * d.dim + e] = srow_src[e];
+      }
+      row = r;
+    } else {
+      uint32_t new_row = kNoRow;
+      for (;;) {
+        const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
+        if (p.found) {
+          row = p.row;
+          if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
+          if (mode == 1) {  // upsert: overwrite the embedding in place
+            float* e = d.emb + (size_t)row * d.dim;
+            for (uint32_t k = g; k < d.dim; k += kBucket) e[k] = srow_src[k];
+          }
+          break;
+        }
+        if (mode == 2) {  // probe only
+          if (g == 0 && missing_list) {
+            const unsigned idx = atomicAdd(&td->c.missing, 1u);
+            missing_list[idx] = (uint32_t)i;
+          }
+          break;
+        }
+        if (p.ins == ~0ull) {
+          if (g == 0) atomicOr(&td->c.error, kErrTableFull);
+          break;
+        }
+        if (new_row == kNoRow) {
+          uint32_t r = 0;
+          if (g == 0) r = alloc_row(td, free_n0, fresh0, d.row_cap);
+          new_row = __shfl_sync(gmask, r, gbase);
+          if (new_row == kNoRow) break;
+        }
+        int ok = 0;
+        if (g == 0) {
+          const unsigned long long expect = p.ins_tomb ? kTombKey : kEmptyKey;
+          ok = atomicCAS(&d.slots[p.ins].key, expect, (unsigned long long)key) == expect;
+        }
+        ok = __shfl_sync(gmask, ok, gbase);
+        if (!ok) continue;  // lost the slot to another key: walk again
+        if (g == 0) {
+          uint2 rt = make_uint2(new_row, tick_now);
+          *reinterpret_cast<uint2*>(&d.slots[p.ins].row) = rt;
+          atomicAdd(&s_ins, 1ull);
+          if (p.ins_tomb) atomicAdd(&s_reuse, 1ull);
+        }
+        init_row(d, new_row, srow_src, g);
+        row = new_row;
+        break;
+      }
+    }
+    if (g == 0) {
+      if (rows32) rows32[i] = row;
+      if (rows64) rows64[i] = row == kNoRow ? -1 : (int64_t)row;
+      if (srow) srow[uslot[i]] = row;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_ins) atomicAdd(&td->c.inserted, s_ins);
+    if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
+  }
+  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+}
+
+// find (no side effects) / lookup_batch (stamp hits, copy or zero rows)
+__global__ void __launch_bounds__(kProbeThreads)
+    k_table_find(TableDev* __restrict__ td, const uint64_t* __restrict__ keys, uint64_t n,
+                 int64_t* rows64, float* out, int stamp) {
+  const TableDesc d = td->d;
+  const uint32_t tick_now = td->c.tick + 1;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t i = group; i < n; i += ngroups) {
+    const uint64_t key = keys[i];
+    uint32_t row = kNoRow;
+    const int sp = special_index(key);
+    if (sp >= 0) {
+      row = td->c.special_row[sp];
+      if (stamp && g == 0 && row != kNoRow) td->c.special_tick[sp] = tick_now;
+    } else {
+      const Probe p = probe_group<false>(d.slots, d.nb_mask, key, g, gbase, gmask);
+      if (p.found) {
+        row = p.row;
+        if (stamp && g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
+      }
+    }
+    if (rows64 && g == 0) rows64[i] = row == kNoRow ? -1 : (int64_t)row;
+    if (out) {
+      float* dst = out + i * (uint64_t)d.dim;
+      if (row != kNoRow) {
+        copy_row_group(d, row, dst, g);
+      } else {
+        for (uint32_t e = g; e < d.dim; e += kBucket) dst[e] = 0.f;
+      }
+    }
+  }
+  if (stamp) {
+    __syncthreads();
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&td->c.blocks_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      td->c.tick = tick_now;
+      td->c.blocks_done = 0;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kProbeThreads)
+    k_table_remove(TableDev* __restrict__ td, const uint64_t* __restrict__ keys, uint64_t n,
+                   uint8_t* removed) {
+  const TableDesc d = td->d;
+  const unsigned long long free_n0 = td->c.free_n;
+  const unsigned long long fresh0 = td->c.fresh_next;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t i = group; i < n; i += ngroups) {
+    const uint64_t key = keys[i];
+    uint32_t row = kNoRow;
+    const int sp = special_index(key);
+    if (sp >= 0) {
+      if (g == 0) row = atomicExch(&td->c.special_row[sp], kNoRow);
+    } else {
+      const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
+      if (p.found && g == 0) {
+        if (atomicCAS(&d.slots[p.slot].key, (unsigned long long)key, kTombKey) == key) {
+          row = p.row;
+          d.slots[p.slot].row = kNoRow;
+        }
+      }
+    }
+    if (g == 0) {
+      if (row != kNoRow) {
+        // push above the launch's free_n0; the epilogue adds `removed`
+        const unsigned long long k = atomicAdd(&td->c.removed, 1ull);
+        d.free_stack[free_n0 + k] = row;
+        if (sp >= 0) atomicAdd(&td->c.tombstones, ~0ull);  // sentinel keys leave no tombstone
+      }
+      if (removed) removed[i] = row != kNoRow;
+    }
+  }
+  launch_epilogue(td, free_n0, fresh0, true, td->c.tick + 1);
+}
+
+// Rehash every occupied slot of `old` into the (empty) new key structure.
+__global__ void __launch_bounds__(kProbeThreads)
+    k_rehash(const Slot* __restrict__ old, uint64_t old_nb, Slot* __restrict__ fresh,
+             uint64_t nb_mask) {
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t b = group; b < old_nb; b += ngroups) {
+    const uint4 mine = ld_slot(old + b * kBucket + g);
+    const uint64_t mykey = (uint64_t)mine.x | ((uint64_t)mine.y << 32);
+    unsigned live = (__ballot_sync(gmask, mykey != kEmptyKey && mykey != kTombKey) >> gbase) & 0xFFu;
+    while (live) {
+      const unsigned j = __ffs(live) - 1;
+      live &= live - 1;
+      const uint64_t key = __shfl_sync(gmask, mykey, gbase + j);
+      const uint32_t row = __shfl_sync(gmask, mine.z, gbase + j);
+      const uint32_t tick = __shfl_sync(gmask, mine.w, gbase + j);
+      for (;;) {
+        const Probe p = probe_group<true>(fresh, nb_mask, key, g, gbase, gmask);
+        int ok = 0;
+        if (g == 0 && p.ins != ~0ull)
+          ok = atomicCAS(&fresh[p.ins].key, kEmptyKey, (unsigned long long)key) == kEmptyKey;
+        ok = __shfl_sync(gmask, ok, gbase);
+        if (ok) {
+          if (g == 0) *reinterpret_cast<uint2*>(&fresh[p.ins].row) = make_uint2(row, tick);
+          break;
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_fill_slots(Slot* s, uint64_t n) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    Slot v;
+    v.key = kEmptyKey;
+    v.row = kNoRow;
+    v.tick = 0;
+    s[i] = v;
+  }
+}
+
+__global__ void k_gather_rows(TableDev* __restrict__ td, const int64_t* __restrict__ rows,
+                              uint64_t n, float* __restrict__ out) {
+  const TableDesc d = td->d;
+  const unsigned g = lane_id() & (kBucket - 1);
+  const uint64_t group = (uint64_t)blockIdx.x * (blockDim.x >> 3) + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * (blockDim.x >> 3);
+  for (uint64_t i = group; i < n; i += ngroups) {
+    const int64_t r = rows[i];
+    float* dst = out + i * (uint64_t)d.dim;
+    if (r >= 0)
+      copy_row_group(d, (uint32_t)r, dst, g);
+    else
+      for (uint32_t e = g; e < d.dim; e += kBucket) dst[e] = 0.f;
+  }
+}
+
+__global__ void k_scatter_state(TableDev* __restrict__ td, const int64_t* __restrict__ rows,
+                                uint64_t n, const float* m, const float* v,
+                                const uint64_t* step) {
+  const TableDesc d = td->d;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * d.dim;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = i / d.dim, e = i % d.dim;
+    const int64_t r = rows[k];
+    if (r < 0) continue;
+    if (m && d.s1) d.s1[(size_t)r * d.dim + e] = m[i];
+    if (v && d.s2) d.s2[(size_t)r * d.dim + e] = v[i];
+    if (step && e == 0) d.step[r] = (uint32_t)step[k];
+  }
+}
+
+__global__ void k_set_ticks(TableDev* __restrict__ td, const uint64_t* __restrict__ keys,
+                            const uint64_t* __restrict__ ticks, uint64_t n) {
+  const TableDesc d = td->d;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t i = group; i < n; i += ngroups) {
+    const int sp = special_index(keys[i]);
+    if (sp >= 0) {
+      if (g == 0) td->c.special_tick[sp] = (uint32_t)ticks[i];
+      continue;
+    }
+    const Probe p = probe_group<false>(d.slots, d.nb_mask, keys[i], g, gbase, gmask);
+    if (p.found && g == 0) d.slots[p.slot].tick = (uint32_t)ticks[i];
+  }
+}
+
+__global__ void k_hash64(const uint64_t* __restrict__ k, uint64_t n, uint64_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = hash64(k[i]);
+}
+__global__ void k_shard_of(const uint64_t* __restrict__ k, uint64_t n, uint32_t world,
+                           uint32_t* __restrict__ out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)(hash64(k[i]) % world);
+}
+
+// ---- host helpers ----------------------------------------------------------
+int alloc_rows(rs_table* t, uint64_t new_cap, cudaStream_t s) {
+  TableDesc& d = t->desc;
+  const uint64_t old = d.row_cap;
+  const size_t D = d.dim;
+  float *emb = nullptr, *s1 = nullptr, *s2 = nullptr;
+  uint32_t *step = nullptr, *fs = nullptr;
+  RS_CUDA(cudaMallocAsync(&emb, new_cap * D * sizeof(float), s));
+  if (d.opt == RS_OPT_ADAM) RS_CUDA(cudaMallocAsync(&s1, new_cap * D * sizeof(float), s));
+  if (d.opt != RS_OPT_NONE) RS_CUDA(cudaMallocAsync(&s2, new_cap * D * sizeof(float), s));
+  RS_CUDA(cudaMallocAsync(&step, new_cap * sizeof(uint32_t), s));
+  RS_CUDA(cudaMallocAsync(&fs, new_cap * sizeof(uint32_t), s));
+  if (old) {
+    RS_CUDA(cudaMemcpyAsync(emb, d.emb, old * D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    if (s1) RS_CUDA(cudaMemcpyAsync(s1, d.s1, old * D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    if (s2) RS_CUDA(cudaMemcpyAsync(s2, d.s2, old * D * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    RS_CUDA(cudaMemcpyAsync(step, d.step, old * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    RS_CUDA(cudaMemcpyAsync(fs, d.free_stack, old * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    RS_CUDA(cudaFreeAsync(d.emb, s));
+    if (d.s1) RS_CUDA(cudaFreeAsync(d.s1, s));
+    if (d.s2) RS_CUDA(cudaFreeAsync(d.s2, s));
+    RS_CUDA(cudaFreeAsync(d.step, s));
+    RS_CUDA(cudaFreeAsync(d.free_stack, s));
+  }
+  d.emb = emb;
+  d.s1 = s1;
+  d.s2 = s2;
+  d.step = step;
+  d.free_stack = fs;
+  d.row_cap = new_cap;
+  RS_CUDA(cudaMemcpyAsync(&t->dev->d, &t->desc, sizeof(TableDesc), cudaMemcpyHostToDevice, s));
+  return RS_OK;
+}
+
+int read_counters(rs_table* t, TableCounters* out, cudaStream_t s) {
+  RS_CUDA(cudaStreamSynchronize(s));
+  RS_CUDA(cudaMemcpy(out, &t->dev->c, sizeof(TableCounters), cudaMemcpyDeviceToHost));
+  if (out->error) {
+    const unsigned e = out->error;
+    return fail(e & kErrCapacity ? RS_ERR_CAPACITY : RS_ERR_INVARIANT,
+                std::string("table device error bits ") + std::to_string(e) +
+                    ((e & kErrRowPool) ? " (row pool exhausted)" : "") +
+                    ((e & kErrTableFull) ? " (probe found no usable slot)" : ""));
+  }
+  t->exact_occ = out->occupied;
+  t->exact_tomb = out->tombstones;
+  t->exact_rows = out->fresh_next;
+  t->exact_requested = t->requested_total;
+  return RS_OK;
+}
+
+int rehash_to(rs_table* t, uint64_t new_cap, cudaStream_t s) {
+  Slot* fresh = nullptr;
+  RS_CUDA(cudaMallocAsync(&fresh, new_cap * sizeof(Slot), s));
+  k_fill_slots<<<grid_for(new_cap, 256, 148 * 16), 256, 0, s>>>(fresh, new_cap);
+  RS_LAUNCH_CHECK("k_fill_slots");
+  const uint64_t old_nb = t->capacity / kBucket;
+  k_rehash<<<grid_for(old_nb, kGroupsPerBlock, 148 * 16), kProbeThreads, 0, s>>>(
+      t->desc.slots, old_nb, fresh, new_cap / kBucket - 1);
+  RS_LAUNCH_CHECK("k_rehash");
+  RS_CUDA(cudaFreeAsync(t->desc.slots, s));
+  t->desc.slots = fresh;
+  t->desc.nb_mask = new_cap / kBucket - 1;
+  t->capacity = new_cap;
+  RS_CUDA(cudaMemcpyAsync(&t->dev->d, &t->desc, sizeof(TableDesc), cudaMemcpyHostToDevice, s));
+  // tombstones are dropped by the rehash (embed_table.cpp:283)
+  RS_CUDA(cudaMemsetAsync(&t->dev->c.tombstones, 0, sizeof(unsigned long long), s));
+  t->exact_tomb = 0;
+  return RS_OK;
+}
+
+}  // namespace
+
+// Best upper bound on (occupied, rows) from the newest completed mirror.
+static void refresh_from_mirror(rs_table* t) {
+  for (int k = 0; k < 2; ++k) {
+    int i = (t->mirror_next + 1 + k) & 1;  // newest first
+    rs_mirror& m = t->mirror[i];
+    if (!m.valid) continue;
+    if (cudaEventQuery(m.ev) != cudaSuccess) continue;
+    if (m.requested_at_copy >= t->exact_requested) {
+      t->exact_occ = m.pinned->occupied;
+      t->exact_tomb = m.pinned->tombstones;
+      t->exact_rows = m.pinned->fresh_next;
+      t->exact_requested = m.requested_at_copy;
+    }
+    break;
+  }
+  (void)cudaGetLastError();
+}
+
+int table_prepare(rs_table* t, uint64_t n, cudaStream_t s) {
+  refresh_from_mirror(t);
+  const double lf = t->cfg.max_load_factor;
+  auto occ_ub = [&]() { return t->exact_occ + (t->requested_total - t->exact_requested); };
+  auto rows_ub = [&]() { return t->exact_rows + (t->requested_total - t->exact_requested); };
+  bool slots_ok = (double)(occ_ub() + t->exact_tomb + n) <= lf * (double)t->capacity;
+  bool rows_ok = rows_ub() + n <= t->desc.row_cap;
+  if (!slots_ok || !rows_ok) {
+    TableCounters c;
+    int st = read_counters(t, &c, s);
+    if (st) return st;
+    if ((double)(c.occupied + c.tombstones + n) > lf * (double)t->capacity) {
+      uint64_t nc = t->capacity;
+      do {
+        nc <<= 1;
+      } while ((double)(c.occupied + n) > lf * (double)nc);
+      st = rehash_to(t, nc, s);
+      if (st) return st;
+    }
+    if (c.fresh_next + n > t->desc.row_cap) {
+      uint64_t want = std::max<uint64_t>(t->desc.row_cap * 2, c.fresh_next + n);
+      const uint64_t cr = std::max<uint32_t>(1, t->cfg.chunk_rows);
+      want = (want + cr - 1) / cr * cr;
+      st = alloc_rows(t, want, s);
+      if (st) return st;
+    }
+  }
+  t->requested_total += n;
+  return RS_OK;
+}
+
+int table_after_op(rs_table* t, cudaStream_t s) {
+  rs_mirror& m = t->mirror[t->mirror_next];
+  RS_CUDA(cudaMemcpyAsync(m.pinned, &t->dev->c, sizeof(TableCounters), cudaMemcpyDeviceToHost, s));
+  RS_CUDA(cudaEventRecord(m.ev, s));
+  m.requested_at_copy = t->requested_total;
+  m.valid = true;
+  t->mirror_next ^= 1;
+  t->host_tick++;
+  return RS_OK;
+}
+
+int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                        uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                        uint32_t* d_srow, cudaStream_t s) {
+  if (n_max == 0) return RS_OK;
+  int st = table_prepare(t, n_max, s);
+  if (st) return st;
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 0, d_rows32, d_rows64, d_uslot, d_srow,
+      nullptr, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert");
+  return table_after_op(t, s);
+}
+
+int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies,
+                      cudaStream_t s) {
+  // bias corrections 1 - beta^step for step in [0, len), host libm pow
+  // (sparse_update.cpp:25-26), so device results match the reference bits.
+  if (t->d_bc && t->bc_beta1 == beta1 && t->bc_beta2 == beta2 && applies + 2 < t->bc_len)
+    return RS_OK;
+  uint64_t len = std::max<uint64_t>(4096, t->bc_len);
+  while (applies + 2 >= len) len *= 2;
+  std::vector<double> h(2 * len);
+  for (uint64_t k = 0; k < len; ++k) {
+    h[k] = 1.0 - std::pow(beta1, static_cast<double>(k));
+    h[len + k] = 1.0 - std::pow(beta2, static_cast<double>(k));
+  }
+  if (t->d_bc) RS_CUDA(cudaFreeAsync(t->d_bc, s));
+  RS_CUDA(cudaMallocAsync(&t->d_bc, 2 * len * sizeof(double), s));
+  RS_CUDA(cudaMemcpyAsync(t->d_bc, h.data(), 2 * len * sizeof(double), cudaMemcpyHostToDevice, s));
+  RS_CUDA(cudaStreamSynchronize(s));  // h goes out of scope
+  t->bc_len = len;
+  t->bc_beta1 = beta1;
+  t->bc_beta2 = beta2;
+  return RS_OK;
+}
+
+
+// ---- bounded tables: evict the oldest (tick, key) before inserting ----------
+// No reference counterpart (SPEC.md:156,165 leave eviction out); semantics
+// frozen in DESIGN.md §3 and restated in oracle.c (or_table_ensure_batch).
+static int grow_u32(uint32_t** p, uint64_t* cap, uint64_t n, cudaStream_t s) {
+  if (*cap >= n) return RS_OK;
+  if (*p) RS_CUDA(cudaFreeAsync(*p, s));
+  *cap = std::max<uint64_t>(n, 1024);
+  RS_CUDA(cudaMallocAsync(p, *cap * sizeof(uint32_t), s));
+  return RS_OK;
+}
+
+// Host-side selection of the k live entries with smallest (tick, key) among
+// those with tick < tick_limit, then a device remove.  Synchronizes.
+int evict_oldest(rs_table* t, uint64_t k, uint64_t tick_limit, uint64_t* evicted,
+                 cudaStream_t s) {
+  if (evicted) *evicted = 0;
+  if (k == 0) return RS_OK;
+  TableCounters c;
+  int st = read_counters(t, &c, s);
+  if (st) return st;
+  std::vector<Slot> slots(t->capacity);
+  RS_CUDA(cudaMemcpy(slots.data(), t->desc.slots, t->capacity * sizeof(Slot),
+                     cudaMemcpyDeviceToHost));
+  struct E {
+    uint32_t tick;
+    uint64_t key;
+  };
+  std::vector<E> cand;
+  cand.reserve(c.occupied + 2);
+  for (const Slot& sl : slots)
+    if (sl.key != kEmptyKey && sl.key != kTombKey && sl.tick < tick_limit)
+      cand.push_back({sl.tick, sl.key});
+  for (int sp = 0; sp < 2; ++sp)
+    if (c.special_row[sp] != kNoRow && c.special_tick[sp] < tick_limit)
+      cand.push_back({c.special_tick[sp], sp == 0 ? kEmptyKey : kTombKey});
+  auto lt = [](const E& a, const E& b) { return a.tick != b.tick ? a.tick < b.tick : a.key < b.key; };
+  if (k > cand.size()) k = cand.size();
+  std::nth_element(cand.begin(), cand.begin() + (k ? k - 1 : 0), cand.end(), lt);
+  std::vector<uint64_t> keys(k);
+  for (uint64_t i = 0; i < k; ++i) keys[i] = cand[i].key;
+  if (t->victims_cap < k) {
+    if (t->d_victims) RS_CUDA(cudaFree(t->d_victims));
+    t->victims_cap = std::max<uint64_t>(k, 1024);
+    RS_CUDA(cudaMalloc(&t->d_victims, t->victims_cap * 8));
+  }
+  RS_CUDA(cudaMemcpy(t->d_victims, keys.data(), k * 8, cudaMemcpyHostToDevice));
+  k_table_remove<<<grid_for(k, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, t->d_victims, k, nullptr);
+  RS_LAUNCH_CHECK("k_table_remove(evict)");
+  st = table_after_op(t, s);
+  if (st) return st;
+  RS_CUDA(cudaStreamSynchronize(s));
+  if (evicted) *evicted = k;
+  return RS_OK;
+}
+
+// ensure for any table; bounded tables probe, evict, then insert the misses.
+int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                     uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                     uint32_t* d_srow, cudaStream_t s) {
+  if (!t->cfg.max_keys)
+    return table_ensure_device(t, d_keys, d_n, n_max, d_rows32, d_rows64, d_uslot, d_srow, s);
+  if (n_max == 0) return RS_OK;
+  int st = grow_u32(&t->d_missing, &t->missing_cap, n_max, s);
+  if (st) return st;
+  RS_CUDA(cudaMemsetAsync(&t->dev->c.missing, 0, sizeof(unsigned int), s));
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 2, d_rows32, d_rows64, d_uslot, d_srow,
+      t->d_missing, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert(probe)");
+  st = table_after_op(t, s);
+  if (st) return st;
+  TableCounters c;
+  st = read_counters(t, &c, s);
+  if (st) return st;
+  uint32_t n = (uint32_t)n_max;
+  if (d_n) RS_CUDA(cudaMemcpy(&n, d_n, 4, cudaMemcpyDeviceToHost));
+  const uint64_t missing = c.missing;
+  if (missing == 0) return RS_OK;
+  const uint64_t found = n - missing;
+  if (c.occupied + missing > t->cfg.max_keys) {
+    const uint64_t need = c.occupied + missing - t->cfg.max_keys;
+    if (need > c.occupied - found)
+      return fail(RS_ERR_CAPACITY, "bounded table: batch of " + std::to_string(n) +
+                                       " keys cannot fit max_keys " +
+                                       std::to_string(t->cfg.max_keys));
+    st = evict_oldest(t, need, c.tick, nullptr, s);
+    if (st) return st;
+  }
+  st = table_prepare(t, missing, s);
+  if (st) return st;
+  // one tick per logical batch: new keys get the probe's tick (eviction's
+  // remove advanced it; rewind so the insert stamps c.tick again)
+  const unsigned int rewind = c.tick - 1;
+  RS_CUDA(cudaMemcpyAsync(&t->dev->c.tick, &rewind, sizeof(unsigned int), cudaMemcpyHostToDevice, s));
+  k_table_upsert<<<grid_for(missing, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, nullptr, (uint32_t)missing, nullptr, 0, d_rows32, d_rows64, d_uslot, d_srow,
+      nullptr, t->d_missing);
+  RS_LAUNCH_CHECK("k_table_upsert(insert missing)");
+  RS_CUDA(cudaStreamSynchronize(s));
+  return table_after_op(t, s);
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+extern "C" {
+
+int rs_hash64_batch(const uint64_t* d_keys, uint64_t n, uint64_t* d_out, void* stream) {
+  if (n == 0) return RS_OK;
+  k_hash64<<<grid_for(n, 256, 148 * 16), 256, 0, S(stream)>>>(d_keys, n, d_out);
+  RS_LAUNCH_CHECK("k_hash64");
+  return RS_OK;
+}
+
+int rs_shard_of_batch(const uint64_t* d_ids, uint64_t n, uint32_t world, uint32_t* d_owner,
+                      void* stream) {
+  if (world == 0) return fail(RS_ERR_CONFIG, "shard_of: world_size must be >= 1");
+  if (n == 0) return RS_OK;
+  k_shard_of<<<grid_for(n, 256, 148 * 16), 256, 0, S(stream)>>>(d_ids, n, world, d_owner);
+  RS_LAUNCH_CHECK("k_shard_of");
+  return RS_OK;
+}
+
+int rs_table_create(const rs_table_config* cfg, rs_table** out) {
+  if (!cfg || !out) return fail(RS_ERR_CONFIG, "rs_table_create: null argument");
+  const rs_table_config c = *cfg;
+  auto pow2 = [](uint64_t x) { return x && !(x & (x - 1)); };
+  // TableConfig::validate (embed_table.cpp:23-38)
+  if (!pow2(c.capacity)) return fail(RS_ERR_CONFIG, "TableConfig: capacity must be a power of two");
+  if (!pow2(c.thread_groups))
+    return fail(RS_ERR_CONFIG, "TableConfig: thread_groups must be a power of two >= 1");
+  if (c.capacity < 2ull * c.thread_groups)
+    return fail(RS_ERR_CONFIG, "TableConfig: capacity must be >= 2 * thread_groups");
+  if (!(c.max_load_factor > 0.0 && c.max_load_factor < 1.0))
+    return fail(RS_ERR_CONFIG, "TableConfig: max_load_factor must be in (0, 1)");
+  if (c.chunk_rows < 1) return fail(RS_ERR_CONFIG, "TableConfig: chunk_rows must be >= 1");
+  if (c.embedding_dim < 1) return fail(RS_ERR_CONFIG, "TableConfig: embedding_dim must be >= 1");
+  if (c.optimizer > RS_OPT_ADAGRAD) return fail(RS_ERR_CONFIG, "TableConfig: unknown optimizer");
+  rs_table* t = new rs_table();
+  t->cfg = c;
+  t->capacity = std::max<uint64_t>(c.capacity, 2 * kBucket);
+  t->desc.dim = c.embedding_dim;
+  t->desc.opt = c.optimizer;
+  cudaStream_t s = nullptr;
+  auto cleanup = [&](int st) {
+    rs_table_destroy(t);
+    return st;
+  };
+  if (cudaMalloc(&t->dev, sizeof(TableDev)) != cudaSuccess)
+    return cleanup(cuda_fail(cudaGetLastError(), "cudaMalloc(TableDev)"));
+  if (cudaMalloc(&t->desc.slots, t->capacity * sizeof(Slot)) != cudaSuccess)
+    return cleanup(cuda_fail(cudaGetLastError(), "cudaMalloc(slots)"));
+  t->desc.nb_mask = t->capacity / kBucket - 1;
+  k_fill_slots<<<grid_for(t->capacity, 256, 148 * 16), 256, 0, s>>>(t->desc.slots, t->capacity);
+  count_launch();
+  TableCounters c0;
+  std::memset(&c0, 0, sizeof(c0));
+  c0.special_row[0] = c0.special_row[1] = kNoRow;
+  if (cudaMemcpy(&t->dev->c, &c0, sizeof(c0), cudaMemcpyHostToDevice) != cudaSuccess)
+    return cleanup(cuda_fail(cudaGetLastError(), "init counters"));
+  uint64_t rows = c.initial_rows ? c.initial_rows
+                                 : (uint64_t)std::ceil((double)t->capacity * c.max_load_factor);
+  if (c.max_keys) rows = std::max<uint64_t>(rows, c.max_keys);
+  rows = std::max<uint64_t>(rows, 16);
+  int st = alloc_rows(t, rows, s);
+  if (st) return cleanup(st);
+  for (auto& m : t->mirror) {
+    if (cudaMallocHost(&m.pinned, sizeof(TableCounters)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(cuda_fail(cudaGetLastError(), "mirror alloc"));
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess)
+    return cleanup(cuda_fail(cudaGetLastError(), "rs_table_create"));
+  *out = t;
+  return RS_OK;
+}
+
+int rs_table_destroy(rs_table* t) {
+  if (!t) return RS_OK;
+  cudaDeviceSynchronize();
+  cudaFree(t->desc.slots);
+  cudaFree(t->desc.emb);
+  cudaFree(t->desc.s1);
+  cudaFree(t->desc.s2);
+  cudaFree(t->desc.step);
+  cudaFree(t->desc.free_stack);
+  cudaFree(t->d_bc);
+  cudaFree(t->dev);
+  for (auto& m : t->mirror) {
+    if (m.pinned) cudaFreeHost(m.pinned);
+    if (m.ev) cudaEventDestroy(m.ev);
+  }
+  delete t;
+  return RS_OK;
+}
+
+int rs_table_stats(rs_table* t, rs_table_info* out) {
+  if (!t || !out) return fail(RS_ERR_CONFIG, "rs_table_stats: null argument");
+  TableCounters c;
+  int st = read_counters(t, &c, nullptr);
+  RS_CUDA(cudaDeviceSynchronize());
+  RS_CUDA(cudaMemcpy(&c, &t->dev->c, sizeof(c), cudaMemcpyDeviceToHost));
+  if (st) return st;
+  out->capacity = t->capacity;
+  out->occupied = c.occupied;
+  out->tombstones = c.tombstones;
+  out->rows_allocated = c.fresh_next;
+  out->rows_free = c.free_n;
+  out->row_capacity = t->desc.row_cap;
+  out->tick = c.tick;
+  out->embedding_dim = t->desc.dim;
+  out->optimizer = t->desc.opt;
+  return RS_OK;
+}
+
+int rs_table_insert(rs_table* t, const uint64_t* d_keys, uint64_t n, const float* d_emb,
+                    void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_insert: null table");
+  if (n == 0) return RS_OK;
+  if (!d_emb) return fail(RS_ERR_CONFIG, "insert: embedding length != embedding_dim");
+  if (t->cfg.max_keys) return fail(RS_ERR_CONFIG, "insert on a bounded table: use rs_table_ensure");
+  cudaStream_t s = S(stream);
+  int st = table_prepare(t, n, s);
+  if (st) return st;
+  k_table_upsert<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, nullptr, (uint32_t)n, d_emb, 1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert(insert)");
+  return table_after_op(t, s);
+}
+
+int rs_table_find(rs_table* t, const uint64_t* d_keys, uint64_t n, int64_t* d_rows, void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_find: null table");
+  if (n == 0) return RS_OK;
+  k_table_find<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, S(stream)>>>(
+      t->dev, d_keys, n, d_rows, nullptr, 0);
+  RS_LAUNCH_CHECK("k_table_find");
+  return RS_OK;
+}
+
+int rs_table_lookup(rs_table* t, const uint64_t* d_keys, uint64_t n, float* d_out, void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_lookup: null table");
+  if (n == 0) return RS_OK;
+  k_table_find<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, S(stream)>>>(
+      t->dev, d_keys, n, nullptr, d_out, 1);
+  RS_LAUNCH_CHECK("k_table_find(lookup)");
+  t->host_tick++;
+  return RS_OK;
+}
+
+int rs_table_gather_rows(rs_table* t, const int64_t* d_rows, uint64_t n, float* d_out,
+                         void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_gather_rows: null table");
+  if (n == 0) return RS_OK;
+  k_gather_rows<<<grid_for(n, 32, 148 * 8), 256, 0, S(stream)>>>(t->dev, d_rows, n, d_out);
+  RS_LAUNCH_CHECK("k_gather_rows");
+  return RS_OK;
+}
+
+int rs_table_remove(rs_table* t, const uint64_t* d_keys, uint64_t n, uint8_t* d_removed,
+                    void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_remove: null table");
+  if (n == 0) return RS_OK;
+  k_table_remove<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, S(stream)>>>(
+      t->dev, d_keys, n, d_removed);
+  RS_LAUNCH_CHECK("k_table_remove");
+  return table_after_op(t, S(stream));
+}
+
+int rs_table_expand(rs_table* t, uint64_t* new_capacity, void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_expand: null table");
+  cudaStream_t s = S(stream);
+  TableCounters c;
+  int st = read_counters(t, &c, s);
+  if (st) return st;
+  // expand_impl (embed_table.cpp:267-272): double at least once, keep
+  // doubling while occupied/capacity exceeds the load ceiling
+  uint64_t nc = t->capacity;
+  do {
+    nc <<= 1;
+  } while ((double)c.occupied > t->cfg.max_load_factor * (double)nc);
+  st = rehash_to(t, nc, s);
+  if (st) return st;
+  RS_CUDA(cudaStreamSynchronize(s));
+  if (new_capacity) *new_capacity = nc;
+  return RS_OK;
+}
+
+int rs_table_ensure(rs_table* t, const uint64_t* d_keys, uint64_t n, int64_t* d_rows,
+                    void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_ensure: null table");
+  return table_ensure_any(t, d_keys, nullptr, n, nullptr, d_rows, nullptr, nullptr, S(stream));
+}
+
+int rs_table_evict(rs_table* t, uint64_t k, uint64_t* evicted, void* stream) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_evict: null table");
+  return evict_oldest(t, k, ~0ull, evicted, S(stream));
+}
+
+int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* emb, float* m,
+                    float* v, uint64_t* step, uint64_t* ts, uint64_t* count) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_export: null table");
+  TableCounters c;
+  int st = read_counters(t, &c, nullptr);
+  if (st) return st;
+  std::vector<Slot> slots(t->capacity);
+  RS_CUDA(cudaMemcpy(slots.data(), t->desc.slots, t->capacity * sizeof(Slot), cudaMemcpyDeviceToHost));
+  struct E {
+    uint64_t key;
+    uint32_t row, tick;
+  };
+  std::vector<E> live;
+  live.reserve(c.occupied + 2);
+  for (const Slot& sl : slots)
+    if (sl.key != kEmptyKey && sl.key != kTombKey) live.push_back({sl.key, sl.row, sl.tick});
+  for (int sp = 0; sp < 2; ++sp)
+    if (c.special_row[sp] != kNoRow)
+      live.push_back({sp == 0 ? kEmptyKey : kTombKey, c.special_row[sp], c.special_tick[sp]});
+  std::sort(live.begin(), live.end(), [](const E& a, const E& b) { return a.key < b.key; });
+  if (count) *count = live.size();
+  if (max_entries == 0) return RS_OK;
+  if (max_entries < live.size()) return fail(RS_ERR_CONFIG, "rs_table_export: buffer too small");
+  const size_t D = t->desc.dim;
+  uint64_t nrows = 0;
+  for (const E& e : live) nrows = std::max<uint64_t>(nrows, (uint64_t)e.row + 1);
+  std::vector<float> he, hm, hv;
+  std::vector<uint32_t> hs;
+  auto pull = [&](std::vector<float>& h, const float* src) -> int {
+    h.resize(nrows * D);
+    if (src && nrows)
+      RS_CUDA(cudaMemcpy(h.data(), src, nrows * D * 4, cudaMemcpyDeviceToHost));
+    else
+      std::fill(h.begin(), h.end(), 0.f);
+    return RS_OK;
+  };
+  if (emb && (st = pull(he, t->desc.emb))) return st;
+  if (m && (st = pull(hm, t->desc.s1))) return st;
+  if (v && (st = pull(hv, t->desc.s2))) return st;
+  if (step) {
+    hs.resize(nrows);
+    if (nrows) RS_CUDA(cudaMemcpy(hs.data(), t->desc.step, nrows * 4, cudaMemcpyDeviceToHost));
+  }
+  for (size_t i = 0; i < live.size(); ++i) {
+    const E& e = live[i];
+    const size_t r = e.row;
+    if (keys) keys[i] = e.key;
+    if (ts) ts[i] = e.tick;
+    if (emb) std::memcpy(emb + i * D, he.data() + r * D, D * 4);
+    if (m) std::memcpy(m + i * D, hm.data() + r * D, D * 4);
+    if (v) std::memcpy(v + i * D, hv.data() + r * D, D * 4);
+    if (step) step[i] = hs[r];
+  }
+  return RS_OK;
+}
+
+int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* emb,
+                    const float* m, const float* v, const uint64_t* step, const uint64_t* ts) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_import: null table");
+  if (n == 0) return RS_OK;
+  const size_t D = t->desc.dim;
+  uint64_t *dk = nullptr, *dstep = nullptr, *dts = nullptr;
+  float *de = nullptr, *dm = nullptr, *dv = nullptr;
+  int64_t* drows = nullptr;
+  RS_CUDA(cudaMalloc(&dk, n * 8));
+  RS_CUDA(cudaMalloc(&de, n * D * 4));
+  RS_CUDA(cudaMalloc(&drows, n * 8));
+  RS_CUDA(cudaMemcpy(dk, keys, n * 8, cudaMemcpyHostToDevice));
+  if (emb)
+    RS_CUDA(cudaMemcpy(de, emb, n * D * 4, cudaMemcpyHostToDevice));
+  else
+    RS_CUDA(cudaMemset(de, 0, n * D * 4));
+  int st = table_prepare(t, n, nullptr);
+  if (st) return st;
+  k_table_upsert<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads>>>(
+      t->dev, dk, nullptr, (uint32_t)n, de, 1, nullptr, drows, nullptr, nullptr, nullptr, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert(import)");
+  st = table_after_op(t, nullptr);
+  if (st) return st;
+  if (m) {
+    RS_CUDA(cudaMalloc(&dm, n * D * 4));
+    RS_CUDA(cudaMemcpy(dm, m, n * D * 4, cudaMemcpyHostToDevice));
+  }
+  if (v) {
+    RS_CUDA(cudaMalloc(&dv, n * D * 4));
+    RS_CUDA(cudaMemcpy(dv, v, n * D * 4, cudaMemcpyHostToDevice));
+  }
+  if (step) {
+    RS_CUDA(cudaMalloc(&dstep, n * 8));
+    RS_CUDA(cudaMemcpy(dstep, step, n * 8, cudaMemcpyHostToDevice));
+  }
+  if (m || v || step) {
+    k_scatter_state<<<grid_for(n * D, 256, 148 * 16), 256>>>(t->dev, drows, n, dm, dv, dstep);
+    RS_LAUNCH_CHECK("k_scatter_state");
+  }
+  if (ts) {
+    RS_CUDA(cudaMalloc(&dts, n * 8));
+    RS_CUDA(cudaMemcpy(dts, ts, n * 8, cudaMemcpyHostToDevice));
+    k_set_ticks<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads>>>(t->dev, dk, dts, n);
+    RS_LAUNCH_CHECK("k_set_ticks");
+  }
+  RS_CUDA(cudaDeviceSynchronize());
+  cudaFree(dk);
+  cudaFree(de);
+  cudaFree(drows);
+  cudaFree(dm);
+  cudaFree(dv);
+  cudaFree(dstep);
+  cudaFree(dts);
+  return RS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,48 @@
+"""Synthetic inputs of the benchmark configs via librsgpu's generator.
+
+Identical (same seed -> same ids) to the reference's generate_workload
+(workload.cpp:280-307) and pseudo_sparse_grad (workload.cpp:348-355); the
+parity tests check that against the reference itself.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check
+
+
+def generate(seed: int, num_sequences: int, mean_len: float, max_len: int, sigma: float,
+             zipf: float, vocab) -> tuple[np.ndarray, np.ndarray]:
+    """-> (lengths[num_sequences] u64, catalog-tagged ids[Σ lengths] u64)."""
+    vocab = np.ascontiguousarray(np.atleast_1d(np.asarray(vocab, dtype=np.uint64)))
+    lengths = np.zeros(num_sequences, np.uint64)
+    cap = int(num_sequences * mean_len * 3) + 4096
+    while True:
+        ids = np.zeros(cap, np.uint64)
+        n = C.c_uint64()
+        st = L.lib().rs_workload_generate(seed, num_sequences, mean_len, max_len, sigma, zipf, len(vocab),
+                                          vocab.ctypes.data, lengths.ctypes.data, ids.ctypes.data, cap,
+                                          C.byref(n))
+        if st == L.RS_OK:
+            return lengths, ids[: n.value].copy()
+        if cap >= num_sequences * max_len:
+            check(st, "generate")
+        cap = min(cap * 2, num_sequences * max_len)
+
+
+def sample_of_tokens(lengths, first_sample_id: int = 1) -> np.ndarray:
+    lengths = np.asarray(lengths, np.int64)
+    return np.repeat(np.arange(first_sample_id, first_sample_id + len(lengths), dtype=np.uint64), lengths)
+
+
+def pseudo_grads(sample_of: torch.Tensor, step: int, dim: int) -> torch.Tensor:
+    """per-token pseudo_sparse_grad(sample_id, step) generated on the device."""
+    s = sample_of.to(device="cuda", dtype=torch.int64).contiguous()
+    out = torch.empty((s.numel(), dim), dtype=torch.float32, device="cuda")
+    check(L.lib().rs_pseudo_grads(s.data_ptr(), s.numel(), step, dim, out.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream), "pseudo_grads")
+    return out

@@ -1,0 +1,308 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the CPU oracle.
+
+Bars: bit-exact for hash/shard, dedup unique + inverse, table
+contents after insert/ensure/remove/expand/evict, forward gathered rows, and
+the optimizer given identical aggregated gradients; aggregated gradients
+within |Δ| <= 1e-5 * Σ|g_i| of the reference's sequential f32 sums.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2505_12663_b200 as P
+from paper_2505_12663_b200 import workload as W
+from oracle.bind import Table
+
+pytestmark = pytest.mark.gpu
+
+TAG1 = 1 << 62  # catalog tag of a single-table workload (k = 1, ordinal 1)
+GRAD_TOL = 1e-5
+
+
+def dev(a):
+    return P.as_keys(a)
+
+
+def np_u64(t):
+    return P.keys_to_numpy(t)
+
+
+# ---------------------------------------------------------------- primitives
+def test_hash64_and_shard_of(cuda, oracle, kat):
+    rng = np.random.default_rng(1)
+    keys = np.concatenate([np.array([c[0] for c in kat["hash64"]["cases"]], np.uint64),
+                           rng.integers(0, 2**63, 5000, dtype=np.uint64) * 2 + 1,
+                           np.array([0, 2**64 - 1, 2**64 - 2], np.uint64)])
+    got = np_u64(P.hash64_batch(keys))
+    want = np.array([oracle.hash64(int(k)) for k in keys], np.uint64)
+    np.testing.assert_array_equal(got, want)
+    for w in (1, 2, 3, 4, 7, 8):
+        s = P.shard_of_batch(keys, w).cpu().numpy()
+        np.testing.assert_array_equal(s, (want % np.uint64(w)).astype(np.int32))
+
+
+# --------------------------------------------------------------------- dedup
+def _dedup_cases():
+    rng = np.random.default_rng(7)
+    yield np.zeros(0, np.uint64)
+    yield np.array([5, 3, 5, 9, 3], np.uint64)  # test_exchange_sim.cpp:77-82
+    yield np.array([4, 8, 15, 16, 23, 42], np.uint64)
+    yield np.full(3000, 77, np.uint64)
+    yield np.arange(2049, dtype=np.uint64)[::-1].copy()
+    yield np.array([2**64 - 1, 0, 2**64 - 2, 2**64 - 1, 0, 1], np.uint64)  # sentinel bit patterns
+    for n in (1, 511, 512, 513, 1025, 40000):
+        yield (rng.zipf(1.1, n) % 100000).astype(np.uint64) + np.uint64(TAG1)
+    _, ids = W.generate(1, 1024, 128.0, 4096, 1.0, 1.1, [1 << 20])  # config 1 batch
+    yield ids
+
+
+def test_dedup_bit_exact(cuda, oracle):
+    ws = P.Workspace(200000)
+    for ids in _dedup_cases():
+        u, inv = P.stage1_dedup(ids, ws)
+        wu, winv = oracle.stage1(ids)
+        np.testing.assert_array_equal(np_u64(u), wu)
+        np.testing.assert_array_equal(inv.cpu().numpy().astype(np.int64), winv)
+
+
+def test_stage2_is_dedup_over_concatenation(cuda, oracle):
+    rng = np.random.default_rng(11)
+    lists = [rng.integers(0, 300, int(rng.integers(0, 200))).astype(np.uint64) for _ in range(8)]
+    wu, off, src, pos = oracle.stage2(lists)
+    u, inv = P.stage1_dedup(np.concatenate(lists))
+    np.testing.assert_array_equal(np_u64(u), wu)
+    # the inverse gives every origin; grouped by unique in (source, position) order
+    inv = inv.cpu().numpy()
+    base = np.cumsum([0] + [len(x) for x in lists])
+    for k in range(len(wu)):
+        js = np.nonzero(inv == k)[0]
+        s = np.searchsorted(base, js, side="right") - 1
+        np.testing.assert_array_equal(s, src[off[k]:off[k + 1]])
+        np.testing.assert_array_equal(js - base[s], pos[off[k]:off[k + 1]])
+
+
+# --------------------------------------------------------------------- table
+def _gpu_table(capacity, dim, opt="adam", **kw):
+    return P.EmbedTable(P.TableConfig(capacity=capacity, embedding_dim=dim, chunk_rows=64, optimizer=opt, **kw))
+
+
+def _compare_contents(gpu, ora, fields=("keys", "emb", "m", "v", "step")):
+    a = gpu.export()
+    b = ora.export()
+    for f in fields:
+        np.testing.assert_array_equal(a[f], b[f].astype(a[f].dtype), err_msg=f)
+
+
+def test_table_model_vs_oracle(cuda, oracle):
+    rng = np.random.default_rng(99)
+    dim = 4
+    g = _gpu_table(16, dim)
+    o = Table(oracle, 16, dim, chunk_rows=64)
+    for it in range(120):
+        op = int(rng.integers(0, 5))
+        keys = np.unique(rng.integers(0, 600, int(rng.integers(1, 40))).astype(np.uint64))
+        rng.shuffle(keys)
+        if op <= 1:
+            emb = rng.standard_normal((len(keys), dim)).astype(np.float32)
+            g.insert(keys, torch.from_numpy(emb))
+            for k, e in zip(keys, emb):
+                o.insert(int(k), e)
+        elif op == 2:
+            rows = g.ensure(keys).cpu().numpy()
+            assert (rows >= 0).all()
+            for k in keys:
+                oracle.table_ensure(o.h, int(k))
+        elif op == 3:
+            rem = g.remove(keys).cpu().numpy()
+            want = [oracle.table_remove(o.h, int(k)) for k in keys]
+            np.testing.assert_array_equal(rem, np.array(want, bool))
+        else:
+            out = g.lookup_batch(np.concatenate([keys, keys])).cpu().numpy()
+            want = np.zeros_like(out)
+            for j, k in enumerate(np.concatenate([keys, keys])):
+                r = oracle.table_find(o.h, int(k))
+                if r >= 0:
+                    want[j] = np.ctypeslib.as_array(oracle.table_emb(o.h, r), (dim,))
+            np.testing.assert_array_equal(out, want)
+        if it in (40, 80):
+            g.expand()
+        assert g.occupied() == oracle.table_occupied(o.h)
+    _compare_contents(g, o)
+    assert g.load_factor() <= 0.75
+
+
+def test_table_expand_keeps_rows(cuda):
+    g = _gpu_table(16, 4)
+    keys = np.arange(5, dtype=np.uint64)
+    g.insert(keys, torch.arange(20, dtype=torch.float32).reshape(5, 4))
+    rows_before = g.find(keys).cpu().numpy()
+    g.remove(np.array([4], np.uint64))
+    assert g.tombstones() == 1
+    assert g.expand() == 32
+    assert g.tombstones() == 0
+    np.testing.assert_array_equal(g.find(keys[:4]).cpu().numpy(), rows_before[:4])  # rows never move
+    assert g.find(np.array([4], np.uint64)).item() == -1
+
+
+def test_sentinel_keys(cuda):
+    g = _gpu_table(64, 4)
+    keys = np.array([2**64 - 1, 2**64 - 2, 0, 7], np.uint64)
+    g.insert(keys, torch.arange(16, dtype=torch.float32).reshape(4, 4))
+    out = g.lookup_batch(keys).cpu().numpy()
+    np.testing.assert_array_equal(out, np.arange(16, dtype=np.float32).reshape(4, 4))
+    assert g.occupied() == 4
+    assert g.remove(keys[:1]).all()
+    assert g.find(keys[:1]).item() == -1 and g.occupied() == 3
+    e = g.export()
+    np.testing.assert_array_equal(e["keys"], np.sort(keys[1:]))
+
+
+def test_lookup_batch_ticks(cuda, oracle):
+    g = _gpu_table(256, 4, opt="none")
+    keys = np.arange(150, dtype=np.uint64)
+    g.insert(keys, torch.zeros(150, 4))
+    t0 = g.tick()
+    q = np.random.default_rng(5).integers(0, 200, 500).astype(np.uint64)
+    out = g.lookup_batch(q).cpu().numpy()
+    assert g.tick() == t0 + 1
+    e = g.export()
+    hit = np.isin(e["keys"], q)
+    assert (e["ts"][hit] == t0 + 1).all() and (e["ts"][~hit] == t0).all()
+    assert (out[q >= 150] == 0).all()
+
+
+# ------------------------------------------------------------- the C1 step
+def _c1_like(seed, num_seq, vocab, dim, opt="adagrad", mean=128.0):
+    lengths, ids = W.generate(seed, num_seq, mean, 4096, 1.0, 1.1, [vocab])
+    keys = np.arange(vocab, dtype=np.uint64) + np.uint64(TAG1)
+    rows = np.zeros((vocab, dim), np.float32)
+    from oracle.bind import Oracle
+    o = Oracle("oracle")
+    for r in range(vocab):
+        o.pseudo_sparse_grad(r, 0, rows[r], dim)
+    g = _gpu_table(1 << max(4, int(np.ceil(np.log2(vocab * 2)))), dim, opt=opt)
+    g.insert(keys, torch.from_numpy(rows))
+    ot = Table(o, 1 << max(4, int(np.ceil(np.log2(vocab * 2)))), dim, chunk_rows=4096)
+    for r in range(vocab):
+        ot.insert(int(keys[r]), rows[r])
+    return lengths, ids, g, ot
+
+
+@pytest.mark.parametrize("dim,opt", [(64, "adagrad"), (64, "adam"), (128, "adagrad"), (32, "adam"), (20, "adagrad")])
+def test_step_vs_oracle(cuda, oracle, dim, opt):
+    vocab = 20000
+    lengths, ids, g, ot = _c1_like(3, 256, vocab, dim, opt)
+    params = P.AdagradParams() if opt == "adagrad" else P.AdamParams()
+    step = P.SparseStep(g, len(ids), params)
+    tok_sample = W.sample_of_tokens(lengths)
+    for s in range(3):
+        # new ids appear too (vivified as zero rows)
+        batch = ids.copy()
+        batch[::97] = np.uint64(TAG1) + np.uint64(vocab + s * 100000) + np.arange(len(batch[::97]), dtype=np.uint64)
+        grads = W.pseudo_grads(torch.from_numpy(tok_sample.view(np.int64)), s, dim)
+        out = step.forward(P.as_keys(batch))
+        sums = step.accumulate(grads)
+        step.backward(grads)
+        torch.cuda.synchronize()
+        # forward: bit-exact with distributed_lookup at W = 1 (vivified rows are zeros)
+        want_out = np.zeros((len(batch), dim), np.float32)
+        oracle.table_lookup_batch(ot.h, batch, len(batch), want_out.reshape(-1))
+        np.testing.assert_array_equal(out.cpu().numpy(), want_out)
+        # dedup results
+        u, inv = oracle.stage1(batch)
+        nu = len(u)
+        # aggregated grads: tolerance vs the sequential f32 sums of the reference
+        g_np = grads.cpu().numpy()
+        ids_acc, sums_ref = oracle.accumulate_np(batch, g_np, dim)
+        order = np.argsort(u)
+        sums_gpu = sums[:nu].cpu().numpy()[order]
+        np.testing.assert_array_equal(ids_acc, u[order])
+        absmass = np.zeros((nu, dim), np.float64)
+        np.add.at(absmass, inv, np.abs(g_np).astype(np.float64))
+        err = np.abs(sums_gpu.astype(np.float64) - sums_ref)
+        assert (err <= GRAD_TOL * absmass[order] + 1e-30).all(), err.max()
+        # optimizer bit-exact given the GPU's aggregated grads (oracle apply)
+        oracle.apply(ot.h, ids_acc, np.ascontiguousarray(sums_gpu).reshape(-1), nu,
+                     1 if opt == "adagrad" else 0, params.lr, getattr(params, "beta1", 0.9),
+                     getattr(params, "beta2", 0.999), params.eps)
+        _compare_contents(g, ot, ("keys", "emb", "v", "step") + (("m",) if opt == "adam" else ()))
+
+
+def test_step_deterministic(cuda):
+    dim = 64
+    lengths, ids = W.generate(4, 128, 128.0, 4096, 1.0, 1.1, [50000])
+    res = []
+    for _ in range(2):
+        g = _gpu_table(1 << 17, dim, opt="adagrad")
+        st = P.SparseStep(g, len(ids), P.AdagradParams())
+        grads = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), 0, dim)
+        out = torch.empty((len(ids), dim), device="cuda")
+        for _ in range(3):
+            st.step(P.as_keys(ids), grads, out)
+        res.append(g.export())
+    for f in ("keys", "emb", "v", "step"):
+        np.testing.assert_array_equal(res[0][f], res[1][f])
+
+
+@pytest.mark.parametrize("opt", ["adam", "adagrad"])
+def test_apply_aggregated_bit_exact(cuda, oracle, opt):
+    rng = np.random.default_rng(61)
+    dim = 64
+    g = _gpu_table(1024, dim, opt=opt)
+    o = Table(oracle, 1024, dim, chunk_rows=64)
+    keys = np.arange(300, dtype=np.uint64) * np.uint64(977)
+    init = rng.standard_normal((300, dim)).astype(np.float32)
+    g.insert(keys, torch.from_numpy(init))
+    for k, e in zip(keys, init):
+        o.insert(int(k), e)
+    params = P.AdamParams(lr=0.003) if opt == "adam" else P.AdagradParams(lr=0.02)
+    for step in range(25):
+        sel = np.sort(rng.choice(np.concatenate([keys, keys[:20] + np.uint64(1)]), 120, replace=False))
+        sums = (rng.standard_normal((120, dim)) * 0.1).astype(np.float32)
+        P.apply_aggregated(g, sel, torch.from_numpy(sums), params)
+        oracle.apply(o.h, sel, sums.reshape(-1), 120, 0 if opt == "adam" else 1, params.lr,
+                     getattr(params, "beta1", 0.9), getattr(params, "beta2", 0.999), params.eps)
+    _compare_contents(g, o, ("keys", "emb", "v", "step") + (("m",) if opt == "adam" else ()))
+
+
+def test_sparse_update_matches_accumulate_apply(cuda, oracle):
+    # GradAccumulator::accumulate + apply over one window, vivifying absent ids
+    rng = np.random.default_rng(67)
+    dim = 32
+    g = _gpu_table(256, dim, opt="adam")
+    o = Table(oracle, 256, dim, chunk_rows=64)
+    ws = P.Workspace(1000)
+    for _ in range(5):
+        ids = rng.integers(0, 40, 700).astype(np.uint64)
+        grads = (rng.integers(0, 100, (700, dim)) / 50.0 - 1.0).astype(np.float32)  # exact in f32 sums
+        P.sparse_update(g, ws, ids, torch.from_numpy(grads).cuda(), P.AdamParams())
+        i2, s2 = oracle.accumulate_np(ids, grads, dim)
+        oracle.apply(o.h, i2, s2.reshape(-1), len(i2), 0, 0.01, 0.9, 0.999, 1e-8)
+    _compare_contents(g, o, ("keys", "emb", "m", "v", "step"))
+
+
+# ------------------------------------------------------- bounded + eviction
+def test_bounded_table_eviction_vs_oracle(cuda, oracle):
+    rng = np.random.default_rng(21)
+    dim, bound = 16, 3000
+    g = _gpu_table(1 << 13, dim, opt="adagrad", max_keys=bound)
+    o = Table(oracle, 1 << 13, dim, chunk_rows=4096)
+    fresh = 10**6
+    for b in range(12):
+        old = rng.integers(0, 4000, 700).astype(np.uint64)
+        new = np.arange(fresh, fresh + 150, dtype=np.uint64)
+        fresh += 150
+        keys = np.unique(np.concatenate([old, new]))
+        rng.shuffle(keys)
+        tick = g.tick() + 1
+        g.ensure(keys)
+        oracle.table_ensure_batch(o.h, keys, len(keys), tick, bound, None)
+        assert g.occupied() == oracle.table_occupied(o.h) <= bound
+        assert g.tick() == tick
+    _compare_contents(g, o, ("keys", "ts", "emb", "v", "step"))
+    # explicit eviction of the k oldest (ts, key)
+    g.evict(100)
+    oracle.table_evict_oldest(o.h, 100)
+    _compare_contents(g, o, ("keys", "ts"))
