@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kScanThreads)
   // last block resets the tile ticket and the status words for the next call
   __syncthreads();
   if (tid == 0) {
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     s_last = atomicAdd(&ctr[1], 1u) == gridDim.x - 1;
   }
   __syncthreads();
@@ -391,18 +391,35 @@ __device__ __forceinline__ void adam_elem(float& w, float& m, float& v, float gf
 // Applies one optimizer step to `row` with the lane-distributed gradient
 // acc[c][j] for elements e = (c*32 + lane)*VEC + j.  Called by a full warp.
 template <int VEC, int CH>
-__device__ __forceinline__ void apply_row(const TableDesc& d, uint32_t row, const float (&acc)[CH][VEC],
-                                          const OptArgs& o) {
+__device__ __forceinline__ void load_vec(const float* __restrict__ src, uint32_t D,
+                                         float (&x)[CH][VEC], bool coherent);
+template <int VEC, int CH>
+__device__ __forceinline__ void store_vec(float* __restrict__ dst, uint32_t D,
+                                          const float (&x)[CH][VEC]);
+
+// Applies one optimizer step to `row` with the lane-distributed gradient
+// acc[c][j] for elements e = (c*32 + lane)*VEC + j.  Called by a full warp.
+// Row loads are issued before the step counter so their latencies overlap.
+template <int VEC, int CH>
+__device__ __forceinline__ void apply_row(const TableDesc& d, uint32_t row,
+                                          const float (&acc)[CH][VEC], const OptArgs& o) {
   const unsigned lane = lane_id();
   const uint32_t D = d.dim;
   if (row == kNoRow) return;
-  double bc1 = 1.0, bc2 = 1.0;
+  float* w = d.emb + (size_t)row * D;
+  float* m = d.s1 ? d.s1 + (size_t)row * D : nullptr;
+  float* v = d.s2 + (size_t)row * D;
+  float wv[CH][VEC], mv[CH][VEC], vv[CH][VEC];
+  load_vec<VEC, CH>(w, D, wv, false);
+  load_vec<VEC, CH>(v, D, vv, false);
+  if (m) load_vec<VEC, CH>(m, D, mv, false);
   uint32_t step = 0;
   if (lane == 0) {
     step = d.step[row] + 1;
     d.step[row] = step;
   }
   step = __shfl_sync(kFull, step, 0);
+  double bc1 = 1.0, bc2 = 1.0;
   if (o.kind == RS_OPT_ADAM) {
     if (step < o.bc_len) {
       bc1 = o.bc[step];
@@ -412,48 +429,19 @@ __device__ __forceinline__ void apply_row(const TableDesc& d, uint32_t row, cons
       bc2 = 1.0 - pow(o.b2, (double)step);
     }
   }
-  float* w = d.emb + (size_t)row * D;
-  float* m = d.s1 ? d.s1 + (size_t)row * D : nullptr;
-  float* v = d.s2 ? d.s2 + (size_t)row * D : nullptr;
 #pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    const uint32_t e0 = ((uint32_t)c * 32 + lane) * VEC;
-    if (VEC == 1 && e0 >= D) continue;
-    float wv[VEC], mv[VEC], vv[VEC];
-    if (VEC == 4) {
-      *reinterpret_cast<float4*>(wv) = *reinterpret_cast<const float4*>(w + e0);
-      if (v) *reinterpret_cast<float4*>(vv) = *reinterpret_cast<const float4*>(v + e0);
-      if (m) *reinterpret_cast<float4*>(mv) = *reinterpret_cast<const float4*>(m + e0);
-    } else if (VEC == 2) {
-      *reinterpret_cast<float2*>(wv) = *reinterpret_cast<const float2*>(w + e0);
-      if (v) *reinterpret_cast<float2*>(vv) = *reinterpret_cast<const float2*>(v + e0);
-      if (m) *reinterpret_cast<float2*>(mv) = *reinterpret_cast<const float2*>(m + e0);
-    } else {
-      wv[0] = w[e0];
-      if (v) vv[0] = v[e0];
-      if (m) mv[0] = m[e0];
-    }
+  for (int c = 0; c < CH; ++c)
 #pragma unroll
     for (int j = 0; j < VEC; ++j) {
+      if (VEC == 1 && (uint32_t)(c * 32 + lane) >= D) continue;
       if (o.kind == RS_OPT_ADAM)
-        adam_elem(wv[j], mv[j], vv[j], acc[c][j], bc1, bc2, o);
+        adam_elem(wv[c][j], mv[c][j], vv[c][j], acc[c][j], bc1, bc2, o);
       else
-        adagrad_elem(wv[j], vv[j], acc[c][j], o);
+        adagrad_elem(wv[c][j], vv[c][j], acc[c][j], o);
     }
-    if (VEC == 4) {
-      *reinterpret_cast<float4*>(w + e0) = *reinterpret_cast<float4*>(wv);
-      if (v) *reinterpret_cast<float4*>(v + e0) = *reinterpret_cast<float4*>(vv);
-      if (m) *reinterpret_cast<float4*>(m + e0) = *reinterpret_cast<float4*>(mv);
-    } else if (VEC == 2) {
-      *reinterpret_cast<float2*>(w + e0) = *reinterpret_cast<float2*>(wv);
-      if (v) *reinterpret_cast<float2*>(v + e0) = *reinterpret_cast<float2*>(vv);
-      if (m) *reinterpret_cast<float2*>(m + e0) = *reinterpret_cast<float2*>(mv);
-    } else {
-      w[e0] = wv[0];
-      if (v) v[e0] = vv[0];
-      if (m) m[e0] = mv[0];
-    }
-  }
+  store_vec<VEC, CH>(w, D, wv);
+  store_vec<VEC, CH>(v, D, vv);
+  if (m) store_vec<VEC, CH>(m, D, mv);
 }
 
 template <int VEC, int CH>
@@ -503,30 +491,88 @@ struct ReduceArgs {
   const float* grads;
   uint32_t n;
   uint32_t ntiles;
-  uint32_t bw;  // bitmap words per warp = ceil(ntiles / 32)
+  uint32_t bw;  // bitmap words = ceil(ntiles / 32)
   const uint32_t* u_ntile;
   const uint32_t* u_poff;
   uint32_t* u_ticket;
-  uint32_t* u_done;
   const uint32_t* urow;
-  float* pbuf;
-  uint32_t* ptile;
-  uint32_t* porder;
+  const uint32_t* n_unique;  // device count of the last dedup
+  float* usum;               // [U x D] sums of single-tile ids
+  float* pbuf;               // [n_part x D] per-(tile, id) partial sums
+  uint32_t* ptile;           // tile of each partial
+  uint32_t* porder;          // scratch: partial index by rank
   TableDev* td;
   float* sums_out;  // accumulate-only mode when non-null
   bool tma;
 };
 
-// K5.  blockDim.x == TT (tokens per tile), one tile per block.
+constexpr uint32_t kWarpMaxParts = 32;  // ids with more partials finish block-cooperatively
+
 template <int VEC, int CH>
-__global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
+__device__ __forceinline__ void zero_acc(float (&x)[CH][VEC]) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) x[c][j] = 0.f;
+}
+template <int VEC, int CH>
+__device__ __forceinline__ void add_acc(float (&x)[CH][VEC], const float (&y)[CH][VEC]) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c)
+#pragma unroll
+    for (int j = 0; j < VEC; ++j) x[c][j] += y[c][j];
+}
+
+template <int VEC, int CH>
+__device__ __forceinline__ void finalize(const ReduceArgs& a, const TableDesc& d, uint32_t uu,
+                                         const float (&acc)[CH][VEC], const OptArgs& o) {
+  if (a.sums_out)
+    store_vec<VEC, CH>(a.sums_out + (size_t)uu * d.dim, d.dim, acc);
+  else
+    apply_row<VEC, CH>(d, __ldg(a.urow + uu), acc, o);
+}
+
+// Ordered sum of partials whose indices (within the id's segment) are given
+// by rank in `order` (smem or global), ranks [r0, r1), PF rows in flight.
+template <int VEC, int CH>
+__device__ __forceinline__ void ordered_sum(const ReduceArgs& a, const uint32_t* order,
+                                            uint32_t poff, uint32_t r0, uint32_t r1, uint32_t D,
+                                            float (&acc)[CH][VEC]) {
+  constexpr int PF = (CH * VEC <= 2) ? 16 : (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+  const unsigned lane = lane_id();
+  zero_acc<VEC, CH>(acc);
+  for (uint32_t r = r0; r < r1; r += 32) {
+    const uint32_t cnt = min(32u, r1 - r);
+    const uint32_t idx = lane < cnt ? order[r + lane] : 0;
+    for (uint32_t j0 = 0; j0 < cnt; j0 += PF) {
+      float x[PF][CH][VEC];
+#pragma unroll
+      for (int jj = 0; jj < PF; ++jj) {
+        const uint32_t i = __shfl_sync(kFull, idx, (j0 + jj) & 31);
+        if (j0 + jj < cnt) load_vec<VEC, CH>(a.pbuf + (size_t)(poff + i) * D, D, x[jj], false);
+      }
+#pragma unroll
+      for (int jj = 0; jj < PF; ++jj)
+        if (j0 + jj < cnt) add_acc<VEC, CH>(acc, x[jj]);
+    }
+  }
+}
+
+// K5.  blockDim.x == TT (tokens per tile, <= 256), one tile per block.
+//  phase 0  TMA bulk copy (UBLKCP) of the tile's contiguous gradient rows
+//  phase 1  group the tile's tokens by unique id in smem (first-occurrence
+//           order), stable ranks -> local CSR; partial tickets
+//  phase 2  warp per group: position-order f32 sum, in place into the group's
+//           first row (no other group reads that row)
+//  phase 3  element-parallel stores: single-tile ids -> usum[u], multi-tile
+//           ids -> pbuf[poff + ticket] tagged with the tile index
+template <int VEC, int CH>
+__global__ void __launch_bounds__(256, 2) k_tile_reduce(ReduceArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t NW = TT >> 5;
   const uint32_t L = 2 * TT;
-  const TableDesc d = a.td->d;
-  const uint32_t D = d.dim;
-  // carve shared memory
+  const uint32_t D = a.td->d.dim;
   float* sg = reinterpret_cast<float*>(smem);  // [TT x D] staged gradients
   unsigned char* p = smem + (size_t)TT * D * 4;
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(p);
@@ -537,11 +583,13 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
   uint32_t* gcnt = lgroup + L;
   uint32_t* goff = gcnt + TT;
   uint32_t* gu = goff + TT;
-  uint32_t* wsum = gu + TT;        // [32]
+  uint32_t* gdst = gu + TT;        // destination row offset (floats) of each group's sum
+  uint32_t* wsum = gdst + TT;      // [32]
   uint32_t* misc = wsum + 32;      // [0] ng
-  uint32_t* bm_all = misc + 32;    // [NW x 2 x bw]
-  uint16_t* wcnt = reinterpret_cast<uint16_t*>(bm_all + (size_t)NW * 2 * a.bw);  // [NW x TT]
-  uint16_t* csr = wcnt + (size_t)NW * TT;                                        // [TT]
+  uint16_t* wcnt = reinterpret_cast<uint16_t*>(misc + 32);  // [NW x TT]
+  uint16_t* csr = wcnt + (size_t)NW * TT;                    // [TT]
+  float* dst_base[2] = {a.usum, a.pbuf};
+  (void)dst_base;
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint32_t tile = blockIdx.x;
@@ -553,7 +601,6 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
     lfirst[i] = kFull;
   }
   for (uint32_t i = tid; i < NW * TT; i += TT) wcnt[i] = 0;
-  // stage this tile's contiguous gradient rows: one TMA bulk copy (UBLKCP)
   if (a.tma) {
     if (tid == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
@@ -580,10 +627,9 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
   }
   __syncthreads();
 
-  // ---- phase 1: group the tile's tokens by unique id (smem), stable ranks
-  const uint32_t t = t0 + tid;
+  // ---- phase 1
   const bool valid = tid < rows;
-  const uint32_t u = valid ? (uint32_t)a.inverse[t] : kFull;
+  const uint32_t u = valid ? (uint32_t)__ldg(a.inverse + t0 + tid) : kFull;
   uint32_t ps = 0;
   if (valid) {
     ps = hash32(u) & (L - 1);
@@ -616,6 +662,17 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
     const uint32_t lg = wsum[warp] + __popc(hb & lanemask_lt());
     lgroup[ps] = lg;
     gu[lg] = u;
+    const uint32_t nt = __ldg(a.u_ntile + u);
+    uint32_t dst;
+    if (nt > 1) {
+      const uint32_t tk = atomicAdd(a.u_ticket + u, 1u);
+      const uint32_t slot = __ldg(a.u_poff + u) + tk;
+      a.ptile[slot] = tile;
+      dst = slot | 0x80000000u;  // partial buffer
+    } else {
+      dst = u;  // usum
+    }
+    gdst[lg] = dst;
   }
   __syncthreads();
   const uint32_t mylg = valid ? lgroup[ps] : (0xFFFF0000u | lane);
@@ -641,7 +698,6 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
       const uint32_t y = __shfl_up_sync(kFull, x, o2);
       if (lane >= (unsigned)o2) x += y;
     }
-    __syncthreads();
     if (lane == 31) wsum[warp] = x;
     __syncthreads();
     if (warp == 0) {
@@ -668,97 +724,146 @@ __global__ void k_reduce_update(ReduceArgs a, OptArgs o) {
   }
   __syncthreads();
 
-  // ---- phase 2: per-group position-order sums, then update / partial
-  uint32_t* bm = bm_all + (size_t)warp * 2 * a.bw;
-  uint32_t* wpre = bm + a.bw;
+  // ---- phase 2: position-order sums
   for (uint32_t g = warp; g < ng; g += NW) {
-    const uint32_t uu = gu[g];
     const uint32_t cnt = gcnt[g];
+    if (cnt < 2) continue;
     const uint32_t base = goff[g];
     float acc[CH][VEC];
-#pragma unroll
-    for (int c = 0; c < CH; ++c)
-#pragma unroll
-      for (int j = 0; j < VEC; ++j) acc[c][j] = 0.f;
-    for (uint32_t k = 0; k < cnt; ++k) {
-      const float* row = sg + (size_t)csr[base + k] * D;
+    load_vec<VEC, CH>(sg + (size_t)csr[base] * D, D, acc, false);
+    for (uint32_t k = 1; k < cnt; ++k) {
       float x[CH][VEC];
-      load_vec<VEC, CH>(row, D, x, false);
-#pragma unroll
-      for (int c = 0; c < CH; ++c)
-#pragma unroll
-        for (int j = 0; j < VEC; ++j) acc[c][j] += x[c][j];
+      load_vec<VEC, CH>(sg + (size_t)csr[base + k] * D, D, x, false);
+      add_acc<VEC, CH>(acc, x);
     }
+    store_vec<VEC, CH>(sg + (size_t)csr[base] * D, D, acc);
+  }
+  __syncthreads();
+
+  // ---- phase 3: element-parallel stores of sums / partials
+  if ((D & 3u) == 0) {
+    const uint32_t D4 = D >> 2;
+    const uint32_t nchunks = ng * D4;
+    for (uint32_t q = tid; q < nchunks; q += TT) {
+      const uint32_t g = q / D4, c = q - g * D4;
+      const float4 sum = *reinterpret_cast<const float4*>(sg + (size_t)csr[goff[g]] * D + 4 * c);
+      const uint32_t dst = gdst[g];
+      float* base = (dst & 0x80000000u) ? a.pbuf + (size_t)(dst & 0x7FFFFFFFu) * D
+                                        : a.usum + (size_t)dst * D;
+      __stcg(reinterpret_cast<float4*>(base) + c, sum);
+    }
+  } else {
+    const uint32_t nchunks = ng * D;
+    for (uint32_t q = tid; q < nchunks; q += TT) {
+      const uint32_t g = q / D, e = q - g * D;
+      const uint32_t dst = gdst[g];
+      float* base = (dst & 0x80000000u) ? a.pbuf + (size_t)(dst & 0x7FFFFFFFu) * D
+                                        : a.usum + (size_t)dst * D;
+      base[e] = sg[(size_t)csr[goff[g]] * D + e];
+    }
+  }
+}
+
+// K6.  Finish every unique id: combine its partials in tile order, then one
+// optimizer step on its row (or store the aggregated sum).  Warp per id;
+// ids are strided over blocks (hot ids have the lowest first-occurrence
+// indices, this spreads them over SMs).  Ids with more than kWarpMaxParts
+// partials are finished by the whole block with a fixed split over warps.
+template <int VEC, int CH>
+__global__ void __launch_bounds__(256) k_finish(ReduceArgs a, OptArgs o) {
+  extern __shared__ __align__(16) unsigned char smem2[];
+  const uint32_t NW = blockDim.x >> 5;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const TableDesc d = a.td->d;
+  const uint32_t D = d.dim;
+  const uint32_t nu = *a.n_unique;
+  uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * 32;  // [NW x 32]
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem2) + NW * 32;        // [bw]
+  uint32_t* wpre = bm + a.bw;                                         // [bw]
+  float* wpart = reinterpret_cast<float*>(wpre + a.bw);               // [NW x D]
+  for (uint32_t uu = blockIdx.x + gridDim.x * warp; uu < nu; uu += gridDim.x * NW) {
     const uint32_t nt = __ldg(a.u_ntile + uu);
-    bool finish = nt <= 1;
-    if (!finish) {
+    float acc[CH][VEC];
+    if (nt <= 1) {
+      load_vec<VEC, CH>(a.usum + (size_t)uu * D, D, acc, false);
+    } else if (nt <= kWarpMaxParts) {
       const uint32_t poff = __ldg(a.u_poff + uu);
-      uint32_t tk = 0;
-      if (lane == 0) tk = atomicAdd(a.u_ticket + uu, 1u);
-      tk = __shfl_sync(kFull, tk, 0);
-      store_vec<VEC, CH>(a.pbuf + (size_t)(poff + tk) * D, D, acc);
-      if (lane == 0) a.ptile[poff + tk] = tile;
-      __threadfence();
+      const uint32_t tl = lane < nt ? __ldg(a.ptile + poff + lane) : kFull;
+      uint32_t r = 0;
+#pragma unroll 8
+      for (uint32_t j = 0; j < nt; ++j) r += __shfl_sync(kFull, tl, j) < tl;
+      if (lane < nt) order_w[r] = lane;
       __syncwarp();
-      uint32_t done = 0;
-      if (lane == 0) done = atomicAdd(a.u_done + uu, 1u);
-      done = __shfl_sync(kFull, done, 0);
-      if (done == nt - 1) {
-        // last arriver: order the partials by tile index and sum in order
-        __threadfence();
-        for (uint32_t i = lane; i < a.bw; i += 32) bm[i] = 0;
-        __syncwarp();
-        for (uint32_t i = lane; i < nt; i += 32) {
-          const uint32_t tl = __ldcg(a.ptile + poff + i);
-          atomicOr(&bm[tl >> 5], 1u << (tl & 31));
-        }
-        __syncwarp();
-        const uint32_t per = (a.bw + 31) / 32;
-        const uint32_t w0 = min(lane * per, a.bw), w1 = min(w0 + per, a.bw);
-        uint32_t loc = 0;
-        for (uint32_t i = w0; i < w1; ++i) loc += __popc(bm[i]);
-        uint32_t x = loc;
+      ordered_sum<VEC, CH>(a, order_w, poff, 0, nt, D, acc);
+      __syncwarp();
+      if (lane == 0) a.u_ticket[uu] = 0;
+    } else {
+      continue;  // finished below by the whole block
+    }
+    finalize<VEC, CH>(a, d, uu, acc, o);
+  }
+  // second pass over this block's ids: the ones with many partials
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t w = k % NW, it = k / NW;
+    const uint64_t uu64 = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * (w + (uint64_t)NW * it);
+    if (uu64 >= nu) {
+      if (w == 0) break;
+      continue;
+    }
+    const uint32_t uu = (uint32_t)uu64;
+    const uint32_t nt = __ldg(a.u_ntile + uu);
+    if (nt <= kWarpMaxParts) continue;
+    const uint32_t poff = __ldg(a.u_poff + uu);
+    __syncthreads();
+    // rank the partials by tile index: block-wide bitmap + prefix popcounts
+    for (uint32_t i = threadIdx.x; i < a.bw; i += blockDim.x) bm[i] = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+      const uint32_t tl = __ldg(a.ptile + poff + i);
+      atomicOr(&bm[tl >> 5], 1u << (tl & 31));
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t per = (a.bw + 31) / 32;
+      const uint32_t w0 = min(lane * per, a.bw), w1 = min(w0 + per, a.bw);
+      uint32_t loc = 0;
+      for (uint32_t i = w0; i < w1; ++i) loc += __popc(bm[i]);
+      uint32_t x = loc;
 #pragma unroll
-        for (int o2 = 1; o2 < 32; o2 <<= 1) {
-          const uint32_t y = __shfl_up_sync(kFull, x, o2);
-          if (lane >= (unsigned)o2) x += y;
-        }
-        uint32_t runp = x - loc;
-        for (uint32_t i = w0; i < w1; ++i) {
-          wpre[i] = runp;
-          runp += __popc(bm[i]);
-        }
-        __syncwarp();
-        for (uint32_t i = lane; i < nt; i += 32) {
-          const uint32_t tl = __ldcg(a.ptile + poff + i);
-          const uint32_t r = wpre[tl >> 5] + __popc(bm[tl >> 5] & ((1u << (tl & 31)) - 1u));
-          a.porder[poff + r] = i;
-        }
-        __threadfence_block();
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < CH; ++c)
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) acc[c][j] = 0.f;
-        for (uint32_t r = 0; r < nt; ++r) {
-          const uint32_t i = __ldcg(a.porder + poff + r);
-          float x2[CH][VEC];
-          load_vec<VEC, CH>(a.pbuf + (size_t)(poff + i) * D, D, x2, true);
-#pragma unroll
-          for (int c = 0; c < CH; ++c)
-#pragma unroll
-            for (int j = 0; j < VEC; ++j) acc[c][j] += x2[c][j];
-        }
-        finish = true;
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o2);
+        if (lane >= (unsigned)o2) x += y;
+      }
+      uint32_t runp = x - loc;
+      for (uint32_t i = w0; i < w1; ++i) {
+        wpre[i] = runp;
+        runp += __popc(bm[i]);
       }
     }
-    if (finish) {
-      if (a.sums_out) {
-        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
-      } else {
-        apply_row<VEC, CH>(d, __ldg(a.urow + uu), acc, o);
-      }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+      const uint32_t tl = __ldg(a.ptile + poff + i);
+      a.porder[poff + wpre[tl >> 5] + __popc(bm[tl >> 5] & ((1u << (tl & 31)) - 1u))] = i;
     }
+    __syncthreads();
+    const uint32_t per = (nt + NW - 1) / NW;
+    const uint32_t r0 = min(warp * per, nt), r1 = min(r0 + per, nt);
+    float part[CH][VEC];
+    ordered_sum<VEC, CH>(a, a.porder + poff, poff, r0, r1, D, part);
+    store_vec<VEC, CH>(wpart + (size_t)warp * D, D, part);
+    __syncthreads();
+    if (warp == 0) {
+      float tot[CH][VEC];
+      zero_acc<VEC, CH>(tot);
+      for (uint32_t w = 0; w < NW; ++w) {
+        float x[CH][VEC];
+        load_vec<VEC, CH>(wpart + (size_t)w * D, D, x, false);
+        add_acc<VEC, CH>(tot, x);
+      }
+      if (lane == 0) a.u_ticket[uu] = 0;
+      finalize<VEC, CH>(a, d, uu, tot, o);
+    }
+    __syncthreads();
   }
 }
 
@@ -793,7 +898,7 @@ Shape shape_for(uint32_t D) {
 
 uint32_t tile_tokens_for_dim(uint32_t D) {
   // keep the staged gradient tile at <= 64 KB so two tiles fit per SM
-  uint32_t tt = 512;
+  uint32_t tt = 256;
   while (tt > 32 && (uint64_t)tt * D * 4 > 65536) tt >>= 1;
   return tt;
 }
@@ -889,11 +994,11 @@ static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, ui
   const uint32_t D = t->desc.dim;
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
-  // partial-sum buffer: at most one partial per (tile, id) pair <= n
+  // partial sums: at most one per (tile, id) pair <= n; usum: one per id <= n
   if (ws->pbuf_floats < n * D) {
     if (ws->pbuf) RS_CUDA(cudaFreeAsync(ws->pbuf, s));
     ws->pbuf_floats = ws->max_tokens * (uint64_t)D;
-    RS_CUDA(cudaMallocAsync(&ws->pbuf, ws->pbuf_floats * sizeof(float), s));
+    RS_CUDA(cudaMallocAsync(&ws->pbuf, 2 * ws->pbuf_floats * sizeof(float), s));
   }
   ReduceArgs a;
   a.inverse = ws->inverse;
@@ -904,28 +1009,34 @@ static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, ui
   a.u_ntile = ws->u_ntile;
   a.u_poff = ws->u_poff;
   a.u_ticket = ws->u_ticket;
-  a.u_done = ws->u_done;
   a.urow = ws->urow;
+  a.n_unique = ws->ctr + 2;
   a.pbuf = ws->pbuf;
+  a.usum = ws->pbuf + ws->pbuf_floats;
   a.ptile = ws->ptile;
   a.porder = ws->porder;
   a.td = t->dev;
   a.sums_out = sums_out;
   a.tma = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_grads) & 15u) == 0);
   const uint32_t NW = TT / 32;
-  const size_t smem = (size_t)TT * D * 4 + 16 + (size_t)(3 * 2 * TT + 3 * TT + 64) * 4 +
-                      (size_t)NW * 2 * a.bw * 4 + (size_t)NW * TT * 2 + (size_t)TT * 2 + 16;
+  const size_t smem5 = (size_t)TT * D * 4 + 16 + (size_t)(3 * 2 * TT + 4 * TT + 64) * 4 +
+                       (size_t)NW * TT * 2 + (size_t)TT * 2 + 16;
+  const size_t smem6 = (size_t)8 * 32 * 4 + (size_t)2 * a.bw * 4 + (size_t)8 * D * 4 + 16;
   const Shape sh = shape_for(D);
-  if (sh.ch > 32) return fail(RS_ERR_CONFIG, "embedding_dim > 1024 unsupported by the reduce");
-  auto go = [&](auto kern) -> int {
-    if (smem > 48 * 1024)
-      RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<ntiles, TT, smem, s>>>(a, o);
-    RS_LAUNCH_CHECK("k_reduce_update");
+  const unsigned grid6 = grid_for(n, 8, 148 * 16);
+  auto go = [&](auto k5, auto k6) -> int {
+    if (smem5 > 48 * 1024)
+      RS_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
+    if (smem6 > 48 * 1024)
+      RS_CUDA(cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6));
+    k5<<<ntiles, TT, smem5, s>>>(a);
+    RS_LAUNCH_CHECK("k_tile_reduce");
+    k6<<<grid6, 256, smem6, s>>>(a, o);
+    RS_LAUNCH_CHECK("k_finish");
     return RS_OK;
   };
 #define RS_SHAPE(V, C) \
-  if (sh.vec == V && sh.ch == C) return go(k_reduce_update<V, C>);
+  if (sh.vec == V && sh.ch == C) return go(k_tile_reduce<V, C>, k_finish<V, C>);
   RS_SHAPE(4, 1) RS_SHAPE(4, 2) RS_SHAPE(4, 3) RS_SHAPE(4, 4)
   RS_SHAPE(2, 1) RS_SHAPE(2, 2)
   RS_SHAPE(1, 1) RS_SHAPE(1, 2) RS_SHAPE(1, 3) RS_SHAPE(1, 4) RS_SHAPE(1, 5) RS_SHAPE(1, 6)
