@@ -41,8 +41,27 @@ struct rs_table {
   uint64_t victims_cap = 0;
 };
 
+struct rs_graph_entry {
+  // everything a captured step bakes in
+  rs_table* t = nullptr;
+  const void* ids = nullptr;
+  const void* grads = nullptr;
+  void* out = nullptr;
+  uint64_t n = 0;
+  int mirror = 0;
+  const void* pbuf = nullptr;
+  unsigned char opt[128] = {0};
+  cudaGraphExec_t exec = nullptr;
+  uint64_t last_use = 0;
+  uint64_t launches = 0;  // rsgpu kernels inside the graph
+};
+
 struct rs_workspace {
   uint64_t max_tokens = 0;
+  cudaStream_t cap_stream = nullptr;  // capture stream for the step graphs
+  std::vector<rs_graph_entry> graphs;
+  uint64_t graph_clock = 0;
+  bool use_graphs = true;
   uint64_t S = 0;  // scratch hash capacity (power of two); index S is the spare slot
   // dedup scratch set (SoA, S+1 entries)
   unsigned long long* skey = nullptr;
@@ -88,6 +107,11 @@ int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n
 int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                      uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
                      uint32_t* d_srow, cudaStream_t s);
+int table_upsert_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                         uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                         uint32_t* d_srow, cudaStream_t s);
+int table_mirror_copy(rs_table* t, int which, cudaStream_t s);
+int table_mirror_commit(rs_table* t, int which, cudaStream_t s);
 int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies, cudaStream_t s);
 // step.cu
 int dedup_run(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint32_t tile,

@@ -116,6 +116,7 @@ void set_error(const std::string& msg);
 int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 void count_launch(uint64_t n = 1);
+uint64_t launches();
 
 #define RS_CUDA(call)                                       \
   do {                                                      \

@@ -507,6 +507,7 @@ struct ReduceArgs {
 };
 
 constexpr uint32_t kWarpMaxParts = 32;  // ids with more partials finish block-cooperatively
+constexpr uint32_t kHotCap = 64;        // per-block list of such ids
 
 template <int VEC, int CH>
 __device__ __forceinline__ void zero_acc(float (&x)[CH][VEC]) {
@@ -538,7 +539,7 @@ template <int VEC, int CH>
 __device__ __forceinline__ void ordered_sum(const ReduceArgs& a, const uint32_t* order,
                                             uint32_t poff, uint32_t r0, uint32_t r1, uint32_t D,
                                             float (&acc)[CH][VEC]) {
-  constexpr int PF = (CH * VEC <= 2) ? 16 : (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+  constexpr int PF = (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
   const unsigned lane = lane_id();
   zero_acc<VEC, CH>(acc);
   for (uint32_t r = r0; r < r1; r += 32) {
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(256, 2) k_tile_reduce(ReduceArgs a) {
 // indices, this spreads them over SMs).  Ids with more than kWarpMaxParts
 // partials are finished by the whole block with a fixed split over warps.
 template <int VEC, int CH>
-__global__ void __launch_bounds__(256) k_finish(ReduceArgs a, OptArgs o) {
+__global__ void __launch_bounds__(256, 3) k_finish(ReduceArgs a, OptArgs o) {
   extern __shared__ __align__(16) unsigned char smem2[];
   const uint32_t NW = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -778,16 +779,22 @@ __global__ void __launch_bounds__(256) k_finish(ReduceArgs a, OptArgs o) {
   const uint32_t D = d.dim;
   const uint32_t nu = *a.n_unique;
   uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * 32;  // [NW x 32]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem2) + NW * 32;        // [bw]
+  uint32_t* hot = reinterpret_cast<uint32_t*>(smem2) + NW * 32;       // [kHotCap]
+  uint32_t* nhot = hot + kHotCap;                                     // [1]
+  uint32_t* bm = nhot + 1;                                            // [bw]
   uint32_t* wpre = bm + a.bw;                                         // [bw]
-  float* wpart = reinterpret_cast<float*>(wpre + a.bw);               // [NW x D]
+  float* wpart = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(wpre + a.bw) + 15) & ~uintptr_t(15));  // [NW x D], 16B aligned
+  if (threadIdx.x == 0) *nhot = 0;
+  __syncthreads();
   for (uint32_t uu = blockIdx.x + gridDim.x * warp; uu < nu; uu += gridDim.x * NW) {
     const uint32_t nt = __ldg(a.u_ntile + uu);
+    const uint32_t poff = __ldg(a.u_poff + uu);
+    const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
     float acc[CH][VEC];
     if (nt <= 1) {
       load_vec<VEC, CH>(a.usum + (size_t)uu * D, D, acc, false);
     } else if (nt <= kWarpMaxParts) {
-      const uint32_t poff = __ldg(a.u_poff + uu);
       const uint32_t tl = lane < nt ? __ldg(a.ptile + poff + lane) : kFull;
       uint32_t r = 0;
 #pragma unroll 8
@@ -798,19 +805,34 @@ __global__ void __launch_bounds__(256) k_finish(ReduceArgs a, OptArgs o) {
       __syncwarp();
       if (lane == 0) a.u_ticket[uu] = 0;
     } else {
+      if (lane == 0) {
+        const uint32_t h = atomicAdd(nhot, 1u);
+        if (h < kHotCap) hot[h] = uu;
+      }
       continue;  // finished below by the whole block
     }
-    finalize<VEC, CH>(a, d, uu, acc, o);
+    if (a.sums_out)
+      store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
+    else
+      apply_row<VEC, CH>(d, row, acc, o);
   }
-  // second pass over this block's ids: the ones with many partials
+  __syncthreads();
+  const uint32_t nh = *nhot;
+  const bool scan = nh > kHotCap;  // overflow: rescan this block's ids (rare)
   for (uint32_t k = 0;; ++k) {
-    const uint32_t w = k % NW, it = k / NW;
-    const uint64_t uu64 = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * (w + (uint64_t)NW * it);
-    if (uu64 >= nu) {
-      if (w == 0) break;
-      continue;
+    uint32_t uu;
+    if (!scan) {
+      if (k >= nh) break;
+      uu = hot[k];
+    } else {
+      const uint32_t w = k % NW, it = k / NW;
+      const uint64_t uu64 = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * (w + (uint64_t)NW * it);
+      if (uu64 >= nu) {
+        if (w == 0) break;
+        continue;
+      }
+      uu = (uint32_t)uu64;
     }
-    const uint32_t uu = (uint32_t)uu64;
     const uint32_t nt = __ldg(a.u_ntile + uu);
     if (nt <= kWarpMaxParts) continue;
     const uint32_t poff = __ldg(a.u_poff + uu);
@@ -989,17 +1011,41 @@ static int opt_args(rs_table* t, const rs_optimizer_params* p, OptArgs* o, cudaS
   return RS_OK;
 }
 
-static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
-                         const OptArgs& o, float* sums_out, cudaStream_t s) {
-  const uint32_t D = t->desc.dim;
-  const uint32_t TT = ws->last_tile;
-  const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
-  // partial sums: at most one per (tile, id) pair <= n; usum: one per id <= n
+// partial sums: at most one per (tile, id) pair <= n; usum: one per id <= n
+static int reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s) {
   if (ws->pbuf_floats < n * D) {
     if (ws->pbuf) RS_CUDA(cudaFreeAsync(ws->pbuf, s));
     ws->pbuf_floats = ws->max_tokens * (uint64_t)D;
     RS_CUDA(cudaMallocAsync(&ws->pbuf, 2 * ws->pbuf_floats * sizeof(float), s));
   }
+  return RS_OK;
+}
+
+// one-time opt-in to large dynamic shared memory for every instantiation
+static int set_smem_attrs() {
+  static int done = 0;
+  if (done) return RS_OK;
+  const int big = 200 * 1024;
+#define RS_ATTR(V, C)                                                                          \
+  RS_CUDA(cudaFuncSetAttribute(k_tile_reduce<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                               big));                                                          \
+  RS_CUDA(cudaFuncSetAttribute(k_finish<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+  RS_ATTR(4, 1) RS_ATTR(4, 2) RS_ATTR(4, 3) RS_ATTR(4, 4)
+  RS_ATTR(2, 1) RS_ATTR(2, 2)
+  RS_ATTR(1, 1) RS_ATTR(1, 2) RS_ATTR(1, 3) RS_ATTR(1, 4) RS_ATTR(1, 5) RS_ATTR(1, 6)
+  RS_ATTR(1, 7) RS_ATTR(1, 8)
+#undef RS_ATTR
+  done = 1;
+  return RS_OK;
+}
+
+static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
+                         const OptArgs& o, float* sums_out, cudaStream_t s) {
+  const uint32_t D = t->desc.dim;
+  const uint32_t TT = ws->last_tile;
+  const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
+  int st = reduce_prepare(ws, D, n, s);
+  if (st) return st;
   ReduceArgs a;
   a.inverse = ws->inverse;
   a.grads = d_grads;
@@ -1021,14 +1067,10 @@ static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, ui
   const uint32_t NW = TT / 32;
   const size_t smem5 = (size_t)TT * D * 4 + 16 + (size_t)(3 * 2 * TT + 4 * TT + 64) * 4 +
                        (size_t)NW * TT * 2 + (size_t)TT * 2 + 16;
-  const size_t smem6 = (size_t)8 * 32 * 4 + (size_t)2 * a.bw * 4 + (size_t)8 * D * 4 + 16;
+  const size_t smem6 = (size_t)8 * 32 * 4 + (kHotCap + 1) * 4 + (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16;
   const Shape sh = shape_for(D);
   const unsigned grid6 = grid_for(n, 8, 148 * 16);
   auto go = [&](auto k5, auto k6) -> int {
-    if (smem5 > 48 * 1024)
-      RS_CUDA(cudaFuncSetAttribute(k5, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem5));
-    if (smem6 > 48 * 1024)
-      RS_CUDA(cudaFuncSetAttribute(k6, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem6));
     k5<<<ntiles, TT, smem5, s>>>(a);
     RS_LAUNCH_CHECK("k_tile_reduce");
     k6<<<grid6, 256, smem6, s>>>(a, o);
@@ -1078,6 +1120,10 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
     rs_workspace_destroy(ws);
     return cuda_fail(cudaGetLastError(), "rs_workspace_create: cudaMalloc");
   }
+  if (set_smem_attrs() != RS_OK || cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    rs_workspace_destroy(ws);
+    return RS_ERR_CUDA;
+  }
   k_dedup_clear_all<<<grid_for(S_ + 1, 256, 148 * 16), 256>>>(ws->skey, ws->sfirstx, ws->scount,
                                                                ws->sntile, S_ + 1);
   count_launch();
@@ -1100,6 +1146,9 @@ int rs_workspace_destroy(rs_workspace* ws) {
                   ws->pbuf,    ws->scan_status, ws->ctr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& g : ws->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (ws->cap_stream) cudaStreamDestroy(ws->cap_stream);
   delete ws;
   return RS_OK;
 }
@@ -1159,11 +1208,101 @@ int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
   return RS_OK;
 }
 
+// All launches of one training step, no host-side work (graph capturable).
+static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                        const float* d_grads, float* d_out, const OptArgs& o, uint32_t TT,
+                        int mirror, cudaStream_t s) {
+  int st = dedup_run(ws, d_ids, n, TT, s);
+  if (st) return st;
+  st = table_upsert_enqueue(t, ws->unique, ws->ctr + 2, n, ws->urow, ws->urow64, ws->u_slot,
+                            ws->srow, s);
+  if (st) return st;
+  st = launch_gather(ws, t, n, d_out, s);
+  if (st) return st;
+  st = launch_reduce(ws, t, d_grads, n, o, nullptr, s);
+  if (st) return st;
+  return table_mirror_copy(t, mirror, s);
+}
+
 int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
             const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream) {
-  int st = rs_forward(ws, t, d_ids, n, d_out, stream);
+  if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_step: null handle");
+  if (t->cfg.max_keys || n == 0 || !ws->use_graphs) {
+    // bounded tables synchronize on the host to evict: no graph
+    int st = rs_forward(ws, t, d_ids, n, d_out, stream);
+    if (st) return st;
+    return rs_backward(ws, t, d_grads, n, opt, stream);
+  }
+  if (n > ws->max_tokens)
+    return fail(RS_ERR_CONFIG, "rs_step: batch exceeds workspace max_tokens");
+  cudaStream_t s = S(stream);
+  OptArgs o;
+  std::memset(&o, 0, sizeof(o));
+  int st = opt_args(t, opt, &o, s);
   if (st) return st;
-  return rs_backward(ws, t, d_grads, n, opt, stream);
+  // host side, outside the graph: capacity bound (may rehash / grow rows on s)
+  st = table_prepare(t, n, s);
+  if (st) return st;
+  const uint32_t TT = tile_tokens_for_dim(t->desc.dim);
+  st = reduce_prepare(ws, t->desc.dim, n, s);
+  if (st) return st;
+  const int mirror = t->mirror_next;
+  static_assert(sizeof(OptArgs) <= sizeof(((rs_graph_entry*)0)->opt), "opt key");
+  rs_graph_entry* hit = nullptr;
+  for (auto& g : ws->graphs) {
+    if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
+        g.mirror == mirror && g.pbuf == ws->pbuf && std::memcmp(g.opt, &o, sizeof(o)) == 0) {
+      hit = &g;
+      break;
+    }
+  }
+  if (!hit) {
+    if (ws->graphs.size() >= 16) {  // evict the least recently used
+      auto lru = std::min_element(ws->graphs.begin(), ws->graphs.end(),
+                                  [](const rs_graph_entry& x, const rs_graph_entry& y) {
+                                    return x.last_use < y.last_use;
+                                  });
+      cudaGraphExecDestroy(lru->exec);
+      ws->graphs.erase(lru);
+    }
+    rs_graph_entry e;
+    e.t = t;
+    e.ids = d_ids;
+    e.grads = d_grads;
+    e.out = d_out;
+    e.n = n;
+    e.mirror = mirror;
+    e.pbuf = ws->pbuf;
+    std::memcpy(e.opt, &o, sizeof(o));
+    cudaStream_t cs = ws->cap_stream;
+    RS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const uint64_t launches_before = launches();
+    st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, TT, mirror, cs);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
+    e.launches = launches() - launches_before;
+    ws->graphs.push_back(e);
+    hit = &ws->graphs.back();
+    // capture only recorded the launches: undo the launch count of the capture
+    count_launch(0 - e.launches);
+  }
+  hit->last_use = ++ws->graph_clock;
+  RS_CUDA(cudaGraphLaunch(hit->exec, s));
+  count_launch(hit->launches);
+  ws->last_n = n;
+  ws->last_tile = TT;
+  ws->last_table = t;
+  ws->have_forward = false;
+  t->applies++;
+  return table_mirror_commit(t, mirror, s);
 }
 
 int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,

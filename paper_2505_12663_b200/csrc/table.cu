@@ -647,6 +647,33 @@ int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n
   return table_after_op(t, s);
 }
 
+// Graph-capturable halves of table_ensure_device (no host work inside).
+int table_upsert_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                         uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                         uint32_t* d_srow, cudaStream_t s) {
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 0, d_rows32, d_rows64, d_uslot, d_srow,
+      nullptr, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert");
+  return RS_OK;
+}
+
+int table_mirror_copy(rs_table* t, int which, cudaStream_t s) {
+  RS_CUDA(cudaMemcpyAsync(t->mirror[which].pinned, &t->dev->c, sizeof(TableCounters),
+                          cudaMemcpyDeviceToHost, s));
+  return RS_OK;
+}
+
+int table_mirror_commit(rs_table* t, int which, cudaStream_t s) {
+  rs_mirror& m = t->mirror[which];
+  RS_CUDA(cudaEventRecord(m.ev, s));
+  m.requested_at_copy = t->requested_total;
+  m.valid = true;
+  t->mirror_next = which ^ 1;
+  t->host_tick++;
+  return RS_OK;
+}
+
 int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies,
                       cudaStream_t s) {
   // bias corrections 1 - beta^step for step in [0, len), host libm pow
