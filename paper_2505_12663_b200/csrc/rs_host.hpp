@@ -85,11 +85,12 @@ struct rs_workspace {
   // cross-tile partial sums
   uint32_t* ptile = nullptr;
   uint32_t* porder = nullptr;
+  uint32_t* hot_list = nullptr;  // ids with > kWarpMaxParts partials (K2)
   float* pbuf = nullptr;
   uint64_t pbuf_floats = 0;
   // scans
   uint64_t* scan_status = nullptr;
-  uint32_t* ctr = nullptr;  // [0] tile ticket [1] blocks done [2] n_unique [3] n_part
+  uint32_t* ctr = nullptr;  // [0] tile ticket [1] blocks done [2] n_unique [3] n_part [4] n_hot
   // last forward
   uint64_t last_n = 0;
   uint32_t last_tile = 0;

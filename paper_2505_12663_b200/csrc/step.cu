@@ -32,6 +32,7 @@ namespace rs {
 namespace {
 
 constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kWarpMaxParts = 32;  // ids with more partials finish block-cooperatively
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
@@ -75,8 +76,10 @@ __global__ void k_dedup_clear_all(unsigned long long* skey, uint32_t* sfirstx, u
 __global__ void k_dedup_tile(const uint64_t* __restrict__ ids, uint32_t n,
                              unsigned long long* __restrict__ skey, uint32_t* __restrict__ sfirstx,
                              uint32_t* __restrict__ scount, uint32_t* __restrict__ sntile,
-                             uint64_t smask, uint64_t spare, uint32_t* __restrict__ slot_of) {
+                             uint64_t smask, uint64_t spare, uint32_t* __restrict__ slot_of,
+                             uint32_t* __restrict__ ctr) {
   extern __shared__ __align__(128) unsigned char smem[];
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr[4] = 0;  // hot-list count, filled by K2
   const uint32_t TT = blockDim.x;
   const uint32_t L = 2 * TT;  // local slots (power of two), index L = sentinel id
   unsigned long long* lkey = reinterpret_cast<unsigned long long*>(smem);
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(kScanThreads)
                     uint64_t* __restrict__ unique, uint32_t* __restrict__ u_slot,
                     uint32_t* __restrict__ u_ntile, uint32_t* __restrict__ u_poff,
                     uint32_t* __restrict__ u_ticket, uint32_t* __restrict__ u_done,
-                    uint64_t* status, uint32_t* ctr, uint32_t ntiles) {
+                    uint64_t* status, uint32_t* ctr, uint32_t ntiles, uint32_t* __restrict__ hot_list) {
   __shared__ uint32_t s_tile;
   __shared__ Pair s_warp[kScanThreads / 32];
   __shared__ Pair s_prefix;
@@ -257,6 +260,7 @@ __global__ void __launch_bounds__(kScanThreads)
       suidx[sl[k]] = ra;
       u_slot[ra] = sl[k];
       u_ntile[ra] = nt[k];
+      if (nt[k] > kWarpMaxParts) hot_list[atomicAdd(&ctr[4], 1u)] = ra;
       u_poff[ra] = run.b;
       u_ticket[ra] = 0;
       u_done[ra] = 0;
@@ -299,42 +303,54 @@ __global__ void k_copy_unique(const uint64_t* __restrict__ src, const uint32_t* 
 }
 
 // ---------------------------------------------------------------------------
-// K4: jagged gather.  LPR lanes per row, float4 per lane, UNR tokens in flight
-// per lane group: the slot -> (unique, row) -> embedding chain is issued for
-// UNR tokens before any store so the dependent loads overlap.
-template <int LPR, int UNR>
-__global__ void __launch_bounds__(256)
+// K4: jagged gather.  A warp takes 32 consecutive tokens: each lane resolves
+// one token's slot -> (unique, row) (coalesced slot_of load, two L2 loads),
+// writes the int32 inverse, then the warp copies the 32 rows with LPR lanes
+// per row and all 128-bit row loads of a batch issued before any store
+// (up to 16 independent LDG.128 in flight per lane).
+template <int LPR>
+__global__ void __launch_bounds__(256, 3)
     k_gather(const uint32_t* __restrict__ slot_of, const uint32_t* __restrict__ suidx,
              const uint32_t* __restrict__ srow, const TableDev* __restrict__ td, uint32_t n,
              int32_t* __restrict__ inverse, float* __restrict__ out) {
-  const uint32_t D = td->d.dim;
-  const uint32_t D4 = D >> 2;
+  constexpr int RPI = 32 / LPR;        // rows per warp instruction
+  constexpr int ITERS = 32 / RPI;      // instructions to cover 32 rows (one float4 per lane each)
+  constexpr int BATCH = ITERS < 8 ? ITERS : 8;
+  const uint32_t D4 = td->d.dim >> 2;
   const float4* __restrict__ emb = reinterpret_cast<const float4*>(td->d.emb);
   float4* __restrict__ o4 = reinterpret_cast<float4*>(out);
-  const uint32_t l = threadIdx.x % LPR;
-  const uint64_t grp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR;
-  const uint64_t ngrp = (uint64_t)gridDim.x * blockDim.x / LPR;
-  for (uint64_t t0 = grp; t0 < n; t0 += ngrp * UNR) {
-    uint32_t u[UNR], r[UNR], s[UNR];
-#pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      const uint64_t t = t0 + (uint64_t)k * ngrp;
-      s[k] = t < n ? __ldg(slot_of + t) : 0;
+  const uint32_t lane = lane_id();
+  const uint32_t sub = lane / LPR, l = lane % LPR;
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t base = w * 32; base < n; base += nw * 32) {
+    const uint64_t t = base + lane;
+    uint32_t u = 0, r = 0;
+    if (t < n) {
+      const uint32_t s = __ldg(slot_of + t);
+      u = __ldcg(suidx + s);
+      r = __ldcg(srow + s);
+      inverse[t] = (int32_t)u;
     }
+    const uint32_t cnt = (n - base) < 32 ? (uint32_t)(n - base) : 32u;
 #pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      const uint64_t t = t0 + (uint64_t)k * ngrp;
-      u[k] = t < n ? __ldcg(suidx + s[k]) : 0;
-      r[k] = t < n ? __ldcg(srow + s[k]) : 0;
-    }
+    for (int b0 = 0; b0 < ITERS; b0 += BATCH) {
+      uint32_t rr[BATCH];
 #pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      const uint64_t t = t0 + (uint64_t)k * ngrp;
-      if (t < n) {
-        if (l == 0) inverse[t] = (int32_t)u[k];
-        const float4* src = emb + (size_t)r[k] * D4;
-        float4* dst = o4 + t * D4;
-        for (uint32_t j = l; j < D4; j += LPR) __stcs(dst + j, __ldg(src + j));
+      for (int k = 0; k < BATCH; ++k) rr[k] = __shfl_sync(kFull, r, (b0 + k) * RPI + sub);
+      for (uint32_t jj = 0; jj < D4; jj += LPR) {  // uniform trip count
+        const uint32_t j = jj + l;
+        float4 v[BATCH];
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+          const uint32_t tok = (b0 + k) * RPI + sub;
+          if (tok < cnt && j < D4) v[k] = __ldg(emb + (size_t)rr[k] * D4 + j);
+        }
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+          const uint32_t tok = (b0 + k) * RPI + sub;
+          if (tok < cnt && j < D4) __stcs(o4 + (base + tok) * D4 + j, v[k]);
+        }
       }
     }
   }
@@ -497,6 +513,8 @@ struct ReduceArgs {
   uint32_t* u_ticket;
   const uint32_t* urow;
   const uint32_t* n_unique;  // device count of the last dedup
+  const uint32_t* n_hot;     // device count of ids with > kWarpMaxParts partials
+  const uint32_t* hot_list;
   float* usum;               // [U x D] sums of single-tile ids
   float* pbuf;               // [n_part x D] per-(tile, id) partial sums
   uint32_t* ptile;           // tile of each partial
@@ -506,8 +524,6 @@ struct ReduceArgs {
   bool tma;
 };
 
-constexpr uint32_t kWarpMaxParts = 32;  // ids with more partials finish block-cooperatively
-constexpr uint32_t kHotCap = 64;        // per-block list of such ids
 
 template <int VEC, int CH>
 __device__ __forceinline__ void zero_acc(float (&x)[CH][VEC]) {
@@ -766,78 +782,56 @@ __global__ void __launch_bounds__(256, 2) k_tile_reduce(ReduceArgs a) {
 }
 
 // K6.  Finish every unique id: combine its partials in tile order, then one
-// optimizer step on its row (or store the aggregated sum).  Warp per id;
-// ids are strided over blocks (hot ids have the lowest first-occurrence
-// indices, this spreads them over SMs).  Ids with more than kWarpMaxParts
-// partials are finished by the whole block with a fixed split over warps.
+// optimizer step on its row (or store the aggregated sum).
+//  blocks [0, hot_blocks): one id with > kWarpMaxParts partials at a time, the
+//    whole block ranks its partials (bitmap over tiles) and splits the ordered
+//    sum over the warps (fixed split -> deterministic)
+//  other blocks: warp per id, no block barriers (ids finish independently)
 template <int VEC, int CH>
-__global__ void __launch_bounds__(256, 3) k_finish(ReduceArgs a, OptArgs o) {
+__global__ void __launch_bounds__(256, 3) k_finish(ReduceArgs a, OptArgs o, uint32_t hot_blocks) {
   extern __shared__ __align__(16) unsigned char smem2[];
   const uint32_t NW = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const TableDesc d = a.td->d;
   const uint32_t D = d.dim;
-  const uint32_t nu = *a.n_unique;
-  uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * 32;  // [NW x 32]
-  uint32_t* hot = reinterpret_cast<uint32_t*>(smem2) + NW * 32;       // [kHotCap]
-  uint32_t* nhot = hot + kHotCap;                                     // [1]
-  uint32_t* bm = nhot + 1;                                            // [bw]
-  uint32_t* wpre = bm + a.bw;                                         // [bw]
-  float* wpart = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(wpre + a.bw) + 15) & ~uintptr_t(15));  // [NW x D], 16B aligned
-  if (threadIdx.x == 0) *nhot = 0;
-  __syncthreads();
-  for (uint32_t uu = blockIdx.x + gridDim.x * warp; uu < nu; uu += gridDim.x * NW) {
-    const uint32_t nt = __ldg(a.u_ntile + uu);
-    const uint32_t poff = __ldg(a.u_poff + uu);
-    const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
-    float acc[CH][VEC];
-    if (nt <= 1) {
-      load_vec<VEC, CH>(a.usum + (size_t)uu * D, D, acc, false);
-    } else if (nt <= kWarpMaxParts) {
-      const uint32_t tl = lane < nt ? __ldg(a.ptile + poff + lane) : kFull;
-      uint32_t r = 0;
+  if (blockIdx.x >= hot_blocks) {
+    uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * 32;  // [NW x 32]
+    const uint32_t nu = *a.n_unique;
+    const uint32_t stride = (gridDim.x - hot_blocks) * NW;
+    for (uint32_t uu = (blockIdx.x - hot_blocks) * NW + warp; uu < nu; uu += stride) {
+      const uint32_t nt = __ldg(a.u_ntile + uu);
+      if (nt > kWarpMaxParts) continue;
+      const uint32_t poff = __ldg(a.u_poff + uu);
+      const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
+      float acc[CH][VEC];
+      if (nt <= 1) {
+        load_vec<VEC, CH>(a.usum + (size_t)uu * D, D, acc, false);
+      } else {
+        const uint32_t tl = lane < nt ? __ldg(a.ptile + poff + lane) : kFull;
+        uint32_t r = 0;
 #pragma unroll 8
-      for (uint32_t j = 0; j < nt; ++j) r += __shfl_sync(kFull, tl, j) < tl;
-      if (lane < nt) order_w[r] = lane;
-      __syncwarp();
-      ordered_sum<VEC, CH>(a, order_w, poff, 0, nt, D, acc);
-      __syncwarp();
-      if (lane == 0) a.u_ticket[uu] = 0;
-    } else {
-      if (lane == 0) {
-        const uint32_t h = atomicAdd(nhot, 1u);
-        if (h < kHotCap) hot[h] = uu;
+        for (uint32_t j = 0; j < nt; ++j) r += __shfl_sync(kFull, tl, j) < tl;
+        if (lane < nt) order_w[r] = lane;
+        __syncwarp();
+        ordered_sum<VEC, CH>(a, order_w, poff, 0, nt, D, acc);
+        __syncwarp();
+        if (lane == 0) a.u_ticket[uu] = 0;
       }
-      continue;  // finished below by the whole block
+      if (a.sums_out)
+        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
+      else
+        apply_row<VEC, CH>(d, row, acc, o);
     }
-    if (a.sums_out)
-      store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
-    else
-      apply_row<VEC, CH>(d, row, acc, o);
+    return;
   }
-  __syncthreads();
-  const uint32_t nh = *nhot;
-  const bool scan = nh > kHotCap;  // overflow: rescan this block's ids (rare)
-  for (uint32_t k = 0;; ++k) {
-    uint32_t uu;
-    if (!scan) {
-      if (k >= nh) break;
-      uu = hot[k];
-    } else {
-      const uint32_t w = k % NW, it = k / NW;
-      const uint64_t uu64 = (uint64_t)blockIdx.x + (uint64_t)gridDim.x * (w + (uint64_t)NW * it);
-      if (uu64 >= nu) {
-        if (w == 0) break;
-        continue;
-      }
-      uu = (uint32_t)uu64;
-    }
-    const uint32_t nt = __ldg(a.u_ntile + uu);
-    if (nt <= kWarpMaxParts) continue;
-    const uint32_t poff = __ldg(a.u_poff + uu);
-    __syncthreads();
-    // rank the partials by tile index: block-wide bitmap + prefix popcounts
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem2);  // [bw]
+  uint32_t* wpre = bm + a.bw;                          // [bw]
+  float* wpart = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(wpre + a.bw) + 15) & ~uintptr_t(15));  // [NW x D]
+  const uint32_t nh = *a.n_hot;
+  for (uint32_t h = blockIdx.x; h < nh; h += hot_blocks) {
+    const uint32_t uu = a.hot_list[h];
+    const uint32_t nt = __ldg(a.u_ntile + uu), poff = __ldg(a.u_poff + uu);
     for (uint32_t i = threadIdx.x; i < a.bw; i += blockDim.x) bm[i] = 0;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
@@ -883,7 +877,10 @@ __global__ void __launch_bounds__(256, 3) k_finish(ReduceArgs a, OptArgs o) {
         add_acc<VEC, CH>(tot, x);
       }
       if (lane == 0) a.u_ticket[uu] = 0;
-      finalize<VEC, CH>(a, d, uu, tot, o);
+      if (a.sums_out)
+        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, tot);
+      else
+        apply_row<VEC, CH>(d, __ldg(a.urow + uu), tot, o);
     }
     __syncthreads();
   }
@@ -942,13 +939,13 @@ int dedup_run(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint32_t TT, 
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   const size_t sm1 = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4);
   k_dedup_tile<<<ntiles, TT, sm1, s>>>(d_ids, (uint32_t)n, ws->skey, ws->sfirstx, ws->scount,
-                                       ws->sntile, ws->S - 1, ws->S, ws->slot_of);
+                                       ws->sntile, ws->S - 1, ws->S, ws->slot_of, ws->ctr);
   RS_LAUNCH_CHECK("k_dedup_tile");
   const uint32_t stiles = (uint32_t)((n + kScanTile - 1) / kScanTile);
   k_dedup_compact<<<stiles, kScanThreads, 0, s>>>(
       d_ids, (uint32_t)n, ws->slot_of, ws->sfirstx, ws->sntile, ws->suidx, ws->unique,
       ws->u_slot, ws->u_ntile, ws->u_poff, ws->u_ticket, ws->u_done, ws->scan_status, ws->ctr,
-      stiles);
+      stiles, ws->hot_list);
   RS_LAUNCH_CHECK("k_dedup_compact");
   ws->last_tile = TT;
   return RS_OK;
@@ -959,10 +956,10 @@ static int launch_gather(rs_workspace* ws, rs_table* t, uint64_t n, float* d_out
   const uint32_t D = t->desc.dim;
   if (D % 4 == 0) {
     const uint32_t d4 = D / 4;
-    const unsigned grid = grid_for(n, 256 / std::min<uint32_t>(32, d4) * 4, 148 * 8);
+    const unsigned grid = grid_for(n, 256, 148 * 16);
 #define RS_GATHER(LPR)                                                                      \
-  k_gather<LPR, 4><<<grid, 256, 0, s>>>(ws->slot_of, ws->suidx, ws->srow, t->dev, (uint32_t)n, \
-                                        ws->inverse, d_out)
+  k_gather<LPR><<<grid, 256, 0, s>>>(ws->slot_of, ws->suidx, ws->srow, t->dev, (uint32_t)n, \
+                                     ws->inverse, d_out)
     if (d4 >= 32)
       RS_GATHER(32);
     else if (d4 >= 16)
@@ -1057,6 +1054,8 @@ static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, ui
   a.u_ticket = ws->u_ticket;
   a.urow = ws->urow;
   a.n_unique = ws->ctr + 2;
+  a.n_hot = ws->ctr + 4;
+  a.hot_list = ws->hot_list;
   a.pbuf = ws->pbuf;
   a.usum = ws->pbuf + ws->pbuf_floats;
   a.ptile = ws->ptile;
@@ -1067,13 +1066,14 @@ static int launch_reduce(rs_workspace* ws, rs_table* t, const float* d_grads, ui
   const uint32_t NW = TT / 32;
   const size_t smem5 = (size_t)TT * D * 4 + 16 + (size_t)(3 * 2 * TT + 4 * TT + 64) * 4 +
                        (size_t)NW * TT * 2 + (size_t)TT * 2 + 16;
-  const size_t smem6 = (size_t)8 * 32 * 4 + (kHotCap + 1) * 4 + (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16;
+  const size_t smem6 = std::max<size_t>((size_t)8 * 32 * 4, (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
+  const uint32_t hot_blocks = 2 * 148;
   const Shape sh = shape_for(D);
-  const unsigned grid6 = grid_for(n, 8, 148 * 16);
+  const unsigned grid6 = hot_blocks + grid_for(n, 8, 148 * 24);
   auto go = [&](auto k5, auto k6) -> int {
     k5<<<ntiles, TT, smem5, s>>>(a);
     RS_LAUNCH_CHECK("k_tile_reduce");
-    k6<<<grid6, 256, smem6, s>>>(a, o);
+    k6<<<grid6, 256, smem6, s>>>(a, o, hot_blocks);
     RS_LAUNCH_CHECK("k_finish");
     return RS_OK;
   };
@@ -1114,7 +1114,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
             A(&ws->slot_of, N * 4) && A(&ws->inverse, N * 4) && A(&ws->unique, N * 8) &&
             A(&ws->u_slot, N * 4) && A(&ws->u_ntile, N * 4) && A(&ws->u_poff, N * 4) &&
             A(&ws->u_ticket, N * 4) && A(&ws->u_done, N * 4) && A(&ws->urow, N * 4) &&
-            A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) && A(&ws->porder, N * 4) &&
+            A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) && A(&ws->porder, N * 4) && A(&ws->hot_list, (N / 32 + 64) * 4) &&
             A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64);
   if (!ok) {
     rs_workspace_destroy(ws);
@@ -1143,7 +1143,7 @@ int rs_workspace_destroy(rs_workspace* ws) {
   void* ptrs[] = {ws->skey,    ws->sfirstx, ws->scount,  ws->sntile,   ws->suidx,  ws->srow,
                   ws->slot_of, ws->inverse, ws->unique,  ws->u_slot,   ws->u_ntile, ws->u_poff,
                   ws->u_ticket, ws->u_done, ws->urow,    ws->urow64,   ws->ptile,  ws->porder,
-                  ws->pbuf,    ws->scan_status, ws->ctr};
+                  ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : ws->graphs)
