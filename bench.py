@@ -154,21 +154,24 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
 
-    # ---- device-timed steps (inputs resident in HBM, L2 flushed between steps)
-    times, uniq, toks = [], 0, 0
+    # ---- device-timed steps (inputs resident in HBM, L2 flushed between
+    # steps).  All K steps are enqueued back to back; each step is bracketed
+    # by its own CUDA events, the flush in between is outside the brackets.
+    uniq_per_batch = [int(np.unique(ids).size) for _, ids in batches]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.rs_kernel_launches()
     with Clocks(local) as clk:
         for k in range(args.steps):
             flush.zero_()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
+            evs[k][0].record(stream)
             one(args.warmup + k)
-            e.record(stream)
-            e.synchronize()
-            times.append(s.elapsed_time(e))
-            uniq += _n_unique(step)
-            toks += dev[(args.warmup + k) % nb][0].numel()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
+    times = [a.elapsed_time(b) for a, b in evs]
+    uniq = sum(uniq_per_batch[(args.warmup + k) % nb] for k in range(args.steps))
+    toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
+    assert _n_unique(step) == uniq_per_batch[(args.warmup + args.steps - 1) % nb], "device n_unique mismatch"
     t_sum = sum(times) / 1e3
     if world > 1:
         tt = torch.tensor([t_sum], dtype=torch.float64, device="cuda")
@@ -186,17 +189,18 @@ def run_ours(args, cfg):
     # ---- end to end through the public API with HOST buffers
     e2e = e2e_pass(args, cfg, batches, step, P, W, rank)
 
-    # ---- roofline of the dominant kernel (segment-reduce + Adagrad)
+    # ---- roofline of the dominant kernel: algorithmic bytes per launch / its
+    # CUDA-event duration (bytes per unit: SURVEY.md §8d)
     hbm, how = peaks()
     D = dim
     T_avg, U_avg = toks / args.steps, uniq / args.steps
     algo = {
-        "reduce_update": 4 * D * T_avg + 16 * D * U_avg,
-        "gather": 4 * D * T_avg + 4 * D * U_avg,
         "dedup": 12 * T_avg + 8 * U_avg,
         "table": 16 * U_avg,
+        "gather_reduce": 8 * D * T_avg + 4 * D * U_avg,
+        "finish_update": 16 * D * U_avg + 8 * U_avg,
     }
-    dom = "reduce_update"
+    dom = max(phases, key=lambda k: phases[k])
     ach = algo[dom] / (phases[dom] / 1e3) / 1e9 if phases.get(dom) else None
     step_bytes = 12 * T_avg + 24 * U_avg + 8 * D * T_avg + 20 * D * U_avg
     res = {
@@ -221,7 +225,8 @@ def run_ours(args, cfg):
         "step_hbm_gbs": step_bytes * world / (t_job / args.steps) / 1e9,
         "step_roofline_frac": step_bytes / (t_job / args.steps) / 1e9 / hbm,
         "kernel_ms": phases,
-        "roofline": {"bound": "hbm", "kernel": "k_reduce_update (segment-reduce + Adagrad)",
+        "kernel_gbs": {k: (algo[k] / (phases[k] / 1e3) / 1e9 if phases[k] else None) for k in algo},
+        "roofline": {"bound": "hbm", "kernel": dom,
                      "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if ach else None,
                      "traffic": None, "peak_source": how,
                      "algorithmic_bytes_per_launch": algo[dom]},
@@ -247,28 +252,26 @@ def _n_unique(step):
     return n.value
 
 
+PHASES = ["dedup", "table", "gather_reduce", "finish_update"]
+
+
 def phase_times(step, dev, nb, args, flush, P):
-    """Average device time per kernel group, CUDA events on the launching stream
-    (forward: dedup+table+gather measured by splitting forward/backward)."""
-    import torch
-    stream = torch.cuda.current_stream()
-    acc = {"forward": 0.0, "reduce_update": 0.0}
+    """Mean device time per kernel group of rs_step, from CUDA events recorded
+    by librsgpu on the launching stream between the kernels (profiling mode
+    runs the same kernels without the graph)."""
+    import ctypes
+    lib = P.lib()
+    P._lib.check(lib.rs_workspace_set_profiling(step.ws.handle, 1), "profiling")
     reps = max(3, min(args.steps, 10))
     for k in range(reps):
         d_ids, d_g, out = dev[k % nb]
         flush.zero_()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-        ev[0].record(stream)
-        step.forward(d_ids, out)
-        ev[1].record(stream)
-        step.backward(d_g)
-        ev[2].record(stream)
-        ev[2].synchronize()
-        acc["forward"] += ev[0].elapsed_time(ev[1])
-        acc["reduce_update"] += ev[1].elapsed_time(ev[2])
-    res = {k: v / reps for k, v in acc.items()}
-    # gather alone: re-run the forward's last kernel shape via lookup of the same rows
-    return res
+        step.step(d_ids, d_g, out)
+    ms = (ctypes.c_double * 8)()
+    cnt = ctypes.c_uint64()
+    P._lib.check(lib.rs_workspace_phase_ms(step.ws.handle, ms, 8, ctypes.byref(cnt)), "phase_ms")
+    P._lib.check(lib.rs_workspace_set_profiling(step.ws.handle, 0), "profiling")
+    return {name: ms[i] for i, name in enumerate(PHASES)}
 
 
 def e2e_pass(args, cfg, batches, step, P, W, rank):
@@ -287,8 +290,9 @@ def e2e_pass(args, cfg, batches, step, P, W, rank):
     d_ids = torch.empty(max_t, dtype=torch.int64, device="cuda")
     d_g = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
     d_out = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
-    times, uniq, h2d, d2h = [], 0, 0, 0
     n = max(3, min(args.steps, 10))
+    uniq_b = [int(np.unique(ids).size) for _, ids in batches]
+    evs = []
     for k in range(n + 2):
         h_ids, g, h_out = host[k % len(host)]
         T = h_ids.numel()
@@ -299,12 +303,15 @@ def e2e_pass(args, cfg, batches, step, P, W, rank):
         step.step(d_ids[:T], d_g[:T], d_out[:T])
         h_out.copy_(d_out[:T], non_blocking=True)
         e.record(stream)
-        e.synchronize()
-        if k >= 2:
-            times.append(s.elapsed_time(e))
-            uniq += _n_unique(step)
-            h2d += h_ids.numel() * 8 + g.numel() * 4
-            d2h += h_out.numel() * 4
+        evs.append((s, e, k))
+    torch.cuda.synchronize()
+    times, uniq, h2d, d2h = [], 0, 0, 0
+    for s, e, k in evs[2:]:
+        h_ids, g, h_out = host[k % len(host)]
+        times.append(s.elapsed_time(e))
+        uniq += uniq_b[k % len(host)]
+        h2d += h_ids.numel() * 8 + g.numel() * 4
+        d2h += h_out.numel() * 4
     t = sum(times) / 1e3
     return {"value": uniq / t, "unit": "unique-ids/s", "h2d_bytes_per_step": h2d // n, "d2h_bytes_per_step": d2h // n,
             "ms_per_step": t / n * 1e3}

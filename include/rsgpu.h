@@ -153,9 +153,19 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
  * optimizer.  No gather. */
 int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
                      const float* d_grads, const rs_optimizer_params* opt, void* stream);
+/* Unique ids of the last forward / sparse update / dedup on this workspace,
+ * in the order of its internal unique index (the index of rs_accumulate's
+ * rows).  The fused step numbers ids in an unspecified order; rs_dedup's is
+ * first-occurrence.  d_out may be NULL to query *n_out.  Synchronizes. */
+int rs_workspace_unique(rs_workspace* ws, uint64_t* d_out, uint64_t cap, uint64_t* n_out);
 /* Results of the last forward on this workspace (device pointers owned by ws). */
 int rs_workspace_results(rs_workspace* ws, const uint64_t** d_unique, const int32_t** d_inverse,
                          const uint32_t** d_n_unique, const int64_t** d_rows);
+/* Per-kernel CUDA-event timing of rs_step (diagnostic; disables graph
+ * capture).  Phases: 0 dedup, 1 table find-or-insert, 2 gather, 3 tile
+ * reduce, 4 finish + optimizer.  rs_workspace_phase_ms returns the mean ms. */
+int rs_workspace_set_profiling(rs_workspace* ws, int on);
+int rs_workspace_phase_ms(rs_workspace* ws, double* ms, uint32_t nphases, uint64_t* count);
 /* n_unique of the last dedup on this workspace (host value).  Synchronizes. */
 int rs_workspace_n_unique(rs_workspace* ws, uint64_t* out);
 /* GradAccumulator::accumulate for one micro-batch (sparse_update.cpp:45-56):

@@ -49,6 +49,7 @@ struct rs_graph_entry {
   void* out = nullptr;
   uint64_t n = 0;
   int mirror = 0;
+  int set = 0;
   const void* pbuf = nullptr;
   unsigned char opt[128] = {0};
   cudaGraphExec_t exec = nullptr;
@@ -56,41 +57,54 @@ struct rs_graph_entry {
   uint64_t launches = 0;  // rsgpu kernels inside the graph
 };
 
+// One dedup scratch hash set (SoA, S+1 slots; slot S holds the id equal to
+// the empty sentinel).  Two sets alternate between calls: each call uses the
+// clean set and cleans the other one (the previous call's) in its kernels,
+// from the dirty list u_slot[0, cnt).
+struct rs_scratch {
+  unsigned long long* skey = nullptr;
+  uint32_t* sfirstx = nullptr;  // ~first position (exact dedup)
+  uint32_t* sntile = nullptr;   // tiles containing the id
+  uint32_t* suidx = nullptr;    // unique index of the slot
+  uint32_t* srow = nullptr;     // table row of the slot
+  uint32_t* u_slot = nullptr;   // slot of each unique id (dirty list)
+  uint32_t* cnt = nullptr;      // device [0] = unique ids in the set
+};
+
 struct rs_workspace {
   uint64_t max_tokens = 0;
+  uint64_t S = 0;  // scratch hash capacity (power of two)
+  rs_scratch set[2];
+  int cur = 0;       // clean set the next call uses
+  int last_set = 0;  // set used by the last call (its results)
   cudaStream_t cap_stream = nullptr;  // capture stream for the step graphs
   std::vector<rs_graph_entry> graphs;
   uint64_t graph_clock = 0;
   bool use_graphs = true;
-  uint64_t S = 0;  // scratch hash capacity (power of two); index S is the spare slot
-  // dedup scratch set (SoA, S+1 entries)
-  unsigned long long* skey = nullptr;
-  uint32_t* sfirstx = nullptr;  // ~first position (atomicMax)
-  uint32_t* scount = nullptr;
-  uint32_t* sntile = nullptr;
-  uint32_t* suidx = nullptr;
-  uint32_t* srow = nullptr;
+  // optional per-kernel CUDA-event timing (forces the non-graph path)
+  bool profiling = false;
+  cudaEvent_t prof_ev[8] = {nullptr};
+  double prof_ms[8] = {0};
+  uint64_t prof_count = 0;
   // per token
   uint32_t* slot_of = nullptr;
   int32_t* inverse = nullptr;
   // per unique
   uint64_t* unique = nullptr;
-  uint32_t* u_slot = nullptr;
   uint32_t* u_ntile = nullptr;
   uint32_t* u_poff = nullptr;
   uint32_t* u_ticket = nullptr;
-  uint32_t* u_done = nullptr;
   uint32_t* urow = nullptr;
   int64_t* urow64 = nullptr;
   // cross-tile partial sums
   uint32_t* ptile = nullptr;
   uint32_t* porder = nullptr;
-  uint32_t* hot_list = nullptr;  // ids with > kWarpMaxParts partials (K2)
-  float* pbuf = nullptr;
+  uint32_t* hot_list = nullptr;  // ids with > kWarpMaxParts partials (KB)
+  float* pbuf = nullptr;         // [pbuf_floats partials | pbuf_floats usum]
   uint64_t pbuf_floats = 0;
   // scans
   uint64_t* scan_status = nullptr;
-  uint32_t* ctr = nullptr;  // [0] tile ticket [1] blocks done [2] n_unique [3] n_part [4] n_hot
+  uint32_t* ctr = nullptr;  // [0] tile ticket [1] blocks done [4] n_hot [5] partial alloc
   // last forward
   uint64_t last_n = 0;
   uint32_t last_tile = 0;
@@ -115,7 +129,5 @@ int table_mirror_copy(rs_table* t, int which, cudaStream_t s);
 int table_mirror_commit(rs_table* t, int which, cudaStream_t s);
 int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies, cudaStream_t s);
 // step.cu
-int dedup_run(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint32_t tile,
-              cudaStream_t s);
 uint32_t tile_tokens_for_dim(uint32_t dim);
 }  // namespace rs

@@ -1,0 +1,167 @@
+// table_dev.cuh -- device building blocks of the dynamic table shared by the
+// table kernels (table.cu) and the fused step kernels (step.cu): grouped
+// bucket probing, the lock-free row allocator, row initialisation and the
+// last-block counter epilogue.  See table.cu for the reference mapping.
+#pragma once
+
+#include "rs_internal.cuh"
+
+namespace rs {
+namespace tdev {
+
+constexpr unsigned kGroupsPerBlock = 32;  // 8-lane groups per 256-thread block
+constexpr unsigned kProbeThreads = kGroupsPerBlock * kBucket;
+
+__device__ __forceinline__ uint4 ld_slot_cg(const Slot* p) {
+  return __ldcg(reinterpret_cast<const uint4*>(p));
+}
+__device__ __forceinline__ uint4 ld_slot(const Slot* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+
+struct Probe {
+  bool found;
+  uint64_t slot;      // slot of the key when found
+  uint32_t row;       // row when found
+  uint32_t tick;      // slot tick when found
+  uint64_t ins;       // insertion slot when not found (~0 = table full)
+  bool ins_tomb;      // insertion slot is a tombstone
+};
+
+// Cooperative probe by the 8 lanes of a group.  `g` = lane within the group,
+// `gbase` = first warp lane of the group, `gmask` = the group's lane mask.
+template <bool kCoherent>
+__device__ __forceinline__ Probe probe_group(const Slot* __restrict__ slots, uint64_t nb_mask,
+                                             uint64_t key, unsigned g, unsigned gbase,
+                                             unsigned gmask) {
+  const uint64_t h = hash64(key);
+  uint64_t b = (h >> 32) & nb_mask;  // high hash bits: decorrelated from shard_of = h % W
+  const uint64_t step = (h | 1ull) & nb_mask;  // odd -> full cycle over nb = 2^k buckets
+  uint64_t tomb = ~0ull;
+  Probe r;
+  r.found = false;
+  r.ins = ~0ull;
+  r.ins_tomb = false;
+  r.row = kNoRow;
+  r.tick = 0;
+  r.slot = ~0ull;
+  for (uint64_t t = 0; t <= nb_mask; ++t) {
+    const uint4 v = kCoherent ? ld_slot_cg(slots + b * kBucket + g) : ld_slot(slots + b * kBucket + g);
+    const uint64_t k = (uint64_t)v.x | ((uint64_t)v.y << 32);
+    const unsigned bm = (__ballot_sync(gmask, k == key) >> gbase) & 0xFFu;
+    const unsigned be = (__ballot_sync(gmask, k == kEmptyKey) >> gbase) & 0xFFu;
+    const unsigned bt = (__ballot_sync(gmask, k == kTombKey) >> gbase) & 0xFFu;
+    if (bm) {
+      const unsigned l = __ffs(bm) - 1;
+      r.found = true;
+      r.slot = b * kBucket + l;
+      r.row = __shfl_sync(gmask, v.z, gbase + l);
+      r.tick = __shfl_sync(gmask, v.w, gbase + l);
+      return r;
+    }
+    if (tomb == ~0ull && bt) tomb = b * kBucket + (__ffs(bt) - 1);
+    if (be) {
+      r.ins = tomb != ~0ull ? tomb : b * kBucket + (__ffs(be) - 1);
+      r.ins_tomb = tomb != ~0ull;
+      return r;
+    }
+    b = (b + step) & nb_mask;
+  }
+  r.ins = tomb;
+  r.ins_tomb = tomb != ~0ull;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t alloc_row(TableDev* td, unsigned long long free_n0,
+                                              unsigned long long fresh0, uint64_t row_cap) {
+  const unsigned long long i = atomicAdd(&td->c.alloc_ctr, 1ull);
+  if (i < free_n0) return td->d.free_stack[free_n0 - 1 - i];  // LIFO reuse first
+  const unsigned long long r = fresh0 + (i - free_n0);
+  if (r >= row_cap) {
+    atomicOr(&td->c.error, kErrRowPool);
+    return kNoRow;
+  }
+  return (uint32_t)r;
+}
+
+// New-row initialisation by the 8 lanes of a group: emb from src (or zeros),
+// optimizer state zeroed (alloc_row + reset_row, embed_table.cpp:144-180).
+__device__ __forceinline__ void init_row(const TableDesc& d, uint32_t row, const float* src,
+                                         unsigned g) {
+  const uint32_t D = d.dim;
+  float* e = d.emb + (size_t)row * D;
+  if ((D & 3u) == 0) {
+    const uint32_t D4 = D >> 2;
+    for (uint32_t i = g; i < D4; i += kBucket) {
+      float4 v = src ? reinterpret_cast<const float4*>(src)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(e)[i] = v;
+      if (d.s1) reinterpret_cast<float4*>(d.s1 + (size_t)row * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (d.s2) reinterpret_cast<float4*>(d.s2 + (size_t)row * D)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  } else {
+    for (uint32_t i = g; i < D; i += kBucket) {
+      e[i] = src ? src[i] : 0.f;
+      if (d.s1) d.s1[(size_t)row * D + i] = 0.f;
+      if (d.s2) d.s2[(size_t)row * D + i] = 0.f;
+    }
+  }
+  if (g == 0) d.step[row] = 0;
+}
+
+__device__ __forceinline__ void copy_row_group(const TableDesc& d, uint32_t row, float* dst,
+                                               unsigned g) {
+  const uint32_t D = d.dim;
+  const float* e = d.emb + (size_t)row * D;
+  if ((D & 3u) == 0) {
+    for (uint32_t i = g; i < (D >> 2); i += kBucket)
+      reinterpret_cast<float4*>(dst)[i] = __ldg(reinterpret_cast<const float4*>(e) + i);
+  } else {
+    for (uint32_t i = g; i < D; i += kBucket) dst[i] = e[i];
+  }
+}
+
+// Last-block epilogue: folds this launch's per-launch counters into the
+// table counters (the "fix-up" of the lock-free row allocator).
+__device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
+                                                unsigned long long fresh0, bool bump_tick,
+                                                uint32_t tick_now) {
+  __syncthreads();
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&td->c.blocks_done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    TableCounters& c = td->c;
+    const unsigned long long used = c.alloc_ctr;
+    if (used <= free_n0) {
+      c.free_n = free_n0 - used;
+    } else {
+      c.free_n = 0;
+      unsigned long long f = fresh0 + (used - free_n0);
+      c.fresh_next = f > td->d.row_cap ? td->d.row_cap : f;
+    }
+    // removals push rows above free_n0 (remove kernel); fold them in
+    c.free_n += c.removed;
+    c.occupied = c.occupied + c.inserted - c.removed;
+    c.tombstones = c.tombstones - c.reused + c.removed;
+    c.alloc_ctr = 0;
+    c.inserted = 0;
+    c.reused = 0;
+    c.removed = 0;
+    if (bump_tick) c.tick = tick_now;
+    c.blocks_done = 0;
+    __threadfence();
+  }
+}
+
+// Keys equal to the two sentinels live in the descriptor (rare path).
+__device__ __forceinline__ int special_index(uint64_t key) {
+  return key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
+}
+
+
+}  // namespace tdev
+}  // namespace rs

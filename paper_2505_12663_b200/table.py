@@ -283,6 +283,14 @@ class SparseStep:
                               _ptr(out), C.byref(self.params.c()), _stream()), "step")
         return out
 
+    def last_unique(self) -> torch.Tensor:
+        """unique ids of the last forward, indexed like accumulate()'s rows."""
+        n = C.c_uint64()
+        check(L.lib().rs_workspace_unique(self.ws.handle, None, 0, C.byref(n)), "last_unique")
+        out = torch.empty(max(n.value, 1), dtype=torch.int64, device="cuda")
+        check(L.lib().rs_workspace_unique(self.ws.handle, _ptr(out), out.numel(), C.byref(n)), "last_unique")
+        return out[: n.value]
+
     def accumulate(self, grads: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
         """aggregated grads of the last forward's unique ids (first-occurrence order)."""
         g = grads.contiguous()

@@ -210,19 +210,22 @@ def test_step_vs_oracle(cuda, oracle, dim, opt):
         want_out = np.zeros((len(batch), dim), np.float32)
         oracle.table_lookup_batch(ot.h, batch, len(batch), want_out.reshape(-1))
         np.testing.assert_array_equal(out.cpu().numpy(), want_out)
-        # dedup results
+        # aggregated grads (rows indexed like step.last_unique()): tolerance
+        # against the sequential f32 sums of the reference
         u, inv = oracle.stage1(batch)
         nu = len(u)
-        # aggregated grads: tolerance vs the sequential f32 sums of the reference
+        gpu_ids = P.keys_to_numpy(step.last_unique())
+        assert len(gpu_ids) == nu and np.array_equal(np.sort(gpu_ids), np.sort(u))
         g_np = grads.cpu().numpy()
         ids_acc, sums_ref = oracle.accumulate_np(batch, g_np, dim)
-        order = np.argsort(u)
+        order = np.argsort(gpu_ids)
         sums_gpu = sums[:nu].cpu().numpy()[order]
-        np.testing.assert_array_equal(ids_acc, u[order])
+        np.testing.assert_array_equal(ids_acc, gpu_ids[order])
         absmass = np.zeros((nu, dim), np.float64)
         np.add.at(absmass, inv, np.abs(g_np).astype(np.float64))
+        mass_sorted = absmass[np.argsort(u)]
         err = np.abs(sums_gpu.astype(np.float64) - sums_ref)
-        assert (err <= GRAD_TOL * absmass[order] + 1e-30).all(), err.max()
+        assert (err <= GRAD_TOL * mass_sorted + 1e-30).all(), err.max()
         # optimizer bit-exact given the GPU's aggregated grads (oracle apply)
         oracle.apply(ot.h, ids_acc, np.ascontiguousarray(sums_gpu).reshape(-1), nu,
                      1 if opt == "adagrad" else 0, params.lr, getattr(params, "beta1", 0.9),
