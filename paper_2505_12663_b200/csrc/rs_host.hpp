@@ -78,6 +78,8 @@ struct rs_workspace {
   int cur = 0;       // clean set the next call uses
   int last_set = 0;  // set used by the last call (its results)
   cudaStream_t cap_stream = nullptr;  // capture stream for the step graphs
+  cudaStream_t aux_stream = nullptr;  // forked branch of the step (reserved)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<rs_graph_entry> graphs;
   uint64_t graph_clock = 0;
   bool use_graphs = true;
@@ -100,6 +102,8 @@ struct rs_workspace {
   uint32_t* ptile = nullptr;
   uint32_t* porder = nullptr;
   uint32_t* hot_list = nullptr;  // ids with > kWarpMaxParts partials (KB)
+  uint32_t* u_cnt = nullptr;     // occurrences per unique id
+  uint32_t* csr_pos = nullptr;   // token positions grouped by id (CSR path)
   float* pbuf = nullptr;         // [pbuf_floats partials | pbuf_floats usum]
   uint64_t pbuf_floats = 0;
   // scans

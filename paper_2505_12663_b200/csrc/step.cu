@@ -15,11 +15,13 @@
 //                 slots of the previous call (double-buffered scratch)
 //   KC k_ftile    per tile: jagged gather out[t] = emb[row(t)] (128-bit row
 //                 copies, 8 in flight per lane) fused with the segment
-//                 reduce: TMA bulk copy (cp.async.bulk -> UBLKCP) of the
-//                 tile's gradient rows into smem, smem grouping, position-order
-//                 sums; single-tile ids -> usum, multi-tile ids -> partial
-//                 tagged with its tile
-//   KD k_finish   per id: partials combined in tile order, one optimizer
+//                 reduce bookkeeping: tokens of ids with <= kCsrMax
+//                 occurrences go into the id's CSR segment; tokens of hot ids
+//                 are summed per (tile, id) in position order from a TMA bulk
+//                 copy (cp.async.bulk -> UBLKCP) of the tile's gradient rows
+//   KD k_finish   per id: CSR ids sort their positions and sum the gradient
+//                 rows in the reference's token order (bit-exact); hot ids
+//                 combine their tile partials in tile order; then one optimizer
 //                 step per row (FP64, explicit _rn, no FMA)
 // The internal unique numbering of the fast step is unspecified (atomic);
 // the exact first-occurrence dedup of stage1_dedup (exchange_sim.cpp:87-98)
@@ -39,10 +41,10 @@ namespace {
 using namespace odev;
 using namespace tdev;
 
-constexpr uint32_t kWarpMaxParts = 32;  // ids with more partials finish block-cooperatively
+constexpr uint32_t kCsrMax = 64;  // ids with at most this many occurrences: exact-order CSR path
 
 // ctr[] slots of the workspace counter block
-enum : int { kCtrTicket = 0, kCtrDone = 1, kCtrNHot = 4, kCtrPartAlloc = 5 };
+enum : int { kCtrTicket = 0, kCtrDone = 1, kCtrNHot = 4, kCtrPartAlloc = 5, kCtrCsrAlloc = 6 };
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
@@ -60,7 +62,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // Device view of one scratch set (see rs_scratch in rs_host.hpp).
 struct SetDev {
   unsigned long long* skey;
-  uint32_t* sfirstx;  // ~first position (exact dedup only)
+  uint32_t* sfirstx;  // exact dedup: ~first position; fast step: occurrence count
   uint32_t* sntile;   // tiles containing the id
   uint32_t* suidx;    // unique index of the slot
   uint32_t* srow;     // table row of the slot
@@ -165,15 +167,18 @@ __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n, SetDev S,
   lt.first = reinterpret_cast<uint32_t*>(lt.key + L + 1);
   lt.gslot = lt.first + L + 1;
   uint32_t* lnew = lt.gslot + L + 1;  // [L + 1] local index of new ids (+1), 0 = not new
+  uint32_t* lcnt = lnew + L + 1;      // [L + 1] occurrences of the id in the tile
   __shared__ uint32_t s_nnew, s_base;
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0) {
     ctr[kCtrNHot] = 0;       // filled by KB
+    ctr[kCtrCsrAlloc] = 0;
     ctr[kCtrPartAlloc] = 0;  // partial segments, allocated by KB
   }
   for (uint32_t i = tid; i <= L; i += TT) {
     lt.key[i] = kEmptyKey;
     lnew[i] = 0;
+    lcnt[i] = 0;
   }
   if (tid == 0) s_nnew = 0;
   __syncthreads();
@@ -186,12 +191,14 @@ __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n, SetDev S,
     id = ids[t];
     h = hash64(id);
     p = local_insert(lt, id, h, tid, false, &rep);
+    atomicAdd(&lcnt[p], 1u);
   }
   __syncthreads();
   if (rep) {
     bool fresh = false;
     const uint64_t gs = scratch_insert(S, id, h, &fresh);
     atomicAdd(&S.sntile[gs], 1u);
+    atomicAdd(&S.sfirstx[gs], lcnt[p]);  // occurrence count
     lt.gslot[p] = (uint32_t)gs;
     if (fresh) lnew[p] = atomicAdd(&s_nnew, 1u) + 1;
   }
@@ -225,6 +232,7 @@ struct FTableArgs {
   uint32_t* urow;
   int64_t* urow64;
   uint32_t* hot_list;
+  uint32_t* u_cnt;
   uint32_t* ctr;
 };
 
@@ -244,35 +252,54 @@ __global__ void __launch_bounds__(256) k_ftable(FTableArgs a) {
   const unsigned g = lane & (kBucket - 1);
   const unsigned gbase = lane & ~(kBucket - 1);
   const unsigned gmask = 0xFFu << gbase;
-  const uint32_t i = blockIdx.x * kGroups + (threadIdx.x >> 3);
-  const bool active = i < nu;
-  __shared__ uint32_t s_part, s_base;
   __shared__ unsigned long long s_ins, s_reuse;
   if (threadIdx.x == 0) {
-    s_part = 0;
     s_ins = 0;
     s_reuse = 0;
   }
   __syncthreads();
-  uint64_t key = 0;
-  uint32_t slot = 0, nt = 0, local = 0;
-  if (active) {
-    key = a.unique[i];
-    slot = a.use.u_slot[i];
-    nt = a.use.sntile[slot];
-    if (g == 0 && nt > 1) local = atomicAdd(&s_part, nt);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_part) s_base = atomicAdd(&a.ctr[kCtrPartAlloc], s_part);
-  __syncthreads();
-  if (active && g == 0) {
-    a.u_ntile[i] = nt;
-    a.u_poff[i] = nt > 1 ? s_base + local : 0;
-    a.u_ticket[i] = 0;
-    if (nt > kWarpMaxParts) a.hot_list[atomicAdd(&a.ctr[kCtrNHot], 1u)] = i;
-  }
-  if (!a.do_table) return;
-  if (active) {
+  // every warp runs the same trip count (shuffles below are warp-wide)
+  const uint32_t per_iter = gridDim.x * kGroups;
+  for (uint32_t base = 0; base < nu; base += per_iter) {
+    const uint32_t i = base + blockIdx.x * kGroups + (threadIdx.x >> 3);
+    const bool active = i < nu;
+    uint64_t key = 0;
+    uint32_t slot = 0, nt = 0, cnt = 0;
+    if (active) {
+      key = a.unique[i];
+      slot = a.use.u_slot[i];
+      nt = a.use.sntile[slot];
+      cnt = a.use.sfirstx[slot];
+    }
+    const bool hot = cnt > kCsrMax;
+    // segments: CSR of the id's token positions (exact-order path) or its
+    // per-tile partial sums (hot path); warp-aggregated allocation
+    const uint32_t want_c = (active && g == 0 && !hot) ? cnt : 0u;
+    const uint32_t want_p = (active && g == 0 && hot) ? nt : 0u;
+    uint32_t ic = want_c, ip = want_p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t yc = __shfl_up_sync(kFull, ic, o);
+      const uint32_t yp = __shfl_up_sync(kFull, ip, o);
+      if (lane >= (unsigned)o) {
+        ic += yc;
+        ip += yp;
+      }
+    }
+    const uint32_t tc = __shfl_sync(kFull, ic, 31), tp = __shfl_sync(kFull, ip, 31);
+    uint32_t bc = 0, bp = 0;
+    if (lane == 0 && tc) bc = atomicAdd(&a.ctr[kCtrCsrAlloc], tc);
+    if (lane == 0 && tp) bp = atomicAdd(&a.ctr[kCtrPartAlloc], tp);
+    bc = __shfl_sync(kFull, bc, 0);
+    bp = __shfl_sync(kFull, bp, 0);
+    if (active && g == 0) {
+      a.u_cnt[i] = cnt;
+      a.u_ntile[i] = hot ? nt : 0u;  // 0 marks the CSR path
+      a.u_poff[i] = hot ? bp + ip - want_p : bc + ic - want_c;
+      a.u_ticket[i] = 0;
+      if (hot) a.hot_list[atomicAdd(&a.ctr[kCtrNHot], 1u)] = i;
+    }
+    if (!a.do_table || !active) continue;
     uint32_t row = kNoRow;
     const int sp = key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
     if (sp >= 0) {
@@ -342,7 +369,7 @@ __global__ void __launch_bounds__(256) k_ftable(FTableArgs a) {
     if (s_ins) atomicAdd(&td->c.inserted, s_ins);
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
-  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  if (a.do_table) launch_epilogue(td, free_n0, fresh0, true, tick_now);
 }
 
 // ---------------------------------------------------------------------------
@@ -360,13 +387,13 @@ struct TileArgs {
   const uint32_t* u_ntile;
   const uint32_t* u_poff;
   uint32_t* u_ticket;
-  float* usum;
   float* pbuf;
   uint32_t* ptile;
+  uint32_t* csr_pos;
 };
 
 template <int VEC, int CH, int LPR>
-__global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
+__global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t NW = TT >> 5;
@@ -471,9 +498,26 @@ __global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
   }
   if (!red) return;
 
-  // ---- group the tile's tokens by unique id (first occurrence in the tile)
+  // ---- ids with <= kCsrMax occurrences: place the token position into the
+  // id's CSR segment (warp-aggregated cursor; the finish kernel sorts it)
+  uint32_t nt = 0;
+  if (valid) nt = __ldg(a.u_ntile + u);
+  const bool csr_tok = valid && nt == 0;
+  {
+    const uint32_t key = csr_tok ? u : (0xFFFF0000u | lane);
+    const unsigned mm0 = __match_any_sync(kFull, key);
+    const uint32_t leader = __ffs(mm0) - 1;
+    uint32_t base = 0;
+    if (csr_tok && lane == leader) base = atomicAdd(a.u_ticket + u, (uint32_t)__popc(mm0));
+    base = __shfl_sync(kFull, base, leader);
+    if (csr_tok)
+      a.csr_pos[__ldg(a.u_poff + u) + base + __popc(mm0 & lanemask_lt())] = t0 + tid;
+  }
+  const bool hotv = valid && nt > 0;
+
+  // ---- hot ids: group the tile's tokens by unique id (first occurrence)
   uint32_t ps = 0;
-  if (valid) {
+  if (hotv) {
     ps = hash32(u) & (L - 1);
     for (;;) {
       const uint32_t prev = atomicCAS(&lkey[ps], kFull, u);
@@ -483,7 +527,7 @@ __global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
     atomicMin(&lfirst[ps], tid);
   }
   __syncthreads();
-  const bool head = valid && lfirst[ps] == tid;
+  const bool head = hotv && lfirst[ps] == tid;
   const unsigned hb = __ballot_sync(kFull, head);
   if (lane == 0) wsum[warp] = __popc(hb);
   __syncthreads();
@@ -504,23 +548,16 @@ __global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
     const uint32_t lg = wsum[warp] + __popc(hb & lanemask_lt());
     lgroup[ps] = lg;
     gu[lg] = u;
-    const uint32_t nt = __ldg(a.u_ntile + u);
-    uint32_t dst;
-    if (nt > 1) {
-      const uint32_t tk = atomicAdd(a.u_ticket + u, 1u);
-      const uint32_t slot = __ldg(a.u_poff + u) + tk;
-      a.ptile[slot] = tile;
-      dst = slot | 0x80000000u;  // partial buffer
-    } else {
-      dst = u;  // usum
-    }
-    gdst[lg] = dst;
+    const uint32_t tk = atomicAdd(a.u_ticket + u, 1u);
+    const uint32_t slot = __ldg(a.u_poff + u) + tk;
+    a.ptile[slot] = tile;
+    gdst[lg] = slot;
   }
   __syncthreads();
-  const uint32_t mylg = valid ? lgroup[ps] : (0xFFFF0000u | lane);
+  const uint32_t mylg = hotv ? lgroup[ps] : (0xFFFF0000u | lane);
   const unsigned mm = __match_any_sync(kFull, mylg);
   const uint32_t rw = __popc(mm & lanemask_lt());
-  if (valid && rw == 0) wcnt[warp * TT + mylg] = (uint16_t)__popc(mm);
+  if (hotv && rw == 0) wcnt[warp * TT + mylg] = (uint16_t)__popc(mm);
   __syncthreads();
   if (tid < ng) {
     uint32_t run = 0;
@@ -556,7 +593,7 @@ __global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
     if (tid < ng) goff[tid] = wsum[warp] + x - v;
   }
   __syncthreads();
-  if (valid) csr[goff[mylg] + wcnt[warp * TT + mylg] + rw] = (uint16_t)tid;
+  if (hotv) csr[goff[mylg] + wcnt[warp * TT + mylg] + rw] = (uint16_t)tid;
   if (a.tma) {
     asm volatile(
         "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
@@ -589,19 +626,13 @@ __global__ void __launch_bounds__(256, 2) k_ftile(TileArgs a) {
     for (uint32_t q = tid; q < nchunks; q += TT) {
       const uint32_t g = q / D4, c = q - g * D4;
       const float4 sum = *reinterpret_cast<const float4*>(sg + (size_t)csr[goff[g]] * D + 4 * c);
-      const uint32_t dst = gdst[g];
-      float* base = (dst & 0x80000000u) ? a.pbuf + (size_t)(dst & 0x7FFFFFFFu) * D
-                                        : a.usum + (size_t)dst * D;
-      __stcg(reinterpret_cast<float4*>(base) + c, sum);
+      __stcg(reinterpret_cast<float4*>(a.pbuf + (size_t)gdst[g] * D) + c, sum);
     }
   } else {
     const uint32_t nchunks = ng * D;
     for (uint32_t q = tid; q < nchunks; q += TT) {
       const uint32_t g = q / D, e = q - g * D;
-      const uint32_t dst = gdst[g];
-      float* base = (dst & 0x80000000u) ? a.pbuf + (size_t)(dst & 0x7FFFFFFFu) * D
-                                        : a.usum + (size_t)dst * D;
-      base[e] = sg[(size_t)csr[goff[g]] * D + e];
+      a.pbuf[(size_t)gdst[g] * D + e] = sg[(size_t)csr[goff[g]] * D + e];
     }
   }
 }
@@ -629,11 +660,13 @@ struct FinishArgs {
   const uint32_t* n_unique;
   const uint32_t* n_hot;
   const uint32_t* hot_list;
-  const uint32_t* u_ntile;
-  const uint32_t* u_poff;
+  const uint32_t* u_ntile;  // 0: CSR path; > 0: tiles holding a partial (hot path)
+  const uint32_t* u_poff;   // CSR offset / partial offset
+  const uint32_t* u_cnt;    // occurrences
   uint32_t* u_ticket;
   const uint32_t* urow;
-  const float* usum;
+  const float* grads;
+  const uint32_t* csr_pos;
   const float* pbuf;
   const uint32_t* ptile;
   uint32_t* porder;
@@ -642,8 +675,8 @@ struct FinishArgs {
   float* sums_out;  // accumulate-only mode when non-null
 };
 
-// Ordered sum of partials with ranks [r0, r1), PF rows in flight.
-template <int VEC, int CH>
+// Sum of rows src(order[k]) for k in [r0, r1) in that order, PF in flight.
+template <int VEC, int CH, bool kPartial>
 __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t* order,
                                             uint32_t poff, uint32_t r0, uint32_t r1, uint32_t D,
                                             float (&acc)[CH][VEC]) {
@@ -658,7 +691,8 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 #pragma unroll
       for (int jj = 0; jj < PF; ++jj) {
         const uint32_t i = __shfl_sync(kFull, idx, (j0 + jj) & 31);
-        if (j0 + jj < cnt) load_vec<VEC, CH>(a.pbuf + (size_t)(poff + i) * D, D, x[jj], false);
+        const float* src = kPartial ? a.pbuf + (size_t)(poff + i) * D : a.grads + (size_t)i * D;
+        if (j0 + jj < cnt) load_vec<VEC, CH>(src, D, x[jj], false);
       }
 #pragma unroll
       for (int jj = 0; jj < PF; ++jj)
@@ -667,10 +701,15 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
   }
 }
 
-//  blocks [0, hot_blocks): one id with > kWarpMaxParts partials at a time; the
-//    whole block ranks its partials (bitmap over tiles) and splits the ordered
-//    sum over the warps (fixed split -> deterministic)
-//  other blocks: warp per id, no block barriers
+// Roles by block index:
+//  [0, hot_blocks)  hot ids (> kCsrMax occurrences), one per block: the
+//                   per-tile partials are ranked by tile (bitmap + prefix
+//                   popcounts) and summed in tile order, split over the warps
+//                   with a fixed split (deterministic, blocked order)
+//  other blocks     warp per CSR id: its <= kCsrMax token positions are
+//                   sorted and the gradient rows summed in position order --
+//                   exactly the reference's accumulate order
+//                   (sparse_update.cpp:49-54), so these sums are bit-exact
 template <int VEC, int CH>
 __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint32_t hot_blocks) {
   extern __shared__ __align__(16) unsigned char smem2[];
@@ -679,28 +718,33 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
   const TableDesc d = a.td->d;
   const uint32_t D = d.dim;
   if (blockIdx.x >= hot_blocks) {
-    uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * 32;  // [NW x 32]
+    uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * kCsrMax;  // [NW x 64]
     const uint32_t nu = *a.n_unique;
     const uint32_t stride = (gridDim.x - hot_blocks) * NW;
     for (uint32_t uu = (blockIdx.x - hot_blocks) * NW + warp; uu < nu; uu += stride) {
-      const uint32_t nt = __ldg(a.u_ntile + uu);
-      if (nt > kWarpMaxParts) continue;
-      const uint32_t poff = __ldg(a.u_poff + uu);
+      if (__ldg(a.u_ntile + uu) != 0) continue;  // hot path
+      const uint32_t c = __ldg(a.u_cnt + uu), off = __ldg(a.u_poff + uu);
       const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
-      float acc[CH][VEC];
-      if (nt <= 1) {
-        load_vec<VEC, CH>(a.usum + (size_t)uu * D, D, acc, false);
-      } else {
-        const uint32_t tl = lane < nt ? __ldg(a.ptile + poff + lane) : kFull;
-        uint32_t r = 0;
-#pragma unroll 8
-        for (uint32_t j = 0; j < nt; ++j) r += __shfl_sync(kFull, tl, j) < tl;
-        if (lane < nt) order_w[r] = lane;
-        __syncwarp();
-        ordered_sum<VEC, CH>(a, order_w, poff, 0, nt, D, acc);
-        __syncwarp();
-        if (lane == 0) a.u_ticket[uu] = 0;
+      const uint32_t p0 = lane < c ? __ldg(a.csr_pos + off + lane) : kFull;
+      const uint32_t p1 = lane + 32 < c ? __ldg(a.csr_pos + off + 32 + lane) : kFull;
+      uint32_t r0 = 0, r1 = 0;
+      for (uint32_t j = 0; j < min(c, 32u); ++j) {
+        const uint32_t q = __shfl_sync(kFull, p0, j);
+        r0 += q < p0;
+        r1 += q < p1;
       }
+      for (uint32_t j = 32; j < c; ++j) {
+        const uint32_t q = __shfl_sync(kFull, p1, j - 32);
+        r0 += q < p0;
+        r1 += q < p1;
+      }
+      if (lane < c) order_w[r0] = p0;
+      if (lane + 32 < c) order_w[r1] = p1;
+      __syncwarp();
+      float acc[CH][VEC];
+      ordered_sum<VEC, CH, false>(a, order_w, 0, 0, c, D, acc);
+      __syncwarp();
+      if (lane == 0) a.u_ticket[uu] = 0;
       if (a.sums_out)
         store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
       else
@@ -749,7 +793,7 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
     const uint32_t per = (nt + NW - 1) / NW;
     const uint32_t r0 = min(warp * per, nt), r1 = min(r0 + per, nt);
     float part[CH][VEC];
-    ordered_sum<VEC, CH>(a, a.porder + poff, poff, r0, r1, D, part);
+    ordered_sum<VEC, CH, true>(a, a.porder + poff, poff, r0, r1, D, part);
     store_vec<VEC, CH>(wpart + (size_t)warp * D, D, part);
     __syncthreads();
     if (warp == 0) {
@@ -1015,6 +1059,7 @@ static int attr_shape() {
 static int set_smem_attrs() {
   static int done = 0;
   if (done) return RS_OK;
+
   int st = attr_shape<4, 1>() | attr_shape<4, 2>() | attr_shape<4, 3>() | attr_shape<4, 4>() |
            attr_shape<2, 1>() | attr_shape<2, 2>() | attr_shape<1, 1>() | attr_shape<1, 2>() |
            attr_shape<1, 3>() | attr_shape<1, 4>() | attr_shape<1, 5>() | attr_shape<1, 6>() |
@@ -1038,6 +1083,7 @@ static FTableArgs ftable_args(rs_workspace* ws, rs_table* t, int use) {
   a.urow = ws->urow;
   a.urow64 = ws->urow64;
   a.hot_list = ws->hot_list;
+  a.u_cnt = ws->u_cnt;
   a.ctr = ws->ctr;
   return a;
 }
@@ -1046,7 +1092,7 @@ static int launch_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, in
                          cudaStream_t s) {
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
-  const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4);
+  const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4 + 4);
   k_fdedup<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, set_dev(ws, use), ws->slot_of, ws->unique,
                                   ws->ctr);
   RS_LAUNCH_CHECK("k_fdedup");
@@ -1058,12 +1104,12 @@ static int fast_dedup_table(rs_workspace* ws, rs_table* t, const uint64_t* d_ids
                             int use, cudaStream_t s) {
   int st = launch_fdedup(ws, d_ids, n, use, s);
   if (st) return st;
-  k_ftable<<<grid_for(n, kGroups, 1u << 30), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
+  k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
   RS_LAUNCH_CHECK("k_ftable");
   return RS_OK;
 }
 
-// partial sums: at most one per (tile, id) pair <= n; usum: one per id <= n
+// partial sums: at most one per (tile, hot id) pair <= n
 static int reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s) {
   if (ws->pbuf_floats < n * D) {
     if (ws->pbuf) RS_CUDA(cudaFreeAsync(ws->pbuf, s));
@@ -1093,8 +1139,8 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.u_poff = ws->u_poff;
   a.u_ticket = ws->u_ticket;
   a.pbuf = ws->pbuf;
-  a.usum = ws->pbuf + ws->pbuf_floats;
   a.ptile = ws->ptile;
+  a.csr_pos = ws->csr_pos;
   if (d_out && D % 4 != 0) {
     k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, a.use, t->dev,
                                                             (uint32_t)n, ws->inverse, d_out);
@@ -1128,8 +1174,8 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
 }
 
 // KD.
-static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const OptArgs& o,
-                         float* sums_out, cudaStream_t s) {
+static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float* d_grads,
+                         const OptArgs& o, float* sums_out, cudaStream_t s) {
   const uint32_t D = t->desc.dim;
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
@@ -1139,25 +1185,27 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   a.hot_list = ws->hot_list;
   a.u_ntile = ws->u_ntile;
   a.u_poff = ws->u_poff;
+  a.u_cnt = ws->u_cnt;
   a.u_ticket = ws->u_ticket;
   a.urow = ws->urow;
+  a.grads = d_grads;
+  a.csr_pos = ws->csr_pos;
   a.pbuf = ws->pbuf;
-  a.usum = ws->pbuf + ws->pbuf_floats;
   a.ptile = ws->ptile;
   a.porder = ws->porder;
   a.bw = (ntiles + 31) / 32;
   a.td = t->dev;
   a.sums_out = sums_out;
   const uint32_t hot_blocks = 2 * 148;
-  const size_t smem =
-      std::max<size_t>((size_t)8 * 32 * 4, (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
+  const size_t smem = std::max<size_t>((size_t)8 * kCsrMax * 4,
+                                       (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
   const unsigned grid = hot_blocks + grid_for(n, 8, 148 * 24);
   const Shape sh = shape_for(D);
-#define RS_FIN(V, C)                                              \
-  if (sh.vec == V && sh.ch == C) {                                \
-    k_finish<V, C><<<grid, 256, smem, s>>>(a, o, hot_blocks);     \
-    RS_LAUNCH_CHECK("k_finish");                                  \
-    return RS_OK;                                                 \
+#define RS_FIN(V, C)                                                 \
+  if (sh.vec == V && sh.ch == C) {                                   \
+    k_finish<V, C><<<grid, 256, smem, s>>>(a, o, hot_blocks);        \
+    RS_LAUNCH_CHECK("k_finish");                                     \
+    return RS_OK;                                                    \
   }
   RS_FIN(4, 1) RS_FIN(4, 2) RS_FIN(4, 3) RS_FIN(4, 4)
   RS_FIN(2, 1) RS_FIN(2, 2)
@@ -1204,7 +1252,7 @@ static int forward_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids,
     FTableArgs a = ftable_args(ws, t, use);
     a.do_clean = false;
     a.do_table = false;
-    k_ftable<<<grid_for(n, kGroups, 1u << 30), kGroups * kBucket, 0, s>>>(a);
+    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
     RS_LAUNCH_CHECK("k_ftable(meta)");
     st = table_ensure_any(t, ws->unique, ws->set[use].cnt, n, ws->urow, ws->urow64,
                           ws->set[use].u_slot, ws->set[use].srow, s);
@@ -1244,14 +1292,17 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   ok = ok && A(&ws->slot_of, N * 4) && A(&ws->inverse, N * 4) && A(&ws->unique, N * 8) &&
        A(&ws->u_ntile, N * 4) && A(&ws->u_poff, N * 4) && A(&ws->u_ticket, N * 4) &&
        A(&ws->urow, N * 4) && A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) &&
-       A(&ws->porder, N * 4) && A(&ws->hot_list, (N / 32 + 64) * 4) &&
+       A(&ws->porder, N * 4) && A(&ws->hot_list, (N / 32 + 64) * 4) && A(&ws->u_cnt, N * 4) && A(&ws->csr_pos, N * 4) &&
        A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64);
   if (!ok) {
     rs_workspace_destroy(ws);
     return cuda_fail(cudaGetLastError(), "rs_workspace_create: cudaMalloc");
   }
   if (set_smem_attrs() != RS_OK ||
-      cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&ws->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&ws->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ws->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ws->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     rs_workspace_destroy(ws);
     return RS_ERR_CUDA;
   }
@@ -1280,7 +1331,7 @@ int rs_workspace_destroy(rs_workspace* ws) {
   }
   void* ptrs[] = {ws->slot_of, ws->inverse, ws->unique, ws->u_ntile,  ws->u_poff,
                   ws->u_ticket, ws->urow,   ws->urow64, ws->ptile,    ws->porder,
-                  ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list};
+                  ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list, ws->u_cnt, ws->csr_pos};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : ws->graphs)
@@ -1288,6 +1339,9 @@ int rs_workspace_destroy(rs_workspace* ws) {
   for (auto& e : ws->prof_ev)
     if (e) cudaEventDestroy(e);
   if (ws->cap_stream) cudaStreamDestroy(ws->cap_stream);
+  if (ws->aux_stream) cudaStreamDestroy(ws->aux_stream);
+  if (ws->ev_fork) cudaEventDestroy(ws->ev_fork);
+  if (ws->ev_join) cudaEventDestroy(ws->ev_join);
   delete ws;
   return RS_OK;
 }
@@ -1368,7 +1422,7 @@ int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
   if (st) return st;
   if ((st = reduce_prepare(ws, t->desc.dim, n, s))) return st;
   if ((st = launch_tile(ws, t, ws->last_set, n, nullptr, d_grads, false, s))) return st;
-  if ((st = launch_finish(ws, t, ws->last_set, n, o, nullptr, s))) return st;
+  if ((st = launch_finish(ws, t, ws->last_set, n, d_grads, o, nullptr, s))) return st;
   t->applies++;
   ws->have_forward = false;  // rows were updated: a second backward would double-apply
   return RS_OK;
@@ -1387,7 +1441,7 @@ int rs_accumulate(rs_workspace* ws, const float* d_grads, uint64_t n, float* d_s
   int st = reduce_prepare(ws, t->desc.dim, n, s);
   if (st) return st;
   if ((st = launch_tile(ws, t, ws->last_set, n, nullptr, d_grads, false, s))) return st;
-  return launch_finish(ws, t, ws->last_set, n, o, d_sums, s);
+  return launch_finish(ws, t, ws->last_set, n, d_grads, o, d_sums, s);
 }
 
 // All launches of one training step, no host-side work (graph capturable).
@@ -1398,12 +1452,12 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
   if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
   if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
-  k_ftable<<<grid_for(n, kGroups, 1u << 30), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
+  k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
   RS_LAUNCH_CHECK("k_ftable");
   if (ev) RS_CUDA(cudaEventRecord(ev[2], s));
   if ((st = launch_tile(ws, t, use, n, d_out, d_grads, true, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[3], s));
-  if ((st = launch_finish(ws, t, use, n, o, nullptr, s))) return st;
+  if ((st = launch_finish(ws, t, use, n, d_grads, o, nullptr, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[4], s));
   return table_mirror_copy(t, mirror, s);
 }
@@ -1524,7 +1578,7 @@ int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   if ((st = reduce_prepare(ws, t->desc.dim, n, s))) return st;
   const int use = ws->cur;
   if ((st = forward_enqueue(ws, t, d_ids, n, nullptr, d_grads, use, s))) return st;
-  if ((st = launch_finish(ws, t, use, n, o, nullptr, s))) return st;
+  if ((st = launch_finish(ws, t, use, n, d_grads, o, nullptr, s))) return st;
   if (!t->cfg.max_keys && (st = table_after_op(t, s))) return st;
   ws->last_set = use;
   ws->cur ^= 1;

@@ -190,14 +190,14 @@ __global__ void __launch_bounds__(kProbeThreads)
     __syncthreads();
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
-      __threadfence();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       s_last = atomicAdd(&td->c.blocks_done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
       td->c.tick = tick_now;
       td->c.blocks_done = 0;
-      __threadfence();
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
   }
 }

@@ -128,12 +128,12 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
   __syncthreads();
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     s_last = atomicAdd(&td->c.blocks_done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     TableCounters& c = td->c;
     const unsigned long long used = c.alloc_ctr;
     if (used <= free_n0) {
@@ -153,7 +153,7 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     c.removed = 0;
     if (bump_tick) c.tick = tick_now;
     c.blocks_done = 0;
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
 }
 
