@@ -83,6 +83,7 @@ struct rs_workspace {
   std::vector<rs_graph_entry> graphs;
   uint64_t graph_clock = 0;
   bool use_graphs = true;
+  bool fork = true;  // run the hot-id finish concurrently on aux_stream
   // optional per-kernel CUDA-event timing (forces the non-graph path)
   bool profiling = false;
   cudaEvent_t prof_ev[8] = {nullptr};

@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "opt_dev.cuh"
@@ -701,6 +702,121 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
   }
 }
 
+// CSR path, element-parallel: G = D/4 threads per id, each owning one float4
+// chunk of the row.  The id's <= kCsrMax token positions are ranked within the
+// group (shuffles), written sorted to smem, and the gradient rows are summed
+// in position order (the reference's accumulate order) -> bit-exact sums.
+template <int G>
+__global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) {
+  constexpr int PPT = (int)(kCsrMax / G);  // positions held per thread
+  __shared__ uint32_t order_s[(256 / G) * kCsrMax];
+  const TableDesc d = a.td->d;
+  const uint32_t D4 = d.dim >> 2;
+  const uint32_t lane = lane_id();
+  const uint32_t gl = lane & (G - 1);
+  const uint32_t gbase = lane & ~(G - 1);
+  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << gbase;
+  const uint32_t gpb = blockDim.x / G;
+  uint32_t* order = order_s + (threadIdx.x / G) * kCsrMax;
+  const uint32_t gid = blockIdx.x * gpb + threadIdx.x / G;
+  const uint32_t ngroups = gridDim.x * gpb;
+  const uint32_t nu = *a.n_unique;
+  const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grads);
+  for (uint32_t uu = gid; uu < nu; uu += ngroups) {
+    if (__ldg(a.u_ntile + uu) != 0) continue;  // hot path (group-uniform)
+    const uint32_t c = __ldg(a.u_cnt + uu), off = __ldg(a.u_poff + uu);
+    const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
+    // issue the row loads early: independent of the gradient sum
+    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), vv = wv, mv = wv;
+    size_t roff = 0;
+    if (!a.sums_out && row != kNoRow) {
+      roff = (size_t)row * d.dim + 4 * gl;
+      wv = *reinterpret_cast<const float4*>(d.emb + roff);
+      vv = *reinterpret_cast<const float4*>(d.s2 + roff);
+      if (d.s1) mv = *reinterpret_cast<const float4*>(d.s1 + roff);
+    }
+    uint32_t p[PPT], r[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const uint32_t k = gl + j * G;
+      p[j] = k < c ? __ldg(a.csr_pos + off + k) : kFull;
+      r[j] = 0;
+    }
+    // rank every held position against all c positions of the id
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq) {
+      if ((uint32_t)(jq * G) >= c) break;
+      for (uint32_t src = 0; src < (uint32_t)G; ++src) {
+        const uint32_t q = __shfl_sync(gmask, p[jq], src, G);
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) r[j] += q < p[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+      if (gl + j * G < c) order[r[j]] = p[j];
+    __syncwarp(gmask);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t k = 0;
+    for (; k + 4 <= c; k += 4) {
+      float4 x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = g4[(size_t)order[k + q] * D4 + gl];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc.x += x[q].x;
+        acc.y += x[q].y;
+        acc.z += x[q].z;
+        acc.w += x[q].w;
+      }
+    }
+    for (; k < c; ++k) {
+      const float4 x = g4[(size_t)order[k] * D4 + gl];
+      acc.x += x.x;
+      acc.y += x.y;
+      acc.z += x.z;
+      acc.w += x.w;
+    }
+    __syncwarp(gmask);
+    if (gl == 0) a.u_ticket[uu] = 0;
+    if (a.sums_out) {
+      reinterpret_cast<float4*>(a.sums_out)[(size_t)uu * D4 + gl] = acc;
+      continue;
+    }
+    if (row == kNoRow) continue;
+    uint32_t st = 0;
+    if (gl == 0) {
+      st = d.step[row] + 1;
+      d.step[row] = st;
+    }
+    st = __shfl_sync(gmask, st, 0, G);
+    double bc1 = 1.0, bc2 = 1.0;
+    if (o.kind == RS_OPT_ADAM) {
+      if (st < o.bc_len) {
+        bc1 = o.bc[st];
+        bc2 = o.bc[o.bc_len + st];
+      } else {
+        bc1 = 1.0 - pow(o.b1, (double)st);
+        bc2 = 1.0 - pow(o.b2, (double)st);
+      }
+    }
+    float* wp = reinterpret_cast<float*>(&wv);
+    float* vp = reinterpret_cast<float*>(&vv);
+    float* mp = reinterpret_cast<float*>(&mv);
+    const float* gp = reinterpret_cast<const float*>(&acc);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (o.kind == RS_OPT_ADAM)
+        adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
+      else
+        adagrad_elem(wp[e], vp[e], gp[e], o);
+    }
+    *reinterpret_cast<float4*>(d.emb + roff) = wv;
+    *reinterpret_cast<float4*>(d.s2 + roff) = vv;
+    if (d.s1) *reinterpret_cast<float4*>(d.s1 + roff) = mv;
+  }
+}
+
 // Roles by block index:
 //  [0, hot_blocks)  hot ids (> kCsrMax occurrences), one per block: the
 //                   per-tile partials are ranked by tile (bitmap + prefix
@@ -1199,20 +1315,45 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   const uint32_t hot_blocks = 2 * 148;
   const size_t smem = std::max<size_t>((size_t)8 * kCsrMax * 4,
                                        (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
-  const unsigned grid = hot_blocks + grid_for(n, 8, 148 * 24);
+  const uint32_t g4 = D % 4 == 0 ? D / 4 : 0;
+  const int G = (g4 >= 2 && g4 <= 32 && !(g4 & (g4 - 1))) ? (int)g4 : 0;
+  // G > 0: CSR ids on s, hot ids concurrently on the forked aux stream
+  const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
+  cudaStream_t hs = s;
+  if (G > 0 && ws->fork) {
+    RS_CUDA(cudaEventRecord(ws->ev_fork, s));
+    RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, ws->ev_fork, 0));
+    hs = ws->aux_stream;
+  }
   const Shape sh = shape_for(D);
-#define RS_FIN(V, C)                                                 \
-  if (sh.vec == V && sh.ch == C) {                                   \
-    k_finish<V, C><<<grid, 256, smem, s>>>(a, o, hot_blocks);        \
-    RS_LAUNCH_CHECK("k_finish");                                     \
-    return RS_OK;                                                    \
+  bool launched = false;
+#define RS_FIN(V, C)                                                   \
+  if (!launched && sh.vec == V && sh.ch == C) {                        \
+    k_finish<V, C><<<grid, 256, smem, hs>>>(a, o, hot_blocks);         \
+    RS_LAUNCH_CHECK("k_finish");                                       \
+    launched = true;                                                   \
   }
   RS_FIN(4, 1) RS_FIN(4, 2) RS_FIN(4, 3) RS_FIN(4, 4)
   RS_FIN(2, 1) RS_FIN(2, 2)
   RS_FIN(1, 1) RS_FIN(1, 2) RS_FIN(1, 3) RS_FIN(1, 4) RS_FIN(1, 5) RS_FIN(1, 6) RS_FIN(1, 7)
   RS_FIN(1, 8)
 #undef RS_FIN
-  return fail(RS_ERR_CONFIG, "embedding_dim " + std::to_string(D) + " unsupported");
+  if (!launched) return fail(RS_ERR_CONFIG, "embedding_dim " + std::to_string(D) + " unsupported");
+  if (G > 0) {
+    const unsigned eg = grid_for(n * (uint64_t)G, 256, 148 * 16);
+#define RS_CSR(GG)                                      \
+  if (G == GG) {                                        \
+    k_finish_csr<GG><<<eg, 256, 0, s>>>(a, o);          \
+    RS_LAUNCH_CHECK("k_finish_csr");                    \
+  }
+    RS_CSR(32) RS_CSR(16) RS_CSR(8) RS_CSR(4) RS_CSR(2)
+#undef RS_CSR
+    if (ws->fork) {
+      RS_CUDA(cudaEventRecord(ws->ev_join, ws->aux_stream));
+      RS_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));  // join
+    }
+  }
+  return RS_OK;
 }
 
 static int opt_args(rs_table* t, const rs_optimizer_params* p, OptArgs* o, cudaStream_t s) {
@@ -1277,6 +1418,8 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
     return fail(RS_ERR_CONFIG, "rs_workspace_create: max_tokens must be in [1, 2^30]");
   rs_workspace* ws = new rs_workspace();
   ws->max_tokens = max_tokens;
+  if (const char* e = getenv("RS_NO_GRAPH")) ws->use_graphs = e[0] == '0';
+  if (const char* e = getenv("RS_NO_FORK")) ws->fork = e[0] == '0';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;
@@ -1529,7 +1672,11 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
       cudaStream_t cs = ws->cap_stream;
       RS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
       const uint64_t before = launches();
+      // a forked branch inside the captured graph measured slower: linear graph
+      const bool fork = ws->fork;
+      ws->fork = false;
       st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, cs, nullptr);
+      ws->fork = fork;
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(cs, &g);
       if (st) {
