@@ -178,6 +178,32 @@ int rs_accumulate(rs_workspace* ws, const float* d_grads, uint64_t n, float* d_s
 int rs_apply_aggregated(rs_table* t, const uint64_t* d_keys, uint64_t n, const float* d_sums,
                         const rs_optimizer_params* opt, void* stream);
 
+/* ---- row-sharded step over the W GPUs of one node (exchange_sim.cpp:117-233) --
+ * One process per GPU.  Each rank owns the keys with hash64(key) % W == rank
+ * (SimCluster::shard_of, exchange_sim.cpp:82-85) in its own rs_table shard.
+ * The ID, embedding and gradient exchanges are peer stores over NVLink into a
+ * symmetric arena each rank exports by CUDA IPC (rs_comm_ipc_handle /
+ * rs_comm_open: the caller exchanges the 64-byte handles, e.g. with
+ * torch.distributed.all_gather_object).  Every rank must call each step. */
+typedef struct rs_comm rs_comm;
+int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_comm** out);
+int rs_comm_ipc_handle(rs_comm* c, void* handle_out /* 64 bytes */);
+int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order */);
+int rs_comm_destroy(rs_comm* c);
+/* distributed_lookup with DedupMode::kTwoStage for this rank's tokens:
+ * d_out [n x dim] bit-exact with the reference's outputs[rank]. */
+int rs_dist_forward(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t n, float* d_out,
+                    void* stream);
+/* per-token grads -> pre-reduced unique rows to the owners -> ordered
+ * stage-2 sum (source, position) -> optimizer on the owners' shards. */
+int rs_dist_backward(rs_comm* c, rs_table* shard, const float* d_grads, uint64_t n,
+                     const rs_optimizer_params* opt, void* stream);
+/* This rank's ExchangeTrace row (exchange_sim.hpp:37-59) for the last step:
+ * ids_sent[W] (to each owner), embs_sent[W] (vectors this owner sent back to
+ * each requester), lookups, ids_requested, ids_received.  Synchronizes. */
+int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
+                  uint64_t* ids_requested, uint64_t* ids_received);
+
 /* ---- table merging (merge_registry.cpp:23-51) ----------------------------- */
 /* encode_tagged_id on device; d_status (optional) receives RS_ERR_RANGE per bad id. */
 int rs_encode_ids(const uint64_t* d_raw, uint64_t n, uint32_t k_bits, uint32_t table_index,

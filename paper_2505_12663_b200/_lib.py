@@ -106,6 +106,13 @@ _SIGS = {
     "rs_workspace_n_unique": (C.c_int, [vp, C.POINTER(u64)]),
     "rs_accumulate": (C.c_int, [vp, vp, u64, vp, vp]),
     "rs_apply_aggregated": (C.c_int, [vp, vp, u64, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_comm_create": (C.c_int, [C.c_int, C.c_int, u64, u32, C.POINTER(vp)]),
+    "rs_comm_ipc_handle": (C.c_int, [vp, vp]),
+    "rs_comm_open": (C.c_int, [vp, vp]),
+    "rs_comm_destroy": (C.c_int, [vp]),
+    "rs_dist_forward": (C.c_int, [vp, vp, vp, u64, vp, vp]),
+    "rs_dist_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
+    "rs_comm_trace": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),

@@ -24,6 +24,13 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = getenv("RS_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 }  // namespace rs
 
 extern "C" {

@@ -117,6 +117,17 @@ struct rs_workspace {
   bool have_forward = false;
 };
 
+// Options of the fused kernels used by the sharded (multi-GPU) step (dist.cu).
+struct rs_dist_opts {
+  const uint32_t* d_n = nullptr;        // device token count (owner side); null: host n
+  const uint32_t* pos_map = nullptr;    // CSR position of each token (owner: origin slot)
+  bool no_stage = false;                // no hot ids possible: no gradient staging
+  const void* gather_view = nullptr;    // rs::TableDev* whose emb = requester receive buffer
+  float* const* peer_dst = nullptr;     // device [W] peer gradient receive bases
+  const uint32_t* send_pos = nullptr;   // per unique id: owner * cap + position
+  uint32_t cap = 0, rank = 0;
+};
+
 namespace rs {
 // table.cu
 int table_prepare(rs_table* t, uint64_t n, cudaStream_t s);  // room for n more keys
@@ -135,4 +146,15 @@ int table_mirror_commit(rs_table* t, int which, cudaStream_t s);
 int table_adam_tables(rs_table* t, double beta1, double beta2, uint64_t applies, cudaStream_t s);
 // step.cu
 uint32_t tile_tokens_for_dim(uint32_t dim);
+int step_set_smem_attrs();
+int step_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
+                const uint32_t* d_n);
+int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_table,
+                bool do_clean, cudaStream_t s);
+int step_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float* d_out,
+              const float* d_grads, bool clean_other, cudaStream_t s, const rs_dist_opts* dopt);
+int step_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float* d_grads,
+                const void* opt_args, float* sums_out, cudaStream_t s, const rs_dist_opts* dopt);
+int step_opt_args(rs_table* t, const rs_optimizer_params* p, void* out, cudaStream_t s);
+int step_reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s);
 }  // namespace rs

@@ -117,6 +117,7 @@ int fail(int status, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
 void count_launch(uint64_t n = 1);
 uint64_t launches();
+bool debug_sync();  // RS_DEBUG_SYNC=1: synchronize after every launch (debugging only)
 
 #define RS_CUDA(call)                                       \
   do {                                                      \
@@ -128,6 +129,7 @@ uint64_t launches();
   do {                                                      \
     ::rs::count_launch();                                   \
     cudaError_t _e = cudaGetLastError();                    \
+    if (_e == cudaSuccess && ::rs::debug_sync()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess) return ::rs::cuda_fail(_e, name); \
   } while (0)
 

@@ -156,9 +156,10 @@ __device__ __forceinline__ uint32_t local_insert(const LocalTable& lt, uint64_t 
 
 // ---------------------------------------------------------------------------
 // KA: fast dedup tile.  blockDim.x == TT.
-__global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n, SetDev S,
+__global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetDev S,
                          uint32_t* __restrict__ slot_of, uint64_t* __restrict__ unique,
-                         uint32_t* __restrict__ ctr) {
+                         uint32_t* __restrict__ ctr, const uint32_t* __restrict__ d_n) {
+  const uint32_t n = d_n ? *d_n : n_host;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t L = 2 * TT;
@@ -391,6 +392,9 @@ struct TileArgs {
   float* pbuf;
   uint32_t* ptile;
   uint32_t* csr_pos;
+  const uint32_t* d_n;      // device token count (null: n)
+  const uint32_t* pos_map;  // CSR value per token (null: token index)
+  bool stage;               // hot ids possible: stage the tile's gradient rows
 };
 
 template <int VEC, int CH, int LPR>
@@ -420,10 +424,12 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const uint32_t tile = blockIdx.x;
   const uint32_t t0 = tile * TT;
-  const uint32_t rows = min(TT, a.n - t0);
+  const uint32_t nn = a.d_n ? *a.d_n : a.n;
   if (a.clean_cnt && tile == 0 && tid == 0) *a.clean_cnt = 0;
+  if (t0 >= nn) return;
+  const uint32_t rows = min(TT, nn - t0);
 
-  if (red) {
+  if (red && a.stage) {
     for (uint32_t i = tid; i < L; i += TT) {
       lkey[i] = kFull;
       lfirst[i] = kFull;
@@ -512,9 +518,11 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
     if (csr_tok && lane == leader) base = atomicAdd(a.u_ticket + u, (uint32_t)__popc(mm0));
     base = __shfl_sync(kFull, base, leader);
     if (csr_tok)
-      a.csr_pos[__ldg(a.u_poff + u) + base + __popc(mm0 & lanemask_lt())] = t0 + tid;
+      a.csr_pos[__ldg(a.u_poff + u) + base + __popc(mm0 & lanemask_lt())] =
+          a.pos_map ? __ldg(a.pos_map + t0 + tid) : t0 + tid;
   }
   const bool hotv = valid && nt > 0;
+  if (!a.stage) return;  // no hot ids possible (sharded owner side)
 
   // ---- hot ids: group the tile's tokens by unique id (first occurrence)
   uint32_t ps = 0;
@@ -674,7 +682,22 @@ struct FinishArgs {
   uint32_t bw;  // bitmap words = ceil(ntiles / 32)
   TableDev* td;
   float* sums_out;  // accumulate-only mode when non-null
+  // sharded requester: the aggregated row of id u goes to the owner's
+  // gradient receive buffer over NVLink (peer store)
+  float* const* peer_dst;
+  const uint32_t* send_pos;
+  uint32_t cap, rank;
+  uint64_t dbg_nrows, dbg_ncsr;  // RS_BOUNDS builds: valid grad rows / csr_pos entries
 };
+
+__device__ __forceinline__ float* sum_dst(const FinishArgs& a, uint32_t uu, uint32_t D) {
+  if (a.peer_dst) {
+    const uint32_t sp = a.send_pos[uu];
+    const uint32_t o = sp / a.cap, j = sp - o * a.cap;
+    return a.peer_dst[o] + ((size_t)a.rank * a.cap + j) * D;
+  }
+  return a.sums_out ? a.sums_out + (size_t)uu * D : nullptr;
+}
 
 // Sum of rows src(order[k]) for k in [r0, r1) in that order, PF in flight.
 template <int VEC, int CH, bool kPartial>
@@ -725,11 +748,18 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
   for (uint32_t uu = gid; uu < nu; uu += ngroups) {
     if (__ldg(a.u_ntile + uu) != 0) continue;  // hot path (group-uniform)
     const uint32_t c = __ldg(a.u_cnt + uu), off = __ldg(a.u_poff + uu);
-    const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
+#ifdef RS_BOUNDS
+    if (c > kCsrMax || off + c > a.dbg_ncsr) {
+      if (gl == 0) printf("k_finish_csr: uu %u c %u off %u ncsr %llu\n", uu, c, off, (unsigned long long)a.dbg_ncsr);
+      continue;
+    }
+#endif
+    const bool sums = a.sums_out || a.peer_dst;
+    const uint32_t row = sums ? 0u : __ldg(a.urow + uu);
     // issue the row loads early: independent of the gradient sum
     float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), vv = wv, mv = wv;
     size_t roff = 0;
-    if (!a.sums_out && row != kNoRow) {
+    if (!sums && row != kNoRow) {
       roff = (size_t)row * d.dim + 4 * gl;
       wv = *reinterpret_cast<const float4*>(d.emb + roff);
       vv = *reinterpret_cast<const float4*>(d.s2 + roff);
@@ -756,6 +786,19 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     for (int j = 0; j < PPT; ++j)
       if (gl + j * G < c) order[r[j]] = p[j];
     __syncwarp(gmask);
+#ifdef RS_BOUNDS
+    {
+      bool bad = false;
+      for (uint32_t k2 = 0; k2 < c; ++k2) bad |= order[k2] >= a.dbg_nrows;
+      if (!sums && row != kNoRow && row >= d.row_cap) bad = true;
+      if (a.peer_dst && a.send_pos[uu] >= a.cap * 64u) bad = true;
+      if (bad) {
+        if (gl == 0) printf("k_finish_csr: uu %u c %u row %u order0 %u nrows %llu sp %u\n", uu, c, row,
+                            order[0], (unsigned long long)a.dbg_nrows, a.peer_dst ? a.send_pos[uu] : 0u);
+        continue;
+      }
+    }
+#endif
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     uint32_t k = 0;
     for (; k + 4 <= c; k += 4) {
@@ -779,8 +822,8 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     }
     __syncwarp(gmask);
     if (gl == 0) a.u_ticket[uu] = 0;
-    if (a.sums_out) {
-      reinterpret_cast<float4*>(a.sums_out)[(size_t)uu * D4 + gl] = acc;
+    if (float* dst = sum_dst(a, uu, d.dim)) {
+      reinterpret_cast<float4*>(dst)[gl] = acc;
       continue;
     }
     if (row == kNoRow) continue;
@@ -815,6 +858,7 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     *reinterpret_cast<float4*>(d.s2 + roff) = vv;
     if (d.s1) *reinterpret_cast<float4*>(d.s1 + roff) = mv;
   }
+  if (a.peer_dst) asm volatile("fence.acq_rel.sys;" ::: "memory");  // publish peer stores
 }
 
 // Roles by block index:
@@ -840,7 +884,7 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
     for (uint32_t uu = (blockIdx.x - hot_blocks) * NW + warp; uu < nu; uu += stride) {
       if (__ldg(a.u_ntile + uu) != 0) continue;  // hot path
       const uint32_t c = __ldg(a.u_cnt + uu), off = __ldg(a.u_poff + uu);
-      const uint32_t row = a.sums_out ? 0u : __ldg(a.urow + uu);
+      const uint32_t row = (a.sums_out || a.peer_dst) ? 0u : __ldg(a.urow + uu);
       const uint32_t p0 = lane < c ? __ldg(a.csr_pos + off + lane) : kFull;
       const uint32_t p1 = lane + 32 < c ? __ldg(a.csr_pos + off + 32 + lane) : kFull;
       uint32_t r0 = 0, r1 = 0;
@@ -861,11 +905,12 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
       ordered_sum<VEC, CH, false>(a, order_w, 0, 0, c, D, acc);
       __syncwarp();
       if (lane == 0) a.u_ticket[uu] = 0;
-      if (a.sums_out)
-        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, acc);
+      if (float* dst = sum_dst(a, uu, D))
+        store_vec<VEC, CH>(dst, D, acc);
       else
         apply_row<VEC, CH>(d, row, acc, o);
     }
+    if (a.peer_dst) asm volatile("fence.acq_rel.sys;" ::: "memory");
     return;
   }
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem2);  // [bw]
@@ -921,8 +966,8 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
         add_acc<VEC, CH>(tot, x);
       }
       if (lane == 0) a.u_ticket[uu] = 0;
-      if (a.sums_out)
-        store_vec<VEC, CH>(a.sums_out + (size_t)uu * D, D, tot);
+      if (float* dst = sum_dst(a, uu, D))
+        store_vec<VEC, CH>(dst, D, tot);
       else
         apply_row<VEC, CH>(d, __ldg(a.urow + uu), tot, o);
     }
@@ -1205,12 +1250,12 @@ static FTableArgs ftable_args(rs_workspace* ws, rs_table* t, int use) {
 }
 
 static int launch_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use,
-                         cudaStream_t s) {
+                         cudaStream_t s, const uint32_t* d_n = nullptr) {
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4 + 4);
   k_fdedup<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, set_dev(ws, use), ws->slot_of, ws->unique,
-                                  ws->ctr);
+                                  ws->ctr, d_n);
   RS_LAUNCH_CHECK("k_fdedup");
   return RS_OK;
 }
@@ -1237,20 +1282,25 @@ static int reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t
 
 // KC with gather and/or reduce.
 static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float* d_out,
-                       const float* d_grads, bool clean_other, cudaStream_t s) {
+                       const float* d_grads, bool clean_other, cudaStream_t s,
+                       const rs_dist_opts* dopt = nullptr) {
   const uint32_t D = t->desc.dim;
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   TileArgs a;
-  a.td = t->dev;
+  a.td = (dopt && dopt->gather_view) ? reinterpret_cast<const TableDev*>(dopt->gather_view) : t->dev;
   a.use = set_dev(ws, use);
+  a.d_n = dopt ? dopt->d_n : nullptr;
+  a.pos_map = dopt ? dopt->pos_map : nullptr;
+  a.stage = !(dopt && dopt->no_stage);
   a.clean_cnt = clean_other ? ws->set[use ^ 1].cnt : nullptr;
   a.slot_of = ws->slot_of;
   a.n = (uint32_t)n;
   a.inverse = ws->inverse;
   a.out = (D % 4 == 0) ? d_out : nullptr;
   a.grads = d_grads;
-  a.tma = d_grads && (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(d_grads) & 15u) == 0);
+  a.tma = a.stage && d_grads && (D % 4 == 0) &&
+          ((reinterpret_cast<uintptr_t>(d_grads) & 15u) == 0);
   a.u_ntile = ws->u_ntile;
   a.u_poff = ws->u_poff;
   a.u_ticket = ws->u_ticket;
@@ -1267,7 +1317,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     }
   }
   const uint32_t NW = TT / 32;
-  const size_t smem = (d_grads ? (size_t)TT * D * 4 : 0) + 16 +
+  const size_t smem = (d_grads && a.stage ? (size_t)TT * D * 4 : 0) + 16 +
                       (size_t)(3 * 2 * TT + 4 * TT + 64) * 4 + (size_t)NW * TT * 2 +
                       (size_t)TT * 2 + 16;
   const Shape sh = shape_for(D);
@@ -1291,7 +1341,8 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
 
 // KD.
 static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float* d_grads,
-                         const OptArgs& o, float* sums_out, cudaStream_t s) {
+                         const OptArgs& o, float* sums_out, cudaStream_t s,
+                         const rs_dist_opts* dopt = nullptr) {
   const uint32_t D = t->desc.dim;
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
@@ -1312,6 +1363,12 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   a.bw = (ntiles + 31) / 32;
   a.td = t->dev;
   a.sums_out = sums_out;
+  a.peer_dst = dopt ? dopt->peer_dst : nullptr;
+  a.send_pos = dopt ? dopt->send_pos : nullptr;
+  a.cap = dopt ? dopt->cap : 0;
+  a.rank = dopt ? dopt->rank : 0;
+  a.dbg_nrows = (dopt && dopt->d_n) ? ws->max_tokens : n;
+  a.dbg_ncsr = ws->max_tokens;
   const uint32_t hot_blocks = 2 * 148;
   const size_t smem = std::max<size_t>((size_t)8 * kCsrMax * 4,
                                        (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
@@ -1402,6 +1459,40 @@ static int forward_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids,
     if ((st = fast_dedup_table(ws, t, d_ids, n, use, s))) return st;
   }
   return launch_tile(ws, t, use, n, d_out, d_grads, true, s);
+}
+
+int step_set_smem_attrs() { return set_smem_attrs(); }
+int step_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
+                const uint32_t* d_n) {
+  return launch_fdedup(ws, d_ids, n, use, s, d_n);
+}
+int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_table,
+                bool do_clean, cudaStream_t s) {
+  FTableArgs a = ftable_args(ws, t, use);
+  a.do_table = do_table;
+  a.do_clean = do_clean;
+  k_ftable<<<grid_for(n_max, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
+  RS_LAUNCH_CHECK("k_ftable");
+  return RS_OK;
+}
+int step_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float* d_out,
+              const float* d_grads, bool clean_other, cudaStream_t s, const rs_dist_opts* dopt) {
+  return launch_tile(ws, t, use, n, d_out, d_grads, clean_other, s, dopt);
+}
+int step_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float* d_grads,
+                const void* opt_args, float* sums_out, cudaStream_t s, const rs_dist_opts* dopt) {
+  OptArgs o;
+  if (opt_args)
+    std::memcpy(&o, opt_args, sizeof(o));
+  else
+    std::memset(&o, 0, sizeof(o));
+  return launch_finish(ws, t, use, n, d_grads, o, sums_out, s, dopt);
+}
+int step_opt_args(rs_table* t, const rs_optimizer_params* p, void* out, cudaStream_t s) {
+  return opt_args(t, p, reinterpret_cast<OptArgs*>(out), s);
+}
+int step_reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s) {
+  return reduce_prepare(ws, D, n, s);
 }
 
 }  // namespace rs
