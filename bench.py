@@ -251,6 +251,185 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_sharded(args, cfg):
+    """N > 1: the row-sharded step, weak scaling.  Each rank owns
+    the keys with hash64(id) % N == rank of the same 2^20-key table, draws its
+    own config-1 batch, and runs forward (two-stage dedup, ids and embeddings
+    exchanged by NVLink peer stores) + backward (pre-reduced grads to the
+    owners, Adagrad on the owner shard).  value = sum over ranks of each rank's
+    unique ids / max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_12663_b200 as P
+    from paper_2505_12663_b200 import workload as W
+    from paper_2505_12663_b200.dist import ShardedTable
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    os.environ.setdefault("RANK", "0")
+    os.environ.setdefault("WORLD_SIZE", "1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dim, vocab = cfg["dim"], cfg["vocab"]
+    nb = max(1, min(args.steps + args.warmup, 6))
+    batches = [W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
+                          cfg["zipf"], [vocab]) for b in range(nb)]
+    mt = torch.tensor([max(len(i) for _, i in batches)], dtype=torch.int64, device="cuda")
+    dist.all_reduce(mt, op=dist.ReduceOp.MAX)  # the arena layout must agree on every rank
+    max_t = int(mt.item())
+    nflat = world * max_t
+    st = ShardedTable(P.TableConfig(capacity=cfg["capacity"] * 2, embedding_dim=dim, optimizer="adagrad",
+                                    chunk_rows=1 << 16, initial_rows=vocab // world + 8 * nflat), max_tokens=max_t)
+    raw = torch.arange(vocab, dtype=torch.int64, device="cuda")
+    st.insert_owned(raw + int(TAG1), W.pseudo_grads(raw, 0, dim))
+    params = P.AdagradParams(lr=0.01, eps=1e-8)
+    dev = []
+    for b, (lengths, ids) in enumerate(batches):
+        d_g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim)
+        dev.append((P.as_keys(ids), d_g, torch.empty((len(ids), dim), device="cuda")))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    lib = P.lib()
+
+    def one(b):
+        d_ids, d_g, out = dev[b % nb]
+        st.step(d_ids, d_g, params, out)
+
+    for w in range(args.warmup):
+        one(w)
+    torch.cuda.synchronize()
+    dist.barrier()
+    uniq_b = [int(np.unique(ids).size) for _, ids in batches]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = lib.rs_kernel_launches()
+    with Clocks(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            one(args.warmup + k)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = lib.rs_kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    t_sum = sum(step_ms) / 1e3
+    uniq = sum(uniq_b[(args.warmup + k) % nb] for k in range(args.steps))
+    toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
+    tr = st.trace()  # last step's ExchangeTrace (all ranks)
+    # per-phase device time (separate pass, CUDA events between the phases)
+    st.set_profiling(True)
+    for k in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        one(k)
+    phases = st.phase_ms()
+    st.set_profiling(False)
+    tt = torch.tensor([t_sum], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    uu = torch.tensor([uniq, toks], dtype=torch.float64, device="cuda")
+    dist.all_reduce(uu)
+    t_job, uniq_job, toks_job = tt.item(), uu[0].item(), uu[1].item()
+    ms = t_job / args.steps * 1e3
+
+    # NVLink bytes of the last step: ids (8 B) + grads (4D) to every other
+    # owner, embeddings (4D) back from every owner; max over ranks
+    ids_sent, embs_sent = tr["ids_sent"].astype(np.float64), tr["embs_sent"].astype(np.float64)
+    off = 1.0 - np.eye(world)
+    out_bytes = (ids_sent * off).sum(1) * (8 + 4 * dim) + (embs_sent * off).sum(1) * 4 * dim
+    nvl_max = float(out_bytes.max())
+
+    # end to end: host ids + grads -> device, the step, gathered rows -> host
+    e2e = e2e_sharded(args, cfg, batches, st, params, P, W)
+    hbm, how = peaks()
+    T_avg, U_avg = toks / args.steps, uniq / args.steps
+    D = dim
+    step_bytes = 12 * T_avg + 24 * U_avg + 8 * D * T_avg + 20 * D * U_avg
+    ach = step_bytes / (ms / 1e3) / 1e9
+    res = {
+        "metric": "unique-ID lookups+updates/sec",
+        "value": uniq_job / t_job,
+        "unit": "unique-ids/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 rows, f64 optimizer math, u64 ids",
+        "data": "synthetic: the reference's generator per rank (seed + 1000*rank), pseudo_sparse_grad gradients",
+        "config": {"workload": cfg["workload"] + "; row-sharded over the ranks (owner = hash64 % N), per-rank batch",
+                   "tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg, "embedding_dim": D,
+                   "table_keys": vocab, "optimizer": "adagrad", "parallelism": f"row-sharded x{world}",
+                   "exchange": "NVLink peer stores from the producing kernels (CUDA IPC arena)",
+                   "l2": "flushed (512 MiB write) between timed steps"},
+        "tokens_per_s": toks_job / t_job,
+        "kernel_ms_rank0": phases,
+        "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        "table_host_syncs_rank0": int(st.shard.info().host_syncs),
+        "roofline": {"bound": "hbm", "kernel": "sharded step (all kernels of one rank)", "achieved": ach,
+                     "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": how,
+                     "algorithmic_bytes_per_launch": step_bytes},
+        "nvlink": {"bytes_per_step_max_rank": nvl_max, "achieved_gbs": nvl_max / (ms / 1e3) / 1e9,
+                   "peak_gbs_per_direction": 900.0,
+                   "trace_last_step": {"ids_sent": tr["ids_sent"].tolist(), "embs_sent": tr["embs_sent"].tolist(),
+                                       "lookups": tr["lookups"].tolist()}},
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    dist.barrier()
+    st.close()
+    dist.destroy_process_group()
+
+
+def e2e_sharded(args, cfg, batches, st, params, P, W):
+    import torch
+    import torch.distributed as dist
+    dim = cfg["dim"]
+    stream = torch.cuda.current_stream()
+    host = []
+    for b, (lengths, ids) in enumerate(batches):
+        h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
+        g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim).cpu().pin_memory()
+        host.append((h_ids, g, torch.empty((len(ids), dim), dtype=torch.float32).pin_memory()))
+    max_t = max(h[0].numel() for h in host)
+    d_ids = torch.empty(max_t, dtype=torch.int64, device="cuda")
+    d_g = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
+    d_out = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
+    n = max(3, min(args.steps, 10))
+    uniq_b = [int(np.unique(ids).size) for _, ids in batches]
+    evs = []
+    dist.barrier()
+    for k in range(n + 2):
+        h_ids, g, h_out = host[k % len(host)]
+        T = h_ids.numel()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        d_ids[:T].copy_(h_ids, non_blocking=True)
+        d_g[:T].copy_(g, non_blocking=True)
+        st.step(d_ids[:T], d_g[:T], params, d_out[:T])
+        h_out.copy_(d_out[:T], non_blocking=True)
+        e.record(stream)
+        evs.append((s, e, k))
+    torch.cuda.synchronize()
+    t, uniq, h2d, d2h = 0.0, 0, 0, 0
+    for s, e, k in evs[2:]:
+        h_ids, g, h_out = host[k % len(host)]
+        t += s.elapsed_time(e) / 1e3
+        uniq += uniq_b[k % len(host)]
+        h2d += h_ids.numel() * 8 + g.numel() * 4
+        d2h += h_out.numel() * 4
+    v = torch.tensor([t, uniq], dtype=torch.float64, device="cuda")
+    tmax = v[:1].clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(v)
+    return {"value": v[1].item() / tmax.item(), "unit": "unique-ids/s", "h2d_bytes_per_step": h2d // n,
+            "d2h_bytes_per_step": d2h // n, "ms_per_step": tmax.item() / n * 1e3}
+
+
 def _n_unique(step):
     import ctypes
 
@@ -407,10 +586,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="run the row-sharded step even at N=1")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         run_reference(args, C1)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
+        run_sharded(args, C1)
     else:
         run_ours(args, C1)
 

@@ -71,6 +71,7 @@ typedef struct {
   uint64_t rows_allocated, rows_free, row_capacity;
   uint64_t tick;
   uint32_t embedding_dim, optimizer;
+  uint64_t host_syncs; /* stream synchronizations the capacity bookkeeping needed so far */
 } rs_table_info;
 
 /* ---- meta ---------------------------------------------------------------- */
@@ -198,9 +199,22 @@ int rs_dist_forward(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t
  * stage-2 sum (source, position) -> optimizer on the owners' shards. */
 int rs_dist_backward(rs_comm* c, rs_table* shard, const float* d_grads, uint64_t n,
                      const rs_optimizer_params* opt, void* stream);
+/* forward + backward in one call (same results), ordered so that no rank
+ * idles on a flag in steady state: reduce while the peers' ids are in
+ * flight, answer + update as owner, gather last.  d_out gets the rows as they
+ * were before this step's update (distributed_lookup semantics). */
+int rs_dist_step(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t n,
+                 const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream);
 /* This rank's ExchangeTrace row (exchange_sim.hpp:37-59) for the last step:
  * ids_sent[W] (to each owner), embs_sent[W] (vectors this owner sent back to
  * each requester), lookups, ids_requested, ids_received.  Synchronizes. */
+/* Per-phase device time of the sharded step (CUDA events on the step's
+ * stream; synchronizes at the end of each step while on, no graphs): phases
+ * req_dedup, send_ids, wait_ids, owner_dedup, owner_table_respond,
+ * wait_embs, gather (rs_dist_step: gather + reduce + sums to the owners),
+ * req_reduce (split API only), wait_grads, owner_update -- mean ms. */
+int rs_comm_set_profiling(rs_comm* c, int on);
+int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count);
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received);
 

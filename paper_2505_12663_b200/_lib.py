@@ -65,7 +65,8 @@ class rs_optimizer_params(C.Structure):
 class rs_table_info(C.Structure):
     _fields_ = [("capacity", C.c_uint64), ("occupied", C.c_uint64), ("tombstones", C.c_uint64),
                 ("rows_allocated", C.c_uint64), ("rows_free", C.c_uint64), ("row_capacity", C.c_uint64),
-                ("tick", C.c_uint64), ("embedding_dim", C.c_uint32), ("optimizer", C.c_uint32)]
+                ("tick", C.c_uint64), ("embedding_dim", C.c_uint32), ("optimizer", C.c_uint32),
+                ("host_syncs", C.c_uint64)]
 
 
 vp = C.c_void_p
@@ -112,6 +113,9 @@ _SIGS = {
     "rs_comm_destroy": (C.c_int, [vp]),
     "rs_dist_forward": (C.c_int, [vp, vp, vp, u64, vp, vp]),
     "rs_dist_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
+    "rs_dist_step": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_comm_set_profiling": (C.c_int, [vp, C.c_int]),
+    "rs_comm_phase_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int, C.POINTER(u64)]),
     "rs_comm_trace": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,

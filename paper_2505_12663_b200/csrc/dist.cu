@@ -32,10 +32,14 @@
 
 #include "opt_dev.cuh"
 #include "rs_host.hpp"
+#include "scratch_dev.cuh"
 #include "table_dev.cuh"
 
 namespace rs {
 namespace {
+
+using namespace tdev;
+using namespace sdev;
 
 constexpr int kMaxWorld = 64;
 
@@ -65,41 +69,54 @@ struct CommDev {
   uint32_t rank, world;
   uint32_t cap;        // ids per (source, destination) region
   uint32_t dim;
-  size_t off_ids, off_emb, off_grad;
-  unsigned long long epoch;
+  size_t off_ids, off_emb, off_grad;  // off_grad: this epoch's gradient buffer
+  unsigned long long* epoch;  // device step counter: bumped by k_send_ids, read by the rest
   unsigned long long* trace;
-  unsigned int* done;  // last-block counter
+  unsigned int* done;  // last-block counters [4]
 };
 
 __device__ __forceinline__ ArenaHdr* hdr_of(const CommDev& c, uint32_t r) {
   return reinterpret_cast<ArenaHdr*>(c.peers[r]);
 }
+__device__ __forceinline__ unsigned long long* flag_of(ArenaHdr* h, int phase, uint32_t src) {
+  return phase == 0 ? &h->sig_ids[src] : phase == 1 ? &h->sig_emb[src] : &h->sig_grad[src];
+}
 
-// Last block of a launch raises `sig` (phase flags) at every peer.
-__device__ __forceinline__ void signal_all(const CommDev& c, int phase) {
-  fence_sys();
-  __syncthreads();
+// Grid-level arrival: each block's stores (peer stores included) are ordered
+// before its arrival by the barrier and a gpu-scope acq_rel atomic; the last
+// block to arrive therefore observes all of them, and its single system fence
+// + st.release.sys flags publish them cumulatively to the peers.  Returns
+// true in the last block.
+__device__ __forceinline__ bool last_block_signal(const CommDev& c, int phase, unsigned int* done) {
   __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(c.done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!last) return;
-  fence_sys();
-  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) {
-    ArenaHdr* h = hdr_of(c, r);
-    unsigned long long* f = phase == 0 ? &h->sig_ids[c.rank]
-                            : phase == 1 ? &h->sig_emb[c.rank]
-                                         : &h->sig_grad[c.rank];
-    st_release_sys(f, c.epoch);
+  if (threadIdx.x == 0) {
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(done) : "memory");
+    last = old == gridDim.x * gridDim.y - 1;
+    if (last) fence_sys();
   }
-  if (threadIdx.x == 0) *c.done = 0;
+  __syncthreads();
+  return last;
+}
+__device__ __forceinline__ void raise_flags(const CommDev& c, int phase, unsigned int* done,
+                                            unsigned long long e) {
+  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x)
+    st_release_sys(flag_of(hdr_of(c, r), phase, c.rank), e);
+  if (threadIdx.x == 0) *done = 0;
 }
 
 // Requester: owner partition of the unique ids, peer stores into ids_in.
-__global__ void k_send_ids(CommDev c, const uint64_t* __restrict__ unique,
-                           const uint32_t* __restrict__ n_unique,
-                           const uint32_t* __restrict__ u_slot, uint32_t* __restrict__ srow,
-                           uint32_t* __restrict__ send_pos, uint32_t* __restrict__ send_cnt,
-                           uint64_t n_tokens) {
+__global__ void __launch_bounds__(256) k_send_ids(CommDev c, const uint64_t* __restrict__ unique,
+                                                  const uint32_t* __restrict__ n_unique,
+                                                  const uint32_t* __restrict__ u_slot,
+                                                  uint32_t* __restrict__ srow,
+                                                  uint32_t* __restrict__ send_pos,
+                                                  uint32_t* __restrict__ send_cnt,
+                                                  uint64_t n_tokens) {
+  // this step's epoch; every block reads it before arriving, the last block
+  // publishes it after raising the flags
+  const unsigned long long e = *c.epoch + 1;
   const uint32_t nu = *n_unique;
   const uint32_t lane = lane_id();
   for (uint32_t base = blockIdx.x * blockDim.x; base < nu; base += gridDim.x * blockDim.x) {
@@ -125,25 +142,16 @@ __global__ void k_send_ids(CommDev c, const uint64_t* __restrict__ unique,
       srow[u_slot[u]] = sp;  // the gather reads emb_in row sp
     }
   }
-  fence_sys();
-  __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) last = atomicAdd(c.done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  fence_sys();
+  if (!last_block_signal(c, 0, c.done + 0)) return;
   for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) {
     hdr_of(c, r)->cnt_in[c.rank] = send_cnt[r];
     c.trace[kTrIdsSent + r] = send_cnt[r];
   }
   if (threadIdx.x == 0) c.trace[kTrRequested] = n_tokens;
-  fence_sys();
   __syncthreads();
-  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) {
-    st_release_sys(&hdr_of(c, r)->sig_ids[c.rank], c.epoch);
-    send_cnt[r] = 0;
-  }
-  if (threadIdx.x == 0) *c.done = 0;
+  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) send_cnt[r] = 0;
+  raise_flags(c, 0, c.done + 0, e);
+  if (threadIdx.x == 0) *c.epoch = e;
 }
 
 // Bounded wait until every source raised flag `phase` for this epoch.
@@ -151,107 +159,214 @@ __global__ void k_wait(CommDev c, int phase) {
   ArenaHdr* h = hdr_of(c, c.rank);
   const uint32_t r = threadIdx.x;
   if (r >= c.world) return;
-  const unsigned long long* f = phase == 0 ? &h->sig_ids[r] : phase == 1 ? &h->sig_emb[r]
-                                                                           : &h->sig_grad[r];
+  const unsigned long long* f = flag_of(h, phase, r);
+  const unsigned long long e = *c.epoch;
   const long long t0 = clock64();
-  while (ld_acquire_sys(f) < c.epoch) {
+  while (ld_acquire_sys(f) < e) {
     if (clock64() - t0 > 40000000000ll) {  // ~20 s: a peer is gone; do not hang the GPU
       c.trace[kTrError] = 1;
       break;
     }
-    __nanosleep(200);
+    __nanosleep(100);
   }
 }
 
-// Owner: received lists -> one source-ordered flat list (stage-2 input).
-__global__ void k_flatten(CommDev c, uint64_t* __restrict__ flat_ids,
-                          uint32_t* __restrict__ flat_pos, uint32_t* __restrict__ d_n2) {
+// Owner KA': stage-2 dedup straight from the receive lists.  A requester
+// sends each id at most once, so an owner-unique id has at most W origins:
+// every received position (src, j) claims the id's scratch slot and appends
+// its origin src*cap + j to the slot's origin row origins[slot*W .. +W)
+// (atomic order; the finish kernel sorts them into (source, position)
+// order, the stage-2 origin order of exchange_sim.cpp:100-115).
+// grid (ceil(cap / 256), W): block (x, src) takes positions x*256.. of src.
+__global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t* __restrict__ origins,
+                                                   uint64_t* __restrict__ unique) {
   const ArenaHdr* h = hdr_of(c, c.rank);
-  const uint32_t src = blockIdx.x;
-  uint32_t off = 0;
-  for (uint32_t r = 0; r < src; ++r) off += h->cnt_in[r];
+  const uint32_t src = blockIdx.y;
   const uint32_t cnt = h->cnt_in[src];
-  const uint64_t* in = reinterpret_cast<const uint64_t*>(c.peers[c.rank] + c.off_ids) +
-                       (size_t)src * c.cap;
-  for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-    flat_ids[off + j] = in[j];
-    flat_pos[off + j] = src * c.cap + j;
-  }
-  if (threadIdx.x == 0) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     c.trace[kTrEmbsSent + src] = cnt;  // two-stage: one vector per received id
     if (src == c.world - 1) {
-      *d_n2 = off + cnt;
-      c.trace[kTrReceived] = off + cnt;
+      uint64_t tot = 0;
+      for (uint32_t r = 0; r < c.world; ++r) tot += h->cnt_in[r];
+      c.trace[kTrReceived] = tot;
     }
+  }
+  if (blockIdx.x * blockDim.x >= cnt) return;  // block-uniform
+  const bool v = j < cnt;
+  bool fresh = false;
+  uint64_t id = 0, gs = 0;
+  if (v) {
+    id = reinterpret_cast<const uint64_t*>(c.peers[c.rank] + c.off_ids)[(size_t)src * c.cap + j];
+    gs = scratch_insert(S, id, hash64(id), &fresh);
+    const uint32_t k = atomicAdd(&S.sntile[gs], 1u);  // origins so far (<= W)
+    origins[gs * c.world + k] = src * c.cap + j;
+  }
+  // unique numbering of the fresh ids: one atomic per warp
+  const unsigned fm = __ballot_sync(0xFFFFFFFFu, fresh);
+  uint32_t base = 0;
+  if (lane_id() == 0 && fm) base = atomicAdd(S.cnt, (uint32_t)__popc(fm));
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  if (fresh) {
+    const uint32_t u = base + __popc(fm & lanemask_lt());
+    S.u_slot[u] = (uint32_t)gs;
+    unique[u] = id;
   }
 }
 
-// Owner: every received position's row, stored into the requester's emb_in.
-template <int LPR>
-__global__ void __launch_bounds__(256) k_respond(CommDev c, const TableDev* __restrict__ td,
-                                                 const uint32_t* __restrict__ slot_of,
-                                                 const uint32_t* __restrict__ srow,
-                                                 const uint32_t* __restrict__ flat_pos,
-                                                 const uint32_t* __restrict__ d_n2,
-                                                 const uint32_t* __restrict__ n_unique2) {
-  const uint32_t n = *d_n2;
-  const uint32_t D4 = td->d.dim >> 2;
-  const float4* __restrict__ emb = reinterpret_cast<const float4*>(td->d.emb);
-  const uint32_t lane = lane_id(), sub = lane / LPR, l = lane % LPR;
-  constexpr int RPW = 32 / LPR;
-  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t p0 = w * RPW; p0 < n; p0 += nw * RPW) {
-    const uint64_t p = p0 + sub;
-    if (p < n) {
-      const uint32_t row = __ldcg(srow + __ldg(slot_of + p));
-      if (row == kNoRow) continue;  // table error (reported by the counters)
-      const uint32_t origin = __ldg(flat_pos + p);
-      const uint32_t src = origin / c.cap, j = origin - src * c.cap;
+// Owner KB': per owner-unique id (8-lane group) find-or-insert on the shard,
+// then the "embedding all-to-all": the row is stored straight into the
+// emb_in of every requester that asked for it (one 128-bit store per lane per
+// step over NVLink).  Also the finish metadata (CSR = the slot's origin row),
+// cleaning of the other scratch set, the table epilogue and the flags.
+struct OwnTableArgs {
+  TableDev* td;
+  SetDev use, clean;
+  const uint32_t* origins;
+  const uint64_t* unique;
+  uint32_t* urow;
+  uint32_t* u_cnt;
+  uint32_t* u_poff;
+  uint32_t* u_ntile;
+  uint32_t* u_ticket;
+};
+
+__global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
+  TableDev* td = a.td;
+  const TableDesc d = td->d;
+  const unsigned long long free_n0 = td->c.free_n;
+  const unsigned long long fresh0 = td->c.fresh_next;
+  const uint32_t tick_now = td->c.tick + 1;
+  clean_set(a.clean, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x,
+            (uint64_t)gridDim.x * blockDim.x);
+  const uint32_t nu = *a.use.cnt;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint32_t D4 = d.dim >> 2;
+  __shared__ unsigned long long s_ins, s_reuse;
+  if (threadIdx.x == 0) {
+    s_ins = 0;
+    s_reuse = 0;
+  }
+  __syncthreads();
+  constexpr unsigned kGroupsPB = 32;
+  for (uint32_t i = blockIdx.x * kGroupsPB + (threadIdx.x >> 3); i < nu; i += gridDim.x * kGroupsPB) {
+    const uint64_t key = a.unique[i];
+    const uint32_t slot = a.use.u_slot[i];
+    const uint32_t cnt = a.use.sntile[slot];
+    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0,
+                                              fresh0, &s_ins, &s_reuse);
+    if (g == 0) {
+      a.urow[i] = row;
+      a.u_cnt[i] = cnt;
+      a.u_poff[i] = slot * c.world;
+      a.u_ntile[i] = 0;  // CSR path of the finish kernel
+      a.u_ticket[i] = 0;
+    }
+    if (row == kNoRow) continue;  // table error (reported through the counters)
+    const float4* e = reinterpret_cast<const float4*>(d.emb) + (size_t)row * D4;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const uint32_t origin = __ldg(a.origins + (size_t)slot * c.world + k);
+      const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
       float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
-                    ((size_t)c.rank * c.cap + j) * D4;
-      for (uint32_t k = l; k < D4; k += LPR) dst[k] = __ldg(emb + (size_t)row * D4 + k);
+                    ((size_t)c.rank * c.cap + jj) * D4;
+      for (uint32_t q = g; q < D4; q += kBucket) dst[q] = __ldg(e + q);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) c.trace[kTrLookups] = *n_unique2;
-  signal_all(c, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_ins) atomicAdd(&td->c.inserted, s_ins);
+    if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
+  }
+  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  if (blockIdx.x == 0 && threadIdx.x == 0) c.trace[kTrLookups] = nu;
+  if (last_block_signal(c, 1, c.done + 1)) raise_flags(c, 1, c.done + 1, *c.epoch);
 }
 
-// Requester: raise the gradient flags after KD stored its rows at the owners.
-__global__ void k_signal(CommDev c, int phase) { signal_all(c, phase); }
+// Raise flag `phase` at every peer (after the kernels that stored the data).
+__global__ void k_signal(CommDev c, int phase) {
+  if (threadIdx.x == 0) fence_sys();
+  __syncthreads();
+  const unsigned long long e = *c.epoch;
+  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x)
+    st_release_sys(flag_of(hdr_of(c, r), phase, c.rank), e);
+}
 
 }  // namespace
 }  // namespace rs
 
 using namespace rs;
 
+struct StepSets {
+  int ru, ou, par;  // requester / owner scratch sets, gradient-buffer parity
+};
+
+struct DistGraph {
+  rs_table* t;
+  const void *ids, *grads, *out;
+  uint64_t n;
+  int mirror, ru, ou, par;
+  const void* pbuf;
+  unsigned char opt[256];
+  cudaGraphExec_t exec;
+  uint64_t last_use, launches;
+};
+
 struct rs_comm {
   int rank = 0, world = 1;
   uint64_t cap = 0;
   uint32_t dim = 0;
   char* arena = nullptr;
-  size_t arena_bytes = 0, off_ids = 0, off_emb = 0, off_grad = 0;
+  size_t arena_bytes = 0, off_ids = 0, off_emb = 0, off_grad[2] = {0, 0};
   char* h_peers[kMaxWorld] = {nullptr};
   char** d_peers = nullptr;
-  float** d_peer_grad = nullptr;
-  unsigned long long epoch = 0;
+  float** d_peer_grad[2] = {nullptr, nullptr};  // per epoch parity
+  unsigned long long epoch = 0;       // host mirror of the device counter (parity)
+  unsigned long long* d_epoch = nullptr;
   unsigned long long* trace = nullptr;
   unsigned int* done = nullptr;
   uint32_t* send_pos = nullptr;
   uint32_t* send_cnt = nullptr;
-  uint64_t* flat_ids = nullptr;
-  uint32_t* flat_pos = nullptr;
-  uint32_t* d_n2 = nullptr;
+  uint32_t* origins = nullptr;  // owner: [scratch slot][W] origin positions
   TableDev* view = nullptr;
   rs_workspace* ws_req = nullptr;
   rs_workspace* ws_own = nullptr;
-  int req_set = 0, own_set = 0;
+  StepSets last_sets{0, 0, 0};
   uint64_t last_n = 0;
   bool have_forward = false;
   rs_table* last_table = nullptr;
+  // profiling: events at the phase boundaries of one step
+  bool profiling = false;
+  cudaEvent_t pev[20] = {};  // [2 * phase]: begin, [2 * phase + 1]: end
+  unsigned pmask = 0;        // phases recorded in the current step
+  double pms[10] = {};
+  uint64_t pcount = 0;
+  // CUDA graphs of rs_dist_step
+  bool use_graphs = true;
+  bool graph_fork = true;
+  cudaStream_t cap_stream = nullptr;
+  std::vector<DistGraph> graphs;
+  uint64_t graph_clock = 0;
 };
 
-static CommDev comm_dev(rs_comm* c) {
+// phases (rs_comm_phase_ms order) and the event pair that brackets each
+enum : int { kPhReqDedup, kPhSendIds, kPhWaitIds, kPhOwnerTable, kPhRespond, kPhWaitEmbs, kPhGather,
+             kPhReqReduce, kPhWaitGrads, kPhOwnerUpdate, kDistPhases };
+
+static int prof_begin(rs_comm* c, int ph, cudaStream_t s) {
+  if (c->profiling) RS_CUDA(cudaEventRecord(c->pev[2 * ph], s));
+  return RS_OK;
+}
+static int prof_end(rs_comm* c, int ph, cudaStream_t s) {
+  if (!c->profiling) return RS_OK;
+  RS_CUDA(cudaEventRecord(c->pev[2 * ph + 1], s));
+  c->pmask |= 1u << ph;
+  return RS_OK;
+}
+
+static CommDev comm_dev(rs_comm* c, int par) {
   CommDev d;
   d.peers = c->d_peers;
   d.rank = c->rank;
@@ -260,8 +375,8 @@ static CommDev comm_dev(rs_comm* c) {
   d.dim = c->dim;
   d.off_ids = c->off_ids;
   d.off_emb = c->off_emb;
-  d.off_grad = c->off_grad;
-  d.epoch = c->epoch;
+  d.off_grad = c->off_grad[par];
+  d.epoch = c->d_epoch;
   d.trace = c->trace;
   d.done = c->done;
   return d;
@@ -269,11 +384,218 @@ static CommDev comm_dev(rs_comm* c) {
 
 static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
+#define RS_TRY(x)              \
+  do {                         \
+    const int _st = (x);       \
+    if (_st) return _st;       \
+  } while (0)
+
+// ---- the five phases of one sharded step -----------------------------------
+// Enqueue-only (no host state changes, no synchronization) so that a whole
+// step can be captured into a CUDA graph; ru / ou are the scratch sets of the
+// requester / owner workspaces, par the gradient-buffer parity of the step.
+// requester: dedup its tokens, partition the unique ids by owner and store
+// them into the owners' receive lists (KA, KB metadata, k_send_ids)
+static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, StepSets ss,
+                     cudaStream_t s) {
+  rs_workspace* wr = c->ws_req;
+  const CommDev cd = comm_dev(c, ss.par);
+  const int ru = ss.ru;
+  RS_TRY(prof_begin(c, kPhReqDedup, s));
+  if (n) {
+    RS_TRY(step_fdedup(wr, d_ids, n, ru, s, nullptr));
+    RS_TRY(step_ftable(wr, t, ru, n, false, true, s));
+  } else {  // idle rank: still clean the other scratch set (KB) and reset its count (KC)
+    RS_CUDA(cudaMemsetAsync(wr->set[ru].cnt, 0, 4, s));
+    RS_TRY(step_ftable(wr, t, ru, 1, false, true, s));
+    RS_CUDA(cudaMemsetAsync(wr->set[ru ^ 1].cnt, 0, 4, s));
+  }
+  RS_TRY(prof_end(c, kPhReqDedup, s));
+  RS_TRY(prof_begin(c, kPhSendIds, s));
+  k_send_ids<<<grid_for(n ? n : 1, 256, 148 * 4), 256, 0, s>>>(
+      cd, wr->unique, wr->set[ru].cnt, wr->set[ru].u_slot, wr->set[ru].srow, c->send_pos,
+      c->send_cnt, n);
+  RS_LAUNCH_CHECK("k_send_ids");
+  RS_TRY(prof_end(c, kPhSendIds, s));
+  return RS_OK;
+}
+
+// owner: stage-2 dedup straight from the receive lists (KA'), then per
+// owner-unique id find-or-insert on the shard (capacity prepared by the
+// caller) and the row stored into every requester that asked for it (KB')
+static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s) {
+  rs_workspace* wo = c->ws_own;
+  const CommDev cd = comm_dev(c, ss.par);
+  const uint64_t nflat = (uint64_t)c->world * c->cap;
+  const int ou = ss.ou;
+  RS_TRY(prof_begin(c, kPhWaitIds, s));
+  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
+  RS_LAUNCH_CHECK("k_wait(ids)");
+  RS_TRY(prof_end(c, kPhWaitIds, s));
+  RS_TRY(prof_begin(c, kPhOwnerTable, s));
+  k_own_dedup<<<dim3((unsigned)((c->cap + 255) / 256), c->world), 256, 0, s>>>(
+      cd, set_dev(wo, ou), c->origins, wo->unique);
+  RS_LAUNCH_CHECK("k_own_dedup");
+  RS_TRY(prof_end(c, kPhOwnerTable, s));
+  RS_TRY(prof_begin(c, kPhRespond, s));
+  OwnTableArgs a;
+  a.td = t->dev;
+  a.use = set_dev(wo, ou);
+  a.clean = set_dev(wo, ou ^ 1);
+  a.origins = c->origins;
+  a.unique = wo->unique;
+  a.urow = wo->urow;
+  a.u_cnt = wo->u_cnt;
+  a.u_poff = wo->u_poff;
+  a.u_ntile = wo->u_ntile;
+  a.u_ticket = wo->u_ticket;
+  k_own_table<<<grid_for(nflat, 32, 148 * 8), 256, 0, s>>>(cd, a);
+  RS_LAUNCH_CHECK("k_own_table");
+  RS_TRY(prof_end(c, kPhRespond, s));
+  RS_CUDA(cudaMemsetAsync(wo->set[ou ^ 1].cnt, 0, 4, s));  // the cleaned set starts empty
+  return RS_OK;
+}
+
+// requester: wait for the rows, expand them to the tokens (KC gather)
+static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSets ss,
+                      cudaStream_t s) {
+  const CommDev cd = comm_dev(c, ss.par);
+  RS_TRY(prof_begin(c, kPhWaitEmbs, s));
+  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+  RS_LAUNCH_CHECK("k_wait(embs)");
+  RS_TRY(prof_end(c, kPhWaitEmbs, s));
+  RS_TRY(prof_begin(c, kPhGather, s));
+  if (n) {
+    rs_dist_opts o;
+    o.gather_view = c->view;
+    RS_TRY(step_tile(c->ws_req, t, ss.ru, n, d_out, nullptr, true, s, &o));
+  }
+  RS_TRY(prof_end(c, kPhGather, s));
+  return RS_OK;
+}
+
+// requester: per unique id sums of its token gradients (KC + KD), each row
+// stored straight into its owner's grad_in, then the gradient flags
+// (partial-sum buffer prepared by the caller)
+static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n, StepSets ss,
+                      cudaStream_t s) {
+  rs_workspace* wr = c->ws_req;
+  const CommDev cd = comm_dev(c, ss.par);
+  RS_TRY(prof_begin(c, kPhReqReduce, s));
+  if (n) {
+    RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, nullptr));
+    rs_dist_opts o;
+    o.peer_dst = c->d_peer_grad[ss.par];
+    o.send_pos = c->send_pos;
+    o.cap = (uint32_t)c->cap;
+    o.rank = (uint32_t)c->rank;
+    RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &o));
+  }
+  k_signal<<<1, 64, 0, s>>>(cd, 2);
+  RS_LAUNCH_CHECK("k_signal(grads)");
+  RS_TRY(prof_end(c, kPhReqReduce, s));
+  return RS_OK;
+}
+
+// requester, fused step: wait for the rows, then ONE pass over the tokens
+// gathers the rows and segment-reduces the gradients (KC), KD stores each
+// unique id's sum straight into its owner's grad_in, then the gradient flags
+static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
+                             const float* d_grads, StepSets ss, cudaStream_t s) {
+  rs_workspace* wr = c->ws_req;
+  const CommDev cd = comm_dev(c, ss.par);
+  RS_TRY(prof_begin(c, kPhWaitEmbs, s));
+  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+  RS_LAUNCH_CHECK("k_wait(embs)");
+  RS_TRY(prof_end(c, kPhWaitEmbs, s));
+  RS_TRY(prof_begin(c, kPhGather, s));
+  if (n) {
+    rs_dist_opts o;
+    o.gather_view = c->view;
+    RS_TRY(step_tile(wr, t, ss.ru, n, d_out, d_grads, true, s, &o));
+    rs_dist_opts f;
+    f.peer_dst = c->d_peer_grad[ss.par];
+    f.send_pos = c->send_pos;
+    f.cap = (uint32_t)c->cap;
+    f.rank = (uint32_t)c->rank;
+    RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &f));
+  }
+  k_signal<<<1, 64, 0, s>>>(cd, 2);
+  RS_LAUNCH_CHECK("k_signal(grads)");
+  RS_TRY(prof_end(c, kPhGather, s));
+  return RS_OK;
+}
+
+// owner: per id sum over its origins in (source, position) order -- the
+// stage-2 origin order -- fused with the optimizer on the shard
+static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cudaStream_t s) {
+  rs_workspace* wo = c->ws_own;
+  const CommDev cd = comm_dev(c, ss.par);
+  const uint64_t nflat = (uint64_t)c->world * c->cap;
+  RS_TRY(prof_begin(c, kPhWaitGrads, s));
+  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 2);
+  RS_LAUNCH_CHECK("k_wait(grads)");
+  RS_TRY(prof_end(c, kPhWaitGrads, s));
+  RS_TRY(prof_begin(c, kPhOwnerUpdate, s));
+  const float* grad_in = reinterpret_cast<const float*>(c->arena + c->off_grad[ss.par]);
+  rs_dist_opts oo;  // at most `world` origins per id: the CSR finish over the origin rows
+  oo.no_hot = true;
+  oo.csr_pos = c->origins;
+  RS_TRY(step_finish(wo, t, ss.ou, nflat, grad_in, ob, nullptr, s, &oo));
+  RS_TRY(prof_end(c, kPhOwnerUpdate, s));
+  return RS_OK;
+}
+
+static int check_call(rs_comm* c, rs_table* t, uint64_t n, const char* who) {
+  if (!c || !t) return fail(RS_ERR_CONFIG, std::string(who) + ": null handle");
+  if (n > c->cap) return fail(RS_ERR_CONFIG, std::string(who) + ": batch exceeds max_tokens");
+  if (t->desc.dim != c->dim) return fail(RS_ERR_CONFIG, std::string(who) + ": table dim != comm dim");
+  if (t->cfg.max_keys)
+    return fail(RS_ERR_CONFIG, std::string(who) + ": bounded shard tables unsupported");
+  if (c->dim % 4) return fail(RS_ERR_CONFIG, std::string(who) + ": needs embedding_dim % 4 == 0");
+  return step_set_smem_attrs();
+}
+
+// host side of a step, outside any graph: shapes, capacity (may rehash or
+// grow the row pool on s), the partial-sum buffer
+static int prepare_step(rs_comm* c, rs_table* t, uint64_t n_reduce, cudaStream_t s) {
+  c->ws_req->last_tile = c->ws_own->last_tile = tile_tokens_for_dim(c->dim);
+  // new keys at this owner <= ids received <= world * max_tokens (the peers'
+  // batch sizes are not known here without a host round trip)
+  RS_TRY(table_prepare(t, (uint64_t)c->world * c->cap, s));
+  if (n_reduce) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n_reduce, s));
+  return RS_OK;
+}
+static StepSets begin_step(rs_comm* c) {
+  c->epoch++;
+  return StepSets{c->ws_req->cur, c->ws_own->cur, (int)(c->epoch & 1)};
+}
+static void end_step(rs_comm* c, StepSets ss) {
+  c->last_sets = ss;
+  c->ws_req->cur = ss.ru ^ 1;
+  c->ws_own->cur = ss.ou ^ 1;
+}
+
+// end of a step: collect the phase times recorded during it (one sync)
+static int prof_step_done(rs_comm* c) {
+  if (!c->profiling) return RS_OK;
+  for (int ph = 0; ph < kDistPhases; ++ph) {
+    if (!(c->pmask & (1u << ph))) continue;
+    RS_CUDA(cudaEventSynchronize(c->pev[2 * ph + 1]));
+    float ms = 0.f;
+    RS_CUDA(cudaEventElapsedTime(&ms, c->pev[2 * ph], c->pev[2 * ph + 1]));
+    c->pms[ph] += ms;
+  }
+  c->pmask = 0;
+  c->pcount++;
+  return RS_OK;
+}
+
 extern "C" {
 
 int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_comm** out) {
   if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world || dim < 1 ||
-      max_tokens < 1)
+      max_tokens < 1 || max_tokens > (1ull << 30) / (uint64_t)world)
     return fail(RS_ERR_CONFIG, "rs_comm_create: bad rank/world/dim/max_tokens");
   rs_comm* c = new rs_comm();
   c->rank = rank;
@@ -281,37 +603,55 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   c->cap = max_tokens;
   c->dim = dim;
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t rows = (size_t)world * max_tokens;
   c->off_ids = align(sizeof(ArenaHdr));
-  c->off_emb = align(c->off_ids + (size_t)world * max_tokens * 8);
-  c->off_grad = align(c->off_emb + (size_t)world * max_tokens * dim * 4);
-  c->arena_bytes = align(c->off_grad + (size_t)world * max_tokens * dim * 4);
-  const uint64_t nflat = (uint64_t)world * max_tokens;
+  c->off_emb = align(c->off_ids + rows * 8);
+  c->off_grad[0] = align(c->off_emb + rows * dim * 4);
+  c->off_grad[1] = align(c->off_grad[0] + rows * dim * 4);
+  c->arena_bytes = align(c->off_grad[1] + rows * dim * 4);
   bool ok = cudaMalloc(&c->arena, c->arena_bytes) == cudaSuccess &&
             cudaMemset(c->arena, 0, sizeof(ArenaHdr)) == cudaSuccess &&
             cudaMalloc(&c->d_peers, kMaxWorld * sizeof(char*)) == cudaSuccess &&
-            cudaMalloc(&c->d_peer_grad, kMaxWorld * sizeof(float*)) == cudaSuccess &&
+            cudaMalloc(&c->d_peer_grad[0], kMaxWorld * sizeof(float*)) == cudaSuccess &&
+            cudaMalloc(&c->d_peer_grad[1], kMaxWorld * sizeof(float*)) == cudaSuccess &&
             cudaMalloc(&c->trace, kTrN * sizeof(unsigned long long)) == cudaSuccess &&
             cudaMemset(c->trace, 0, kTrN * sizeof(unsigned long long)) == cudaSuccess &&
             cudaMalloc(&c->done, 16) == cudaSuccess && cudaMemset(c->done, 0, 16) == cudaSuccess &&
             cudaMalloc(&c->send_pos, max_tokens * 4) == cudaSuccess &&
             cudaMalloc(&c->send_cnt, kMaxWorld * 4) == cudaSuccess &&
             cudaMemset(c->send_cnt, 0, kMaxWorld * 4) == cudaSuccess &&
-            cudaMalloc(&c->flat_ids, nflat * 8) == cudaSuccess &&
-            cudaMalloc(&c->flat_pos, nflat * 4) == cudaSuccess &&
-            cudaMalloc(&c->d_n2, 16) == cudaSuccess && cudaMalloc(&c->view, sizeof(TableDev)) == cudaSuccess;
+            cudaMalloc(&c->view, sizeof(TableDev)) == cudaSuccess &&
+            cudaMalloc(&c->d_epoch, 8) == cudaSuccess && cudaMemset(c->d_epoch, 0, 8) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
+    rs_comm_destroy(c);
     return fail(RS_ERR_CUDA, "rs_comm_create: cudaMalloc of the arena failed");
   }
   TableDev v;
   std::memset(&v, 0, sizeof(v));
   v.d.emb = reinterpret_cast<float*>(c->arena + c->off_emb);
   v.d.dim = dim;
-  v.d.row_cap = nflat;
-  cudaMemcpy(c->view, &v, sizeof(v), cudaMemcpyHostToDevice);
+  v.d.row_cap = rows;
+  RS_CUDA(cudaMemcpy(c->view, &v, sizeof(v), cudaMemcpyHostToDevice));
   int st = rs_workspace_create(max_tokens, &c->ws_req);
-  if (!st) st = rs_workspace_create(nflat, &c->ws_own);
-  if (st) return st;
+  if (!st) st = rs_workspace_create(rows, &c->ws_own);
+  if (st) {
+    rs_comm_destroy(c);
+    return st;
+  }
+  const uint64_t oslots = (c->ws_own->S + 1) * (uint64_t)world;  // u_poff = slot * W is 32-bit
+  if (oslots > 0xFFFFFFFFull) {
+    rs_comm_destroy(c);
+    return fail(RS_ERR_CONFIG, "rs_comm_create: world * max_tokens too large for the origin rows");
+  }
+  if (cudaMalloc(&c->origins, oslots * 4) != cudaSuccess) {
+    cudaGetLastError();
+    rs_comm_destroy(c);
+    return fail(RS_ERR_CUDA, "rs_comm_create: cudaMalloc of the origin rows failed");
+  }
+  if (const char* e = getenv("RS_NO_GRAPH")) c->use_graphs = e[0] == '0';
+  if (const char* e = getenv("RS_DIST_GRAPH_FORK")) c->graph_fork = e[0] != '0';
+  RS_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
   c->h_peers[rank] = c->arena;
   *out = c;
   return RS_OK;
@@ -335,10 +675,12 @@ int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order
     RS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->h_peers[r] = static_cast<char*>(p);
   }
-  std::vector<float*> g(kMaxWorld, nullptr);
-  for (int r = 0; r < c->world; ++r) g[r] = reinterpret_cast<float*>(c->h_peers[r] + c->off_grad);
   RS_CUDA(cudaMemcpy(c->d_peers, c->h_peers, kMaxWorld * sizeof(char*), cudaMemcpyHostToDevice));
-  RS_CUDA(cudaMemcpy(c->d_peer_grad, g.data(), kMaxWorld * sizeof(float*), cudaMemcpyHostToDevice));
+  for (int b = 0; b < 2; ++b) {
+    std::vector<float*> g(kMaxWorld, nullptr);
+    for (int r = 0; r < c->world; ++r) g[r] = reinterpret_cast<float*>(c->h_peers[r] + c->off_grad[b]);
+    RS_CUDA(cudaMemcpy(c->d_peer_grad[b], g.data(), kMaxWorld * sizeof(float*), cudaMemcpyHostToDevice));
+  }
   return RS_OK;
 }
 
@@ -347,104 +689,41 @@ int rs_comm_destroy(rs_comm* c) {
   cudaDeviceSynchronize();
   for (int r = 0; r < c->world; ++r)
     if (r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
-  void* ps[] = {c->arena, c->d_peers, c->d_peer_grad, c->trace, c->done, c->send_pos,
-                c->send_cnt, c->flat_ids, c->flat_pos, c->d_n2, c->view};
+  void* ps[] = {c->arena, c->d_peers, c->d_peer_grad[0], c->d_peer_grad[1], c->trace, c->done,
+                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch};
   for (void* p : ps)
     if (p) cudaFree(p);
+  for (auto& e : c->pev)
+    if (e) cudaEventDestroy(e);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   rs_workspace_destroy(c->ws_req);
   rs_workspace_destroy(c->ws_own);
   delete c;
   return RS_OK;
 }
 
-// Forward of the sharded step: this rank's tokens d_ids[n] against the
-// shard table `t` it owns.  Every rank of the group must call it for the
-// same step.  d_out [n x dim] = bit-exact distributed_lookup outputs.
+// distributed_lookup (exchange_sim.cpp:117-233, two-stage) for this rank's
+// tokens against the shard it owns.  Every rank of the group must call it
+// for the same step.  d_out [n x dim] = bit-exact outputs[rank].
 int rs_dist_forward(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, float* d_out,
                     void* stream) {
-  if (!c || !t) return fail(RS_ERR_CONFIG, "rs_dist_forward: null handle");
-  if (n > c->cap) return fail(RS_ERR_CONFIG, "rs_dist_forward: batch exceeds max_tokens");
-  if (t->desc.dim != c->dim) return fail(RS_ERR_CONFIG, "rs_dist_forward: table dim != comm dim");
-  if (t->cfg.max_keys) return fail(RS_ERR_CONFIG, "rs_dist_forward: bounded shard tables unsupported");
+  RS_TRY(check_call(c, t, n, "rs_dist_forward"));
   cudaStream_t s = S(stream);
-  int st = step_set_smem_attrs();
-  if (st) return st;
-  c->epoch++;
-  const CommDev cd = comm_dev(c);
-  rs_workspace* wr = c->ws_req;
-  rs_workspace* wo = c->ws_own;
-  const uint64_t nflat = (uint64_t)c->world * c->cap;
-  // ---- requester: dedup, metadata for the backward, ids to the owners
-  wr->last_tile = tile_tokens_for_dim(c->dim);
-  const int ru = wr->cur;
-  if (n) {
-    if ((st = step_fdedup(wr, d_ids, n, ru, s, nullptr))) return st;
-    if ((st = step_ftable(wr, t, ru, n, false, true, s))) return st;
-  } else {  // idle rank: still clean the other scratch set (KB) and reset its count (KC)
-    RS_CUDA(cudaMemsetAsync(wr->set[ru].cnt, 0, 4, s));
-    if ((st = step_ftable(wr, t, ru, 1, false, true, s))) return st;
-    RS_CUDA(cudaMemsetAsync(wr->set[ru ^ 1].cnt, 0, 4, s));
-  }
-  k_send_ids<<<grid_for(n ? n : 1, 256, 148 * 4), 256, 0, s>>>(
-      cd, wr->unique, wr->set[ru].cnt, wr->set[ru].u_slot, wr->set[ru].srow, c->send_pos,
-      c->send_cnt, n);
-  RS_LAUNCH_CHECK("k_send_ids");
-  // ---- owner: stage-2 dedup of what it received, find-or-insert, respond
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
-  RS_LAUNCH_CHECK("k_wait(ids)");
-  k_flatten<<<c->world, 256, 0, s>>>(cd, c->flat_ids, c->flat_pos, c->d_n2);
-  RS_LAUNCH_CHECK("k_flatten");
-  wo->last_tile = tile_tokens_for_dim(c->dim);
-  const int ou = wo->cur;
-  // new keys at this owner <= ids received <= world * max_tokens (the peers'
-  // batch sizes are not known here without a host round trip)
-  if ((st = table_prepare(t, nflat, s))) return st;
-  if ((st = step_fdedup(wo, c->flat_ids, nflat, ou, s, c->d_n2))) return st;
-  if ((st = step_ftable(wo, t, ou, nflat, true, true, s))) return st;
-  {
-    const uint32_t d4 = c->dim / 4;
-    const unsigned grid = grid_for(nflat / 8 + 1, 8, 148 * 8);
-#define RS_RESP(LPR)                                                                   \
-  k_respond<LPR><<<grid, 256, 0, s>>>(cd, t->dev, wo->slot_of, wo->set[ou].srow, c->flat_pos, \
-                                      c->d_n2, wo->set[ou].cnt)
-    if (c->dim % 4 != 0) return fail(RS_ERR_CONFIG, "sharded step needs dim % 4 == 0");
-    if (d4 >= 32)
-      RS_RESP(32);
-    else if (d4 >= 16)
-      RS_RESP(16);
-    else if (d4 >= 8)
-      RS_RESP(8);
-    else if (d4 >= 4)
-      RS_RESP(4);
-    else if (d4 >= 2)
-      RS_RESP(2);
-    else
-      RS_RESP(1);
-#undef RS_RESP
-    RS_LAUNCH_CHECK("k_respond");
-  }
-  // clean-up bookkeeping of the owner workspace (KC normally zeroes the other count)
-  RS_CUDA(cudaMemsetAsync(wo->set[ou ^ 1].cnt, 0, 4, s));
-  if ((st = table_after_op(t, s))) return st;
-  // ---- requester: gather from the received rows
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
-  RS_LAUNCH_CHECK("k_wait(embs)");
-  if (n) {
-    rs_dist_opts o;
-    o.gather_view = c->view;
-    if ((st = step_tile(wr, t, ru, n, d_out, nullptr, true, s, &o))) return st;
-  }
-  c->req_set = ru;
-  c->own_set = ou;
-  wr->cur ^= 1;
-  wo->cur ^= 1;
+  RS_TRY(prepare_step(c, t, 0, s));
+  const StepSets ss = begin_step(c);
+  RS_TRY(req_front(c, t, d_ids, n, ss, s));
+  RS_TRY(owner_lookup(c, t, ss, s));
+  RS_TRY(table_after_op(t, s));
+  RS_TRY(req_gather(c, t, n, d_out, ss, s));
+  end_step(c, ss);
   c->last_n = n;
   c->last_table = t;
   c->have_forward = true;
   return RS_OK;
 }
 
-// Backward of the sharded step: this rank's token gradients d_grads[n x dim].
+// Backward of the last forward: this rank's token gradients d_grads[n x dim].
 int rs_dist_backward(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
                      const rs_optimizer_params* opt, void* stream) {
   if (!c || !t) return fail(RS_ERR_CONFIG, "rs_dist_backward: null handle");
@@ -452,37 +731,120 @@ int rs_dist_backward(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
     return fail(RS_ERR_CONFIG, "rs_dist_backward: must follow rs_dist_forward on the same batch");
   cudaStream_t s = S(stream);
   alignas(16) unsigned char ob[256];
-  int st = step_opt_args(t, opt, ob, s);
-  if (st) return st;
-  const CommDev cd = comm_dev(c);
-  rs_workspace* wr = c->ws_req;
-  rs_workspace* wo = c->ws_own;
-  const uint64_t nflat = (uint64_t)c->world * c->cap;
-  // ---- requester: per unique id sums, stored into the owners' grad_in
-  if (n) {
-    if ((st = step_reduce_prepare(wr, c->dim, n, s))) return st;
-    if ((st = step_tile(wr, t, c->req_set, n, nullptr, d_grads, false, s, nullptr))) return st;
-    rs_dist_opts o;
-    o.peer_dst = c->d_peer_grad;
-    o.send_pos = c->send_pos;
-    o.cap = (uint32_t)c->cap;
-    o.rank = (uint32_t)c->rank;
-    if ((st = step_finish(wr, t, c->req_set, n, d_grads, nullptr, nullptr, s, &o))) return st;
-  }
-  k_signal<<<1, 64, 0, s>>>(cd, 2);
-  RS_LAUNCH_CHECK("k_signal(grads)");
-  // ---- owner: ordered sum over origins + optimizer on the shard
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 2);
-  RS_LAUNCH_CHECK("k_wait(grads)");
-  const float* grad_in = reinterpret_cast<const float*>(c->arena + c->off_grad);
-  rs_dist_opts oo;  // owner side: at most `world` origins per id -> CSR path only
-  oo.d_n = c->d_n2;
-  oo.pos_map = c->flat_pos;
-  oo.no_stage = true;
-  if ((st = step_tile(wo, t, c->own_set, nflat, nullptr, grad_in, false, s, &oo))) return st;
-  if ((st = step_finish(wo, t, c->own_set, nflat, grad_in, ob, nullptr, s, nullptr))) return st;
+  std::memset(ob, 0, sizeof(ob));
+  RS_TRY(step_opt_args(t, opt, ob, s));
+  if (n) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n, s));
+  RS_TRY(req_reduce(c, t, d_grads, n, c->last_sets, s));
+  RS_TRY(owner_update(c, t, ob, c->last_sets, s));
   t->applies++;
   c->have_forward = false;
+  return prof_step_done(c);
+}
+
+// The whole step in one call: ids out, owner lookup + answer, then one fused
+// gather + segment-reduce pass over this rank's tokens whose per-id sums go
+// straight to the owners, then the owner update.  Identical results to
+// rs_dist_forward + rs_dist_backward (the owner answers with the rows as they
+// were before this step's update).  Replayed from a CUDA graph per
+// (buffers, n, parities) -- the flags' epoch lives on the device.
+int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
+                 float* d_out, const rs_optimizer_params* opt, void* stream) {
+  RS_TRY(check_call(c, t, n, "rs_dist_step"));
+  cudaStream_t s = S(stream);
+  alignas(16) unsigned char ob[256];
+  std::memset(ob, 0, sizeof(ob));
+  RS_TRY(step_opt_args(t, opt, ob, s));
+  RS_TRY(prepare_step(c, t, n, s));
+  const StepSets ss = begin_step(c);
+  const int mirror = t->mirror_next;
+  auto enqueue = [&](cudaStream_t q) -> int {
+    RS_TRY(req_front(c, t, d_ids, n, ss, q));
+    RS_TRY(owner_lookup(c, t, ss, q));
+    RS_TRY(table_mirror_copy(t, mirror, q));
+    RS_TRY(req_gather_reduce(c, t, n, d_out, d_grads, ss, q));
+    return owner_update(c, t, ob, ss, q);
+  };
+  if (c->profiling || !c->use_graphs) {
+    RS_TRY(enqueue(s));
+  } else {
+    DistGraph* hit = nullptr;
+    for (auto& g : c->graphs)
+      if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
+          g.mirror == mirror && g.ru == ss.ru && g.ou == ss.ou && g.par == ss.par &&
+          g.pbuf == c->ws_req->pbuf && std::memcmp(g.opt, ob, sizeof(ob)) == 0) {
+        hit = &g;
+        break;
+      }
+    if (!hit) {
+      if (c->graphs.size() >= 16) {  // evict the least recently used
+        auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                    [](const DistGraph& x, const DistGraph& y) {
+                                      return x.last_use < y.last_use;
+                                    });
+        cudaGraphExecDestroy(lru->exec);
+        c->graphs.erase(lru);
+      }
+      DistGraph e;
+      e.t = t;
+      e.ids = d_ids;
+      e.grads = d_grads;
+      e.out = d_out;
+      e.n = n;
+      e.mirror = mirror;
+      e.ru = ss.ru;
+      e.ou = ss.ou;
+      e.par = ss.par;
+      e.pbuf = c->ws_req->pbuf;
+      std::memcpy(e.opt, ob, sizeof(ob));
+      // hot-id finish as a forked graph branch (RS_DIST_GRAPH_FORK=0: linear)
+      const bool f0 = c->ws_req->fork, f1 = c->ws_own->fork;
+      c->ws_req->fork = c->ws_req->fork && c->graph_fork;
+      c->ws_own->fork = false;
+      const uint64_t before = launches();
+      RS_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const int st = enqueue(c->cap_stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
+      c->ws_req->fork = f0;
+      c->ws_own->fork = f1;
+      if (st) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
+      e.launches = launches() - before;
+      count_launch(0 - e.launches);  // capture only recorded the launches
+      c->graphs.push_back(e);
+      hit = &c->graphs.back();
+    }
+    hit->last_use = ++c->graph_clock;
+    RS_CUDA(cudaGraphLaunch(hit->exec, s));
+    count_launch(hit->launches);
+  }
+  RS_TRY(table_mirror_commit(t, mirror, s));
+  end_step(c, ss);
+  t->applies++;
+  c->have_forward = false;
+  return prof_step_done(c);
+}
+
+int rs_comm_set_profiling(rs_comm* c, int on) {
+  if (!c) return fail(RS_ERR_CONFIG, "rs_comm_set_profiling: null comm");
+  if (on && !c->pev[0])
+    for (auto& e : c->pev) RS_CUDA(cudaEventCreate(&e));
+  c->profiling = on != 0;
+  for (auto& m : c->pms) m = 0;
+  c->pcount = 0;
+  return RS_OK;
+}
+
+int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count) {
+  if (!c || !ms) return fail(RS_ERR_CONFIG, "rs_comm_phase_ms: null argument");
+  for (int k = 0; k < n && k < kDistPhases; ++k) ms[k] = c->pcount ? c->pms[k] / c->pcount : 0.0;
+  if (count) *count = c->pcount;
   return RS_OK;
 }
 

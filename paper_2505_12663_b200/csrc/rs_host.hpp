@@ -18,6 +18,7 @@ struct rs_mirror {
 };
 
 struct rs_table {
+  uint64_t host_syncs = 0;  // read_counters calls (stream syncs)
   rs_table_config cfg{};
   rs::TableDev* dev = nullptr;   // device descriptor + counters
   rs::TableDesc desc{};          // host copy of the pointer section
@@ -122,6 +123,8 @@ struct rs_dist_opts {
   const uint32_t* d_n = nullptr;        // device token count (owner side); null: host n
   const uint32_t* pos_map = nullptr;    // CSR position of each token (owner: origin slot)
   bool no_stage = false;                // no hot ids possible: no gradient staging
+  bool no_hot = false;                  // finish: skip the hot-id kernel (none possible)
+  const uint32_t* csr_pos = nullptr;    // finish: CSR position array (null: the workspace's)
   const void* gather_view = nullptr;    // rs::TableDev* whose emb = requester receive buffer
   float* const* peer_dst = nullptr;     // device [W] peer gradient receive bases
   const uint32_t* send_pos = nullptr;   // per unique id: owner * cap + position

@@ -34,6 +34,7 @@
 
 #include "opt_dev.cuh"
 #include "rs_host.hpp"
+#include "scratch_dev.cuh"
 #include "table_dev.cuh"
 
 namespace rs {
@@ -41,6 +42,7 @@ namespace {
 
 using namespace odev;
 using namespace tdev;
+using namespace sdev;
 
 constexpr uint32_t kCsrMax = 64;  // ids with at most this many occurrences: exact-order CSR path
 
@@ -60,31 +62,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// Device view of one scratch set (see rs_scratch in rs_host.hpp).
-struct SetDev {
-  unsigned long long* skey;
-  uint32_t* sfirstx;  // exact dedup: ~first position; fast step: occurrence count
-  uint32_t* sntile;   // tiles containing the id
-  uint32_t* suidx;    // unique index of the slot
-  uint32_t* srow;     // table row of the slot
-  uint32_t* u_slot;   // slot of each unique id (= the set's dirty list)
-  uint32_t* cnt;      // [0] number of unique ids in the set
-  uint64_t smask;     // capacity - 1
-  uint64_t spare;     // slot of the id equal to the empty sentinel
-};
-
-// ---------------------------------------------------------------------------
-// Scratch cleaning: reset the slots listed by a set's dirty list.
-__device__ __forceinline__ void clean_set(const SetDev& c, uint64_t gtid, uint64_t gthreads) {
-  const uint32_t prev = *c.cnt;
-  for (uint64_t i = gtid; i <= prev; i += gthreads) {
-    const uint64_t s = i < prev ? c.u_slot[i] : c.spare;
-    c.skey[s] = kEmptyKey;
-    c.sfirstx[s] = 0;
-    c.sntile[s] = 0;
-  }
-}
-
 __global__ void k_clean(SetDev c) {
   clean_set(c, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
 }
@@ -97,29 +74,6 @@ __global__ void k_clear_all(SetDev c, uint64_t n) {
     c.sntile[i] = 0;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) *c.cnt = 0;
-}
-
-// Probe the global scratch for `id` (linear probing on the low hash bits),
-// claiming an empty slot.  Returns the slot; *fresh = slot newly claimed.
-__device__ __forceinline__ uint64_t scratch_insert(const SetDev& S, uint64_t id, uint64_t h,
-                                                   bool* fresh) {
-  if (id == kEmptyKey) {
-    *fresh = atomicCAS(&S.skey[S.spare], kEmptyKey, 0ull) == kEmptyKey;
-    return S.spare;
-  }
-  uint64_t gs = h & S.smask;
-  for (;;) {
-    const unsigned long long prev = atomicCAS(&S.skey[gs], kEmptyKey, (unsigned long long)id);
-    if (prev == kEmptyKey) {
-      *fresh = true;
-      return gs;
-    }
-    if (prev == id) {
-      *fresh = false;
-      return gs;
-    }
-    gs = (gs + 1) & S.smask;
-  }
 }
 
 // Block-local dedup of the tile's ids in smem.  Returns the local slot of the
@@ -302,64 +256,8 @@ __global__ void __launch_bounds__(256) k_ftable(FTableArgs a) {
       if (hot) a.hot_list[atomicAdd(&a.ctr[kCtrNHot], 1u)] = i;
     }
     if (!a.do_table || !active) continue;
-    uint32_t row = kNoRow;
-    const int sp = key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
-    if (sp >= 0) {
-      uint32_t r = kNoRow;
-      int fresh = 0;
-      if (g == 0) {
-        r = td->c.special_row[sp];
-        if (r == kNoRow) {
-          const uint32_t nr = alloc_row(td, free_n0, fresh0, d.row_cap);
-          if (nr != kNoRow) {
-            const unsigned int prev = atomicCAS(&td->c.special_row[sp], kNoRow, nr);
-            r = prev == kNoRow ? nr : prev;
-            fresh = prev == kNoRow;
-            if (fresh) atomicAdd(&s_ins, 1ull);
-          }
-        }
-        if (r != kNoRow) td->c.special_tick[sp] = tick_now;
-      }
-      r = __shfl_sync(gmask, r, gbase);
-      fresh = __shfl_sync(gmask, fresh, gbase);
-      if (fresh) init_row(d, r, nullptr, g);
-      row = r;
-    } else {
-      uint32_t new_row = kNoRow;
-      for (;;) {
-        const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
-        if (p.found) {
-          row = p.row;
-          if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
-          break;
-        }
-        if (p.ins == ~0ull) {
-          if (g == 0) atomicOr(&td->c.error, kErrTableFull);
-          break;
-        }
-        if (new_row == kNoRow) {
-          uint32_t r = 0;
-          if (g == 0) r = alloc_row(td, free_n0, fresh0, d.row_cap);
-          new_row = __shfl_sync(gmask, r, gbase);
-          if (new_row == kNoRow) break;
-        }
-        int ok = 0;
-        if (g == 0) {
-          const unsigned long long expect = p.ins_tomb ? kTombKey : kEmptyKey;
-          ok = atomicCAS(&d.slots[p.ins].key, expect, (unsigned long long)key) == expect;
-        }
-        ok = __shfl_sync(gmask, ok, gbase);
-        if (!ok) continue;
-        if (g == 0) {
-          *reinterpret_cast<uint2*>(&d.slots[p.ins].row) = make_uint2(new_row, tick_now);
-          atomicAdd(&s_ins, 1ull);
-          if (p.ins_tomb) atomicAdd(&s_reuse, 1ull);
-        }
-        init_row(d, new_row, nullptr, g);
-        row = new_row;
-        break;
-      }
-    }
+    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0,
+                                              &s_ins, &s_reuse);
     if (g == 0) {
       a.urow[i] = row;
       a.urow64[i] = row == kNoRow ? -1 : (int64_t)row;
@@ -858,7 +756,6 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     *reinterpret_cast<float4*>(d.s2 + roff) = vv;
     if (d.s1) *reinterpret_cast<float4*>(d.s1 + roff) = mv;
   }
-  if (a.peer_dst) asm volatile("fence.acq_rel.sys;" ::: "memory");  // publish peer stores
 }
 
 // Roles by block index:
@@ -910,7 +807,6 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
       else
         apply_row<VEC, CH>(d, row, acc, o);
     }
-    if (a.peer_dst) asm volatile("fence.acq_rel.sys;" ::: "memory");
     return;
   }
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem2);  // [bw]
@@ -1186,20 +1082,6 @@ uint32_t tile_tokens_for_dim(uint32_t D) {
 }
 
 // ---- host side -------------------------------------------------------------
-static SetDev set_dev(rs_workspace* ws, int k) {
-  const rs_scratch& x = ws->set[k];
-  SetDev s;
-  s.skey = x.skey;
-  s.sfirstx = x.sfirstx;
-  s.sntile = x.sntile;
-  s.suidx = x.suidx;
-  s.srow = x.srow;
-  s.u_slot = x.u_slot;
-  s.cnt = x.cnt;
-  s.smask = ws->S - 1;
-  s.spare = ws->S;
-  return s;
-}
 
 // every k_ftile / k_finish instantiation opts in to large dynamic smem once
 template <int V, int C, int LPR>
@@ -1356,7 +1238,7 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   a.u_ticket = ws->u_ticket;
   a.urow = ws->urow;
   a.grads = d_grads;
-  a.csr_pos = ws->csr_pos;
+  a.csr_pos = (dopt && dopt->csr_pos) ? dopt->csr_pos : ws->csr_pos;
   a.pbuf = ws->pbuf;
   a.ptile = ws->ptile;
   a.porder = ws->porder;
@@ -1368,7 +1250,7 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   a.cap = dopt ? dopt->cap : 0;
   a.rank = dopt ? dopt->rank : 0;
   a.dbg_nrows = (dopt && dopt->d_n) ? ws->max_tokens : n;
-  a.dbg_ncsr = ws->max_tokens;
+  a.dbg_ncsr = (dopt && dopt->csr_pos) ? ~0ull : ws->max_tokens;
   const uint32_t hot_blocks = 2 * 148;
   const size_t smem = std::max<size_t>((size_t)8 * kCsrMax * 4,
                                        (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
@@ -1377,13 +1259,14 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   // G > 0: CSR ids on s, hot ids concurrently on the forked aux stream
   const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
   cudaStream_t hs = s;
-  if (G > 0 && ws->fork) {
+  const bool fork = G > 0 && ws->fork && !(dopt && dopt->no_hot);
+  if (fork) {
     RS_CUDA(cudaEventRecord(ws->ev_fork, s));
     RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, ws->ev_fork, 0));
     hs = ws->aux_stream;
   }
   const Shape sh = shape_for(D);
-  bool launched = false;
+  bool launched = G > 0 && dopt && dopt->no_hot;  // owner side: no hot ids possible
 #define RS_FIN(V, C)                                                   \
   if (!launched && sh.vec == V && sh.ch == C) {                        \
     k_finish<V, C><<<grid, 256, smem, hs>>>(a, o, hot_blocks);         \
@@ -1405,7 +1288,7 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   }
     RS_CSR(32) RS_CSR(16) RS_CSR(8) RS_CSR(4) RS_CSR(2)
 #undef RS_CSR
-    if (ws->fork) {
+    if (fork) {
       RS_CUDA(cudaEventRecord(ws->ev_join, ws->aux_stream));
       RS_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));  // join
     }

@@ -386,6 +386,7 @@ int alloc_rows(rs_table* t, uint64_t new_cap, cudaStream_t s) {
 }
 
 int read_counters(rs_table* t, TableCounters* out, cudaStream_t s) {
+  t->host_syncs++;
   RS_CUDA(cudaStreamSynchronize(s));
   RS_CUDA(cudaMemcpy(out, &t->dev->c, sizeof(TableCounters), cudaMemcpyDeviceToHost));
   if (out->error) {
@@ -752,9 +753,11 @@ int rs_table_stats(rs_table* t, rs_table_info* out) {
   if (!t || !out) return fail(RS_ERR_CONFIG, "rs_table_stats: null argument");
   TableCounters c;
   int st = read_counters(t, &c, nullptr);
+  t->host_syncs--;  // the stats call itself is not bookkeeping
   RS_CUDA(cudaDeviceSynchronize());
   RS_CUDA(cudaMemcpy(&c, &t->dev->c, sizeof(c), cudaMemcpyDeviceToHost));
   if (st) return st;
+  out->host_syncs = t->host_syncs;
   out->capacity = t->capacity;
   out->occupied = c.occupied;
   out->tombstones = c.tombstones;

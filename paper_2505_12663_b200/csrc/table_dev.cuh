@@ -120,6 +120,77 @@ __device__ __forceinline__ void copy_row_group(const TableDesc& d, uint32_t row,
   }
 }
 
+// Find-or-insert-zero of one key by an 8-lane group (grouped bucket probing;
+// keys must be distinct within a launch).  Returns the row (kNoRow on a full
+// table / exhausted row pool, with the error bit set); stamps the batch tick.
+__device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const TableDesc& d,
+                                                         uint64_t key, unsigned g, unsigned gbase,
+                                                         unsigned gmask, uint32_t tick_now,
+                                                         unsigned long long free_n0,
+                                                         unsigned long long fresh0,
+                                                         unsigned long long* s_ins,
+                                                         unsigned long long* s_reuse) {
+  uint32_t row = kNoRow;
+  const int sp = key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
+  if (sp >= 0) {
+    uint32_t r = kNoRow;
+    int fresh = 0;
+    if (g == 0) {
+      r = td->c.special_row[sp];
+      if (r == kNoRow) {
+        const uint32_t nr = alloc_row(td, free_n0, fresh0, d.row_cap);
+        if (nr != kNoRow) {
+          const unsigned int prev = atomicCAS(&td->c.special_row[sp], kNoRow, nr);
+          r = prev == kNoRow ? nr : prev;
+          fresh = prev == kNoRow;
+          if (fresh) atomicAdd(s_ins, 1ull);
+        }
+      }
+      if (r != kNoRow) td->c.special_tick[sp] = tick_now;
+    }
+    r = __shfl_sync(gmask, r, gbase);
+    fresh = __shfl_sync(gmask, fresh, gbase);
+    if (fresh) init_row(d, r, nullptr, g);
+    row = r;
+  } else {
+    uint32_t new_row = kNoRow;
+    for (;;) {
+      const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
+      if (p.found) {
+        row = p.row;
+        if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
+        break;
+      }
+      if (p.ins == ~0ull) {
+        if (g == 0) atomicOr(&td->c.error, kErrTableFull);
+        break;
+      }
+      if (new_row == kNoRow) {
+        uint32_t r = 0;
+        if (g == 0) r = alloc_row(td, free_n0, fresh0, d.row_cap);
+        new_row = __shfl_sync(gmask, r, gbase);
+        if (new_row == kNoRow) break;
+      }
+      int ok = 0;
+      if (g == 0) {
+        const unsigned long long expect = p.ins_tomb ? kTombKey : kEmptyKey;
+        ok = atomicCAS(&d.slots[p.ins].key, expect, (unsigned long long)key) == expect;
+      }
+      ok = __shfl_sync(gmask, ok, gbase);
+      if (!ok) continue;
+      if (g == 0) {
+        *reinterpret_cast<uint2*>(&d.slots[p.ins].row) = make_uint2(new_row, tick_now);
+        atomicAdd(s_ins, 1ull);
+        if (p.ins_tomb) atomicAdd(s_reuse, 1ull);
+      }
+      init_row(d, new_row, nullptr, g);
+      row = new_row;
+      break;
+    }
+  }
+  return row;
+}
+
 // Last-block epilogue: folds this launch's per-launch counters into the
 // table counters (the "fix-up" of the lock-free row allocator).
 __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,

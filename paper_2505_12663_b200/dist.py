@@ -18,7 +18,7 @@ import torch.distributed as dist
 
 from . import _lib as L
 from ._lib import check
-from .table import EmbedTable, TableConfig, _ptr, _stream, as_keys
+from .table import EmbedTable, TableConfig, _ptr, _stream, as_keys, shard_of_batch
 
 
 def exchange_handles(handle: bytes, group=None) -> list[bytes]:
@@ -45,16 +45,16 @@ class ShardedTable:
         buf = (C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
         check(L.lib().rs_comm_open(self._c, buf), "rs_comm_open")
 
-    def owner_of(self, keys: np.ndarray) -> np.ndarray:
-        from .table import hash64_batch, keys_to_numpy
-        return (keys_to_numpy(hash64_batch(keys)) % np.uint64(self.world)).astype(np.int64)
+    def owner_of(self, keys) -> torch.Tensor:
+        """shard_of(id, W) = hash64(id) % W per key (exchange_sim.cpp:82-85), on the device."""
+        return shard_of_batch(keys, self.world)
 
     def insert_owned(self, keys, emb: torch.Tensor) -> None:
         """Insert the rows whose keys this rank owns (keys/emb given for all ranks)."""
-        keys = np.asarray(keys, np.uint64)
-        mine = np.nonzero(self.owner_of(keys) == self.rank)[0]
-        if len(mine):
-            self.shard.insert(keys[mine], emb[torch.from_numpy(mine).to(emb.device)])
+        k = as_keys(keys)
+        mine = torch.nonzero(self.owner_of(k) == self.rank).flatten()
+        if mine.numel():
+            self.shard.insert(k[mine], emb.to("cuda")[mine])
 
     def forward(self, ids, out: torch.Tensor | None = None) -> torch.Tensor:
         k = as_keys(ids)
@@ -68,6 +68,16 @@ class ShardedTable:
         g = grads.contiguous()
         check(L.lib().rs_dist_backward(self._c, self.shard.handle, _ptr(g), g.shape[0], C.byref(params.c()),
                                        _stream()), "rs_dist_backward")
+
+    def step(self, ids, grads: torch.Tensor, params, out: torch.Tensor | None = None) -> torch.Tensor:
+        """forward + backward in one call (rs_dist_step); returns the gathered rows."""
+        k = as_keys(ids)
+        g = grads.contiguous()
+        if out is None:
+            out = torch.empty((k.numel(), self.dim), dtype=torch.float32, device="cuda")
+        check(L.lib().rs_dist_step(self._c, self.shard.handle, _ptr(k), k.numel(), _ptr(g), _ptr(out),
+                                   C.byref(params.c()), _stream()), "rs_dist_step")
+        return out
 
     def trace_row(self) -> dict:
         ids = np.zeros(self.world, np.uint64)
@@ -86,6 +96,20 @@ class ShardedTable:
                     lookups=np.array([r["lookups"] for r in rows], np.uint64),
                     ids_requested=sum(r["ids_requested"] for r in rows),
                     ids_received=sum(r["ids_received"] for r in rows))
+
+    # phases of rs_comm_phase_ms; in the fused step "gather" is the fused
+    # gather + segment-reduce + sums-to-owners pass and "req_reduce" is 0
+    PHASES = ("req_dedup", "send_ids", "wait_ids", "owner_dedup", "owner_table_respond", "wait_embs", "gather",
+              "req_reduce", "wait_grads", "owner_update")
+
+    def set_profiling(self, on: bool) -> None:
+        check(L.lib().rs_comm_set_profiling(self._c, int(on)), "rs_comm_set_profiling")
+
+    def phase_ms(self) -> dict:
+        ms = (C.c_double * len(self.PHASES))()
+        cnt = C.c_uint64()
+        check(L.lib().rs_comm_phase_ms(self._c, ms, len(self.PHASES), C.byref(cnt)), "rs_comm_phase_ms")
+        return {k: ms[i] for i, k in enumerate(self.PHASES)}
 
     def close(self):
         if self._c:

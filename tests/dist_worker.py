@@ -61,7 +61,7 @@ def main():
             o.table_insert(o.cluster_shard(cl, s), int(k), np.ascontiguousarray(e))
 
     pool = np.concatenate([keys, fresh])
-    for step in range(5):
+    for step in range(6):
         counts = [int(rng.integers(1, max_tokens)) for _ in range(W)]
         if step == 2:
             counts[W - 1] = 0  # an idle rank still takes part in the exchange
@@ -72,8 +72,12 @@ def main():
                 for n in counts]
         grads = [(rng.integers(-64, 64, (n, dim)) / 64.0).astype(np.float32) for n in counts]
         ids_t = torch.from_numpy(reqs[rank].astype(np.uint64).view(np.int64)).cuda()
-        out = st.forward(ids_t)
-        st.backward(torch.from_numpy(grads[rank]).cuda(), params)
+        g_t = torch.from_numpy(grads[rank]).cuda()
+        if step % 2 == 0:  # the split API (distributed_lookup, then accumulate/apply) ...
+            out = st.forward(ids_t)
+            st.backward(g_t, params)
+        else:  # ... and the fused step must give identical results
+            out = st.step(ids_t, g_t, params)
         tr = st.trace()
         outs = [None] * W
         dist.all_gather_object(outs, out.cpu().numpy())
