@@ -127,7 +127,7 @@ def run_ours(args, cfg):
     table.insert(raw + int(TAG1), init)
     del init
     # distinct batches (weak scaling: each rank its own seed stream)
-    nb = max(1, min(args.steps + args.warmup, 6))
+    nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
     batches = []
     for b in range(nb):
         lengths, ids = W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"],
@@ -148,6 +148,9 @@ def run_ours(args, cfg):
         d_ids, d_g, out = dev[b % nb]
         step.step(d_ids, d_g, out)
 
+    # warm-up: at least W steps and every batch once (one CUDA graph per
+    # batch buffer set is captured on first use -- never inside the timed region)
+    args.warmup = max(args.warmup, nb)
     for w in range(args.warmup):
         one(w)
     torch.cuda.synchronize()
@@ -161,11 +164,13 @@ def run_ours(args, cfg):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.rs_kernel_launches()
     with Clocks(local) as clk:
+        h0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
             one(args.warmup + k)
             evs[k][1].record(stream)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host enqueue time per step
         torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
     times = [a.elapsed_time(b) for a, b in evs]
@@ -230,6 +235,7 @@ def run_ours(args, cfg):
                    "parallelism": "replicas" if world > 1 else "single",
                    "l2": "flushed (512 MiB write) between timed steps"},
         "tokens_per_s": toks_job / t_job,
+        "host_enqueue_ms_per_step": host_ms,
         "step_hbm_gbs": step_bytes * world / (t_job / args.steps) / 1e9,
         "step_roofline_frac": step_bytes / (t_job / args.steps) / 1e9 / hbm,
         "kernel_ms": phases,
@@ -273,7 +279,7 @@ def run_sharded(args, cfg):
     os.environ.setdefault("WORLD_SIZE", "1")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dim, vocab = cfg["dim"], cfg["vocab"]
-    nb = max(1, min(args.steps + args.warmup, 6))
+    nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
     batches = [W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
                           cfg["zipf"], [vocab]) for b in range(nb)]
     mt = torch.tensor([max(len(i) for _, i in batches)], dtype=torch.int64, device="cuda")
@@ -297,6 +303,7 @@ def run_sharded(args, cfg):
         d_ids, d_g, out = dev[b % nb]
         st.step(d_ids, d_g, params, out)
 
+    args.warmup = max(args.warmup, nb)  # every batch's graph captured before timing
     for w in range(args.warmup):
         one(w)
     torch.cuda.synchronize()
@@ -305,14 +312,19 @@ def run_sharded(args, cfg):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.rs_kernel_launches()
     with Clocks(local) as clk:
+        h0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             evs[k][0].record(stream)
             one(args.warmup + k)
             evs[k][1].record(stream)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host enqueue time per step
         torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
     step_ms = [a.elapsed_time(b) for a, b in evs]
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, {"sum_ms": sum(step_ms), "median_ms": statistics.median(step_ms),
+                                      "host_enqueue_ms_per_step": host_ms})
     t_sum = sum(step_ms) / 1e3
     uniq = sum(uniq_b[(args.warmup + k) % nb] for k in range(args.steps))
     toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
@@ -366,6 +378,7 @@ def run_sharded(args, cfg):
         "tokens_per_s": toks_job / t_job,
         "kernel_ms_rank0": phases,
         "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
+        "per_rank": per_rank,
         "table_host_syncs_rank0": int(st.shard.info().host_syncs),
         "roofline": {"bound": "hbm", "kernel": "sharded step (all kernels of one rank)", "achieved": ach,
                      "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": how,
@@ -403,7 +416,8 @@ def e2e_sharded(args, cfg, batches, st, params, P, W):
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
     evs = []
     dist.barrier()
-    for k in range(n + 2):
+    warm = 2 * len(host)  # every (batch, parity) graph captured before timing
+    for k in range(warm + n):
         h_ids, g, h_out = host[k % len(host)]
         T = h_ids.numel()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -416,7 +430,7 @@ def e2e_sharded(args, cfg, batches, st, params, P, W):
         evs.append((s, e, k))
     torch.cuda.synchronize()
     t, uniq, h2d, d2h = 0.0, 0, 0, 0
-    for s, e, k in evs[2:]:
+    for s, e, k in evs[warm:]:
         h_ids, g, h_out = host[k % len(host)]
         t += s.elapsed_time(e) / 1e3
         uniq += uniq_b[k % len(host)]
@@ -480,7 +494,8 @@ def e2e_pass(args, cfg, batches, step, P, W, rank):
     n = max(3, min(args.steps, 10))
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
     evs = []
-    for k in range(n + 2):
+    warm = 2 * len(host)  # every (batch, scratch parity) graph captured before timing
+    for k in range(warm + n):
         h_ids, g, h_out = host[k % len(host)]
         T = h_ids.numel()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -493,7 +508,7 @@ def e2e_pass(args, cfg, batches, step, P, W, rank):
         evs.append((s, e, k))
     torch.cuda.synchronize()
     times, uniq, h2d, d2h = [], 0, 0, 0
-    for s, e, k in evs[2:]:
+    for s, e, k in evs[warm:]:
         h_ids, g, h_out = host[k % len(host)]
         times.append(s.elapsed_time(e))
         uniq += uniq_b[k % len(host)]
