@@ -218,10 +218,62 @@ int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count);
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received);
 
-/* ---- table merging (merge_registry.cpp:23-51) ----------------------------- */
-/* encode_tagged_id on device; d_status (optional) receives RS_ERR_RANGE per bad id. */
+/* ---- table merging (merge_registry.cpp:23-176) ---------------------------- */
+/* encode_tagged_id on device (merge_registry.cpp:23-33); synchronizes,
+ * RS_ERR_RANGE if an index or raw id is out of range. */
 int rs_encode_ids(const uint64_t* d_raw, uint64_t n, uint32_t k_bits, uint32_t table_index,
                   uint32_t index_limit, uint64_t* d_out, void* stream);
+
+/* Pooling / FeatureConfig (merge_registry.hpp:28-43) */
+enum { RS_POOL_NONE = 0, RS_POOL_SUM = 1, RS_POOL_MEAN = 2 };
+typedef struct {
+  const char* feature_name;
+  uint32_t embedding_dim;
+  const char* const* lookup_tables;
+  uint32_t n_lookup_tables;
+  uint32_t pooling; /* RS_POOL_* */
+} rs_feature_config;
+
+/* plan_merge (merge_registry.cpp:69-110): same groups, member order, k bits
+ * and ConfigError cases (RS_ERR_CONFIG, reference message text). */
+typedef struct rs_merge_plan rs_merge_plan;
+int rs_plan_merge(const rs_feature_config* configs, uint32_t n, rs_merge_plan** out);
+int rs_merge_plan_destroy(rs_merge_plan* plan);
+uint32_t rs_merge_plan_groups(const rs_merge_plan* plan);
+int rs_merge_plan_group(const rs_merge_plan* plan, uint32_t group, uint32_t* embedding_dim,
+                        uint32_t* k_bits, uint32_t* n_members);
+/* member table i in [1, m] of a group (MergeGroup::member_tables[i - 1]); NULL if none */
+const char* rs_merge_plan_member(const rs_merge_plan* plan, uint32_t group, uint32_t index);
+/* MergePlan::group_index_for + MergeGroup::table_index_of (unknown table: RS_ERR_CONFIG) */
+int rs_merge_plan_find(const rs_merge_plan* plan, const char* table, uint32_t* group,
+                       uint32_t* index);
+
+/* HashTableCollection (merge_registry.hpp:90-105): one device table per
+ * group, the prototype config with the group's embedding dim. */
+typedef struct rs_collection rs_collection;
+int rs_collection_create(const rs_merge_plan* plan, const rs_table_config* prototype,
+                         rs_collection** out);
+int rs_collection_destroy(rs_collection* c);
+rs_table* rs_collection_table(rs_collection* c, uint32_t group);
+/* collection_lookup (merge_registry.cpp:112-158): per raw id, every lookup
+ * table's row (zero-vivified), pooled none / sum (table order) / mean
+ * (sum * (1.0f / n)); d_out [n x embedding_dim].  Synchronizes: RS_ERR_RANGE
+ * if a raw id exceeds its group's payload width (no table touched then). */
+int rs_collection_lookup(rs_collection* c, const rs_feature_config* feature,
+                         const uint64_t* d_raw_ids, uint64_t n, float* d_out, void* stream);
+
+/* run_workload's per-token routing (workload.cpp:431-447, 506-531): decode
+ * the catalog tag (TableCatalog, ordinals 1..n_catalog in catalog order) and
+ * re-encode into the merged group's id space.  rs_route_tagged is a stable
+ * partition by group: d_gids / d_pos hold group 0's tokens in token order,
+ * then group 1's, ...; h_counts[groups] (optional) synchronizes and reports
+ * decode / encode range errors (RS_ERR_RANGE). */
+typedef struct rs_router rs_router;
+int rs_router_create(const rs_merge_plan* plan, const char* const* catalog_names,
+                     uint32_t n_catalog, rs_router** out);
+int rs_router_destroy(rs_router* r);
+int rs_route_tagged(rs_router* r, const uint64_t* d_tagged, uint64_t n, uint64_t* d_gids,
+                    uint32_t* d_pos, uint64_t* h_counts, void* stream);
 
 /* ---- synthetic inputs (workload.cpp:103-152, 280-307, 348-355) ------------ */
 /* generate_workload: per-sample lengths + catalog-tagged ids (k = bit_width(tables)) */

@@ -275,6 +275,94 @@ int ref_decode_tagged_id(uint32_t k, uint32_t lim, uint64_t tagged, uint32_t* id
   }
   return 0;
 }
+// Feature specs cross the C boundary as text:
+//   "name|dim|pooling|table1,table2;name2|..."   pooling 0 none, 1 sum, 2 mean
+static std::vector<FeatureConfig> parse_features(const char* spec) {
+  std::vector<FeatureConfig> out;
+  std::stringstream all(spec);
+  std::string item;
+  while (std::getline(all, item, ';')) {
+    if (item.empty()) continue;
+    std::stringstream f(item);
+    std::string name, dim, pool, tables;
+    std::getline(f, name, '|');
+    std::getline(f, dim, '|');
+    std::getline(f, pool, '|');
+    std::getline(f, tables, '|');
+    FeatureConfig c;
+    c.feature_name = name;
+    c.embedding_dim = static_cast<uint32_t>(std::stoul(dim));
+    const int p = std::stoi(pool);
+    c.pooling = p == 0 ? Pooling::kNone : (p == 1 ? Pooling::kSum : Pooling::kMean);
+    std::stringstream t(tables);
+    std::string tab;
+    while (std::getline(t, tab, ',')) c.lookup_tables.push_back(tab);
+    out.push_back(std::move(c));
+  }
+  return out;
+}
+
+// plan -> "dim:k:member1,member2|dim:k:..." (group order, member order)
+int ref_plan_merge(const char* spec, char* out, uint64_t cap) {
+  GUARD({
+    const std::vector<FeatureConfig> f = parse_features(spec);
+    const MergePlan plan = plan_merge(f);
+    std::string s;
+    for (size_t g = 0; g < plan.groups.size(); ++g) {
+      if (g) s += "|";
+      s += std::to_string(plan.groups[g].embedding_dim) + ":" +
+           std::to_string(plan.groups[g].k_bits) + ":";
+      for (size_t i = 0; i < plan.groups[g].member_tables.size(); ++i)
+        s += (i ? "," : "") + plan.groups[g].member_tables[i];
+    }
+    if (s.size() + 1 > cap) return 4;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+  });
+  return 0;
+}
+
+struct RefCollection {
+  std::vector<FeatureConfig> features;
+  HashTableCollection coll;
+};
+
+void* ref_collection_create(const char* spec, uint64_t capacity, uint32_t chunk_rows, int* status) {
+  try {
+    std::vector<FeatureConfig> f = parse_features(spec);
+    TableConfig proto;
+    proto.capacity = capacity;
+    proto.chunk_rows = chunk_rows;
+    proto.embedding_dim = 1;
+    MergePlan plan = plan_merge(f);
+    *status = 0;
+    return new RefCollection{f, HashTableCollection(std::move(plan), proto)};
+  } catch (const std::exception& e) {
+    *status = status_of(e);
+    return nullptr;
+  }
+}
+void ref_collection_destroy(void* h) { delete static_cast<RefCollection*>(h); }
+void* ref_collection_table(void* h, uint64_t g) { return &static_cast<RefCollection*>(h)->coll.table(g); }
+// out [n x feature dim]; 0, or 1 ConfigError, 5 overflow/range of an id
+int ref_collection_lookup(void* h, const char* feature, const uint64_t* raw, uint64_t n, float* out) {
+  RefCollection* c = static_cast<RefCollection*>(h);
+  try {
+    for (const FeatureConfig& f : c->features) {
+      if (f.feature_name != feature) continue;
+      const auto rows = c->coll.lookup(f, std::span<const uint64_t>(raw, n));
+      for (uint64_t i = 0; i < n; ++i) std::memcpy(out + i * f.embedding_dim, rows[i].data(), f.embedding_dim * 4);
+      return 0;
+    }
+    return 1;
+  } catch (const std::overflow_error&) {
+    return 5;
+  } catch (const std::out_of_range&) {
+    return 5;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 uint64_t ref_closest_prefix(const uint64_t* cums, uint64_t n, uint64_t target) {
   return closest_prefix(std::span<const uint64_t>(cums, n), target);
 }

@@ -57,6 +57,11 @@ class rs_table_config(C.Structure):
                 ("initial_rows", C.c_uint64), ("max_keys", C.c_uint64)]
 
 
+class rs_feature_config(C.Structure):
+    _fields_ = [("feature_name", C.c_char_p), ("embedding_dim", C.c_uint32),
+                ("lookup_tables", C.POINTER(C.c_char_p)), ("n_lookup_tables", C.c_uint32), ("pooling", C.c_uint32)]
+
+
 class rs_optimizer_params(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double)]
@@ -117,6 +122,19 @@ _SIGS = {
     "rs_comm_set_profiling": (C.c_int, [vp, C.c_int]),
     "rs_comm_phase_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int, C.POINTER(u64)]),
     "rs_comm_trace": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "rs_plan_merge": (C.c_int, [C.POINTER(rs_feature_config), u32, C.POINTER(vp)]),
+    "rs_merge_plan_destroy": (C.c_int, [vp]),
+    "rs_merge_plan_groups": (u32, [vp]),
+    "rs_merge_plan_group": (C.c_int, [vp, u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(u32)]),
+    "rs_merge_plan_member": (C.c_char_p, [vp, u32, u32]),
+    "rs_merge_plan_find": (C.c_int, [vp, C.c_char_p, C.POINTER(u32), C.POINTER(u32)]),
+    "rs_collection_create": (C.c_int, [vp, C.POINTER(rs_table_config), C.POINTER(vp)]),
+    "rs_collection_destroy": (C.c_int, [vp]),
+    "rs_collection_table": (vp, [vp, u32]),
+    "rs_collection_lookup": (C.c_int, [vp, C.POINTER(rs_feature_config), vp, u64, vp, vp]),
+    "rs_router_create": (C.c_int, [vp, C.POINTER(C.c_char_p), u32, C.POINTER(vp)]),
+    "rs_router_destroy": (C.c_int, [vp]),
+    "rs_route_tagged": (C.c_int, [vp, vp, u64, vp, vp, vp, vp]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),

@@ -76,7 +76,7 @@ struct TableCounters {
   unsigned int special_row[2];     // rows of the keys equal to kEmptyKey / kTombKey
   unsigned int special_tick[2];
   unsigned int missing;            // per-launch count of missing keys (probe mode)
-  unsigned int pad;
+  unsigned int returned;           // per-launch rows handed back (lost duplicate inserts)
 };
 
 struct TableDev {

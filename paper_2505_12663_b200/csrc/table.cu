@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(kProbeThreads)
       for (;;) {
         const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
         if (p.found) {
-          row = p.row;
+          row = p.row == kNoRow ? wait_row(d.slots, p.slot) : p.row;
+          if (g == 0 && new_row != kNoRow) return_row(td, free_n0, new_row);
           if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
           if (mode == 1) {  // upsert: overwrite the embedding in place
             float* e = d.emb + (size_t)row * d.dim;

@@ -84,6 +84,14 @@ __device__ __forceinline__ uint32_t alloc_row(TableDev* td, unsigned long long f
   return (uint32_t)r;
 }
 
+// A row allocated for a key that a concurrent duplicate inserted first goes
+// back to the free stack (above the launch's free_n0; the epilogue moves it
+// down to the top of the surviving stack).
+__device__ __forceinline__ void return_row(TableDev* td, unsigned long long free_n0, uint32_t row) {
+  const unsigned int k = atomicAdd(&td->c.returned, 1u);
+  td->d.free_stack[free_n0 + k] = row;
+}
+
 // New-row initialisation by the 8 lanes of a group: emb from src (or zeros),
 // optimizer state zeroed (alloc_row + reset_row, embed_table.cpp:144-180).
 __device__ __forceinline__ void init_row(const TableDesc& d, uint32_t row, const float* src,
@@ -120,8 +128,17 @@ __device__ __forceinline__ void copy_row_group(const TableDesc& d, uint32_t row,
   }
 }
 
+// A slot whose key was just claimed by a concurrent insert of the same key in
+// this launch still has row == kNoRow (empty and tombstoned slots always do):
+// wait for the inserter to publish it.
+__device__ __forceinline__ uint32_t wait_row(Slot* slots, uint64_t slot) {
+  uint32_t r;
+  while ((r = ld_acquire32(&slots[slot].row)) == kNoRow) __nanosleep(32);
+  return r;
+}
+
 // Find-or-insert-zero of one key by an 8-lane group (grouped bucket probing;
-// keys must be distinct within a launch).  Returns the row (kNoRow on a full
+// duplicate keys within a launch resolve to the same row).  Returns the row (kNoRow on a full
 // table / exhausted row pool, with the error bit set); stamps the batch tick.
 __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const TableDesc& d,
                                                          uint64_t key, unsigned g, unsigned gbase,
@@ -157,7 +174,8 @@ __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const Tab
     for (;;) {
       const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
       if (p.found) {
-        row = p.row;
+        row = p.row == kNoRow ? wait_row(d.slots, p.slot) : p.row;
+        if (g == 0 && new_row != kNoRow) return_row(td, free_n0, new_row);
         if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
         break;
       }
@@ -214,6 +232,11 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
       unsigned long long f = fresh0 + (used - free_n0);
       c.fresh_next = f > td->d.row_cap ? td->d.row_cap : f;
     }
+    // rows handed back by lost duplicate inserts sit at [free_n0, +returned)
+    for (unsigned int k = 0; k < c.returned; ++k)
+      td->d.free_stack[c.free_n + k] = td->d.free_stack[free_n0 + k];
+    c.free_n += c.returned;
+    c.returned = 0;
     // removals push rows above free_n0 (remove kernel); fold them in
     c.free_n += c.removed;
     c.occupied = c.occupied + c.inserted - c.removed;

@@ -315,3 +315,24 @@ def test_bounded_table_eviction_vs_oracle(cuda, oracle):
     g.evict(100)
     oracle.table_evict_oldest(o.h, 100)
     _compare_contents(g, o, ("keys", "ts"))
+
+
+def test_ensure_duplicate_keys_in_one_batch(cuda, oracle):
+    # ensure (embed_table.cpp:243-248) with every key repeated inside one batch:
+    # one row per key, no row leaked, same contents as sequential ensures
+    rng = np.random.default_rng(8)
+    dim = 8
+    g = _gpu_table(1 << 10, dim, opt="adam")
+    o = Table(oracle, 1 << 10, dim, chunk_rows=64)
+    for _ in range(6):
+        keys = rng.integers(0, 300, 4000).astype(np.uint64)  # ~13 copies per key
+        rows = g.ensure(keys).cpu().numpy()
+        for k in keys:
+            oracle.table_ensure(o.h, int(k))
+        first = {}
+        for k, r in zip(keys, rows):
+            assert first.setdefault(int(k), r) == r
+        i = g.info()
+        assert i.occupied == o.o.table_occupied(o.h)
+        assert i.rows_allocated - i.rows_free == i.occupied  # nothing leaked
+    _compare_contents(g, o, ("keys", "emb", "m", "v", "step"))
