@@ -275,6 +275,37 @@ int rs_router_destroy(rs_router* r);
 int rs_route_tagged(rs_router* r, const uint64_t* d_tagged, uint64_t n, uint64_t* d_gids,
                     uint32_t* d_pos, uint64_t* h_counts, void* stream);
 
+/* ---- dynamic sequence balancing (seq_batcher.cpp, workload.cpp:368-469) --- */
+/* closest_prefix (seq_batcher.cpp:22-34); n == 0: RS_ERR_CONFIG */
+int rs_closest_prefix(const uint64_t* cumsums, uint64_t n, uint64_t target, uint64_t* k_out);
+/* ChunkSource: fill up to cap (sample id, token count) pairs, *n_out of them;
+ * return 0 once exhausted (SequenceBatcher's std::function<bool(chunk&)>). */
+typedef int (*rs_chunk_source)(void* ctx, uint64_t* sample_ids, uint64_t* token_counts,
+                               uint64_t cap, uint64_t* n_out);
+typedef struct rs_seq_batcher rs_seq_batcher;
+/* SequenceBatcher (seq_batcher.cpp:36-78, Alg. 1); target < 1: RS_ERR_CONFIG */
+int rs_seq_batcher_create(uint64_t target_tokens, rs_chunk_source source, void* ctx,
+                          uint64_t max_chunk, rs_seq_batcher** out);
+int rs_seq_batcher_destroy(rs_seq_batcher* b);
+/* next_batch: *n_out samples in arrival order, 0 when done; a zero-token
+ * sample: RS_ERR_INVARIANT */
+int rs_seq_batcher_next(rs_seq_batcher* b, uint64_t* sample_ids, uint64_t* token_counts,
+                        uint64_t cap, uint64_t* n_out);
+uint64_t rs_seq_batcher_buffered_tokens(const rs_seq_batcher* b);
+uint64_t rs_seq_batcher_buffered_samples(const rs_seq_batcher* b);
+/* rank per sequence: round robin (the reference's split, workload.cpp:461-469)
+ * or longest-processing-time-first on CostModel::sample_compute a*len+b*len^2
+ * (workload.hpp:106-109); load_out[world] (optional) the cost per rank */
+enum { RS_PARTITION_ROUND_ROBIN = 0, RS_PARTITION_COST_LPT = 1 };
+int rs_partition_sequences(const uint64_t* lengths, uint64_t n, uint32_t world, uint32_t policy,
+                           double a, double b, uint32_t* rank_out, double* load_out);
+/* imbalance_report (seq_batcher.cpp:140-152) */
+int rs_imbalance_report(const uint64_t* per_worker_tokens, uint64_t n, uint64_t* max_tokens,
+                        uint64_t* min_tokens, double* spread);
+/* weighted_grad_combine (seq_batcher.cpp:80-138); grads [workers x dim] */
+int rs_weighted_grad_combine(const uint64_t* batch_sizes, const double* grads, uint64_t workers,
+                             uint64_t dim, double* out);
+
 /* ---- synthetic inputs (workload.cpp:103-152, 280-307, 348-355) ------------ */
 /* generate_workload: per-sample lengths + catalog-tagged ids (k = bit_width(tables)) */
 int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len,

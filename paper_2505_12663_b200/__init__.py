@@ -6,6 +6,8 @@ mirror of the reference interface.  No CPU fallback exists.
 """
 from ._lib import (CapacityError, ConfigError, CudaError, InvariantError, IoError, RangeError,
                    RecsparseError, build, lib)
+from .batcher import (SequenceBatcher, SequenceSample, closest_prefix, imbalance_report, partition_sequences,
+                      weighted_grad_combine)
 from .merge import (FeatureConfig, HashTableCollection, MergeGroup, MergePlan, Pooling, Router, catalog_from,
                     collection_lookup, decode_tagged_id, encode_tagged_id, plan_merge)
 from .table import (AdagradParams, AdamParams, EmbedTable, SparseStep, TableConfig, Workspace,
@@ -13,6 +15,8 @@ from .table import (AdagradParams, AdamParams, EmbedTable, SparseStep, TableConf
                     sparse_update, stage1_dedup)
 
 __all__ = [
+    "SequenceBatcher", "SequenceSample", "closest_prefix", "imbalance_report", "partition_sequences",
+    "weighted_grad_combine",
     "FeatureConfig", "HashTableCollection", "MergeGroup", "MergePlan", "Pooling", "Router", "catalog_from",
     "collection_lookup", "decode_tagged_id", "encode_tagged_id", "plan_merge",
     "AdagradParams", "AdamParams", "CapacityError", "ConfigError", "CudaError", "EmbedTable",

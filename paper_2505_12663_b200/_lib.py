@@ -76,6 +76,8 @@ class rs_table_info(C.Structure):
 
 vp = C.c_void_p
 u64, u32, i32 = C.c_uint64, C.c_uint32, C.c_int32
+rs_chunk_source = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.c_uint64,
+                              C.POINTER(C.c_uint64))
 
 # name -> (restype, argtypes)
 _SIGS = {
@@ -135,6 +137,15 @@ _SIGS = {
     "rs_router_create": (C.c_int, [vp, C.POINTER(C.c_char_p), u32, C.POINTER(vp)]),
     "rs_router_destroy": (C.c_int, [vp]),
     "rs_route_tagged": (C.c_int, [vp, vp, u64, vp, vp, vp, vp]),
+    "rs_closest_prefix": (C.c_int, [vp, u64, u64, C.POINTER(u64)]),
+    "rs_seq_batcher_create": (C.c_int, [u64, rs_chunk_source, vp, u64, C.POINTER(vp)]),
+    "rs_seq_batcher_destroy": (C.c_int, [vp]),
+    "rs_seq_batcher_next": (C.c_int, [vp, vp, vp, u64, C.POINTER(u64)]),
+    "rs_seq_batcher_buffered_tokens": (u64, [vp]),
+    "rs_seq_batcher_buffered_samples": (u64, [vp]),
+    "rs_partition_sequences": (C.c_int, [vp, u64, u32, u32, C.c_double, C.c_double, vp, vp]),
+    "rs_imbalance_report": (C.c_int, [vp, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_double)]),
+    "rs_weighted_grad_combine": (C.c_int, [vp, vp, u64, u64, vp]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),
