@@ -220,6 +220,12 @@ class Router:
         check(L.lib().rs_route_tagged(self._h, _ptr(k), n, _ptr(gids), _ptr(pos), counts, _stream()), "route")
         return gids, pos, list(counts)
 
+    def route_async(self, tagged: torch.Tensor, gids: torch.Tensor, pos: torch.Tensor) -> None:
+        """Same routing, no synchronization (group sizes known to the caller;
+        range errors are not reported)."""
+        check(L.lib().rs_route_tagged(self._h, _ptr(tagged), tagged.numel(), _ptr(gids), _ptr(pos), None,
+                                      _stream()), "route")
+
     def __del__(self):
         try:
             if self._h:
