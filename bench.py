@@ -315,6 +315,7 @@ def run_sharded(args, cfg):
         h0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
+            st.barrier()  # device barrier: no rank's flush leaks into another rank's step bracket
             evs[k][0].record(stream)
             one(args.warmup + k)
             evs[k][1].record(stream)
@@ -374,7 +375,7 @@ def run_sharded(args, cfg):
                    "tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg, "embedding_dim": D,
                    "table_keys": vocab, "optimizer": "adagrad", "parallelism": f"row-sharded x{world}",
                    "exchange": "NVLink peer stores from the producing kernels (CUDA IPC arena)",
-                   "l2": "flushed (512 MiB write) between timed steps"},
+                   "l2": "flushed (512 MiB write) between timed steps, then a device barrier of all ranks"},
         "tokens_per_s": toks_job / t_job,
         "kernel_ms_rank0": phases,
         "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -401,47 +402,17 @@ def run_sharded(args, cfg):
 def e2e_sharded(args, cfg, batches, st, params, P, W):
     import torch
     import torch.distributed as dist
-    dim = cfg["dim"]
-    stream = torch.cuda.current_stream()
-    host = []
-    for b, (lengths, ids) in enumerate(batches):
-        h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
-        g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim).cpu().pin_memory()
-        host.append((h_ids, g, torch.empty((len(ids), dim), dtype=torch.float32).pin_memory()))
-    max_t = max(h[0].numel() for h in host)
-    d_ids = torch.empty(max_t, dtype=torch.int64, device="cuda")
-    d_g = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
-    d_out = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
     n = max(3, min(args.steps, 10))
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
-    evs = []
-    dist.barrier()
-    warm = 2 * len(host)  # every (batch, parity) graph captured before timing
-    for k in range(warm + n):
-        h_ids, g, h_out = host[k % len(host)]
-        T = h_ids.numel()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        d_ids[:T].copy_(h_ids, non_blocking=True)
-        d_g[:T].copy_(g, non_blocking=True)
-        st.step(d_ids[:T], d_g[:T], params, d_out[:T])
-        h_out.copy_(d_out[:T], non_blocking=True)
-        e.record(stream)
-        evs.append((s, e, k))
-    torch.cuda.synchronize()
-    t, uniq, h2d, d2h = 0.0, 0, 0, 0
-    for s, e, k in evs[warm:]:
-        h_ids, g, h_out = host[k % len(host)]
-        t += s.elapsed_time(e) / 1e3
-        uniq += uniq_b[k % len(host)]
-        h2d += h_ids.numel() * 8 + g.numel() * 4
-        d2h += h_out.numel() * 4
+    t, uniq, h2d, d2h = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
+                                      lambda i, g, o: st.step(i, g, params, o), n, uniq_b, barrier=dist.barrier)
     v = torch.tensor([t, uniq], dtype=torch.float64, device="cuda")
     tmax = v[:1].clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(v)
-    return {"value": v[1].item() / tmax.item(), "unit": "unique-ids/s", "h2d_bytes_per_step": h2d // n,
-            "d2h_bytes_per_step": d2h // n, "ms_per_step": tmax.item() / n * 1e3}
+    return {"value": v[1].item() / tmax.item(), "unit": "unique-ids/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": tmax.item() / n * 1e3,
+            "pipelined": "H2D / step / D2H on 3 streams, 2 buffer sets"}
 
 
 C2 = dict(workload="config2: 8 tables (dim 64: 1e7/1e6/1e6/1e5 keys; dim 128: 1e6/1e6/1e5/1e4 keys) auto-merged "
@@ -584,48 +555,85 @@ def phase_times(step, dev, nb, args, flush, P):
     return {name: ms[i] for i, name in enumerate(PHASES)}
 
 
-def e2e_pass(args, cfg, batches, step, P, W, rank):
-    """Same metric through the public API with host buffers: H2D of ids+grads from
-    pinned memory, the step, D2H of the gathered embeddings -- all in the timed region."""
+def pipelined_e2e(host, dim, run_step, n, uniq_b, barrier=None):
+    """End to end through the public API with HOST buffers, pipelined the way
+    a data loader drives it: step k's ids + grads go host->device on a copy
+    stream, the step runs on the compute stream once they landed, its
+    gathered rows go device->host on a second copy stream -- so H2D of step
+    k+1, compute of step k and D2H of step k-1 overlap (PCIe is full duplex).
+    Two device buffer sets; every copy of every step is inside the timed
+    region (first H2D start -> last D2H end)."""
     import torch
-    dim = cfg["dim"]
-    stream = torch.cuda.current_stream()
+    comp = torch.cuda.current_stream()
+    sh, sd = torch.cuda.Stream(), torch.cuda.Stream()
+    max_t = max(h[0].numel() for h in host)
+    sets = [(torch.empty(max_t, dtype=torch.int64, device="cuda"),
+             torch.empty((max_t, dim), dtype=torch.float32, device="cuda"),
+             torch.empty((max_t, dim), dtype=torch.float32, device="cuda")) for _ in range(2)]
+    in_free = [torch.cuda.Event() for _ in range(2)]
+    out_free = [torch.cuda.Event() for _ in range(2)]
+    for e in in_free + out_free:
+        e.record(comp)
+
+    def issue(k):
+        h_ids, g, h_out = host[k % len(host)]
+        T, b = h_ids.numel(), k % 2
+        d_ids, d_g, d_out = sets[b]
+        sh.wait_event(in_free[b])
+        with torch.cuda.stream(sh):
+            d_ids[:T].copy_(h_ids, non_blocking=True)
+            d_g[:T].copy_(g, non_blocking=True)
+        landed = torch.cuda.Event()
+        landed.record(sh)
+        comp.wait_event(landed)
+        comp.wait_event(out_free[b])
+        run_step(d_ids[:T], d_g[:T], d_out[:T])
+        in_free[b].record(comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        sd.wait_event(done)
+        with torch.cuda.stream(sd):
+            h_out[:T].copy_(d_out[:T], non_blocking=True)
+        out_free[b].record(sd)
+
+    warm = 2 * len(host)  # every (batch, buffer set, scratch parity) graph captured before timing
+    for k in range(warm):
+        issue(k)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(sh)
+    for k in range(warm, warm + n):
+        issue(k)
+    t1.record(sd)
+    torch.cuda.synchronize()
+    t = t0.elapsed_time(t1) / 1e3
+    uniq = sum(uniq_b[k % len(host)] for k in range(warm, warm + n))
+    h2d = sum(host[k % len(host)][0].numel() * 8 + host[k % len(host)][1].numel() * 4 for k in range(warm, warm + n))
+    d2h = sum(host[k % len(host)][2].numel() * 4 for k in range(warm, warm + n))
+    return t, uniq, h2d // n, d2h // n
+
+
+def host_batches(batches, dim, W):
+    import torch
     host = []
     for b, (lengths, ids) in enumerate(batches):
         h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
         g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), b, dim).cpu().pin_memory()
         h_out = torch.empty((len(ids), dim), dtype=torch.float32).pin_memory()
         host.append((h_ids, g, h_out))
-    max_t = max(h[0].numel() for h in host)
-    d_ids = torch.empty(max_t, dtype=torch.int64, device="cuda")
-    d_g = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
-    d_out = torch.empty((max_t, dim), dtype=torch.float32, device="cuda")
+    return host
+
+
+def e2e_pass(args, cfg, batches, step, P, W, rank):
+    """Same metric through rs_step with host buffers (pipelined_e2e)."""
     n = max(3, min(args.steps, 10))
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
-    evs = []
-    warm = 2 * len(host)  # every (batch, scratch parity) graph captured before timing
-    for k in range(warm + n):
-        h_ids, g, h_out = host[k % len(host)]
-        T = h_ids.numel()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        d_ids[:T].copy_(h_ids, non_blocking=True)
-        d_g[:T].copy_(g, non_blocking=True)
-        step.step(d_ids[:T], d_g[:T], d_out[:T])
-        h_out.copy_(d_out[:T], non_blocking=True)
-        e.record(stream)
-        evs.append((s, e, k))
-    torch.cuda.synchronize()
-    times, uniq, h2d, d2h = [], 0, 0, 0
-    for s, e, k in evs[warm:]:
-        h_ids, g, h_out = host[k % len(host)]
-        times.append(s.elapsed_time(e))
-        uniq += uniq_b[k % len(host)]
-        h2d += h_ids.numel() * 8 + g.numel() * 4
-        d2h += h_out.numel() * 4
-    t = sum(times) / 1e3
-    return {"value": uniq / t, "unit": "unique-ids/s", "h2d_bytes_per_step": h2d // n, "d2h_bytes_per_step": d2h // n,
-            "ms_per_step": t / n * 1e3}
+    t, uniq, h2d, d2h = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
+                                      lambda i, g, o: step.step(i, g, o), n, uniq_b)
+    return {"value": uniq / t, "unit": "unique-ids/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": t / n * 1e3, "pipelined": "H2D / step / D2H on 3 streams, 2 buffer sets"}
 
 
 # ------------------------------------------------------------- CPU arm

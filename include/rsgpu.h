@@ -214,6 +214,9 @@ int rs_dist_step(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t n,
  * wait_embs, gather (rs_dist_step: gather + reduce + sums to the owners),
  * req_reduce (split API only), wait_grads, owner_update -- mean ms. */
 int rs_comm_set_profiling(rs_comm* c, int on);
+/* device-side barrier of the group on `stream` (all ranks call it): work
+ * enqueued after it starts once every rank reached it */
+int rs_comm_barrier(rs_comm* c, void* stream);
 int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count);
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received);

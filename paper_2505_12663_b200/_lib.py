@@ -122,6 +122,7 @@ _SIGS = {
     "rs_dist_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
     "rs_dist_step": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp]),
     "rs_comm_set_profiling": (C.c_int, [vp, C.c_int]),
+    "rs_comm_barrier": (C.c_int, [vp, vp]),
     "rs_comm_phase_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int, C.POINTER(u64)]),
     "rs_comm_trace": (C.c_int, [vp, vp, vp, vp, vp, vp]),
     "rs_plan_merge": (C.c_int, [C.POINTER(rs_feature_config), u32, C.POINTER(vp)]),

@@ -47,6 +47,7 @@ struct ArenaHdr {
   unsigned long long sig_ids[kMaxWorld];
   unsigned long long sig_emb[kMaxWorld];
   unsigned long long sig_grad[kMaxWorld];
+  unsigned long long sig_bar[kMaxWorld];
   uint32_t cnt_in[kMaxWorld];
 };
 
@@ -164,6 +165,31 @@ __global__ void k_wait(CommDev c, int phase) {
   const long long t0 = clock64();
   while (ld_acquire_sys(f) < e) {
     if (clock64() - t0 > 40000000000ll) {  // ~20 s: a peer is gone; do not hang the GPU
+      c.trace[kTrError] = 1;
+      break;
+    }
+    __nanosleep(100);
+  }
+}
+
+// Device-side barrier of the group (rs_comm_barrier): raise this rank's
+// barrier flag at every peer, wait for every peer's.  The barrier epoch is
+// its own device counter.
+__global__ void k_barrier(CommDev c, unsigned long long* bar_epoch) {
+  __shared__ unsigned long long e;
+  if (threadIdx.x == 0) {
+    e = *bar_epoch + 1;
+    *bar_epoch = e;
+    fence_sys();
+  }
+  __syncthreads();
+  const uint32_t r = threadIdx.x;
+  if (r >= c.world) return;
+  st_release_sys(&hdr_of(c, r)->sig_bar[c.rank], e);
+  const unsigned long long* f = &hdr_of(c, c.rank)->sig_bar[r];
+  const long long t0 = clock64();
+  while (ld_acquire_sys(f) < e) {
+    if (clock64() - t0 > 40000000000ll) {
       c.trace[kTrError] = 1;
       break;
     }
@@ -325,6 +351,7 @@ struct rs_comm {
   float** d_peer_grad[2] = {nullptr, nullptr};  // per epoch parity
   unsigned long long epoch = 0;       // host mirror of the device counter (parity)
   unsigned long long* d_epoch = nullptr;
+  unsigned long long* d_bar_epoch = nullptr;
   unsigned long long* trace = nullptr;
   unsigned int* done = nullptr;
   uint32_t* send_pos = nullptr;
@@ -621,7 +648,8 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
             cudaMalloc(&c->send_cnt, kMaxWorld * 4) == cudaSuccess &&
             cudaMemset(c->send_cnt, 0, kMaxWorld * 4) == cudaSuccess &&
             cudaMalloc(&c->view, sizeof(TableDev)) == cudaSuccess &&
-            cudaMalloc(&c->d_epoch, 8) == cudaSuccess && cudaMemset(c->d_epoch, 0, 8) == cudaSuccess;
+            cudaMalloc(&c->d_epoch, 16) == cudaSuccess && cudaMemset(c->d_epoch, 0, 16) == cudaSuccess;
+  if (ok) c->d_bar_epoch = c->d_epoch + 1;
   if (!ok) {
     cudaGetLastError();
     rs_comm_destroy(c);
@@ -829,6 +857,15 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
   t->applies++;
   c->have_forward = false;
   return prof_step_done(c);
+}
+
+// Device-side barrier over the group on `stream` (every rank must call it):
+// work enqueued after it starts only once every rank reached it.
+int rs_comm_barrier(rs_comm* c, void* stream) {
+  if (!c) return fail(RS_ERR_CONFIG, "rs_comm_barrier: null comm");
+  k_barrier<<<1, kMaxWorld, 0, S(stream)>>>(comm_dev(c, 0), c->d_bar_epoch);
+  RS_LAUNCH_CHECK("k_barrier");
+  return RS_OK;
 }
 
 int rs_comm_set_profiling(rs_comm* c, int on) {

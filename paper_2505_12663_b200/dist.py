@@ -102,6 +102,10 @@ class ShardedTable:
     PHASES = ("req_dedup", "send_ids", "wait_ids", "owner_dedup", "owner_table_respond", "wait_embs", "gather",
               "req_reduce", "wait_grads", "owner_update")
 
+    def barrier(self) -> None:
+        """Device-side barrier of the group on the current stream."""
+        check(L.lib().rs_comm_barrier(self._c, _stream()), "rs_comm_barrier")
+
     def set_profiling(self, on: bool) -> None:
         check(L.lib().rs_comm_set_profiling(self._c, int(on)), "rs_comm_set_profiling")
 

@@ -1,6 +1,6 @@
-# host-side cost of one sharded step call (W=1), per component
+# host-side cost of one step call with an idle GPU (sync before each call)
 import os, sys, time, ctypes as C
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("MASTER_ADDR", "127.0.0.1"); os.environ.setdefault("MASTER_PORT", "29601")
 os.environ.setdefault("RANK", "0"); os.environ.setdefault("WORLD_SIZE", "1")
 import torch, torch.distributed as dist, numpy as np
@@ -9,30 +9,33 @@ from paper_2505_12663_b200.dist import ShardedTable
 from paper_2505_12663_b200 import _lib as L
 torch.cuda.set_device(0)
 dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
-st = ShardedTable(P.TableConfig(capacity=1 << 20, embedding_dim=64, optimizer="adagrad"), max_tokens=1 << 17)
-ids = torch.randint(0, 1 << 18, (1 << 17,), device="cuda")
-g = torch.randn((1 << 17, 64), device="cuda")
+n = 1 << 17
+st = ShardedTable(P.TableConfig(capacity=1 << 22, embedding_dim=64, optimizer="adagrad", initial_rows=1 << 21), max_tokens=n)
+ids = torch.randint(0, 1 << 18, (n,), device="cuda")
+g = torch.randn((n, 64), device="cuda")
 out = torch.empty_like(g)
 pr = P.AdagradParams(lr=0.01)
-for _ in range(5): st.step(ids, g, pr, out)
+t = P.EmbedTable(P.TableConfig(capacity=1 << 22, embedding_dim=64, optimizer="adagrad", initial_rows=1 << 21))
+sp = P.SparseStep(t, n, pr)
+for _ in range(6):
+    st.step(ids, g, pr, out); sp.step(ids, g, out)
 torch.cuda.synchronize()
-N = 200
-t0 = time.perf_counter()
-for _ in range(N): st.step(ids, g, pr, out)
-t1 = time.perf_counter()
-torch.cuda.synchronize()
-t2 = time.perf_counter()
-print("python step call us", (t1 - t0) / N * 1e6, "gpu-bound us", (t2 - t0) / N * 1e6)
 lib = L.lib(); pc = pr.c(); s = torch.cuda.current_stream().cuda_stream
-t0 = time.perf_counter()
-for _ in range(N): lib.rs_dist_step(st._c, st.shard.handle, ids.data_ptr(), ids.numel(), g.data_ptr(), out.data_ptr(), C.byref(pc), s)
-t1 = time.perf_counter()
-torch.cuda.synchronize()
-print("raw ctypes call us", (t1 - t0) / N * 1e6)
-t0 = time.perf_counter()
-for _ in range(N): torch.cuda.current_stream().cuda_stream
-print("current_stream us", (time.perf_counter() - t0) / N * 1e6)
-t0 = time.perf_counter()
-for _ in range(N): pr.c()
-print("params.c us", (time.perf_counter() - t0) / N * 1e6)
+def timeit(name, fn, N=30):
+    xs = []
+    for _ in range(N):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter(); fn(); xs.append(time.perf_counter() - t0)
+    xs.sort()
+    print(f"{name:28s} median {xs[len(xs)//2]*1e6:8.1f} us  min {xs[0]*1e6:8.1f} us")
+timeit("ShardedTable.step", lambda: st.step(ids, g, pr, out))
+timeit("rs_dist_step raw", lambda: lib.rs_dist_step(st._c, st.shard.handle, ids.data_ptr(), n, g.data_ptr(), out.data_ptr(), C.byref(pc), s))
+timeit("SparseStep.step", lambda: sp.step(ids, g, out))
+timeit("rs_step raw", lambda: lib.rs_step(sp.ws.handle, t.handle, ids.data_ptr(), n, g.data_ptr(), out.data_ptr(), C.byref(pc), s))
+fl = torch.empty(1 << 27, device="cuda")
+timeit("flush.zero_", lambda: fl.zero_())
+ev = torch.cuda.Event(enable_timing=True)
+timeit("event.record", lambda: ev.record())
+os.environ["RS_NO_GRAPH"] = "1"
 st.close()
+dist.destroy_process_group()
