@@ -32,6 +32,7 @@
 
 #include "opt_dev.cuh"
 #include "rs_host.hpp"
+#include "dist_sync.cuh"
 #include "scratch_dev.cuh"
 #include "table_dev.cuh"
 
@@ -54,16 +55,6 @@ struct ArenaHdr {
 // trace slots (per rank, device u64)
 enum : int { kTrIdsSent = 0, kTrEmbsSent = kMaxWorld, kTrLookups = 2 * kMaxWorld,
              kTrRequested, kTrReceived, kTrError, kTrN };
-
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 struct CommDev {
   char* const* peers;  // [W] arena base of every rank (own included), device-visible
@@ -155,22 +146,6 @@ __global__ void __launch_bounds__(256) k_send_ids(CommDev c, const uint64_t* __r
   if (threadIdx.x == 0) *c.epoch = e;
 }
 
-// Bounded wait until every source raised flag `phase` for this epoch.
-__global__ void k_wait(CommDev c, int phase) {
-  ArenaHdr* h = hdr_of(c, c.rank);
-  const uint32_t r = threadIdx.x;
-  if (r >= c.world) return;
-  const unsigned long long* f = flag_of(h, phase, r);
-  const unsigned long long e = *c.epoch;
-  const long long t0 = clock64();
-  while (ld_acquire_sys(f) < e) {
-    if (clock64() - t0 > 40000000000ll) {  // ~20 s: a peer is gone; do not hang the GPU
-      c.trace[kTrError] = 1;
-      break;
-    }
-    __nanosleep(100);
-  }
-}
 
 // Device-side barrier of the group (rs_comm_barrier): raise this rank's
 // barrier flag at every peer, wait for every peer's.  The barrier epoch is
@@ -197,6 +172,21 @@ __global__ void k_barrier(CommDev c, unsigned long long* bar_epoch) {
   }
 }
 
+// One-block wait until every source raised flag `phase` for this step.  The
+// data kernels after it re-check their flags in the prologue (cheap then);
+// a 1-block waiter is what keeps a concurrently running producer on the
+// other stream of this GPU from being starved of SMs by spinning blocks.
+__global__ void k_wait(CommDev c, int phase) {
+  __shared__ unsigned long long e;
+  if (threadIdx.x == 0) {
+    e = *c.epoch + (phase == 0 ? 1 : 0);  // the owner's step starts here
+    if (phase == 0) *c.epoch = e;
+  }
+  __syncthreads();
+  const uint32_t r = threadIdx.x;
+  if (r < c.world) spin_flag(flag_of(hdr_of(c, c.rank), phase, r), e, c.trace + kTrError);
+}
+
 // Owner KA': stage-2 dedup straight from the receive lists.  A requester
 // sends each id at most once, so an owner-unique id has at most W origins:
 // every received position (src, j) claims the id's scratch slot and appends
@@ -208,16 +198,10 @@ __global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t
                                                    uint64_t* __restrict__ unique) {
   const ArenaHdr* h = hdr_of(c, c.rank);
   const uint32_t src = blockIdx.y;
-  const uint32_t cnt = h->cnt_in[src];
+  if (threadIdx.x == 0) spin_flag(&h->sig_ids[src], *c.epoch, c.trace + kTrError);  // src's ids landed
+  __syncthreads();
+  const uint32_t cnt = h->cnt_in[src];  // ordered after the acquire by the barrier
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    c.trace[kTrEmbsSent + src] = cnt;  // two-stage: one vector per received id
-    if (src == c.world - 1) {
-      uint64_t tot = 0;
-      for (uint32_t r = 0; r < c.world; ++r) tot += h->cnt_in[r];
-      c.trace[kTrReceived] = tot;
-    }
-  }
   if (blockIdx.x * blockDim.x >= cnt) return;  // block-uniform
   const bool v = j < cnt;
   bool fresh = false;
@@ -307,7 +291,16 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
   launch_epilogue(td, free_n0, fresh0, true, tick_now);
-  if (blockIdx.x == 0 && threadIdx.x == 0) c.trace[kTrLookups] = nu;
+  if (blockIdx.x == 0) {  // every source's flag was observed by k_own_dedup
+    const ArenaHdr* h = hdr_of(c, c.rank);
+    uint64_t tot = 0;
+    for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) c.trace[kTrEmbsSent + r] = h->cnt_in[r];
+    if (threadIdx.x == 0) {
+      for (uint32_t r = 0; r < c.world; ++r) tot += h->cnt_in[r];
+      c.trace[kTrReceived] = tot;  // two-stage: one vector back per received id
+      c.trace[kTrLookups] = nu;
+    }
+  }
   if (last_block_signal(c, 1, c.done + 1)) raise_flags(c, 1, c.done + 1, *c.epoch);
 }
 
@@ -352,6 +345,9 @@ struct rs_comm {
   unsigned long long epoch = 0;       // host mirror of the device counter (parity)
   unsigned long long* d_epoch = nullptr;
   unsigned long long* d_bar_epoch = nullptr;
+  unsigned long long** d_sig_grad_ptrs = nullptr;  // [W] &peer(r)->sig_grad[rank]
+  const unsigned long long* own_sig_emb = nullptr;  // this arena's sig_emb[W]
+  const unsigned long long* own_sig_grad = nullptr; // this arena's sig_grad[W]
   unsigned long long* trace = nullptr;
   unsigned int* done = nullptr;
   uint32_t* send_pos = nullptr;
@@ -373,7 +369,10 @@ struct rs_comm {
   // CUDA graphs of rs_dist_step
   bool use_graphs = true;
   bool graph_fork = true;
+  bool one_stream = false;          // RS_DIST_ONE_STREAM=1: both roles on the caller's stream
   cudaStream_t cap_stream = nullptr;
+  cudaStream_t own_stream = nullptr;  // owner role runs here, concurrently with the requester's
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<DistGraph> graphs;
   uint64_t graph_clock = 0;
 };
@@ -393,7 +392,31 @@ static int prof_end(rs_comm* c, int ph, cudaStream_t s) {
   return RS_OK;
 }
 
-static CommDev comm_dev(rs_comm* c, int par) {
+// Each role keeps its own device step counter -- the requester's is bumped
+// by k_send_ids, the owner's by its first wait -- so a role never reads the
+// other stream's counter before that stream advanced it.
+enum Role : int { kRequester = 0, kOwner = 1 };
+static unsigned long long* role_epoch(rs_comm* c, Role r) { return c->d_epoch + (r == kOwner ? 2 : 0); }
+
+static rs_dist_sync wait_sync(rs_comm* c, const unsigned long long* flags, Role role) {
+  rs_dist_sync y;
+  y.wait_flags = flags;
+  y.wait_n = (uint32_t)c->world;
+  y.epoch = role_epoch(c, role);
+  y.error = c->trace + kTrError;
+  return y;
+}
+static rs_dist_sync signal_sync(rs_comm* c) {  // requester role
+  rs_dist_sync y;
+  y.epoch = role_epoch(c, kRequester);
+  y.sig_flags = c->d_sig_grad_ptrs;
+  y.sig_n = (uint32_t)c->world;
+  y.sig_done = c->done + 2;
+  y.error = c->trace + kTrError;
+  return y;
+}
+
+static CommDev comm_dev(rs_comm* c, int par, Role role) {
   CommDev d;
   d.peers = c->d_peers;
   d.rank = c->rank;
@@ -403,7 +426,7 @@ static CommDev comm_dev(rs_comm* c, int par) {
   d.off_ids = c->off_ids;
   d.off_emb = c->off_emb;
   d.off_grad = c->off_grad[par];
-  d.epoch = c->d_epoch;
+  d.epoch = role_epoch(c, role);
   d.trace = c->trace;
   d.done = c->done;
   return d;
@@ -426,7 +449,7 @@ static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, StepSets ss,
                      cudaStream_t s) {
   rs_workspace* wr = c->ws_req;
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
   const int ru = ss.ru;
   RS_TRY(prof_begin(c, kPhReqDedup, s));
   if (n) {
@@ -452,7 +475,7 @@ static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
 // caller) and the row stored into every requester that asked for it (KB')
 static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s) {
   rs_workspace* wo = c->ws_own;
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kOwner);
   const uint64_t nflat = (uint64_t)c->world * c->cap;
   const int ou = ss.ou;
   RS_TRY(prof_begin(c, kPhWaitIds, s));
@@ -486,7 +509,7 @@ static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s) {
 // requester: wait for the rows, expand them to the tokens (KC gather)
 static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSets ss,
                       cudaStream_t s) {
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhWaitEmbs, s));
   k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
   RS_LAUNCH_CHECK("k_wait(embs)");
@@ -495,6 +518,7 @@ static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSet
   if (n) {
     rs_dist_opts o;
     o.gather_view = c->view;
+    o.sync = wait_sync(c, c->own_sig_emb, kRequester);  // the owners' rows landed
     RS_TRY(step_tile(c->ws_req, t, ss.ru, n, d_out, nullptr, true, s, &o));
   }
   RS_TRY(prof_end(c, kPhGather, s));
@@ -507,7 +531,7 @@ static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSet
 static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n, StepSets ss,
                       cudaStream_t s) {
   rs_workspace* wr = c->ws_req;
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhReqReduce, s));
   if (n) {
     RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, nullptr));
@@ -516,10 +540,12 @@ static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
     o.send_pos = c->send_pos;
     o.cap = (uint32_t)c->cap;
     o.rank = (uint32_t)c->rank;
+    o.sync = signal_sync(c);  // the last finish block raises the gradient flags
     RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &o));
+  } else {  // idle rank: the owners still wait for its (empty) gradients
+    k_signal<<<1, 64, 0, s>>>(cd, 2);
+    RS_LAUNCH_CHECK("k_signal(grads)");
   }
-  k_signal<<<1, 64, 0, s>>>(cd, 2);
-  RS_LAUNCH_CHECK("k_signal(grads)");
   RS_TRY(prof_end(c, kPhReqReduce, s));
   return RS_OK;
 }
@@ -530,7 +556,7 @@ static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
 static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
                              const float* d_grads, StepSets ss, cudaStream_t s) {
   rs_workspace* wr = c->ws_req;
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhWaitEmbs, s));
   k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
   RS_LAUNCH_CHECK("k_wait(embs)");
@@ -539,16 +565,19 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
   if (n) {
     rs_dist_opts o;
     o.gather_view = c->view;
+    o.sync = wait_sync(c, c->own_sig_emb, kRequester);  // the owners' rows landed
     RS_TRY(step_tile(wr, t, ss.ru, n, d_out, d_grads, true, s, &o));
     rs_dist_opts f;
     f.peer_dst = c->d_peer_grad[ss.par];
     f.send_pos = c->send_pos;
     f.cap = (uint32_t)c->cap;
     f.rank = (uint32_t)c->rank;
+    f.sync = signal_sync(c);  // the last finish block raises the gradient flags
     RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &f));
+  } else {
+    k_signal<<<1, 64, 0, s>>>(cd, 2);
+    RS_LAUNCH_CHECK("k_signal(grads)");
   }
-  k_signal<<<1, 64, 0, s>>>(cd, 2);
-  RS_LAUNCH_CHECK("k_signal(grads)");
   RS_TRY(prof_end(c, kPhGather, s));
   return RS_OK;
 }
@@ -557,7 +586,7 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
 // stage-2 origin order -- fused with the optimizer on the shard
 static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cudaStream_t s) {
   rs_workspace* wo = c->ws_own;
-  const CommDev cd = comm_dev(c, ss.par);
+  const CommDev cd = comm_dev(c, ss.par, kOwner);
   const uint64_t nflat = (uint64_t)c->world * c->cap;
   RS_TRY(prof_begin(c, kPhWaitGrads, s));
   k_wait<<<1, kMaxWorld, 0, s>>>(cd, 2);
@@ -568,6 +597,7 @@ static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cu
   rs_dist_opts oo;  // at most `world` origins per id: the CSR finish over the origin rows
   oo.no_hot = true;
   oo.csr_pos = c->origins;
+  oo.sync = wait_sync(c, c->own_sig_grad, kOwner);  // every requester's sums landed
   RS_TRY(step_finish(wo, t, ss.ou, nflat, grad_in, ob, nullptr, s, &oo));
   RS_TRY(prof_end(c, kPhOwnerUpdate, s));
   return RS_OK;
@@ -601,6 +631,26 @@ static void end_step(rs_comm* c, StepSets ss) {
   c->last_sets = ss;
   c->ws_req->cur = ss.ru ^ 1;
   c->ws_own->cur = ss.ou ^ 1;
+}
+
+// The owner role runs on its own stream, concurrently with the requester
+// role on the caller's: fork returns the owner stream (ordered after
+// everything enqueued so far), join orders the caller's stream after it.
+static int fork_owner(rs_comm* c, cudaStream_t q, cudaStream_t* own) {
+  if (c->one_stream) {
+    *own = q;
+    return RS_OK;
+  }
+  RS_CUDA(cudaEventRecord(c->ev_fork, q));
+  RS_CUDA(cudaStreamWaitEvent(c->own_stream, c->ev_fork, 0));
+  *own = c->own_stream;
+  return RS_OK;
+}
+static int join_owner(rs_comm* c, cudaStream_t q, cudaStream_t own) {
+  if (own == q) return RS_OK;
+  RS_CUDA(cudaEventRecord(c->ev_join, own));
+  RS_CUDA(cudaStreamWaitEvent(q, c->ev_join, 0));
+  return RS_OK;
 }
 
 // end of a step: collect the phase times recorded during it (one sync)
@@ -648,8 +698,9 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
             cudaMalloc(&c->send_cnt, kMaxWorld * 4) == cudaSuccess &&
             cudaMemset(c->send_cnt, 0, kMaxWorld * 4) == cudaSuccess &&
             cudaMalloc(&c->view, sizeof(TableDev)) == cudaSuccess &&
-            cudaMalloc(&c->d_epoch, 16) == cudaSuccess && cudaMemset(c->d_epoch, 0, 16) == cudaSuccess;
+            cudaMalloc(&c->d_epoch, 32) == cudaSuccess && cudaMemset(c->d_epoch, 0, 32) == cudaSuccess;
   if (ok) c->d_bar_epoch = c->d_epoch + 1;
+  ok = ok && cudaMalloc(&c->d_sig_grad_ptrs, kMaxWorld * sizeof(void*)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     rs_comm_destroy(c);
@@ -679,7 +730,11 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   }
   if (const char* e = getenv("RS_NO_GRAPH")) c->use_graphs = e[0] == '0';
   if (const char* e = getenv("RS_DIST_GRAPH_FORK")) c->graph_fork = e[0] != '0';
+  if (const char* e = getenv("RS_DIST_ONE_STREAM")) c->one_stream = e[0] == '1';
   RS_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  RS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   c->h_peers[rank] = c->arena;
   *out = c;
   return RS_OK;
@@ -704,6 +759,14 @@ int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order
     c->h_peers[r] = static_cast<char*>(p);
   }
   RS_CUDA(cudaMemcpy(c->d_peers, c->h_peers, kMaxWorld * sizeof(char*), cudaMemcpyHostToDevice));
+  {
+    std::vector<unsigned long long*> f(kMaxWorld, nullptr);
+    for (int r = 0; r < c->world; ++r)
+      f[r] = &reinterpret_cast<ArenaHdr*>(c->h_peers[r])->sig_grad[c->rank];
+    RS_CUDA(cudaMemcpy(c->d_sig_grad_ptrs, f.data(), kMaxWorld * sizeof(void*), cudaMemcpyHostToDevice));
+    c->own_sig_emb = reinterpret_cast<ArenaHdr*>(c->arena)->sig_emb;
+    c->own_sig_grad = reinterpret_cast<ArenaHdr*>(c->arena)->sig_grad;
+  }
   for (int b = 0; b < 2; ++b) {
     std::vector<float*> g(kMaxWorld, nullptr);
     for (int r = 0; r < c->world; ++r) g[r] = reinterpret_cast<float*>(c->h_peers[r] + c->off_grad[b]);
@@ -718,13 +781,16 @@ int rs_comm_destroy(rs_comm* c) {
   for (int r = 0; r < c->world; ++r)
     if (r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
   void* ps[] = {c->arena, c->d_peers, c->d_peer_grad[0], c->d_peer_grad[1], c->trace, c->done,
-                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch};
+                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch, c->d_sig_grad_ptrs};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : c->pev)
     if (e) cudaEventDestroy(e);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   rs_workspace_destroy(c->ws_req);
   rs_workspace_destroy(c->ws_own);
   delete c;
@@ -740,10 +806,13 @@ int rs_dist_forward(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, 
   cudaStream_t s = S(stream);
   RS_TRY(prepare_step(c, t, 0, s));
   const StepSets ss = begin_step(c);
+  cudaStream_t own;
+  RS_TRY(fork_owner(c, s, &own));
   RS_TRY(req_front(c, t, d_ids, n, ss, s));
-  RS_TRY(owner_lookup(c, t, ss, s));
-  RS_TRY(table_after_op(t, s));
+  RS_TRY(owner_lookup(c, t, ss, own));
+  RS_TRY(table_after_op(t, own));
   RS_TRY(req_gather(c, t, n, d_out, ss, s));
+  RS_TRY(join_owner(c, s, own));
   end_step(c, ss);
   c->last_n = n;
   c->last_table = t;
@@ -762,16 +831,20 @@ int rs_dist_backward(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
   std::memset(ob, 0, sizeof(ob));
   RS_TRY(step_opt_args(t, opt, ob, s));
   if (n) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n, s));
+  cudaStream_t own;
+  RS_TRY(fork_owner(c, s, &own));
   RS_TRY(req_reduce(c, t, d_grads, n, c->last_sets, s));
-  RS_TRY(owner_update(c, t, ob, c->last_sets, s));
+  RS_TRY(owner_update(c, t, ob, c->last_sets, own));
+  RS_TRY(join_owner(c, s, own));
   t->applies++;
   c->have_forward = false;
   return prof_step_done(c);
 }
 
-// The whole step in one call: ids out, owner lookup + answer, then one fused
-// gather + segment-reduce pass over this rank's tokens whose per-id sums go
-// straight to the owners, then the owner update.  Identical results to
+// The whole step in one call, the two roles on two streams: the requester
+// (dedup, ids out, segment-reduce with the sums stored at the owners, then
+// the gather once the rows landed) overlaps the owner (stage 2, find-or-
+// insert + answer, update once the sums landed).  Identical results to
 // rs_dist_forward + rs_dist_backward (the owner answers with the rows as they
 // were before this step's update).  Replayed from a CUDA graph per
 // (buffers, n, parities) -- the flags' epoch lives on the device.
@@ -786,11 +859,24 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
   const StepSets ss = begin_step(c);
   const int mirror = t->mirror_next;
   auto enqueue = [&](cudaStream_t q) -> int {
+    if (c->one_stream) {  // both roles in one stream: fused gather + reduce pass
+      RS_TRY(req_front(c, t, d_ids, n, ss, q));
+      RS_TRY(owner_lookup(c, t, ss, q));
+      RS_TRY(table_mirror_copy(t, mirror, q));
+      RS_TRY(req_gather_reduce(c, t, n, d_out, d_grads, ss, q));
+      return owner_update(c, t, ob, ss, q);
+    }
+    // requester on q: dedup, ids out, reduce + sums out, then the gather;
+    // owner on its stream: stage 2, table + answer, then the update
+    cudaStream_t own;
+    RS_TRY(fork_owner(c, q, &own));
     RS_TRY(req_front(c, t, d_ids, n, ss, q));
-    RS_TRY(owner_lookup(c, t, ss, q));
-    RS_TRY(table_mirror_copy(t, mirror, q));
-    RS_TRY(req_gather_reduce(c, t, n, d_out, d_grads, ss, q));
-    return owner_update(c, t, ob, ss, q);
+    RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
+    RS_TRY(owner_lookup(c, t, ss, own));
+    RS_TRY(table_mirror_copy(t, mirror, own));
+    RS_TRY(owner_update(c, t, ob, ss, own));
+    RS_TRY(req_gather(c, t, n, d_out, ss, q));
+    return join_owner(c, q, own);
   };
   if (c->profiling || !c->use_graphs) {
     RS_TRY(enqueue(s));
@@ -863,7 +949,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
 // work enqueued after it starts only once every rank reached it.
 int rs_comm_barrier(rs_comm* c, void* stream) {
   if (!c) return fail(RS_ERR_CONFIG, "rs_comm_barrier: null comm");
-  k_barrier<<<1, kMaxWorld, 0, S(stream)>>>(comm_dev(c, 0), c->d_bar_epoch);
+  k_barrier<<<1, kMaxWorld, 0, S(stream)>>>(comm_dev(c, 0, kRequester), c->d_bar_epoch);
   RS_LAUNCH_CHECK("k_barrier");
   return RS_OK;
 }

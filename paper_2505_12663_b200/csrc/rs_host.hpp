@@ -118,8 +118,23 @@ struct rs_workspace {
   bool have_forward = false;
 };
 
+// Cross-GPU synchronisation folded into the step kernels (sharded step):
+// a prologue wait on flags in this rank's arena, and a grid-level arrival
+// whose last block raises flags at the peers (dist_sync.cuh).
+struct rs_dist_sync {
+  const unsigned long long* wait_flags = nullptr;  // [wait_n] flags to wait for (null: none)
+  uint32_t wait_n = 0;
+  const unsigned long long* epoch = nullptr;       // device step epoch
+  unsigned long long* const* sig_flags = nullptr;  // [sig_n] peer flag words to raise (null: none)
+  uint32_t sig_n = 0;
+  unsigned int* sig_done = nullptr;                // arrival counter of the signalling kernels
+  uint32_t sig_total = 0;                          // blocks arriving (set by the launcher)
+  unsigned long long* error = nullptr;             // set on a wait timeout
+};
+
 // Options of the fused kernels used by the sharded (multi-GPU) step (dist.cu).
 struct rs_dist_opts {
+  rs_dist_sync sync;                    // waits / signals folded into the kernels
   const uint32_t* d_n = nullptr;        // device token count (owner side); null: host n
   const uint32_t* pos_map = nullptr;    // CSR position of each token (owner: origin slot)
   bool no_stage = false;                // no hot ids possible: no gradient staging

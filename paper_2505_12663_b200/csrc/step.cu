@@ -34,6 +34,7 @@
 
 #include "opt_dev.cuh"
 #include "rs_host.hpp"
+#include "dist_sync.cuh"
 #include "scratch_dev.cuh"
 #include "table_dev.cuh"
 
@@ -293,6 +294,7 @@ struct TileArgs {
   const uint32_t* d_n;      // device token count (null: n)
   const uint32_t* pos_map;  // CSR value per token (null: token index)
   bool stage;               // hot ids possible: stage the tile's gradient rows
+  rs_dist_sync sync;        // sharded step: wait for the peers' rows before gathering
 };
 
 template <int VEC, int CH, int LPR>
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   const uint32_t nn = a.d_n ? *a.d_n : a.n;
   if (a.clean_cnt && tile == 0 && tid == 0) *a.clean_cnt = 0;
   if (t0 >= nn) return;
+  dist_wait(a.sync);
   const uint32_t rows = min(TT, nn - t0);
 
   if (red && a.stage) {
@@ -391,7 +394,8 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
 #pragma unroll
         for (int k = 0; k < BATCH; ++k) {
           const uint32_t tok = (b0 + k) * RPI + sub;
-          if (tok < cnt && j < D4) v[k] = __ldg(emb + (size_t)rr[k] * D4 + j);
+          if (tok < cnt && j < D4)  // rows written by peers this step: L2 (coherent) loads
+            v[k] = a.sync.wait_flags ? __ldcg(emb + (size_t)rr[k] * D4 + j) : __ldg(emb + (size_t)rr[k] * D4 + j);
         }
 #pragma unroll
         for (int k = 0; k < BATCH; ++k) {
@@ -586,6 +590,7 @@ struct FinishArgs {
   const uint32_t* send_pos;
   uint32_t cap, rank;
   uint64_t dbg_nrows, dbg_ncsr;  // RS_BOUNDS builds: valid grad rows / csr_pos entries
+  rs_dist_sync sync;             // sharded step: prologue wait / grid-level signal
 };
 
 __device__ __forceinline__ float* sum_dst(const FinishArgs& a, uint32_t uu, uint32_t D) {
@@ -641,6 +646,7 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
   uint32_t* order = order_s + (threadIdx.x / G) * kCsrMax;
   const uint32_t gid = blockIdx.x * gpb + threadIdx.x / G;
   const uint32_t ngroups = gridDim.x * gpb;
+  dist_wait(a.sync);
   const uint32_t nu = *a.n_unique;
   const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grads);
   for (uint32_t uu = gid; uu < nu; uu += ngroups) {
@@ -756,6 +762,7 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     *reinterpret_cast<float4*>(d.s2 + roff) = vv;
     if (d.s1) *reinterpret_cast<float4*>(d.s1 + roff) = mv;
   }
+  dist_arrive(a.sync);
 }
 
 // Roles by block index:
@@ -774,6 +781,7 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const TableDesc d = a.td->d;
   const uint32_t D = d.dim;
+  dist_wait(a.sync);
   if (blockIdx.x >= hot_blocks) {
     uint32_t* order_w = reinterpret_cast<uint32_t*>(smem2) + warp * kCsrMax;  // [NW x 64]
     const uint32_t nu = *a.n_unique;
@@ -807,6 +815,7 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
       else
         apply_row<VEC, CH>(d, row, acc, o);
     }
+    dist_arrive(a.sync);
     return;
   }
   uint32_t* bm = reinterpret_cast<uint32_t*>(smem2);  // [bw]
@@ -869,6 +878,7 @@ __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint
     }
     __syncthreads();
   }
+  dist_arrive(a.sync);
 }
 
 // Optimizer-only apply for pre-aggregated sums (GradAccumulator::apply given
@@ -1175,6 +1185,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.d_n = dopt ? dopt->d_n : nullptr;
   a.pos_map = dopt ? dopt->pos_map : nullptr;
   a.stage = !(dopt && dopt->no_stage);
+  if (dopt) a.sync = dopt->sync;
   a.clean_cnt = clean_other ? ws->set[use ^ 1].cnt : nullptr;
   a.slot_of = ws->slot_of;
   a.n = (uint32_t)n;
@@ -1267,6 +1278,11 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   }
   const Shape sh = shape_for(D);
   bool launched = G > 0 && dopt && dopt->no_hot;  // owner side: no hot ids possible
+  const unsigned eg = G > 0 ? grid_for(n * (uint64_t)G, 256, 148 * 16) : 0;
+  if (dopt) {  // the blocks of both finish kernels arrive on one counter
+    a.sync = dopt->sync;
+    a.sync.sig_total = (launched ? 0u : grid) + eg;
+  }
 #define RS_FIN(V, C)                                                   \
   if (!launched && sh.vec == V && sh.ch == C) {                        \
     k_finish<V, C><<<grid, 256, smem, hs>>>(a, o, hot_blocks);         \
@@ -1280,7 +1296,6 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
 #undef RS_FIN
   if (!launched) return fail(RS_ERR_CONFIG, "embedding_dim " + std::to_string(D) + " unsupported");
   if (G > 0) {
-    const unsigned eg = grid_for(n * (uint64_t)G, 256, 148 * 16);
 #define RS_CSR(GG)                                      \
   if (G == GG) {                                        \
     k_finish_csr<GG><<<eg, 256, 0, s>>>(a, o);          \
