@@ -31,6 +31,15 @@ sys.path.insert(0, ROOT)
 C1 = dict(workload="config1: 1 dynamic table dim 64, 2^20 keys, batch 1024 seqs (mean 128, max 4096, sigma 1.0), "
                    "Zipf 1.1, dedup+lookup+Adagrad", dim=64, vocab=1 << 20, seqs=1024, mean=128.0, max_len=4096,
           sigma=1.0, zipf=1.1, seed=1, capacity=1 << 22)
+C4 = dict(workload="config4: row-sharded table of 100M pre-populated keys, dim 128, Zipf 1.1 over 1e8, per-rank batch "
+                   "1024 seqs (mean 128, max 4096, sigma 1.0), dedup+lookup+Adagrad, ids/embeddings/gradients over NVLink",
+          dim=128, vocab=100_000_000, seqs=1024, mean=128.0, max_len=4096, sigma=1.0, zipf=1.1, seed=4,
+          capacity=None)
+C5 = dict(workload="config5: long-tail sequences (lognormal sigma 1.5, mean 128, max 4096), a pool of 1024 x N "
+                   "sequences per step assigned to the N ranks by the cost model (LPT on a*len + b*len^2, "
+                   "CostModel defaults a=1, b=0.01), sharded 2^20-key table dim 64, dedup+lookup+Adagrad",
+          dim=64, vocab=1 << 20, seqs=1024, mean=128.0, max_len=4096, sigma=1.5, zipf=1.1, seed=5,
+          capacity=1 << 22, pooled=True)
 TAG1 = np.uint64(1 << 62)
 L2_FLUSH_BYTES = 512 << 20
 
@@ -119,13 +128,14 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dim, vocab = cfg["dim"], cfg["vocab"]
 
-    # table: 2^20 keys pre-populated with pseudo_sparse_grad(k, 0) rows (bench_main.cpp:105-108)
-    table = P.EmbedTable(P.TableConfig(capacity=cfg["capacity"], embedding_dim=dim, optimizer="adagrad",
+    # table: every key pre-populated with pseudo_sparse_grad(k, 0) rows (bench_main.cpp:105-108)
+    cap = cfg["capacity"] or 1 << int(np.ceil(np.log2((vocab + (1 << 20)) / 0.6)))
+    table = P.EmbedTable(P.TableConfig(capacity=cap, embedding_dim=dim, optimizer="adagrad",
                                        chunk_rows=1 << 16, initial_rows=vocab + (1 << 20)))
-    raw = torch.arange(vocab, dtype=torch.int64, device="cuda")
-    init = W.pseudo_grads(raw, 0, dim)
-    table.insert(raw + int(TAG1), init)
-    del init
+    for lo in range(0, vocab, 1 << 24):
+        raw = torch.arange(lo, min(vocab, lo + (1 << 24)), dtype=torch.int64, device="cuda")
+        table.insert(raw + int(TAG1), W.pseudo_grads(raw, 0, dim))
+    del raw
     # distinct batches (weak scaling: each rank its own seed stream)
     nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
     batches = []
@@ -248,7 +258,7 @@ def run_ours(args, cfg):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and cfg is C1:
         res["cpu_baseline"] = cpu_baseline(cfg, batches, budget_s=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(res), flush=True)
@@ -280,16 +290,42 @@ def run_sharded(args, cfg):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dim, vocab = cfg["dim"], cfg["vocab"]
     nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
-    batches = [W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
-                          cfg["zipf"], [vocab]) for b in range(nb)]
+    balance = None
+    if cfg.get("pooled"):
+        # config 5: one pool of sequences per step, every rank computes the same
+        # assignment (rs_partition_sequences) and takes its share
+        policy = P.batcher.COST_LPT if args.balance == "lpt" else P.batcher.ROUND_ROBIN
+        batches, spreads, cost_spreads = [], [], []
+        for b in range(nb):
+            lengths, ids = W.generate(cfg["seed"] + b, cfg["seqs"] * world, cfg["mean"], cfg["max_len"],
+                                      cfg["sigma"], cfg["zipf"], [vocab])
+            ranks, load = P.partition_sequences(lengths, world, policy, 1.0, 0.01)
+            starts = np.concatenate([[0], np.cumsum(lengths.astype(np.int64))])
+            mine = np.nonzero(ranks == rank)[0]
+            ids_r = np.concatenate([ids[starts[i]:starts[i + 1]] for i in mine]) if len(mine) else ids[:0]
+            batches.append((lengths[mine], ids_r))
+            tok = np.array([lengths[ranks == r].sum() for r in range(world)], np.uint64)
+            spreads.append(P.imbalance_report(tok).spread)
+            cost_spreads.append(float((load.max() - load.min()) / load.max()) if load.max() > 0 else 0.0)
+        balance = {"policy": args.balance, "token_spread_mean": float(np.mean(spreads)),
+                   "cost_spread_mean": float(np.mean(cost_spreads))}
+    else:
+        batches = [W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
+                              cfg["zipf"], [vocab]) for b in range(nb)]
     mt = torch.tensor([max(len(i) for _, i in batches)], dtype=torch.int64, device="cuda")
     dist.all_reduce(mt, op=dist.ReduceOp.MAX)  # the arena layout must agree on every rank
     max_t = int(mt.item())
     nflat = world * max_t
-    st = ShardedTable(P.TableConfig(capacity=cfg["capacity"] * 2, embedding_dim=dim, optimizer="adagrad",
-                                    chunk_rows=1 << 16, initial_rows=vocab // world + 8 * nflat), max_tokens=max_t)
-    raw = torch.arange(vocab, dtype=torch.int64, device="cuda")
-    st.insert_owned(raw + int(TAG1), W.pseudo_grads(raw, 0, dim))
+    # shard sized for its keys + the W * max_tokens new-key headroom of a step
+    rows = vocab // world + vocab // (8 * world) + 8 * nflat
+    cap = cfg["capacity"] * 2 if cfg.get("capacity") else 1 << int(np.ceil(np.log2(rows / 0.6)))
+    st = ShardedTable(P.TableConfig(capacity=cap, embedding_dim=dim, optimizer="adagrad",
+                                    chunk_rows=1 << 16, initial_rows=rows), max_tokens=max_t)
+    for lo in range(0, vocab, 1 << 24):  # every rank inserts the keys it owns
+        raw = torch.arange(lo, min(vocab, lo + (1 << 24)), dtype=torch.int64, device="cuda")
+        st.insert_owned(raw + int(TAG1), W.pseudo_grads(raw, 0, dim))
+    del raw
+    torch.cuda.synchronize()
     params = P.AdagradParams(lr=0.01, eps=1e-8)
     dev = []
     for b, (lengths, ids) in enumerate(batches):
@@ -380,6 +416,7 @@ def run_sharded(args, cfg):
         "kernel_ms_rank0": phases,
         "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         "per_rank": per_rank,
+        "balance": balance,
         "table_host_syncs_rank0": int(st.shard.info().host_syncs),
         "roofline": {"bound": "hbm", "kernel": "sharded step (all kernels of one rank)", "achieved": ach,
                      "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": None, "peak_source": how,
@@ -719,13 +756,22 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="run the row-sharded step even at N=1")
-    ap.add_argument("--config", default="c1", choices=["c1", "c2"], help="BASELINE config (default: the headline c1)")
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c4", "c5"],
+                    help="BASELINE config (default: the headline c1; c4 = the sharded 100M-key table; "
+                         "c5 = long-tail sequences balanced across the ranks)")
+    ap.add_argument("--balance", default="lpt", choices=["lpt", "rr"], help="config 5 rank assignment")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.config == "c2" and args.impl == "ours":
         run_c2(args, C2)
     elif args.impl == "reference":
         run_reference(args, C1)
+    elif args.config == "c5":
+        run_sharded(args, C5)
+    elif args.config == "c4" and (int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded):
+        run_sharded(args, C4)
+    elif args.config == "c4":
+        run_ours(args, C4)
     elif int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:
         run_sharded(args, C1)
     else:

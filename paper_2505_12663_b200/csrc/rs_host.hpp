@@ -73,6 +73,7 @@ struct rs_scratch {
 };
 
 struct rs_workspace {
+  bool graph_fork = false;  // hot-id finish as a forked branch inside captured graphs
   uint64_t max_tokens = 0;
   uint64_t S = 0;  // scratch hash capacity (power of two)
   rs_scratch set[2];

@@ -1409,6 +1409,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   ws->max_tokens = max_tokens;
   if (const char* e = getenv("RS_NO_GRAPH")) ws->use_graphs = e[0] == '0';
   if (const char* e = getenv("RS_NO_FORK")) ws->fork = e[0] == '0';
+  if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] == '1';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;
@@ -1663,7 +1664,7 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
       const uint64_t before = launches();
       // a forked branch inside the captured graph measured slower: linear graph
       const bool fork = ws->fork;
-      ws->fork = false;
+      ws->fork = ws->fork && ws->graph_fork;
       st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, cs, nullptr);
       ws->fork = fork;
       cudaGraph_t g = nullptr;
