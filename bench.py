@@ -561,6 +561,96 @@ def run_c2(args, cfg):
     print(json.dumps(res), flush=True)
 
 
+C3 = dict(workload="config3: insert/evict-heavy stream: bounded table (max_keys 2^22, starts full), dim 128, "
+                   "batch 1024 seqs (mean 128, max 4096, sigma 1.0), Zipf 1.1 over the resident ids with 20% of "
+                   "each batch's unique ids replaced by never-seen ids; every batch inserts and evicts the oldest "
+                   "(tick, key)", dim=128, bound=1 << 22, seqs=1024, mean=128.0, max_len=4096, sigma=1.0, zipf=1.1,
+          seed=3, new_frac=0.2)
+
+
+def run_c3(args, cfg):
+    """Config 3 on one GPU: the fused step on a bounded table (probe, evict the
+    oldest (tick, key) beyond the bound, insert the misses, gather, reduce,
+    update).  value = unique ids / time."""
+    import torch
+
+    import paper_2505_12663_b200 as P
+    from paper_2505_12663_b200 import workload as W
+
+    torch.cuda.set_device(0)
+    dim, bound = cfg["dim"], cfg["bound"]
+    table = P.EmbedTable(P.TableConfig(capacity=1 << int(np.ceil(np.log2(bound / 0.6))), embedding_dim=dim,
+                                       optimizer="adagrad", chunk_rows=1 << 16, initial_rows=bound + (1 << 20),
+                                       max_keys=bound))
+    for lo in range(0, bound, 1 << 22):  # starts full at the bound
+        raw = torch.arange(lo, min(bound, lo + (1 << 22)), dtype=torch.int64, device="cuda")
+        table.ensure(raw + int(TAG1))
+    rng = np.random.default_rng(cfg["seed"])
+    fresh = np.uint64((1 << 62) + bound)
+    nb = 6
+    batches = []
+    for b in range(nb + args.steps + max(args.warmup, 3)):  # new ids never repeat across steps
+        lengths, ids = W.generate(cfg["seed"] + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
+                                  cfg["zipf"], [bound])
+        u, inv = np.unique(ids, return_inverse=True)
+        pick = rng.random(len(u)) < cfg["new_frac"]
+        u = u.copy()
+        u[pick] = fresh + np.arange(int(pick.sum()), dtype=np.uint64)
+        fresh += np.uint64(int(pick.sum()))
+        batches.append((lengths, u[inv], len(u), int(pick.sum())))
+    max_t = max(len(x[1]) for x in batches)
+    step = P.SparseStep(table, max_t, P.AdagradParams(lr=0.01, eps=1e-8))
+    out = torch.empty((max_t, dim), device="cuda")
+    dev = []
+    for b, (lengths, ids, nu, nnew) in enumerate(batches):
+        dev.append((P.as_keys(ids), W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)),
+                                                   b, dim), nu, nnew))
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    lib = P.lib()
+    k0 = max(args.warmup, 3)
+    for k in range(k0):
+        d_ids, d_g, _, _ = dev[k]
+        step.step(d_ids, d_g, out[:d_ids.numel()])
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = lib.rs_kernel_launches()
+    syncs0 = table.info().host_syncs
+    with Clocks(0) as clk:
+        for k in range(args.steps):
+            d_ids, d_g, _, _ = dev[k0 + k]
+            flush.zero_()
+            evs[k][0].record(stream)
+            step.step(d_ids, d_g, out[:d_ids.numel()])
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = lib.rs_kernel_launches() - launches0
+    ms = [a.elapsed_time(b) for a, b in evs]
+    t = sum(ms) / 1e3
+    uniq = sum(dev[k0 + k][2] for k in range(args.steps))
+    new = sum(dev[k0 + k][3] for k in range(args.steps))
+    syncs = table.info().host_syncs - syncs0
+    toks = sum(dev[k0 + k][0].numel() for k in range(args.steps))
+    assert table.occupied() == bound
+    hbm, how = peaks()
+    T, U, Nn = toks / args.steps, uniq / args.steps, new / args.steps
+    byt = 12 * T + 24 * U + 8 * dim * T + 20 * dim * U + Nn * (16 + 16 + 16 + 8 * dim)  # + evict/insert slots, row init
+    ach = byt / (t / args.steps) / 1e9
+    res = {"metric": "unique-ID lookups+updates/sec", "value": uniq / t, "unit": "unique-ids/s", "n_gpus": 1,
+           "steps": args.steps, "warmup": k0, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 optimizer math, u64 ids",
+           "data": "synthetic: the reference's generator + a monotone counter of never-seen ids",
+           "config": {"workload": cfg["workload"], "tokens_per_step": T, "unique_per_step": U,
+                      "new_ids_per_step": Nn, "evictions_per_step": Nn,
+                      "l2": "flushed (512 MiB write) between timed steps"},
+           "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "frac": ach / hbm, "traffic": None, "peak_source": how, "algorithmic_bytes_per_launch": byt},
+           "victim_selection": "device radix select over (tick, key) (evict.cu), no host round trip",
+           "table_host_syncs_in_timed_region": int(syncs),
+           "gpu_launches": int(launches), "clocks": clk.summary()}
+    print(json.dumps(res), flush=True)
+
+
 def _n_unique(step):
     import ctypes
 
@@ -756,7 +846,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="run the row-sharded step even at N=1")
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c4", "c5"],
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "c5"],
                     help="BASELINE config (default: the headline c1; c4 = the sharded 100M-key table; "
                          "c5 = long-tail sequences balanced across the ranks)")
     ap.add_argument("--balance", default="lpt", choices=["lpt", "rr"], help="config 5 rank assignment")
@@ -764,6 +854,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     if args.config == "c2" and args.impl == "ours":
         run_c2(args, C2)
+    elif args.config == "c3" and args.impl == "ours":
+        run_c3(args, C3)
     elif args.impl == "reference":
         run_reference(args, C1)
     elif args.config == "c5":

@@ -40,6 +40,12 @@ struct rs_table {
   uint64_t missing_cap = 0;
   uint64_t* d_victims = nullptr;
   uint64_t victims_cap = 0;
+  // device victim selection (evict.cu)
+  void* d_evict = nullptr;          // EvictState
+  uint32_t* d_cand = nullptr;       // 2 x candidate lists
+  uint32_t* d_victim_idx = nullptr;
+  uint64_t evict_cap = 0, victim_idx_cap = 0;
+  uint64_t buf_gen = 0;  // bumps when a buffer baked into captured graphs is reallocated
 };
 
 struct rs_graph_entry {
@@ -52,6 +58,7 @@ struct rs_graph_entry {
   int mirror = 0;
   int set = 0;
   const void* pbuf = nullptr;
+  uint64_t tcap = 0, tgen = 0;  // table capacity / buffer generation baked into the graph
   unsigned char opt[128] = {0};
   cudaGraphExec_t exec = nullptr;
   uint64_t last_use = 0;
@@ -154,6 +161,17 @@ int table_after_op(rs_table* t, cudaStream_t s);             // enqueue counter 
 int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                         uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
                         uint32_t* d_srow, cudaStream_t s);
+// evict.cu: device victim selection + removal (bounded ensure after the
+// probe: explicit_k == 0; explicit evict: explicit_k = k)
+int evict_device(rs_table* t, const uint32_t* d_n, uint64_t n_host, uint64_t explicit_k,
+                 cudaStream_t s);
+int evict_count(rs_table* t, uint64_t* out, cudaStream_t s);
+int evict_prepare(rs_table* t, uint64_t max_victims);  // host: size the selection buffers
+// bounded ensure split for graph capture: host part, then enqueue-only part
+int table_bounded_prepare(rs_table* t, uint64_t n_max, cudaStream_t s);
+int table_bounded_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                          uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                          uint32_t* d_srow, cudaStream_t s);  // victims of the last selection (syncs)
 int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                      uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
                      uint32_t* d_srow, cudaStream_t s);

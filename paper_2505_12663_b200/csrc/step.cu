@@ -1583,10 +1583,25 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
                         int mirror, cudaStream_t s, cudaEvent_t* ev) {
   int st;
   if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
-  if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
-  if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
-  k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
-  RS_LAUNCH_CHECK("k_ftable");
+  if (t->cfg.max_keys) {  // bounded: dedup + metadata, then probe / evict / insert on the device
+    k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
+    RS_LAUNCH_CHECK("k_clean");
+    if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
+    if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
+    FTableArgs a = ftable_args(ws, t, use);
+    a.do_clean = false;
+    a.do_table = false;
+    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
+    RS_LAUNCH_CHECK("k_ftable(meta)");
+    if ((st = table_bounded_enqueue(t, ws->unique, ws->set[use].cnt, n, ws->urow, ws->urow64,
+                                    ws->set[use].u_slot, ws->set[use].srow, s)))
+      return st;
+  } else {
+    if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
+    if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
+    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
+    RS_LAUNCH_CHECK("k_ftable");
+  }
   if (ev) RS_CUDA(cudaEventRecord(ev[2], s));
   if ((st = launch_tile(ws, t, use, n, d_out, d_grads, true, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[3], s));
@@ -1598,8 +1613,7 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
 int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
             const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream) {
   if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_step: null handle");
-  if (t->cfg.max_keys || n == 0) {
-    // bounded tables synchronize on the host to evict: no graph
+  if (n == 0) {
     int st = rs_forward(ws, t, d_ids, n, d_out, stream);
     if (st) return st;
     return rs_backward(ws, t, d_grads, n, opt, stream);
@@ -1610,8 +1624,9 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
   int st = opt_args(t, opt, &o, s);
   if (st) return st;
   if ((st = set_smem_attrs())) return st;
-  // host side, outside the graph: capacity bound (may rehash / grow rows on s)
-  if ((st = table_prepare(t, n, s))) return st;
+  // host side, outside the graph: capacity bound (may rehash / grow rows on s),
+  // bounded tables also size the device victim selection
+  if ((st = t->cfg.max_keys ? table_bounded_prepare(t, n, s) : table_prepare(t, n, s))) return st;
   ws->last_tile = tile_tokens_for_dim(t->desc.dim);
   if ((st = reduce_prepare(ws, t->desc.dim, n, s))) return st;
   const int mirror = t->mirror_next;
@@ -1634,7 +1649,8 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
     rs_graph_entry* hit = nullptr;
     for (auto& g : ws->graphs) {
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
-          g.mirror == mirror && g.set == use && g.pbuf == ws->pbuf &&
+          g.mirror == mirror && g.set == use && g.pbuf == ws->pbuf && g.tcap == t->capacity &&
+          g.tgen == t->buf_gen &&
           std::memcmp(g.opt, &o, sizeof(o)) == 0) {
         hit = &g;
         break;
@@ -1658,6 +1674,8 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
       e.mirror = mirror;
       e.set = use;
       e.pbuf = ws->pbuf;
+      e.tcap = t->capacity;
+      e.tgen = t->buf_gen;
       std::memcpy(e.opt, &o, sizeof(o));
       cudaStream_t cs = ws->cap_stream;
       RS_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));

@@ -563,46 +563,34 @@ static int grow_u32(uint32_t** p, uint64_t* cap, uint64_t n, cudaStream_t s) {
 
 // Host-side selection of the k live entries with smallest (tick, key) among
 // those with tick < tick_limit, then a device remove.  Synchronizes.
-int evict_oldest(rs_table* t, uint64_t k, uint64_t tick_limit, uint64_t* evicted,
-                 cudaStream_t s) {
-  if (evicted) *evicted = 0;
-  if (k == 0) return RS_OK;
-  TableCounters c;
-  int st = read_counters(t, &c, s);
+// Bounded ensure, host part: missing list, capacity for the misses (from the
+// async counter mirror; no synchronization in steady state), selection buffers.
+int table_bounded_prepare(rs_table* t, uint64_t n_max, cudaStream_t s) {
+  const uint64_t cap0 = t->missing_cap;
+  int st = grow_u32(&t->d_missing, &t->missing_cap, n_max, s);
   if (st) return st;
-  std::vector<Slot> slots(t->capacity);
-  RS_CUDA(cudaMemcpy(slots.data(), t->desc.slots, t->capacity * sizeof(Slot),
-                     cudaMemcpyDeviceToHost));
-  struct E {
-    uint32_t tick;
-    uint64_t key;
-  };
-  std::vector<E> cand;
-  cand.reserve(c.occupied + 2);
-  for (const Slot& sl : slots)
-    if (sl.key != kEmptyKey && sl.key != kTombKey && sl.tick < tick_limit)
-      cand.push_back({sl.tick, sl.key});
-  for (int sp = 0; sp < 2; ++sp)
-    if (c.special_row[sp] != kNoRow && c.special_tick[sp] < tick_limit)
-      cand.push_back({c.special_tick[sp], sp == 0 ? kEmptyKey : kTombKey});
-  auto lt = [](const E& a, const E& b) { return a.tick != b.tick ? a.tick < b.tick : a.key < b.key; };
-  if (k > cand.size()) k = cand.size();
-  std::nth_element(cand.begin(), cand.begin() + (k ? k - 1 : 0), cand.end(), lt);
-  std::vector<uint64_t> keys(k);
-  for (uint64_t i = 0; i < k; ++i) keys[i] = cand[i].key;
-  if (t->victims_cap < k) {
-    if (t->d_victims) RS_CUDA(cudaFree(t->d_victims));
-    t->victims_cap = std::max<uint64_t>(k, 1024);
-    RS_CUDA(cudaMalloc(&t->d_victims, t->victims_cap * 8));
-  }
-  RS_CUDA(cudaMemcpy(t->d_victims, keys.data(), k * 8, cudaMemcpyHostToDevice));
-  k_table_remove<<<grid_for(k, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
-      t->dev, t->d_victims, k, nullptr);
-  RS_LAUNCH_CHECK("k_table_remove(evict)");
-  st = table_after_op(t, s);
+  if (t->missing_cap != cap0) t->buf_gen++;
+  if ((st = table_prepare(t, n_max, s))) return st;
+  return evict_prepare(t, n_max);
+}
+
+// Bounded ensure, device part: probe (stamp hits, list misses), the device
+// victim selection (oldest (tick, key) beyond the bound) with the tick
+// rewound to the batch tick, then the insert of the misses.
+int table_bounded_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                          uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
+                          uint32_t* d_srow, cudaStream_t s) {
+  RS_CUDA(cudaMemsetAsync(&t->dev->c.missing, 0, sizeof(unsigned int), s));
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 2, d_rows32, d_rows64, d_uslot, d_srow,
+      t->d_missing, nullptr);
+  RS_LAUNCH_CHECK("k_table_upsert(probe)");
+  int st = evict_device(t, d_n, n_max, 0, s);
   if (st) return st;
-  RS_CUDA(cudaStreamSynchronize(s));
-  if (evicted) *evicted = k;
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, &t->dev->c.missing, (uint32_t)n_max, nullptr, 0, d_rows32, d_rows64, d_uslot,
+      d_srow, nullptr, t->d_missing);
+  RS_LAUNCH_CHECK("k_table_upsert(insert missing)");
   return RS_OK;
 }
 
@@ -613,43 +601,9 @@ int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, u
   if (!t->cfg.max_keys)
     return table_ensure_device(t, d_keys, d_n, n_max, d_rows32, d_rows64, d_uslot, d_srow, s);
   if (n_max == 0) return RS_OK;
-  int st = grow_u32(&t->d_missing, &t->missing_cap, n_max, s);
+  int st = table_bounded_prepare(t, n_max, s);
+  if (!st) st = table_bounded_enqueue(t, d_keys, d_n, n_max, d_rows32, d_rows64, d_uslot, d_srow, s);
   if (st) return st;
-  RS_CUDA(cudaMemsetAsync(&t->dev->c.missing, 0, sizeof(unsigned int), s));
-  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
-      t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 2, d_rows32, d_rows64, d_uslot, d_srow,
-      t->d_missing, nullptr);
-  RS_LAUNCH_CHECK("k_table_upsert(probe)");
-  st = table_after_op(t, s);
-  if (st) return st;
-  TableCounters c;
-  st = read_counters(t, &c, s);
-  if (st) return st;
-  uint32_t n = (uint32_t)n_max;
-  if (d_n) RS_CUDA(cudaMemcpy(&n, d_n, 4, cudaMemcpyDeviceToHost));
-  const uint64_t missing = c.missing;
-  if (missing == 0) return RS_OK;
-  const uint64_t found = n - missing;
-  if (c.occupied + missing > t->cfg.max_keys) {
-    const uint64_t need = c.occupied + missing - t->cfg.max_keys;
-    if (need > c.occupied - found)
-      return fail(RS_ERR_CAPACITY, "bounded table: batch of " + std::to_string(n) +
-                                       " keys cannot fit max_keys " +
-                                       std::to_string(t->cfg.max_keys));
-    st = evict_oldest(t, need, c.tick, nullptr, s);
-    if (st) return st;
-  }
-  st = table_prepare(t, missing, s);
-  if (st) return st;
-  // one tick per logical batch: new keys get the probe's tick (eviction's
-  // remove advanced it; rewind so the insert stamps c.tick again)
-  const unsigned int rewind = c.tick - 1;
-  RS_CUDA(cudaMemcpyAsync(&t->dev->c.tick, &rewind, sizeof(unsigned int), cudaMemcpyHostToDevice, s));
-  k_table_upsert<<<grid_for(missing, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
-      t->dev, d_keys, nullptr, (uint32_t)missing, nullptr, 0, d_rows32, d_rows64, d_uslot, d_srow,
-      nullptr, t->d_missing);
-  RS_LAUNCH_CHECK("k_table_upsert(insert missing)");
-  RS_CUDA(cudaStreamSynchronize(s));
   return table_after_op(t, s);
 }
 
@@ -742,6 +696,9 @@ int rs_table_destroy(rs_table* t) {
   cudaFree(t->desc.free_stack);
   cudaFree(t->d_bc);
   cudaFree(t->dev);
+  if (t->d_evict) cudaFree(t->d_evict);
+  if (t->d_cand) cudaFree(t->d_cand);
+  if (t->d_victim_idx) cudaFree(t->d_victim_idx);
   for (auto& m : t->mirror) {
     if (m.pinned) cudaFreeHost(m.pinned);
     if (m.ev) cudaEventDestroy(m.ev);
@@ -851,7 +808,14 @@ int rs_table_ensure(rs_table* t, const uint64_t* d_keys, uint64_t n, int64_t* d_
 
 int rs_table_evict(rs_table* t, uint64_t k, uint64_t* evicted, void* stream) {
   if (!t) return fail(RS_ERR_CONFIG, "rs_table_evict: null table");
-  return evict_oldest(t, k, ~0ull, evicted, S(stream));
+  if (evicted) *evicted = 0;
+  if (k == 0) return RS_OK;
+  cudaStream_t s = S(stream);
+  int st = evict_prepare(t, k);
+  if (!st) st = evict_device(t, nullptr, 0, k, s);
+  if (!st) st = table_after_op(t, s);
+  if (!st) st = evict_count(t, evicted, s);  // synchronizes
+  return st;
 }
 
 int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* emb, float* m,

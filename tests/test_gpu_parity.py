@@ -336,3 +336,90 @@ def test_ensure_duplicate_keys_in_one_batch(cuda, oracle):
         assert i.occupied == o.o.table_occupied(o.h)
         assert i.rows_allocated - i.rows_free == i.occupied  # nothing leaked
     _compare_contents(g, o, ("keys", "emb", "m", "v", "step"))
+
+
+@pytest.mark.parametrize("spread", [1, 5000])
+def test_device_eviction_vs_oracle(cuda, oracle, spread):
+    # bounded ensure with the device victim selection: ties in tick broken by
+    # key (one initial tick for every key), ticks spread over many batches
+    # (spread > 4096 exercises the narrowing tick windows), sentinel keys
+    rng = np.random.default_rng(31 + spread)
+    dim, bound = 8, 2000
+    g = _gpu_table(1 << 12, dim, opt="adagrad", max_keys=bound)
+    o = Table(oracle, 1 << 12, dim, chunk_rows=4096)
+    init = rng.choice(1 << 40, bound - 2, replace=False).astype(np.uint64)
+    init = np.concatenate([init, np.array([~np.uint64(0), ~np.uint64(0) - np.uint64(1)], np.uint64)])
+    for lo in range(0, bound, 500):  # several initial ticks
+        keys = init[lo:lo + 500]
+        tick = g.tick() + 1
+        g.ensure(keys)
+        oracle.table_ensure_batch(o.h, keys, len(keys), tick, bound, None)
+    if spread > 1:
+        # spread the ticks of touched keys over > 4096 batch ops: lookups of an
+        # absent key advance the tick and stamp nothing
+        for _ in range(3):
+            for _ in range(1500):
+                g.lookup_batch(np.array([1], np.uint64))
+            sel = rng.choice(init, 50, replace=False)
+            tick = g.tick() + 1
+            g.ensure(sel)
+            oracle.table_ensure_batch(o.h, sel, len(sel), tick, bound, None)
+    fresh = np.uint64(1 << 50)
+    for b in range(10):
+        old = rng.choice(init, 300)
+        new = fresh + np.arange(120, dtype=np.uint64)
+        fresh += np.uint64(120)
+        keys = np.unique(np.concatenate([old, new]))
+        tick = g.tick() + 1
+        g.ensure(keys)
+        oracle.table_ensure_batch(o.h, keys, len(keys), tick, bound, None)
+        assert g.occupied() == oracle.table_occupied(o.h) == bound
+    _compare_contents(g, o, ("keys", "ts", "emb", "v", "step"))
+    for k in (1, 77, 600):
+        g.evict(k)
+        oracle.table_evict_oldest(o.h, k)
+        _compare_contents(g, o, ("keys", "ts"))
+
+
+def test_bounded_step_graph_equals_eager_and_oracle_keys(cuda, oracle):
+    # the fused step on a bounded table replays from a CUDA graph (device
+    # eviction, no host round trip); it must equal the eager forward/backward
+    # path bit for bit, and its key set / ticks must follow the oracle's
+    # ensure_batch eviction semantics
+    rng = np.random.default_rng(41)
+    dim, bound = 32, 1500
+    tabs = [_gpu_table(1 << 12, dim, opt="adagrad", max_keys=bound) for _ in range(2)]
+    o = Table(oracle, 1 << 12, dim, chunk_rows=4096)
+    init = np.arange(bound, dtype=np.uint64) * np.uint64(7919)
+    for t in tabs:
+        t.ensure(init)
+    tick0 = tabs[0].tick()
+    oracle.table_ensure_batch(o.h, init, len(init), tick0, bound, None)
+    steps = [P.SparseStep(t, 6000, P.AdagradParams(lr=0.05)) for t in tabs]
+    fresh = np.uint64(1 << 45)
+    buf_ids = torch.empty(6000, dtype=torch.int64, device="cuda")
+    buf_g = torch.empty((6000, dim), device="cuda")
+    outs = [torch.empty((6000, dim), device="cuda") for _ in tabs]
+    for b in range(8):
+        base = init[rng.integers(0, 900, 3000)]  # a batch must fit the bound
+        new = fresh + rng.integers(0, 400, 1000).astype(np.uint64)
+        fresh += np.uint64(400)
+        ids = np.concatenate([base, new])
+        rng.shuffle(ids)
+        n = len(ids)
+        buf_ids[:n] = P.as_keys(ids)
+        buf_g[:n] = torch.from_numpy((rng.integers(-64, 64, (n, dim)) / 64.0).astype(np.float32)).cuda()
+        tick = tabs[0].tick() + 1
+        steps[0].step(buf_ids[:n], buf_g[:n], outs[0][:n])        # graph path
+        steps[1].forward(buf_ids[:n], outs[1][:n])                # eager path
+        steps[1].backward(buf_g[:n])
+        torch.testing.assert_close(outs[0][:n], outs[1][:n], rtol=0, atol=0)
+        u = np.unique(ids)
+        oracle.table_ensure_batch(o.h, u, len(u), tick, bound, None)
+        assert tabs[0].occupied() == tabs[1].occupied() == bound
+    a, b2 = tabs[0].export(), tabs[1].export()
+    for f in ("keys", "emb", "v", "step", "ts"):
+        np.testing.assert_array_equal(a[f], b2[f], err_msg=f)
+    oo = o.export()
+    np.testing.assert_array_equal(a["keys"], oo["keys"])
+    np.testing.assert_array_equal(a["ts"], oo["ts"].astype(a["ts"].dtype))
