@@ -155,27 +155,54 @@ __global__ void __launch_bounds__(256) k_route_count(const uint64_t* __restrict_
   if (threadIdx.x < m.n_groups) counts[(uint64_t)blockIdx.x * m.n_groups + threadIdx.x] = c[threadIdx.x];
 }
 
-// exclusive scan over blocks per group (one block; group-major offsets:
-// group g's tokens start at total of groups < g)
-__global__ void k_route_scan(uint32_t* __restrict__ counts, uint32_t nblocks, uint32_t G,
-                             uint64_t* __restrict__ group_counts) {
-  __shared__ uint64_t tot[kMaxRouteGroups];
-  const uint32_t g = threadIdx.x;
-  if (g < G) {
-    uint64_t run = 0;
-    for (uint32_t b = 0; b < nblocks; ++b) {
-      const uint32_t v = counts[(uint64_t)b * G + g];
-      counts[(uint64_t)b * G + g] = (uint32_t)run;
-      run += v;
-    }
-    tot[g] = run;
-    group_counts[g] = run;
-  }
+// exclusive scan over blocks per group (one block of 1024 threads; group
+// after group; offsets are group-major: group g starts after all tokens of
+// groups < g)
+__global__ void __launch_bounds__(1024) k_route_scan(uint32_t* __restrict__ counts, uint32_t nblocks,
+                                                     uint32_t G, uint64_t* __restrict__ group_counts) {
+  __shared__ uint32_t wsum[32];
+  __shared__ uint64_t s_start;
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  if (t == 0) s_start = 0;
   __syncthreads();
-  if (g < G) {
-    uint64_t start = 0;
-    for (uint32_t h = 0; h < g; ++h) start += tot[h];
-    for (uint32_t b = 0; b < nblocks; ++b) counts[(uint64_t)b * G + g] += (uint32_t)start;
+  for (uint32_t g = 0; g < G; ++g) {
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < nblocks; b0 += 1024) {
+      const uint32_t b = b0 + t;
+      const uint32_t v = b < nblocks ? counts[(uint64_t)b * G + g] : 0u;
+      uint32_t x = v;  // inclusive warp scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+      }
+      if (lane == 31) wsum[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t wv = wsum[lane];
+        uint32_t z = wv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, z, o);
+          if (lane >= (uint32_t)o) z += y;
+        }
+        wsum[lane] = z - wv;  // exclusive warp offsets
+      }
+      __syncthreads();
+      const uint32_t excl = carry + wsum[warp] + x - v;
+      if (b < nblocks) counts[(uint64_t)b * G + g] = (uint32_t)s_start + excl;
+      const uint32_t tot = __shfl_sync(0xFFFFFFFFu, wsum[31] + x, 31);  // block total (warp 31's view)
+      __syncthreads();
+      if (warp == 31) wsum[0] = tot;  // broadcast the chunk total
+      __syncthreads();
+      carry += wsum[0];
+      __syncthreads();
+    }
+    if (t == 0) {
+      group_counts[g] = carry;
+      s_start += carry;
+    }
+    __syncthreads();
   }
 }
 
@@ -513,7 +540,7 @@ int rs_route_tagged(rs_router* r, const uint64_t* d_tagged, uint64_t n, uint64_t
   RS_CUDA(cudaMemsetAsync(r->err, 0, 4, s));
   k_route_count<<<nb, 256, 0, s>>>(d_tagged, n, r->m, r->counts, r->err);
   RS_LAUNCH_CHECK("k_route_count");
-  k_route_scan<<<1, kMaxRouteGroups, 0, s>>>(r->counts, nb, G, r->d_group_counts);
+  k_route_scan<<<1, 1024, 0, s>>>(r->counts, nb, G, r->d_group_counts);
   RS_LAUNCH_CHECK("k_route_scan");
   k_route_scatter<<<nb, 256, 0, s>>>(d_tagged, n, r->m, r->counts, d_gids, d_pos, r->err);
   RS_LAUNCH_CHECK("k_route_scatter");

@@ -80,7 +80,7 @@ struct rs_scratch {
 };
 
 struct rs_workspace {
-  bool graph_fork = false;  // hot-id finish as a forked branch inside captured graphs
+  bool graph_fork = true;  // hot-id finish as a forked branch inside captured graphs (RS_GRAPH_FORK=0: linear)
   uint64_t max_tokens = 0;
   uint64_t S = 0;  // scratch hash capacity (power of two)
   rs_scratch set[2];

@@ -195,7 +195,7 @@ struct FTableArgs {
 
 constexpr unsigned kGroups = 32;  // 8-lane groups per 256-thread block
 
-__global__ void __launch_bounds__(256) k_ftable(FTableArgs a) {
+__global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
   TableDev* td = a.td;
   const TableDesc d = td->d;
   const unsigned long long free_n0 = td->c.free_n;
@@ -1409,7 +1409,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   ws->max_tokens = max_tokens;
   if (const char* e = getenv("RS_NO_GRAPH")) ws->use_graphs = e[0] == '0';
   if (const char* e = getenv("RS_NO_FORK")) ws->fork = e[0] == '0';
-  if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] == '1';
+  if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] != '0';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;

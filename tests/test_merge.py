@@ -210,12 +210,12 @@ def test_route_tagged_gpu_vs_oracle(cuda):
     names, _, cat_k = M.catalog_from(features)
     router = P.Router(plan, names)
     rng = np.random.default_rng(3)
-    for n in (0, 1, 1023, 1024, 1025, 70001):
-        ords = rng.integers(0, 9, n)  # ordinal 0 = untagged ids (identity of group 0)
-        raws = rng.integers(0, 1 << 40, n)
-        tagged = np.array([(int(o) << (63 - cat_k)) | int(r) for o, r in zip(ords, raws)], np.uint64)
+    for n in (0, 1, 1023, 1024, 1025, 70001, 1_300_001):  # > 1024 route blocks: chunked scan
+        ords = rng.integers(0, 9, n).astype(np.uint64)  # ordinal 0 = untagged ids (identity of group 0)
+        raws = rng.integers(0, 1 << 40, n).astype(np.uint64)
+        tagged = (ords << np.uint64(63 - cat_k)) | raws
         gids, pos, counts = router.route(tagged)
-        want_ids, want_pos = M.route_tagged(tagged, features)
+        want_ids, want_pos = (M.route_tagged if n < 100_000 else M.route_tagged_np)(tagged, features)
         assert counts == [len(x) for x in want_ids]
         np.testing.assert_array_equal(P.keys_to_numpy(gids), np.concatenate(want_ids) if n else np.zeros(0, np.uint64))
         np.testing.assert_array_equal(pos.cpu().numpy(), np.concatenate(want_pos) if n else np.zeros(0))
