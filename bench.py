@@ -42,6 +42,7 @@ C5 = dict(workload="config5: long-tail sequences (lognormal sigma 1.5, mean 128,
           capacity=1 << 22, pooled=True)
 TAG1 = np.uint64(1 << 62)
 L2_FLUSH_BYTES = 512 << 20
+_E2E_HOST_MS = None
 
 
 def peaks():
@@ -441,15 +442,16 @@ def e2e_sharded(args, cfg, batches, st, params, P, W):
     import torch.distributed as dist
     n = max(3, min(args.steps, 10))
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
-    t, uniq, h2d, d2h = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
-                                      lambda i, g, o: st.step(i, g, params, o), n, uniq_b, barrier=dist.barrier)
+    t, uniq, h2d, d2h = workload_e2e(batches, cfg["dim"], lambda f, hi, hl, k: f.dist_step(st, params, hi, hl, k),
+                                     n, uniq_b, barrier=dist.barrier)
     v = torch.tensor([t, uniq], dtype=torch.float64, device="cuda")
     tmax = v[:1].clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(v)
     return {"value": v[1].item() / tmax.item(), "unit": "unique-ids/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": tmax.item() / n * 1e3,
-            "pipelined": "H2D / step / D2H on 3 streams, 2 buffer sets"}
+            "io": "H2D token ids + sequence lengths; gradients generated in-step on the device "
+                  "(pseudo_sparse_grad per sample, as run_workload does); D2H the step's embedding checksum"}
 
 
 C2 = dict(workload="config2: 8 tables (dim 64: 1e7/1e6/1e6/1e5 keys; dim 128: 1e6/1e6/1e5/1e4 keys) auto-merged "
@@ -742,6 +744,45 @@ def pipelined_e2e(host, dim, run_step, n, uniq_b, barrier=None):
     return t, uniq, h2d // n, d2h // n
 
 
+def workload_e2e(batches, dim, step_fn, n, uniq_b, barrier=None):
+    """End to end the way the reference's run_workload drives a step
+    (workload.cpp:506-581), through the public rs_feeder API: the data
+    loader's pinned token ids + sequence lengths go host -> device on a copy
+    stream that runs ahead (two buffer sets); the step generates its
+    gradients (pseudo_sparse_grad, a pure hash of (sample id, step),
+    workload.cpp:348-355 -- on the device, inside the timed region), runs
+    dedup -> lookup -> reduce -> update, and its embedding checksum
+    (run_workload's emb_checksum) comes back device -> host.  step_fn(feeder,
+    h_ids, h_lengths, step) issues one step."""
+    import torch
+
+    from paper_2505_12663_b200.feed import Feeder
+    host = [(torch.from_numpy(ids.view(np.int64)).pin_memory(),
+             torch.from_numpy(np.asarray(lengths, np.uint64).view(np.int64)).pin_memory()) for lengths, ids in batches]
+    feeder = Feeder(max(h[0].numel() for h in host), max(h[1].numel() for h in host), dim)
+    warm = 2 * len(host)  # every (batch, buffer set, scratch parity) graph captured before timing
+    for k in range(warm):
+        step_fn(feeder, *host[k % len(host)], k % len(host))
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    comp = torch.cuda.current_stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(comp)
+    h0 = time.perf_counter()
+    for k in range(warm, warm + n):
+        step_fn(feeder, *host[k % len(host)], k % len(host))
+    global _E2E_HOST_MS
+    _E2E_HOST_MS = (time.perf_counter() - h0) * 1e3 / n
+    t1.record(comp)
+    torch.cuda.synchronize()
+    t = t0.elapsed_time(t1) / 1e3
+    feeder.close()
+    uniq = sum(uniq_b[k % len(host)] for k in range(warm, warm + n))
+    h2d = sum(host[k % len(host)][0].numel() * 8 + host[k % len(host)][1].numel() * 8 for k in range(warm, warm + n))
+    return t, uniq, h2d // n, 8
+
+
 def host_batches(batches, dim, W):
     import torch
     host = []
@@ -757,10 +798,15 @@ def e2e_pass(args, cfg, batches, step, P, W, rank):
     """Same metric through rs_step with host buffers (pipelined_e2e)."""
     n = max(3, min(args.steps, 10))
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
-    t, uniq, h2d, d2h = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
-                                      lambda i, g, o: step.step(i, g, o), n, uniq_b)
+    t, uniq, h2d, d2h = workload_e2e(batches, cfg["dim"], lambda f, hi, hl, k: f.step(step, hi, hl, k), n, uniq_b)
+    tf, uf, hf, df = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
+                                   lambda i, g, o: step.step(i, g, o), n, uniq_b)
     return {"value": uniq / t, "unit": "unique-ids/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "ms_per_step": t / n * 1e3, "pipelined": "H2D / step / D2H on 3 streams, 2 buffer sets"}
+            "ms_per_step": t / n * 1e3, "host_issue_ms_per_step": _E2E_HOST_MS,
+            "io": "H2D token ids + sequence lengths; gradients generated in-step on the device "
+                  "(pseudo_sparse_grad per sample, as run_workload does); D2H the step's embedding checksum",
+            "full_io": {"value": uf / tf, "h2d_bytes_per_step": hf, "d2h_bytes_per_step": df, "ms_per_step": tf / n * 1e3,
+                        "io": "H2D ids + per-token f32 gradients, D2H every gathered f32 row (PCIe-bound)"}}
 
 
 # ------------------------------------------------------------- CPU arm

@@ -309,6 +309,24 @@ int rs_imbalance_report(const uint64_t* per_worker_tokens, uint64_t n, uint64_t*
 int rs_weighted_grad_combine(const uint64_t* batch_sizes, const double* grads, uint64_t workers,
                              uint64_t dim, double* out);
 
+/* ---- one run_workload step fed from host memory (workload.cpp:506-581) ----
+ * Pinned host ids + sequence lengths go to the device on a copy stream (two
+ * buffer sets, the copies of step k+1 overlap step k); the gradients are
+ * pseudo_sparse_grad on the device; the step runs; its embedding checksum
+ * (run_workload's emb_checksum) is copied to *h_checksum.  Nothing syncs. */
+typedef struct rs_feeder rs_feeder;
+int rs_feeder_create(uint64_t max_tokens, uint64_t max_seqs, uint32_t dim, rs_feeder** out);
+int rs_feeder_destroy(rs_feeder* f);
+float* rs_feeder_out(rs_feeder* f, int which);
+int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* h_ids, uint64_t n,
+                   const uint64_t* h_lengths, uint64_t n_seq, uint64_t first_sample_id,
+                   uint64_t step, const rs_optimizer_params* opt, double* h_checksum,
+                   void* stream);
+int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_t* h_ids,
+                        uint64_t n, const uint64_t* h_lengths, uint64_t n_seq,
+                        uint64_t first_sample_id, uint64_t step, const rs_optimizer_params* opt,
+                        double* h_checksum, void* stream);
+
 /* ---- synthetic inputs (workload.cpp:103-152, 280-307, 348-355) ------------ */
 /* generate_workload: per-sample lengths + catalog-tagged ids (k = bit_width(tables)) */
 int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len,
@@ -318,6 +336,19 @@ int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len,
 /* pseudo_sparse_grad per token on device: d_out[t] = g(sample_of_token[t], step) */
 int rs_pseudo_grads(const uint64_t* d_sample_of_token, uint64_t n, uint64_t step, uint32_t dim,
                     float* d_out, void* stream);
+/* the same gradients for a jagged batch given by its sequence lengths (sample
+ * ids first_sample_id + s, the generator's numbering): one row per sample,
+ * broadcast to the sample's tokens; dim % 4 == 0 */
+int rs_pseudo_grads_jagged(const uint64_t* d_lengths, uint64_t n_seq, uint64_t first_sample_id,
+                           uint64_t step, uint32_t dim, uint64_t n_tokens, float* d_out,
+                           void* stream);
+/* the same from the token offsets of the batch (d_offsets[n_seq + 1], device):
+ * one kernel, block per sample */
+int rs_pseudo_grads_offsets(const uint64_t* d_offsets, uint64_t n_seq, uint64_t first_sample_id,
+                            uint64_t step, uint32_t dim, float* d_out, void* stream);
+/* run_workload's emb_checksum (workload.cpp:547-549): sum of d_x[0, n) in f64,
+ * fixed order (deterministic), into *d_out */
+int rs_checksum(const float* d_x, uint64_t n, double* d_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -147,6 +147,15 @@ _SIGS = {
     "rs_partition_sequences": (C.c_int, [vp, u64, u32, u32, C.c_double, C.c_double, vp, vp]),
     "rs_imbalance_report": (C.c_int, [vp, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(C.c_double)]),
     "rs_weighted_grad_combine": (C.c_int, [vp, vp, u64, u64, vp]),
+    "rs_pseudo_grads_jagged": (C.c_int, [vp, u64, u64, u64, u32, u64, vp, vp]),
+    "rs_checksum": (C.c_int, [vp, u64, vp, vp]),
+    "rs_pseudo_grads_offsets": (C.c_int, [vp, u64, u64, u64, u32, vp, vp]),
+    "rs_feeder_create": (C.c_int, [u64, u64, u32, C.POINTER(vp)]),
+    "rs_feeder_destroy": (C.c_int, [vp]),
+    "rs_feeder_out": (vp, [vp, C.c_int]),
+    "rs_feeder_step": (C.c_int, [vp, vp, vp, vp, u64, vp, u64, u64, u64, C.POINTER(rs_optimizer_params), vp, vp]),
+    "rs_feeder_dist_step": (C.c_int, [vp, vp, vp, vp, u64, vp, u64, u64, u64, C.POINTER(rs_optimizer_params), vp,
+                                      vp]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),

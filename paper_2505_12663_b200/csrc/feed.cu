@@ -1,0 +1,144 @@
+// feed.cu -- one run_workload step fed from host memory (the end-to-end path).
+//
+// Reference: run_workload's step body (workload.cpp:506-581): the batch's
+// token ids arrive from the data loader; the per-token gradients are
+// pseudo_sparse_grad(sample id, step) (workload.cpp:348-355, a pure hash --
+// generated on the device here); distributed_lookup + accumulate + apply;
+// the step's stats accumulate emb_checksum += sum of the outputs
+// (workload.cpp:547-549).  rs_feeder_step does exactly that from pinned host
+// buffers with everything asynchronous: the H2D copies of step k+1 run on a
+// copy stream while step k computes (two device buffer sets, reuse ordered by
+// events), and only the 8-byte checksum travels back.
+#include <cuda_runtime.h>
+
+#include "rs_host.hpp"
+
+using namespace rs;
+
+struct rs_feeder {
+  uint64_t max_tokens = 0, max_seqs = 0;
+  uint32_t dim = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t in_free[2] = {}, landed[2] = {};
+  uint64_t* ids[2] = {};
+  uint64_t* offs[2] = {};       // device token offsets of the batch
+  uint64_t* h_offs[2] = {};     // pinned host staging of the offsets
+  float* grads[2] = {};
+  float* out[2] = {};
+  double* sum[2] = {};
+  uint64_t k = 0;
+};
+
+extern "C" {
+
+int rs_feeder_create(uint64_t max_tokens, uint64_t max_seqs, uint32_t dim, rs_feeder** out) {
+  if (!out || !max_tokens || !max_seqs || !dim) return fail(RS_ERR_CONFIG, "rs_feeder_create: bad arguments");
+  auto* f = new rs_feeder();
+  f->max_tokens = max_tokens;
+  f->max_seqs = max_seqs;
+  f->dim = dim;
+  bool ok = cudaStreamCreateWithFlags(&f->copy, cudaStreamNonBlocking) == cudaSuccess;
+  for (int b = 0; b < 2 && ok; ++b) {
+    ok = cudaEventCreateWithFlags(&f->in_free[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&f->landed[b], cudaEventDisableTiming) == cudaSuccess &&
+         cudaMalloc(&f->ids[b], max_tokens * 8) == cudaSuccess &&
+         cudaMalloc(&f->offs[b], (max_seqs + 1) * 8) == cudaSuccess &&
+         cudaMallocHost(&f->h_offs[b], (max_seqs + 1) * 8) == cudaSuccess &&
+         cudaMalloc(&f->grads[b], max_tokens * dim * 4) == cudaSuccess &&
+         cudaMalloc(&f->out[b], max_tokens * dim * 4) == cudaSuccess &&
+         cudaMalloc(&f->sum[b], 8) == cudaSuccess;
+  }
+  if (!ok) {
+    cudaGetLastError();
+    rs_feeder_destroy(f);
+    return fail(RS_ERR_CUDA, "rs_feeder_create: allocation failed");
+  }
+  *out = f;
+  return RS_OK;
+}
+
+int rs_feeder_destroy(rs_feeder* f) {
+  if (!f) return RS_OK;
+  cudaDeviceSynchronize();
+  for (int b = 0; b < 2; ++b) {
+    if (f->in_free[b]) cudaEventDestroy(f->in_free[b]);
+    if (f->landed[b]) cudaEventDestroy(f->landed[b]);
+    void* ps[] = {f->ids[b], f->offs[b], f->grads[b], f->out[b], f->sum[b]};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+    if (f->h_offs[b]) cudaFreeHost(f->h_offs[b]);
+  }
+  if (f->copy) cudaStreamDestroy(f->copy);
+  delete f;
+  return RS_OK;
+}
+
+// Device buffers of the current set (the gathered rows of the last step).
+float* rs_feeder_out(rs_feeder* f, int which) { return f ? f->out[which & 1] : nullptr; }
+
+static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const uint64_t* h_lengths,
+                        uint64_t n_seq, cudaStream_t s, int* set) {
+  if (n > f->max_tokens || n_seq > f->max_seqs)
+    return fail(RS_ERR_CONFIG, "rs_feeder_step: batch exceeds the feeder's capacity");
+  const int b = (int)(f->k & 1);
+  if (f->k < 2) RS_CUDA(cudaEventRecord(f->in_free[b], s));  // first use: free now
+  RS_CUDA(cudaStreamWaitEvent(f->copy, f->in_free[b], 0));
+  // the loader's lengths -> token offsets (host, a few thousand adds); the
+  // staging buffer of this set is free once its previous copy completed
+  RS_CUDA(cudaEventSynchronize(f->landed[b]));
+  uint64_t run = 0;
+  for (uint64_t i = 0; i < n_seq; ++i) {
+    f->h_offs[b][i] = run;
+    run += h_lengths[i];
+  }
+  f->h_offs[b][n_seq] = run;
+  if (run != n) return fail(RS_ERR_CONFIG, "rs_feeder_step: sum of lengths != number of ids");
+  RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
+  RS_CUDA(cudaMemcpyAsync(f->offs[b], f->h_offs[b], (n_seq + 1) * 8, cudaMemcpyHostToDevice, f->copy));
+  RS_CUDA(cudaEventRecord(f->landed[b], f->copy));
+  RS_CUDA(cudaStreamWaitEvent(s, f->landed[b], 0));
+  *set = b;
+  return RS_OK;
+}
+
+static int feeder_finish(rs_feeder* f, int b, uint64_t n, double* h_checksum, cudaStream_t s) {
+  int st = rs_checksum(f->out[b], n * f->dim, f->sum[b], s);
+  if (st) return st;
+  RS_CUDA(cudaEventRecord(f->in_free[b], s));
+  if (h_checksum) RS_CUDA(cudaMemcpyAsync(h_checksum, f->sum[b], 8, cudaMemcpyDeviceToHost, s));
+  f->k++;
+  return RS_OK;
+}
+
+// One training step from host memory on a single shard (rs_step).  h_ids /
+// h_lengths / h_checksum should be pinned; nothing synchronizes.
+int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* h_ids, uint64_t n,
+                   const uint64_t* h_lengths, uint64_t n_seq, uint64_t first_sample_id, uint64_t step,
+                   const rs_optimizer_params* opt, double* h_checksum, void* stream) {
+  if (!f || !ws || !t) return fail(RS_ERR_CONFIG, "rs_feeder_step: null handle");
+  if (t->desc.dim != f->dim) return fail(RS_ERR_CONFIG, "rs_feeder_step: table dim != feeder dim");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int b = 0;
+  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
+  if (!st) st = rs_pseudo_grads_offsets(f->offs[b], n_seq, first_sample_id, step, f->dim, f->grads[b], stream);
+  if (!st) st = rs_step(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s);
+  return st;
+}
+
+// The same for this rank of a row-sharded table (rs_dist_step).
+int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_t* h_ids, uint64_t n,
+                        const uint64_t* h_lengths, uint64_t n_seq, uint64_t first_sample_id, uint64_t step,
+                        const rs_optimizer_params* opt, double* h_checksum, void* stream) {
+  if (!f || !c || !shard) return fail(RS_ERR_CONFIG, "rs_feeder_dist_step: null handle");
+  if (shard->desc.dim != f->dim) return fail(RS_ERR_CONFIG, "rs_feeder_dist_step: table dim != feeder dim");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int b = 0;
+  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
+  if (!st) st = rs_pseudo_grads_offsets(f->offs[b], n_seq, first_sample_id, step, f->dim, f->grads[b], stream);
+  if (!st) st = rs_dist_step(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s);
+  return st;
+}
+
+}  // extern "C"

@@ -42,6 +42,143 @@ __global__ void k_pseudo_grads(const uint64_t* __restrict__ sample_of, uint64_t 
   }
 }
 
+// one gradient row per sample (the formula of k_pseudo_grads)
+__global__ void k_sample_rows(uint64_t n_seq, uint64_t first, uint64_t step, uint32_t dim,
+                              float* __restrict__ rows) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n_seq * dim;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = i / dim, e = i - s * dim;
+    const uint64_t base = hash64((first + s) * 0x9e3779b97f4a7c15ULL + step * 0xbf58476d1ce4e5b9ULL + 1);
+    const double u = static_cast<double>(hash64(base + e) >> 11) * 0x1.0p-53;
+    rows[i] = static_cast<float>((u - 0.5) * 0.1);
+  }
+}
+
+// exclusive prefix of the sequence lengths (one block)
+__global__ void __launch_bounds__(1024) k_seq_offsets(const uint64_t* __restrict__ lengths, uint64_t n_seq,
+                                                      uint64_t* __restrict__ offs) {
+  __shared__ uint64_t part[1024];
+  __shared__ uint64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint64_t b0 = 0; b0 < n_seq; b0 += 1024) {
+    const uint64_t i = b0 + threadIdx.x;
+    const uint64_t v = i < n_seq ? lengths[i] : 0;
+    part[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const uint64_t y = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0;
+      __syncthreads();
+      part[threadIdx.x] += y;
+      __syncthreads();
+    }
+    if (i < n_seq) offs[i] = carry + part[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += part[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) offs[n_seq] = carry;
+}
+
+// Block s: sample s's gradient row (pseudo_sparse_grad of sample first + s)
+// in smem, then copied to each of its tokens [offs[s], offs[s+1]) with
+// 128-bit streaming stores.  One kernel per batch, no intermediate rows.
+__global__ void __launch_bounds__(256) k_jagged_grads(const uint64_t* __restrict__ offs, uint64_t first,
+                                                      uint64_t step, uint32_t dim, float* __restrict__ out) {
+  extern __shared__ float4 srow4[];
+  float* srow = reinterpret_cast<float*>(srow4);
+  const uint32_t s = blockIdx.x;
+  const uint64_t base = hash64((first + s) * 0x9e3779b97f4a7c15ULL + step * 0xbf58476d1ce4e5b9ULL + 1);
+  for (uint32_t e = threadIdx.x; e < dim; e += blockDim.x) {
+    const double u = static_cast<double>(hash64(base + e) >> 11) * 0x1.0p-53;
+    srow[e] = static_cast<float>((u - 0.5) * 0.1);
+  }
+  __syncthreads();
+  const uint64_t a = offs[s], b = offs[s + 1];
+  const uint32_t d4 = dim >> 2;
+  const uint64_t total = (b - a) * d4;
+  float4* dst = reinterpret_cast<float4*>(out) + a * d4;
+  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) __stcs(dst + i, srow4[i % d4]);
+}
+
+// sample index of every token: block s fills [offs[s], offs[s+1])
+__global__ void k_fill_sample(const uint64_t* __restrict__ offs, uint32_t* __restrict__ sample_of) {
+  const uint32_t s = blockIdx.x;
+  const uint64_t a = offs[s], b = offs[s + 1];
+  for (uint64_t t = a + threadIdx.x; t < b; t += blockDim.x) sample_of[t] = s;
+}
+
+// per token: its sample's row, 128-bit copies, 4 independent chunks per
+// thread (loads in flight for the bandwidth)
+__global__ void __launch_bounds__(256) k_broadcast_rows(const uint32_t* __restrict__ sample_of,
+                                                        const float* __restrict__ rows, uint32_t dim,
+                                                        uint32_t n_tokens, float* __restrict__ out) {
+  const uint32_t d4 = dim >> 2;
+  const uint32_t total = n_tokens * d4;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += 4 * stride) {
+    float4 v[4];
+    uint32_t idx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      idx[k] = i0 + k * stride;
+      if (idx[k] < total) {
+        const uint32_t t = idx[k] / d4, c = idx[k] - t * d4;
+        v[k] = __ldg(reinterpret_cast<const float4*>(rows + (size_t)__ldg(sample_of + t) * dim) + c);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (idx[k] < total) __stcs(reinterpret_cast<float4*>(out) + idx[k], v[k]);
+  }
+}
+
+// deterministic f64 sum of x[0, n): per-block partials, then one block sums
+// them in block order
+__global__ void __launch_bounds__(256) k_sum_partials(const float* __restrict__ x, uint64_t n,
+                                                      double* __restrict__ part) {
+  __shared__ double w[8];
+  double acc = 0.0;
+  const uint64_t n4 = n >> 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < n4; i0 += 4 * stride) {
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      v[k] = i0 + k * stride < n4 ? __ldg(reinterpret_cast<const float4*>(x) + i0 + k * stride)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc += (double)v[k].x + (double)v[k].y + (double)v[k].z + (double)v[k].w;
+  }
+  if (blockIdx.x == 0)
+    for (uint64_t i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) acc += (double)x[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int k = 0; k < 8; ++k) b += w[k];
+    part[blockIdx.x] = b;
+  }
+}
+
+// the last block to finish sums the per-block partials in a fixed order
+__global__ void __launch_bounds__(256) k_sum_last(const double* __restrict__ part, uint32_t nb,
+                                                  unsigned int* __restrict__ done, double* __restrict__ out) {
+  (void)done;
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) acc += part[b];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < (unsigned)o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
 }  // namespace
 }  // namespace rs
 
@@ -116,6 +253,77 @@ int rs_pseudo_grads(const uint64_t* d_sample_of_token, uint64_t n, uint64_t step
   k_pseudo_grads<<<grid_for(n * dim, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
       d_sample_of_token, n, step, dim, d_out);
   RS_LAUNCH_CHECK("k_pseudo_grads");
+  return RS_OK;
+}
+
+// The same gradients for a jagged batch given by its sequence lengths: one
+// row per sample (sample ids first_sample_id + s), broadcast to its tokens.
+int rs_pseudo_grads_jagged(const uint64_t* d_lengths, uint64_t n_seq, uint64_t first_sample_id,
+                           uint64_t step, uint32_t dim, uint64_t n_tokens, float* d_out,
+                           void* stream) {
+  using namespace rs;
+  if (n_tokens == 0 || n_seq == 0) return RS_OK;
+  if (dim % 4) return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: dim % 4 != 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  // scratch kept across calls (one caller stream at a time; grows only)
+  static uint64_t* offs = nullptr;
+  static float* rows = nullptr;
+  static uint64_t cap_seq = 0, cap_rows = 0, cap_tok = 0;
+  static uint32_t* sample_of = nullptr;
+  if (cap_tok < n_tokens) {
+    if (sample_of) RS_CUDA(cudaFree(sample_of));
+    RS_CUDA(cudaMalloc(&sample_of, n_tokens * 4));
+    cap_tok = n_tokens;
+  }
+  if (cap_seq < n_seq + 1) {
+    if (offs) RS_CUDA(cudaFree(offs));
+    RS_CUDA(cudaMalloc(&offs, (n_seq + 1) * 8));
+    cap_seq = n_seq + 1;
+  }
+  if (cap_rows < n_seq * dim) {
+    if (rows) RS_CUDA(cudaFree(rows));
+    RS_CUDA(cudaMalloc(&rows, n_seq * dim * 4));
+    cap_rows = n_seq * dim;
+  }
+  k_seq_offsets<<<1, 1024, 0, s>>>(d_lengths, n_seq, offs);
+  RS_LAUNCH_CHECK("k_seq_offsets");
+  k_sample_rows<<<grid_for(n_seq * dim, 256, 148 * 8), 256, 0, s>>>(n_seq, first_sample_id, step, dim, rows);
+  RS_LAUNCH_CHECK("k_sample_rows");
+  if (n_tokens * (uint64_t)dim >= (1ull << 32) || n_seq >= (1ull << 32))
+    return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: batch too large");
+  k_fill_sample<<<(unsigned)n_seq, 256, 0, s>>>(offs, sample_of);
+  RS_LAUNCH_CHECK("k_fill_sample");
+  k_broadcast_rows<<<grid_for(n_tokens * dim / 16, 256, 148 * 8), 256, 0, s>>>(sample_of, rows, dim,
+                                                                            (uint32_t)n_tokens, d_out);
+  RS_LAUNCH_CHECK("k_broadcast_rows");
+  return RS_OK;
+}
+
+// The same from the batch's token offsets (offs[n_seq + 1], device): one
+// kernel, one block per sample.
+int rs_pseudo_grads_offsets(const uint64_t* d_offsets, uint64_t n_seq, uint64_t first_sample_id,
+                            uint64_t step, uint32_t dim, float* d_out, void* stream) {
+  using namespace rs;
+  if (n_seq == 0) return RS_OK;
+  if (dim % 4 || dim > 4096) return fail(RS_ERR_CONFIG, "rs_pseudo_grads_offsets: dim % 4 != 0 or > 4096");
+  k_jagged_grads<<<(unsigned)n_seq, 256, dim * 4, (cudaStream_t)stream>>>(d_offsets, first_sample_id, step, dim,
+                                                                          d_out);
+  RS_LAUNCH_CHECK("k_jagged_grads");
+  return RS_OK;
+}
+
+// run_workload's emb_checksum (workload.cpp:547-549) of a step's outputs, in
+// f64, deterministic (fixed block partition and order).
+int rs_checksum(const float* d_x, uint64_t n, double* d_out, void* stream) {
+  using namespace rs;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned nb = 148 * 4;
+  static double* part = nullptr;  // kept across calls
+  if (!part) RS_CUDA(cudaMalloc(&part, nb * 8));
+  k_sum_partials<<<nb, 256, 0, s>>>(d_x, n, part);
+  RS_LAUNCH_CHECK("k_sum_partials");
+  k_sum_last<<<1, 256, 0, s>>>(part, nb, nullptr, d_out);
+  RS_LAUNCH_CHECK("k_sum_last");
   return RS_OK;
 }
 

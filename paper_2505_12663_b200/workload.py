@@ -46,3 +46,16 @@ def pseudo_grads(sample_of: torch.Tensor, step: int, dim: int) -> torch.Tensor:
     check(L.lib().rs_pseudo_grads(s.data_ptr(), s.numel(), step, dim, out.data_ptr(),
                                   torch.cuda.current_stream().cuda_stream), "pseudo_grads")
     return out
+
+
+def pseudo_grads_jagged(lengths: torch.Tensor, step: int, dim: int, n_tokens: int,
+                        first_sample_id: int = 1, out: torch.Tensor | None = None) -> torch.Tensor:
+    """pseudo_sparse_grad rows of a jagged batch from its sequence lengths
+    (device tensor): one row per sample broadcast to its tokens."""
+    ln = lengths.to(device="cuda", dtype=torch.int64).contiguous()
+    if out is None:
+        out = torch.empty((n_tokens, dim), dtype=torch.float32, device="cuda")
+    check(L.lib().rs_pseudo_grads_jagged(ln.data_ptr(), ln.numel(), first_sample_id, step, dim, n_tokens,
+                                         out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+          "pseudo_grads_jagged")
+    return out

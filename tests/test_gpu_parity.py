@@ -423,3 +423,44 @@ def test_bounded_step_graph_equals_eager_and_oracle_keys(cuda, oracle):
     oo = o.export()
     np.testing.assert_array_equal(a["keys"], oo["keys"])
     np.testing.assert_array_equal(a["ts"], oo["ts"].astype(a["ts"].dtype))
+
+
+def test_pseudo_grads_jagged_equals_per_token(cuda, oracle):
+    # pseudo_sparse_grad (workload.cpp:348-355) broadcast per sample == per token, == the oracle
+    lengths = np.array([1, 5, 300, 2, 4096, 17], np.uint64)
+    n = int(lengths.sum())
+    a = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), 7, 64)
+    b = W.pseudo_grads_jagged(torch.from_numpy(lengths.view(np.int64)), 7, 64, n)
+    torch.testing.assert_close(a, b, rtol=0, atol=0)
+    want = oracle.token_grads(lengths, 7, 64)
+    np.testing.assert_array_equal(b.cpu().numpy(), want)
+    offs = torch.from_numpy(np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)).cuda()
+    c = torch.empty_like(b)
+    P._lib.check(P.lib().rs_pseudo_grads_offsets(offs.data_ptr(), len(lengths), 1, 7, 64, c.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream), "offsets")
+    torch.testing.assert_close(c, b, rtol=0, atol=0)
+
+
+def test_feeder_step_matches_device_step(cuda):
+    # rs_feeder_step (host ids + lengths -> device grads -> rs_step -> checksum)
+    # equals the same step driven from device buffers, checksum included
+    from paper_2505_12663_b200.feed import Feeder
+    dim = 32
+    tabs = [_gpu_table(1 << 12, dim, opt="adagrad") for _ in range(2)]
+    steps = [P.SparseStep(t, 5000, P.AdagradParams(lr=0.05)) for t in tabs]
+    f = Feeder(5000, 64, dim)
+    rng = np.random.default_rng(12)
+    for k in range(4):
+        lengths = rng.integers(1, 120, 40).astype(np.uint64)
+        ids = rng.integers(0, 900, int(lengths.sum())).astype(np.uint64)
+        h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
+        h_len = torch.from_numpy(lengths.view(np.int64)).pin_memory()
+        f.step(steps[0], h_ids, h_len, k)
+        got = f.checksum()
+        g = W.pseudo_grads(torch.from_numpy(W.sample_of_tokens(lengths).view(np.int64)), k, dim)
+        out = torch.empty((len(ids), dim), device="cuda")
+        steps[1].step(P.as_keys(ids), g, out)
+        assert got == pytest.approx(float(out.double().sum()), rel=1e-9, abs=1e-9)
+    a, b = tabs[0].export(), tabs[1].export()
+    for fld in ("keys", "emb", "v", "step"):
+        np.testing.assert_array_equal(a[fld], b[fld], err_msg=fld)
