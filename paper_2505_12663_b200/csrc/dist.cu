@@ -8,8 +8,8 @@
 // exchanges are peer stores over NVLink into a symmetric "arena" each rank
 // exports with CUDA IPC, issued by the kernels that produce the data:
 //
-//   requester  KA dedup -> KB metadata -> k_send_ids: owner partition of the
-//              unique ids, ids stored straight into the owner's ids_in
+//   requester  KA dedup -> KB metadata + owner partition of the unique ids,
+//              ids stored straight into the owner's ids_in (k_ftable)
 //   owner      wait ids -> k_flatten -> KA stage-2 dedup over the
 //              source-ordered concatenation -> KB find-or-insert on the shard
 //              -> k_respond: each received position's row stored straight
@@ -62,7 +62,7 @@ struct CommDev {
   uint32_t cap;        // ids per (source, destination) region
   uint32_t dim;
   size_t off_ids, off_emb, off_grad;  // off_grad: this epoch's gradient buffer
-  unsigned long long* epoch;  // device step counter: bumped by k_send_ids, read by the rest
+  unsigned long long* epoch;  // device step counter of the role (requester: bumped by KB)
   unsigned long long* trace;
   unsigned int* done;  // last-block counters [4]
 };
@@ -97,55 +97,6 @@ __device__ __forceinline__ void raise_flags(const CommDev& c, int phase, unsigne
     st_release_sys(flag_of(hdr_of(c, r), phase, c.rank), e);
   if (threadIdx.x == 0) *done = 0;
 }
-
-// Requester: owner partition of the unique ids, peer stores into ids_in.
-__global__ void __launch_bounds__(256) k_send_ids(CommDev c, const uint64_t* __restrict__ unique,
-                                                  const uint32_t* __restrict__ n_unique,
-                                                  const uint32_t* __restrict__ u_slot,
-                                                  uint32_t* __restrict__ srow,
-                                                  uint32_t* __restrict__ send_pos,
-                                                  uint32_t* __restrict__ send_cnt,
-                                                  uint64_t n_tokens) {
-  // this step's epoch; every block reads it before arriving, the last block
-  // publishes it after raising the flags
-  const unsigned long long e = *c.epoch + 1;
-  const uint32_t nu = *n_unique;
-  const uint32_t lane = lane_id();
-  for (uint32_t base = blockIdx.x * blockDim.x; base < nu; base += gridDim.x * blockDim.x) {
-    const uint32_t u = base + threadIdx.x;
-    const bool v = u < nu;
-    uint64_t id = 0;
-    uint32_t o = 0xFFFFFFFFu;
-    if (v) {
-      id = unique[u];
-      o = (uint32_t)(hash64(id) % c.world);  // shard_of (exchange_sim.cpp:84)
-    }
-    const unsigned mm = __match_any_sync(0xFFFFFFFFu, v ? o : (0xFFFF0000u | lane));
-    const uint32_t leader = __ffs(mm) - 1;
-    uint32_t j0 = 0;
-    if (v && lane == leader) j0 = atomicAdd(&send_cnt[o], (uint32_t)__popc(mm));
-    j0 = __shfl_sync(0xFFFFFFFFu, j0, leader);
-    if (v) {
-      const uint32_t j = j0 + __popc(mm & lanemask_lt());
-      uint64_t* dst = reinterpret_cast<uint64_t*>(c.peers[o] + c.off_ids);
-      dst[(size_t)c.rank * c.cap + j] = id;  // NVLink store into the owner's arena
-      const uint32_t sp = o * c.cap + j;
-      send_pos[u] = sp;
-      srow[u_slot[u]] = sp;  // the gather reads emb_in row sp
-    }
-  }
-  if (!last_block_signal(c, 0, c.done + 0)) return;
-  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) {
-    hdr_of(c, r)->cnt_in[c.rank] = send_cnt[r];
-    c.trace[kTrIdsSent + r] = send_cnt[r];
-  }
-  if (threadIdx.x == 0) c.trace[kTrRequested] = n_tokens;
-  __syncthreads();
-  for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) send_cnt[r] = 0;
-  raise_flags(c, 0, c.done + 0, e);
-  if (threadIdx.x == 0) *c.epoch = e;
-}
-
 
 // Device-side barrier of the group (rs_comm_barrier): raise this rank's
 // barrier flag at every peer, wait for every peer's.  The barrier epoch is
@@ -346,6 +297,8 @@ struct rs_comm {
   unsigned long long* d_epoch = nullptr;
   unsigned long long* d_bar_epoch = nullptr;
   unsigned long long** d_sig_grad_ptrs = nullptr;  // [W] &peer(r)->sig_grad[rank]
+  unsigned long long** d_sig_ids_ptrs = nullptr;   // [W] &peer(r)->sig_ids[rank]
+  uint32_t** d_cnt_ptrs = nullptr;                 // [W] &peer(r)->cnt_in[rank]
   const unsigned long long* own_sig_emb = nullptr;  // this arena's sig_emb[W]
   const unsigned long long* own_sig_grad = nullptr; // this arena's sig_grad[W]
   unsigned long long* trace = nullptr;
@@ -393,7 +346,7 @@ static int prof_end(rs_comm* c, int ph, cudaStream_t s) {
 }
 
 // Each role keeps its own device step counter -- the requester's is bumped
-// by k_send_ids, the owner's by its first wait -- so a role never reads the
+// by KB's id send, the owner's by its first wait -- so a role never reads the
 // other stream's counter before that stream advanced it.
 enum Role : int { kRequester = 0, kOwner = 1 };
 static unsigned long long* role_epoch(rs_comm* c, Role r) { return c->d_epoch + (r == kOwner ? 2 : 0); }
@@ -445,28 +398,40 @@ static cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 // step can be captured into a CUDA graph; ru / ou are the scratch sets of the
 // requester / owner workspaces, par the gradient-buffer parity of the step.
 // requester: dedup its tokens, partition the unique ids by owner and store
-// them into the owners' receive lists (KA, KB metadata, k_send_ids)
+// them into the owners' receive lists (KA, KB metadata + send)
 static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, StepSets ss,
                      cudaStream_t s) {
   rs_workspace* wr = c->ws_req;
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   const int ru = ss.ru;
   RS_TRY(prof_begin(c, kPhReqDedup, s));
+  // KB (metadata) also partitions the unique ids by owner and stores them
+  // into the owners' receive lists; its last block raises the ids flags
+  rs_dist_send snd;
+  snd.peers = c->d_peers;
+  snd.off_ids = c->off_ids;
+  snd.cap = (uint32_t)c->cap;
+  snd.world = (uint32_t)c->world;
+  snd.rank = (uint32_t)c->rank;
+  snd.send_cnt = c->send_cnt;
+  snd.send_pos = c->send_pos;
+  snd.cnt_ptrs = c->d_cnt_ptrs;
+  snd.flag_ptrs = c->d_sig_ids_ptrs;
+  snd.epoch = role_epoch(c, kRequester);
+  snd.done = c->done + 0;
+  snd.trace_ids_sent = c->trace + kTrIdsSent;
+  snd.trace_requested = c->trace + kTrRequested;
+  snd.n_tokens = n;
   if (n) {
     RS_TRY(step_fdedup(wr, d_ids, n, ru, s, nullptr));
-    RS_TRY(step_ftable(wr, t, ru, n, false, true, s));
-  } else {  // idle rank: still clean the other scratch set (KB) and reset its count (KC)
+    RS_TRY(step_ftable(wr, t, ru, n, false, true, s, &snd));
+  } else {  // idle rank: still clean the other scratch set (KB), send nothing, raise the flags
     RS_CUDA(cudaMemsetAsync(wr->set[ru].cnt, 0, 4, s));
-    RS_TRY(step_ftable(wr, t, ru, 1, false, true, s));
+    RS_TRY(step_ftable(wr, t, ru, 1, false, true, s, &snd));
     RS_CUDA(cudaMemsetAsync(wr->set[ru ^ 1].cnt, 0, 4, s));
   }
   RS_TRY(prof_end(c, kPhReqDedup, s));
-  RS_TRY(prof_begin(c, kPhSendIds, s));
-  k_send_ids<<<grid_for(n ? n : 1, 256, 148 * 4), 256, 0, s>>>(
-      cd, wr->unique, wr->set[ru].cnt, wr->set[ru].u_slot, wr->set[ru].srow, c->send_pos,
-      c->send_cnt, n);
-  RS_LAUNCH_CHECK("k_send_ids");
-  RS_TRY(prof_end(c, kPhSendIds, s));
+  (void)cd;
   return RS_OK;
 }
 
@@ -700,7 +665,9 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
             cudaMalloc(&c->view, sizeof(TableDev)) == cudaSuccess &&
             cudaMalloc(&c->d_epoch, 32) == cudaSuccess && cudaMemset(c->d_epoch, 0, 32) == cudaSuccess;
   if (ok) c->d_bar_epoch = c->d_epoch + 1;
-  ok = ok && cudaMalloc(&c->d_sig_grad_ptrs, kMaxWorld * sizeof(void*)) == cudaSuccess;
+  ok = ok && cudaMalloc(&c->d_sig_grad_ptrs, kMaxWorld * sizeof(void*)) == cudaSuccess &&
+       cudaMalloc(&c->d_sig_ids_ptrs, kMaxWorld * sizeof(void*)) == cudaSuccess &&
+       cudaMalloc(&c->d_cnt_ptrs, kMaxWorld * sizeof(void*)) == cudaSuccess;
   if (!ok) {
     cudaGetLastError();
     rs_comm_destroy(c);
@@ -764,6 +731,11 @@ int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order
     for (int r = 0; r < c->world; ++r)
       f[r] = &reinterpret_cast<ArenaHdr*>(c->h_peers[r])->sig_grad[c->rank];
     RS_CUDA(cudaMemcpy(c->d_sig_grad_ptrs, f.data(), kMaxWorld * sizeof(void*), cudaMemcpyHostToDevice));
+    for (int r = 0; r < c->world; ++r) f[r] = &reinterpret_cast<ArenaHdr*>(c->h_peers[r])->sig_ids[c->rank];
+    RS_CUDA(cudaMemcpy(c->d_sig_ids_ptrs, f.data(), kMaxWorld * sizeof(void*), cudaMemcpyHostToDevice));
+    std::vector<uint32_t*> q(kMaxWorld, nullptr);
+    for (int r = 0; r < c->world; ++r) q[r] = &reinterpret_cast<ArenaHdr*>(c->h_peers[r])->cnt_in[c->rank];
+    RS_CUDA(cudaMemcpy(c->d_cnt_ptrs, q.data(), kMaxWorld * sizeof(void*), cudaMemcpyHostToDevice));
     c->own_sig_emb = reinterpret_cast<ArenaHdr*>(c->arena)->sig_emb;
     c->own_sig_grad = reinterpret_cast<ArenaHdr*>(c->arena)->sig_grad;
   }
@@ -781,7 +753,8 @@ int rs_comm_destroy(rs_comm* c) {
   for (int r = 0; r < c->world; ++r)
     if (r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
   void* ps[] = {c->arena, c->d_peers, c->d_peer_grad[0], c->d_peer_grad[1], c->trace, c->done,
-                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch, c->d_sig_grad_ptrs};
+                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch, c->d_sig_grad_ptrs,
+                c->d_sig_ids_ptrs, c->d_cnt_ptrs};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : c->pev)

@@ -140,6 +140,24 @@ struct rs_dist_sync {
   unsigned long long* error = nullptr;             // set on a wait timeout
 };
 
+// The requester's id send folded into the table-metadata kernel (KB): the
+// owner partition of the unique ids, stored straight into the owners'
+// receive lists, then counts + flags raised by the last block (dist.cu).
+struct rs_dist_send {
+  char* const* peers = nullptr;                  // [W] arena bases (null: no send)
+  size_t off_ids = 0;                            // receive lists in the arena
+  uint32_t cap = 0, world = 1, rank = 0;
+  uint32_t* send_cnt = nullptr;                  // [W] cursors (zero between steps)
+  uint32_t* send_pos = nullptr;                  // per unique id: owner * cap + j
+  uint32_t* const* cnt_ptrs = nullptr;           // [W] &peer(r)->cnt_in[rank]
+  unsigned long long* const* flag_ptrs = nullptr;  // [W] &peer(r)->sig_ids[rank]
+  unsigned long long* epoch = nullptr;           // requester step counter (bumped here)
+  unsigned int* done = nullptr;                  // last-block counter
+  unsigned long long* trace_ids_sent = nullptr;  // [W]
+  unsigned long long* trace_requested = nullptr;
+  uint64_t n_tokens = 0;
+};
+
 // Options of the fused kernels used by the sharded (multi-GPU) step (dist.cu).
 struct rs_dist_opts {
   rs_dist_sync sync;                    // waits / signals folded into the kernels
@@ -187,7 +205,7 @@ int step_set_smem_attrs();
 int step_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
                 const uint32_t* d_n);
 int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_table,
-                bool do_clean, cudaStream_t s);
+                bool do_clean, cudaStream_t s, const rs_dist_send* send = nullptr);
 int step_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float* d_out,
               const float* d_grads, bool clean_other, cudaStream_t s, const rs_dist_opts* dopt);
 int step_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float* d_grads,

@@ -191,6 +191,7 @@ struct FTableArgs {
   uint32_t* hot_list;
   uint32_t* u_cnt;
   uint32_t* ctr;
+  rs_dist_send send;  // sharded requester: ids to their owners (peers == null: off)
 };
 
 constexpr unsigned kGroups = 32;  // 8-lane groups per 256-thread block
@@ -256,6 +257,22 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       a.u_ticket[i] = 0;
       if (hot) a.hot_list[atomicAdd(&a.ctr[kCtrNHot], 1u)] = i;
     }
+    if (a.send.peers) {  // owner partition: one lane per group holds the id
+      const bool mine = active && g == 0;
+      const uint32_t o = mine ? (uint32_t)(hash64(key) % a.send.world) : 0u;
+      const unsigned mm = __match_any_sync(kFull, mine ? o : (0xFFFF0000u | lane));
+      const uint32_t leader = __ffs(mm) - 1;
+      uint32_t j0 = 0;
+      if (mine && lane == leader) j0 = atomicAdd(&a.send.send_cnt[o], (uint32_t)__popc(mm));
+      j0 = __shfl_sync(kFull, j0, leader);
+      if (mine) {
+        const uint32_t j = j0 + __popc(mm & lanemask_lt());
+        reinterpret_cast<uint64_t*>(a.send.peers[o] + a.send.off_ids)[(size_t)a.send.rank * a.send.cap + j] = key;
+        const uint32_t sp = o * a.send.cap + j;
+        a.send.send_pos[i] = sp;
+        a.use.srow[slot] = sp;  // the gather reads the received row sp
+      }
+    }
     if (!a.do_table || !active) continue;
     const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0,
                                               &s_ins, &s_reuse);
@@ -271,6 +288,35 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
   if (a.do_table) launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  if (a.send.peers) {  // last block: counts + ids flags at every owner (step epoch e)
+    __shared__ bool last;
+    __shared__ unsigned long long e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      e = *a.send.epoch + 1;  // read before arriving; published by the last block
+      unsigned int old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.send.done) : "memory");
+      last = old == gridDim.x - 1;
+      if (last) fence_sys();
+    }
+    __syncthreads();
+    if (last) {
+      for (uint32_t r = threadIdx.x; r < a.send.world; r += blockDim.x) {
+        *a.send.cnt_ptrs[r] = a.send.send_cnt[r];
+        a.send.trace_ids_sent[r] = a.send.send_cnt[r];
+      }
+      if (threadIdx.x == 0) *a.send.trace_requested = a.send.n_tokens;
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < a.send.world; r += blockDim.x) {
+        st_release_sys(a.send.flag_ptrs[r], e);
+        a.send.send_cnt[r] = 0;
+      }
+      if (threadIdx.x == 0) {
+        *a.send.epoch = e;
+        *a.send.done = 0;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1365,10 +1411,11 @@ int step_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use, cu
   return launch_fdedup(ws, d_ids, n, use, s, d_n);
 }
 int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_table,
-                bool do_clean, cudaStream_t s) {
+                bool do_clean, cudaStream_t s, const rs_dist_send* send) {
   FTableArgs a = ftable_args(ws, t, use);
   a.do_table = do_table;
   a.do_clean = do_clean;
+  if (send) a.send = *send;
   k_ftable<<<grid_for(n_max, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
   RS_LAUNCH_CHECK("k_ftable");
   return RS_OK;

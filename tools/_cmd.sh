@@ -1,4 +1,4 @@
-timeout 400 python bench.py --config c4 --steps 10 --warmup 3 > gpurun_out/c4_1p.log 2>&1
-for b in lpt rr; do timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=2 --master-addr 127.0.0.1 --master-port 29581 bench.py --config c5 --balance $b --gpus 2 --steps 10 --warmup 3 > gpurun_out/c5_$b.log 2>&1; done
-grep '^{' gpurun_out/c4_1p.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c4 plain', d['n_gpus'], round(d['ms_per_step'],4), round(d['value']/1e6,1), round(d['e2e']['value']/1e6,1), d['roofline']['kernel'], round(d['roofline']['frac'],3))" || tail -5 gpurun_out/c4_1p.log
-for b in lpt rr; do grep '^{' gpurun_out/c5_$b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c5', d['n_gpus'], round(d['ms_per_step'],4), round(d['value']/1e6,1), d['balance'], [round(r['sum_ms'],2) for r in d['per_rank']])" || tail -5 gpurun_out/c5_$b.log; done
+timeout 240 python -m pytest tests/test_dist.py -x -q -m gpu > gpurun_out/d.log 2>&1; rc=$?; tail -2 gpurun_out/d.log
+if [ $rc -ne 0 ]; then grep -E "^E  " gpurun_out/d.log | grep -v "File\|\^\^" | head -12; exit 1; fi
+for n in 2; do timeout 150 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 29561 bench.py --gpus $n --steps 20 --warmup 3 > gpurun_out/b${n}.log 2>&1; done
+grep '^{' gpurun_out/b2.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['n_gpus'], round(d['ms_per_step'],4), round(d['value']/1e6,1), round(d['e2e']['value']/1e6,1), {k: round(v*1e3,1) for k,v in d['kernel_ms_rank0'].items()})"
