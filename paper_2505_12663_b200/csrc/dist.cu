@@ -325,7 +325,8 @@ struct rs_comm {
   bool one_stream = false;          // RS_DIST_ONE_STREAM=1: both roles on the caller's stream
   cudaStream_t cap_stream = nullptr;
   cudaStream_t own_stream = nullptr;  // owner role runs here, concurrently with the requester's
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t gather_stream = nullptr;  // the requester's gather, concurrent with its reduce
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_meta = nullptr, ev_gjoin = nullptr;
   std::vector<DistGraph> graphs;
   uint64_t graph_clock = 0;
 };
@@ -702,6 +703,9 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   RS_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  RS_CUDA(cudaStreamCreateWithFlags(&c->gather_stream, cudaStreamNonBlocking));
+  RS_CUDA(cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
   c->h_peers[rank] = c->arena;
   *out = c;
   return RS_OK;
@@ -764,6 +768,9 @@ int rs_comm_destroy(rs_comm* c) {
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->gather_stream) cudaStreamDestroy(c->gather_stream);
+  if (c->ev_meta) cudaEventDestroy(c->ev_meta);
+  if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
   rs_workspace_destroy(c->ws_req);
   rs_workspace_destroy(c->ws_own);
   delete c;
@@ -844,11 +851,17 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     cudaStream_t own;
     RS_TRY(fork_owner(c, q, &own));
     RS_TRY(req_front(c, t, d_ids, n, ss, q));
+    // the gather needs only the metadata (and the rows): it runs on its own
+    // stream, concurrently with the segment-reduce of the same tokens
+    RS_CUDA(cudaEventRecord(c->ev_meta, q));
+    RS_CUDA(cudaStreamWaitEvent(c->gather_stream, c->ev_meta, 0));
     RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
     RS_TRY(owner_lookup(c, t, ss, own));
     RS_TRY(table_mirror_copy(t, mirror, own));
     RS_TRY(owner_update(c, t, ob, ss, own));
-    RS_TRY(req_gather(c, t, n, d_out, ss, q));
+    RS_TRY(req_gather(c, t, n, d_out, ss, c->gather_stream));
+    RS_CUDA(cudaEventRecord(c->ev_gjoin, c->gather_stream));
+    RS_CUDA(cudaStreamWaitEvent(q, c->ev_gjoin, 0));
     return join_owner(c, q, own);
   };
   if (c->profiling || !c->use_graphs) {
