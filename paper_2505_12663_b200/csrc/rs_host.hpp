@@ -46,6 +46,7 @@ struct rs_table {
   uint32_t* d_victim_idx = nullptr;
   uint64_t evict_cap = 0, victim_idx_cap = 0;
   uint64_t buf_gen = 0;  // bumps when a buffer baked into captured graphs is reallocated
+  bool evict_tmin_valid = false;  // the device selection may start its tick window at its last min
 };
 
 struct rs_graph_entry {

@@ -876,6 +876,7 @@ int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* em
 
 int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* emb,
                     const float* m, const float* v, const uint64_t* step, const uint64_t* ts) {
+  if (t) t->evict_tmin_valid = false;  // imported ticks may lie below the last selection's min
   if (!t) return fail(RS_ERR_CONFIG, "rs_table_import: null table");
   if (n == 0) return RS_OK;
   const size_t D = t->desc.dim;
