@@ -327,6 +327,22 @@ int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_
                         uint64_t first_sample_id, uint64_t step, const rs_optimizer_params* opt,
                         double* h_checksum, void* stream);
 
+/* ---- elastic checkpoint (checkpoint.hpp:25-54, checkpoint.cpp) ----------------
+ * The reference's little-endian shard file; records in key order with slot =
+ * ordinal (device slots are not the reference's probe positions), so files
+ * are byte-deterministic and save -> load -> save is byte-identical.  Loads
+ * follow load_cluster: modulo file selection + ownership refilter when the
+ * world size changes; tick fast-forwarded to the newest stamp.  All sync. */
+typedef struct {
+  uint32_t version, world_size, shard_rank, embedding_dim;
+  uint64_t capacity, entry_count;
+} rs_ckpt_header;
+int rs_ckpt_shard_file_name(uint32_t rank, uint32_t world_size, char* out, uint64_t cap);
+int rs_ckpt_save_shard(rs_table* t, uint32_t rank, uint32_t world_size, const char* path);
+int rs_ckpt_read_header(const char* path, rs_ckpt_header* out);
+int rs_ckpt_load_shard(rs_table* t, const char* dir, uint32_t saved_world, uint32_t new_world,
+                       uint32_t rank);
+
 /* ---- synthetic inputs (workload.cpp:103-152, 280-307, 348-355) ------------ */
 /* generate_workload: per-sample lengths + catalog-tagged ids (k = bit_width(tables)) */
 int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len,

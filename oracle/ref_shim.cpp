@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "recsparse/checkpoint.hpp"
 #include "recsparse/common.hpp"
 #include "recsparse/embed_table.hpp"
 #include "recsparse/exchange_sim.hpp"
@@ -360,6 +361,26 @@ int ref_collection_lookup(void* h, const char* feature, const uint64_t* raw, uin
     return 5;
   } catch (const std::exception& e) {
     return status_of(e);
+  }
+}
+
+// ---- checkpoint (checkpoint.hpp) ------------------------------------------
+int ref_ckpt_save_cluster(void* cluster, const char* dir) {
+  GUARD(save_cluster(*static_cast<SimCluster*>(cluster), dir));
+  return 0;
+}
+void* ref_ckpt_load_cluster(const char* dir, uint32_t saved_world, uint32_t new_world, uint64_t capacity,
+                            uint32_t dim, uint32_t chunk_rows, int* status) {
+  try {
+    TableConfig cfg;
+    cfg.capacity = capacity;
+    cfg.embedding_dim = dim;
+    cfg.chunk_rows = chunk_rows;
+    *status = 0;
+    return new SimCluster(load_cluster(dir, saved_world, new_world, cfg));
+  } catch (const std::exception& e) {
+    *status = status_of(e);
+    return nullptr;
   }
 }
 

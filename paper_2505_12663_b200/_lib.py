@@ -62,6 +62,11 @@ class rs_feature_config(C.Structure):
                 ("lookup_tables", C.POINTER(C.c_char_p)), ("n_lookup_tables", C.c_uint32), ("pooling", C.c_uint32)]
 
 
+class rs_ckpt_header(C.Structure):
+    _fields_ = [("version", C.c_uint32), ("world_size", C.c_uint32), ("shard_rank", C.c_uint32),
+                ("embedding_dim", C.c_uint32), ("capacity", C.c_uint64), ("entry_count", C.c_uint64)]
+
+
 class rs_optimizer_params(C.Structure):
     _fields_ = [("kind", C.c_uint32), ("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
                 ("eps", C.c_double)]
@@ -156,6 +161,10 @@ _SIGS = {
     "rs_feeder_step": (C.c_int, [vp, vp, vp, vp, u64, vp, u64, u64, u64, C.POINTER(rs_optimizer_params), vp, vp]),
     "rs_feeder_dist_step": (C.c_int, [vp, vp, vp, vp, u64, vp, u64, u64, u64, C.POINTER(rs_optimizer_params), vp,
                                       vp]),
+    "rs_ckpt_shard_file_name": (C.c_int, [u32, u32, C.c_char_p, u64]),
+    "rs_ckpt_save_shard": (C.c_int, [vp, u32, u32, C.c_char_p]),
+    "rs_ckpt_read_header": (C.c_int, [C.c_char_p, C.POINTER(rs_ckpt_header)]),
+    "rs_ckpt_load_shard": (C.c_int, [vp, C.c_char_p, u32, u32, u32]),
     "rs_encode_ids": (C.c_int, [vp, u64, u32, u32, u32, vp, vp]),
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),

@@ -919,6 +919,15 @@ int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* 
     RS_CUDA(cudaMemcpy(dts, ts, n * 8, cudaMemcpyHostToDevice));
     k_set_ticks<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads>>>(t->dev, dk, dts, n);
     RS_LAUNCH_CHECK("k_set_ticks");
+    // bump_tick(max ts) (embed_table.hpp:159-161): stamps stay monotone after a reload
+    const uint64_t mx = *std::max_element(ts, ts + n);
+    unsigned int cur = 0;
+    RS_CUDA(cudaDeviceSynchronize());
+    RS_CUDA(cudaMemcpy(&cur, &t->dev->c.tick, 4, cudaMemcpyDeviceToHost));
+    if (mx > cur) {
+      const unsigned int v32 = (unsigned int)mx;
+      RS_CUDA(cudaMemcpy(&t->dev->c.tick, &v32, 4, cudaMemcpyHostToDevice));
+    }
   }
   RS_CUDA(cudaDeviceSynchronize());
   cudaFree(dk);
