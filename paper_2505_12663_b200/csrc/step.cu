@@ -1132,7 +1132,12 @@ int lpr_for(uint32_t D) {
 
 uint32_t tile_tokens_for_dim(uint32_t D) {
   // staged gradient tile <= 64 KB so two tiles fit per SM
-  uint32_t tt = 256;
+  static const uint32_t cap = [] {
+    const char* e = getenv("RS_TILE_MAX");  // experiments: 64 / 128 / 256
+    const uint32_t v = e ? (uint32_t)atoi(e) : 256u;
+    return (v == 64 || v == 128 || v == 256) ? v : 256u;
+  }();
+  uint32_t tt = cap;
   while (tt > 32 && (uint64_t)tt * D * 4 > 65536) tt >>= 1;
   return tt;
 }
