@@ -362,6 +362,10 @@ int rs_pseudo_grads_jagged(const uint64_t* d_lengths, uint64_t n_seq, uint64_t f
  * one kernel, block per sample */
 int rs_pseudo_grads_offsets(const uint64_t* d_offsets, uint64_t n_seq, uint64_t first_sample_id,
                             uint64_t step, uint32_t dim, float* d_out, void* stream);
+/* the same from a work list of (sample, token begin, token end) u32 triples
+ * (device), one balanced block per triple */
+int rs_pseudo_grads_chunks(const void* d_work, uint32_t n_chunks, uint64_t first_sample_id,
+                           uint64_t step, uint32_t dim, float* d_out, void* stream);
 /* run_workload's emb_checksum (workload.cpp:547-549): sum of d_x[0, n) in f64,
  * fixed order (deterministic), into *d_out */
 int rs_checksum(const float* d_x, uint64_t n, double* d_out, void* stream);

@@ -155,6 +155,7 @@ _SIGS = {
     "rs_pseudo_grads_jagged": (C.c_int, [vp, u64, u64, u64, u32, u64, vp, vp]),
     "rs_checksum": (C.c_int, [vp, u64, vp, vp]),
     "rs_pseudo_grads_offsets": (C.c_int, [vp, u64, u64, u64, u32, vp, vp]),
+    "rs_pseudo_grads_chunks": (C.c_int, [vp, u32, u64, u64, u32, vp, vp]),
     "rs_feeder_create": (C.c_int, [u64, u64, u32, C.POINTER(vp)]),
     "rs_feeder_destroy": (C.c_int, [vp]),
     "rs_feeder_out": (vp, [vp, C.c_int]),

@@ -11,9 +11,13 @@
 // events), and only the 8-byte checksum travels back.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "rs_host.hpp"
 
 using namespace rs;
+
+static constexpr uint64_t kChunkTok = 512;  // tokens per block of the gradient kernel
 
 struct rs_feeder {
   uint64_t max_tokens = 0, max_seqs = 0;
@@ -23,6 +27,9 @@ struct rs_feeder {
   uint64_t* ids[2] = {};
   uint64_t* offs[2] = {};       // device token offsets of the batch
   uint64_t* h_offs[2] = {};     // pinned host staging of the offsets
+  uint32_t* chunks[2] = {};     // device work list of the gradient kernel
+  uint32_t* h_chunks[2] = {};   // pinned staging: (sample, t0, t1) triples
+  uint32_t n_chunks[2] = {0, 0};
   float* grads[2] = {};
   float* out[2] = {};
   double* sum[2] = {};
@@ -44,6 +51,8 @@ int rs_feeder_create(uint64_t max_tokens, uint64_t max_seqs, uint32_t dim, rs_fe
          cudaMalloc(&f->ids[b], max_tokens * 8) == cudaSuccess &&
          cudaMalloc(&f->offs[b], (max_seqs + 1) * 8) == cudaSuccess &&
          cudaMallocHost(&f->h_offs[b], (max_seqs + 1) * 8) == cudaSuccess &&
+         cudaMalloc(&f->chunks[b], (max_seqs + max_tokens / kChunkTok + 1) * 12) == cudaSuccess &&
+         cudaMallocHost(&f->h_chunks[b], (max_seqs + max_tokens / kChunkTok + 1) * 12) == cudaSuccess &&
          cudaMalloc(&f->grads[b], max_tokens * dim * 4) == cudaSuccess &&
          cudaMalloc(&f->out[b], max_tokens * dim * 4) == cudaSuccess &&
          cudaMalloc(&f->sum[b], 8) == cudaSuccess;
@@ -63,10 +72,11 @@ int rs_feeder_destroy(rs_feeder* f) {
   for (int b = 0; b < 2; ++b) {
     if (f->in_free[b]) cudaEventDestroy(f->in_free[b]);
     if (f->landed[b]) cudaEventDestroy(f->landed[b]);
-    void* ps[] = {f->ids[b], f->offs[b], f->grads[b], f->out[b], f->sum[b]};
+    void* ps[] = {f->ids[b], f->offs[b], f->grads[b], f->out[b], f->sum[b], f->chunks[b]};
     for (void* p : ps)
       if (p) cudaFree(p);
     if (f->h_offs[b]) cudaFreeHost(f->h_offs[b]);
+    if (f->h_chunks[b]) cudaFreeHost(f->h_chunks[b]);
   }
   if (f->copy) cudaStreamDestroy(f->copy);
   delete f;
@@ -87,14 +97,23 @@ static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const u
   // staging buffer of this set is free once its previous copy completed
   RS_CUDA(cudaEventSynchronize(f->landed[b]));
   uint64_t run = 0;
+  uint32_t nc = 0;
   for (uint64_t i = 0; i < n_seq; ++i) {
     f->h_offs[b][i] = run;
+    // balanced work list of the gradient kernel: <= kChunkTok tokens per block
+    for (uint64_t t0 = run; t0 < run + h_lengths[i]; t0 += kChunkTok) {
+      f->h_chunks[b][3 * nc] = (uint32_t)i;
+      f->h_chunks[b][3 * nc + 1] = (uint32_t)t0;
+      f->h_chunks[b][3 * nc + 2] = (uint32_t)std::min<uint64_t>(t0 + kChunkTok, run + h_lengths[i]);
+      ++nc;
+    }
     run += h_lengths[i];
   }
   f->h_offs[b][n_seq] = run;
+  f->n_chunks[b] = nc;
   if (run != n) return fail(RS_ERR_CONFIG, "rs_feeder_step: sum of lengths != number of ids");
   RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
-  RS_CUDA(cudaMemcpyAsync(f->offs[b], f->h_offs[b], (n_seq + 1) * 8, cudaMemcpyHostToDevice, f->copy));
+  RS_CUDA(cudaMemcpyAsync(f->chunks[b], f->h_chunks[b], (size_t)nc * 12, cudaMemcpyHostToDevice, f->copy));
   RS_CUDA(cudaEventRecord(f->landed[b], f->copy));
   RS_CUDA(cudaStreamWaitEvent(s, f->landed[b], 0));
   *set = b;
@@ -120,7 +139,7 @@ int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
-  if (!st) st = rs_pseudo_grads_offsets(f->offs[b], n_seq, first_sample_id, step, f->dim, f->grads[b], stream);
+  if (!st) st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
   if (!st) st = rs_step(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
   if (!st) st = feeder_finish(f, b, n, h_checksum, s);
   return st;
@@ -135,7 +154,7 @@ int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
-  if (!st) st = rs_pseudo_grads_offsets(f->offs[b], n_seq, first_sample_id, step, f->dim, f->grads[b], stream);
+  if (!st) st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
   if (!st) st = rs_dist_step(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
   if (!st) st = feeder_finish(f, b, n, h_checksum, s);
   return st;

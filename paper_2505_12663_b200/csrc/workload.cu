@@ -101,6 +101,29 @@ __global__ void __launch_bounds__(256) k_jagged_grads(const uint64_t* __restrict
   for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) __stcs(dst + i, srow4[i % d4]);
 }
 
+// Chunked variant: block i handles work item (sample s, token range
+// [t0, t1)) -- long samples are split so the blocks are balanced.
+struct GradChunk {
+  uint32_t s;
+  uint32_t t0, t1;
+};
+__global__ void __launch_bounds__(256) k_jagged_grads_chunks(const GradChunk* __restrict__ work, uint64_t first,
+                                                             uint64_t step, uint32_t dim, float* __restrict__ out) {
+  extern __shared__ float4 srow4c[];
+  float* srow = reinterpret_cast<float*>(srow4c);
+  const GradChunk w = work[blockIdx.x];
+  const uint64_t base = hash64((first + w.s) * 0x9e3779b97f4a7c15ULL + step * 0xbf58476d1ce4e5b9ULL + 1);
+  for (uint32_t e = threadIdx.x; e < dim; e += blockDim.x) {
+    const double u = static_cast<double>(hash64(base + e) >> 11) * 0x1.0p-53;
+    srow[e] = static_cast<float>((u - 0.5) * 0.1);
+  }
+  __syncthreads();
+  const uint32_t d4 = dim >> 2;
+  const uint64_t total = (uint64_t)(w.t1 - w.t0) * d4;
+  float4* dst = reinterpret_cast<float4*>(out) + (uint64_t)w.t0 * d4;
+  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) __stcs(dst + i, srow4c[i % d4]);
+}
+
 // sample index of every token: block s fills [offs[s], offs[s+1])
 __global__ void k_fill_sample(const uint64_t* __restrict__ offs, uint32_t* __restrict__ sample_of) {
   const uint32_t s = blockIdx.x;
@@ -133,11 +156,13 @@ __global__ void __launch_bounds__(256) k_broadcast_rows(const uint32_t* __restri
   }
 }
 
-// deterministic f64 sum of x[0, n): per-block partials, then one block sums
-// them in block order
+// deterministic f64 sum of x[0, n): per-block partials (4 loads in flight per
+// thread); the last block to finish combines them in a fixed tree order
 __global__ void __launch_bounds__(256) k_sum_partials(const float* __restrict__ x, uint64_t n,
-                                                      double* __restrict__ part) {
-  __shared__ double w[8];
+                                                      double* __restrict__ part, unsigned int* __restrict__ done,
+                                                      double* __restrict__ out) {
+  __shared__ double w[256];
+  __shared__ bool last;
   double acc = 0.0;
   const uint64_t n4 = n >> 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -152,31 +177,32 @@ __global__ void __launch_bounds__(256) k_sum_partials(const float* __restrict__ 
   }
   if (blockIdx.x == 0)
     for (uint64_t i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) acc += (double)x[i];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
-  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = 0.0;
-    for (int k = 0; k < 8; ++k) b += w[k];
-    part[blockIdx.x] = b;
-  }
-}
-
-// the last block to finish sums the per-block partials in a fixed order
-__global__ void __launch_bounds__(256) k_sum_last(const double* __restrict__ part, uint32_t nb,
-                                                  unsigned int* __restrict__ done, double* __restrict__ out) {
-  (void)done;
-  __shared__ double sh[256];
-  double acc = 0.0;
-  for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) acc += part[b];
-  sh[threadIdx.x] = acc;
+  w[threadIdx.x] = acc;
   __syncthreads();
   for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < (unsigned)o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    if (threadIdx.x < (unsigned)o) w[threadIdx.x] += w[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = sh[0];
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = w[0];
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a2 = 0.0;
+  for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) a2 += __ldcg(part + b);
+  w[threadIdx.x] = a2;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < (unsigned)o) w[threadIdx.x] += w[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out = w[0];
+    *done = 0;
+  }
 }
 
 }  // namespace
@@ -312,18 +338,34 @@ int rs_pseudo_grads_offsets(const uint64_t* d_offsets, uint64_t n_seq, uint64_t 
   return RS_OK;
 }
 
+// From a host-built work list of (sample, token range) chunks (device copy):
+// balanced blocks, one kernel.
+int rs_pseudo_grads_chunks(const void* d_work, uint32_t n_chunks, uint64_t first_sample_id, uint64_t step,
+                           uint32_t dim, float* d_out, void* stream) {
+  using namespace rs;
+  if (n_chunks == 0) return RS_OK;
+  if (dim % 4 || dim > 4096) return fail(RS_ERR_CONFIG, "rs_pseudo_grads_chunks: dim % 4 != 0 or > 4096");
+  k_jagged_grads_chunks<<<n_chunks, 256, dim * 4, (cudaStream_t)stream>>>(
+      static_cast<const GradChunk*>(d_work), first_sample_id, step, dim, d_out);
+  RS_LAUNCH_CHECK("k_jagged_grads_chunks");
+  return RS_OK;
+}
+
 // run_workload's emb_checksum (workload.cpp:547-549) of a step's outputs, in
 // f64, deterministic (fixed block partition and order).
 int rs_checksum(const float* d_x, uint64_t n, double* d_out, void* stream) {
   using namespace rs;
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned nb = 148 * 4;
-  static double* part = nullptr;  // kept across calls
-  if (!part) RS_CUDA(cudaMalloc(&part, nb * 8));
-  k_sum_partials<<<nb, 256, 0, s>>>(d_x, n, part);
+  static double* part = nullptr;  // kept across calls (one stream at a time)
+  static unsigned int* done = nullptr;
+  if (!part) {
+    RS_CUDA(cudaMalloc(&part, nb * 8));
+    RS_CUDA(cudaMalloc(&done, 4));
+    RS_CUDA(cudaMemset(done, 0, 4));
+  }
+  k_sum_partials<<<nb, 256, 0, s>>>(d_x, n, part, done, d_out);
   RS_LAUNCH_CHECK("k_sum_partials");
-  k_sum_last<<<1, 256, 0, s>>>(part, nb, nullptr, d_out);
-  RS_LAUNCH_CHECK("k_sum_last");
   return RS_OK;
 }
 
