@@ -140,3 +140,23 @@ def weighted_grad_combine(batch_sizes, grads) -> np.ndarray:
     check(L.lib().rs_weighted_grad_combine(bs.ctypes.data, g.ctypes.data, len(bs), g.shape[1], out.ctypes.data),
           "weighted_grad_combine")
     return out
+
+
+def weighted_grad_allreduce(batch_size: int, grad, group=None):
+    """The dense side of a step across ranks (workload.cpp:583-601 +
+    weighted_grad_combine, seq_batcher.cpp:80-138): every rank contributes
+    its per-sample mean gradient weighted by its batch size; one all-reduce
+    of [b * g, b] (f64, NCCL on GPU tensors / gloo on CPU) gives
+    sum_i b_i g_i / sum_i b_i on every rank.  The reduction order is the
+    collective's, so the result matches weighted_grad_combine to f64
+    rounding, not bit for bit."""
+    import torch
+    import torch.distributed as dist
+    g = torch.as_tensor(grad, dtype=torch.float64)
+    if batch_size < 1:
+        raise L.ConfigError("weighted_grad_combine: batch sizes must be >= 1")
+    buf = torch.empty(g.numel() + 1, dtype=torch.float64, device=g.device)
+    buf[:-1] = g.reshape(-1) * float(batch_size)
+    buf[-1] = float(batch_size)
+    dist.all_reduce(buf, group=group)
+    return (buf[:-1] * (1.0 / buf[-1])).reshape(g.shape)

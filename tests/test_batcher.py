@@ -100,3 +100,41 @@ def test_imbalance_and_weighted_combine():
         assert got[e] == acc * inv  # workers in fixed order, bit-identical (seq_batcher.cpp:127-135)
     with pytest.raises(P.ConfigError):
         P.weighted_grad_combine([0, 1], g[:2])
+
+
+def _allreduce_worker(rank, world, port, q):
+    import sys as _s
+    import os as _o
+    _s.path.insert(0, _o.path.dirname(_o.path.dirname(_o.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_2505_12663_b200 as P2
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    rng = np.random.default_rng(rank)
+    b = int(rng.integers(1, 50))
+    g = rng.standard_normal(17)
+    out = P2.batcher.weighted_grad_allreduce(b, g)
+    q.put((rank, b, g, out.numpy()))
+    dist.destroy_process_group()
+
+
+def test_weighted_grad_allreduce_gloo_world2():
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_allreduce_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(60)
+        assert p.exitcode == 0
+    bs = np.array([r[1] for r in res], np.uint64)
+    gs = np.stack([r[2] for r in res])
+    want = P.weighted_grad_combine(bs, gs)
+    for r in res:
+        np.testing.assert_allclose(r[3], want, rtol=1e-14, atol=1e-15)
