@@ -81,6 +81,9 @@ struct rs_scratch {
 };
 
 struct rs_workspace {
+  // KC split (RS_SPLIT_KC=0: one pass): the hot-id pass is launched by the finish
+  bool split_kc = true;
+  bool kc_forked = false;  // the hot tile pass was launched on aux_stream (launch_finish joins)
   bool graph_fork = true;  // hot-id finish as a forked branch inside captured graphs (RS_GRAPH_FORK=0: linear)
   uint64_t max_tokens = 0;
   uint64_t S = 0;  // scratch hash capacity (power of two)

@@ -343,8 +343,13 @@ struct TileArgs {
   rs_dist_sync sync;        // sharded step: wait for the peers' rows before gathering
 };
 
-template <int VEC, int CH, int LPR>
-__global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
+// MODE kTileFull: gather + CSR placement + hot-id tile partials (one pass);
+// kTileGatherCsr: gather + CSR placement only (no staging smem: many blocks
+// per SM); kTileHot: hot-id tile partials only (runs beside the CSR finish)
+enum : int { kTileFull = 0, kTileGatherCsr = 1, kTileHot = 2 };
+
+template <int VEC, int CH, int LPR, int MODE>
+__global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? 4 : 3) k_ftile(TileArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t NW = TT >> 5;
@@ -352,7 +357,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   const uint32_t D = a.td->d.dim;
   const bool red = a.grads != nullptr;
   float* sg = reinterpret_cast<float*>(smem);  // [TT x D] staged gradients (reduce)
-  unsigned char* p = smem + (red ? (size_t)TT * D * 4 : 0);
+  unsigned char* p = smem + ((MODE != kTileGatherCsr && red) ? (size_t)TT * D * 4 : 0);
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(p);
   p += 16;
   uint32_t* lkey = reinterpret_cast<uint32_t*>(p);
@@ -376,7 +381,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   dist_wait(a.sync);
   const uint32_t rows = min(TT, nn - t0);
 
-  if (red && a.stage) {
+  if (MODE != kTileGatherCsr && red && a.stage) {
     for (uint32_t i = tid; i < L; i += TT) {
       lkey[i] = kFull;
       lfirst[i] = kFull;
@@ -418,7 +423,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   }
 
   // ---- gather: warp w copies the rows of tokens [32w, 32w + 32)
-  if (a.out) {
+  if (MODE != kTileHot && a.out) {
     if (valid) a.inverse[t0 + tid] = (int32_t)u;
     constexpr int RPI = 32 / LPR;
     constexpr int ITERS = 32 / RPI;
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
   uint32_t nt = 0;
   if (valid) nt = __ldg(a.u_ntile + u);
   const bool csr_tok = valid && nt == 0;
-  {
+  if (MODE != kTileHot) {
     const uint32_t key = csr_tok ? u : (0xFFFF0000u | lane);
     const unsigned mm0 = __match_any_sync(kFull, key);
     const uint32_t leader = __ffs(mm0) - 1;
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(256, 3) k_ftile(TileArgs a) {
           a.pos_map ? __ldg(a.pos_map + t0 + tid) : t0 + tid;
   }
   const bool hotv = valid && nt > 0;
-  if (!a.stage) return;  // no hot ids possible (sharded owner side)
+  if (MODE == kTileGatherCsr || !a.stage) return;  // no hot part here / none possible
 
   // ---- hot ids: group the tile's tokens by unique id (first occurrence)
   uint32_t ps = 0;
@@ -1147,8 +1152,11 @@ uint32_t tile_tokens_for_dim(uint32_t D) {
 // every k_ftile / k_finish instantiation opts in to large dynamic smem once
 template <int V, int C, int LPR>
 static int attr_tile() {
-  RS_CUDA(cudaFuncSetAttribute(k_ftile<V, C, LPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RS_CUDA(cudaFuncSetAttribute(k_ftile<V, C, LPR, kTileFull>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                200 * 1024));
+  if (LPR == 1)
+    RS_CUDA(cudaFuncSetAttribute(k_ftile<V, C, 1, kTileHot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
   return RS_OK;
 }
 template <int V, int C>
@@ -1266,11 +1274,45 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
                       (size_t)TT * 2 + 16;
   const Shape sh = shape_for(D);
   const int lpr = lpr_for(D);
-#define RS_TILE(V, C, LP)                                   \
-  if (sh.vec == V && sh.ch == C && lpr == LP) {             \
-    k_ftile<V, C, LP><<<ntiles, TT, smem, s>>>(a);          \
-    RS_LAUNCH_CHECK("k_ftile");                             \
-    return RS_OK;                                           \
+  // single-GPU reduce: gather + CSR placement now (no staging smem, many
+  // blocks per SM); the hot-id partials run in launch_finish beside the CSR
+  // finish, which needs only the CSR placement
+  const bool split = ws->split_kc && d_grads && a.stage && !dopt && D % 4 == 0;
+  if (split) {
+    // the hot pass needs only KA / KB: with the fork it runs on the aux
+    // stream concurrently with the gather + CSR pass (and later the CSR
+    // finish); launch_finish joins
+    TileArgs a2 = a;
+    a2.out = nullptr;
+    a2.clean_cnt = nullptr;
+    cudaStream_t hs = s;
+    if (ws->fork) {
+      RS_CUDA(cudaEventRecord(ws->ev_fork, s));
+      RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, ws->ev_fork, 0));
+      hs = ws->aux_stream;
+      ws->kc_forked = true;
+    }
+    bool kc2 = false;
+#define RS_HOT(V, C)                                                           \
+  if (!kc2 && sh.vec == V && sh.ch == C) {                                     \
+    k_ftile<V, C, 1, kTileHot><<<ntiles, TT, smem, hs>>>(a2);                  \
+    RS_LAUNCH_CHECK("k_ftile(hot)");                                           \
+    kc2 = true;                                                                \
+  }
+    RS_HOT(4, 1) RS_HOT(4, 2) RS_HOT(4, 3) RS_HOT(4, 4) RS_HOT(2, 1) RS_HOT(2, 2)
+    RS_HOT(1, 1) RS_HOT(1, 2) RS_HOT(1, 3) RS_HOT(1, 4) RS_HOT(1, 5) RS_HOT(1, 6) RS_HOT(1, 7)
+    RS_HOT(1, 8)
+#undef RS_HOT
+    if (!kc2) return fail(RS_ERR_INVARIANT, "launch_tile: no hot tile kernel for this shape");
+  }
+#define RS_TILE(V, C, LP)                                                     \
+  if (sh.vec == V && sh.ch == C && lpr == LP) {                               \
+    if (split)                                                                \
+      k_ftile<V, C, LP, kTileGatherCsr><<<ntiles, TT, 16, s>>>(a);            \
+    else                                                                      \
+      k_ftile<V, C, LP, kTileFull><<<ntiles, TT, smem, s>>>(a);               \
+    RS_LAUNCH_CHECK("k_ftile");                                               \
+    return RS_OK;                                                             \
   }
 #define RS_TILE_ALL(V, C) \
   RS_TILE(V, C, 1) RS_TILE(V, C, 2) RS_TILE(V, C, 4) RS_TILE(V, C, 8) RS_TILE(V, C, 16) RS_TILE(V, C, 32)
@@ -1321,8 +1363,18 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   // G > 0: CSR ids on s, hot ids concurrently on the forked aux stream
   const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
   cudaStream_t hs = s;
-  const bool fork = G > 0 && ws->fork && !(dopt && dopt->no_hot);
-  if (fork) {
+  bool fork = G > 0 && ws->fork && !(dopt && dopt->no_hot);
+  if (ws->kc_forked) {  // the hot tile pass already runs on the aux stream
+    ws->kc_forked = false;
+    if (G > 0) {
+      hs = ws->aux_stream;
+      fork = true;
+    } else {  // one finish kernel for both paths: join first
+      RS_CUDA(cudaEventRecord(ws->ev_join, ws->aux_stream));
+      RS_CUDA(cudaStreamWaitEvent(s, ws->ev_join, 0));
+      fork = false;
+    }
+  } else if (fork) {
     RS_CUDA(cudaEventRecord(ws->ev_fork, s));
     RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, ws->ev_fork, 0));
     hs = ws->aux_stream;
@@ -1462,6 +1514,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   if (const char* e = getenv("RS_NO_GRAPH")) ws->use_graphs = e[0] == '0';
   if (const char* e = getenv("RS_NO_FORK")) ws->fork = e[0] == '0';
   if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] != '0';
+  if (const char* e = getenv("RS_SPLIT_KC")) ws->split_kc = e[0] != '0';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;
@@ -1684,8 +1737,13 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
   const int mirror = t->mirror_next;
   const int use = ws->cur;
   if (ws->profiling || !ws->use_graphs) {
+    // profiling runs the kernels one after another (no fork) so that every
+    // phase's events bracket only its own kernels
+    const bool f0 = ws->fork;
+    if (ws->profiling) ws->fork = false;
     st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, s,
                       ws->profiling ? ws->prof_ev : nullptr);
+    ws->fork = f0;
     if (st) return st;
     if (ws->profiling) {
       RS_CUDA(cudaEventSynchronize(ws->prof_ev[4]));
