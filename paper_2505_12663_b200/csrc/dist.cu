@@ -500,7 +500,8 @@ static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhReqReduce, s));
   if (n) {
-    RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, nullptr));
+    rs_dist_opts one_pass;  // (a dopt: the one-pass KC -- the split measured slower here)
+    RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, &one_pass));
     rs_dist_opts o;
     o.peer_dst = c->d_peer_grad[ss.par];
     o.send_pos = c->send_pos;
