@@ -149,6 +149,12 @@ int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
                 const rs_optimizer_params* opt, void* stream);
 int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
             const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream);
+/* rs_step plus run_workload's per-step emb_checksum (workload.cpp:547-549):
+ * *d_checksum (device f64) = the sum of every value written to d_out, computed
+ * inside the gather kernel (fixed reduction tree: deterministic). */
+int rs_step_checksum(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, float* d_out, const rs_optimizer_params* opt,
+                     double* d_checksum, void* stream);
 /* GradAccumulator::accumulate + apply for one window (sparse_update.cpp:45-83):
  * dedup ids, zero-vivify absent ids, segment-reduce grads fused with the
  * optimizer.  No gather. */

@@ -111,6 +111,7 @@ _SIGS = {
     "rs_forward": (C.c_int, [vp, vp, vp, u64, vp, vp]),
     "rs_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
     "rs_step": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_step_checksum": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp, vp]),
     "rs_sparse_update": (C.c_int, [vp, vp, vp, u64, vp, C.POINTER(rs_optimizer_params), vp]),
     "rs_workspace_results": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "rs_workspace_set_profiling": (C.c_int, [vp, C.c_int]),

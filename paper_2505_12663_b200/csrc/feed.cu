@@ -112,16 +112,20 @@ static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const u
   f->h_offs[b][n_seq] = run;
   f->n_chunks[b] = nc;
   if (run != n) return fail(RS_ERR_CONFIG, "rs_feeder_step: sum of lengths != number of ids");
-  RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
-  RS_CUDA(cudaMemcpyAsync(f->chunks[b], f->h_chunks[b], (size_t)nc * 12, cudaMemcpyHostToDevice, f->copy));
+  static const int skip = getenv("RS_FEED_SKIP") ? atoi(getenv("RS_FEED_SKIP")) : 0;  // profiling only
+  if (!(skip & 1) || f->k < 2) {
+    RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
+    RS_CUDA(cudaMemcpyAsync(f->chunks[b], f->h_chunks[b], (size_t)nc * 12, cudaMemcpyHostToDevice, f->copy));
+  }
   RS_CUDA(cudaEventRecord(f->landed[b], f->copy));
   RS_CUDA(cudaStreamWaitEvent(s, f->landed[b], 0));
   *set = b;
   return RS_OK;
 }
 
-static int feeder_finish(rs_feeder* f, int b, uint64_t n, double* h_checksum, cudaStream_t s) {
-  int st = rs_checksum(f->out[b], n * f->dim, f->sum[b], s);
+static int feeder_finish(rs_feeder* f, int b, uint64_t n, double* h_checksum, cudaStream_t s,
+                         bool summed) {
+  int st = summed ? RS_OK : rs_checksum(f->out[b], n * f->dim, f->sum[b], s);
   if (st) return st;
   RS_CUDA(cudaEventRecord(f->in_free[b], s));
   if (h_checksum) RS_CUDA(cudaMemcpyAsync(h_checksum, f->sum[b], 8, cudaMemcpyDeviceToHost, s));
@@ -139,9 +143,11 @@ int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* 
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
-  if (!st) st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
-  if (!st) st = rs_step(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
-  if (!st) st = feeder_finish(f, b, n, h_checksum, s);
+  static const int skip = getenv("RS_FEED_SKIP") ? atoi(getenv("RS_FEED_SKIP")) : 0;  // profiling only
+  if (!st && (!(skip & 2) || f->k < 2))
+    st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
+  if (!st) st = rs_step_checksum(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, f->sum[b], stream);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s, true);
   return st;
 }
 
@@ -156,7 +162,7 @@ int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
   if (!st) st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
   if (!st) st = rs_dist_step(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
-  if (!st) st = feeder_finish(f, b, n, h_checksum, s);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s, false);
   return st;
 }
 

@@ -55,6 +55,7 @@ struct rs_graph_entry {
   const void* ids = nullptr;
   const void* grads = nullptr;
   void* out = nullptr;
+  double* csum = nullptr;
   uint64_t n = 0;
   int mirror = 0;
   int set = 0;
@@ -84,6 +85,14 @@ struct rs_workspace {
   // KC split (RS_SPLIT_KC=0: one pass): the hot-id pass is launched by the finish
   bool split_kc = true;
   bool kc_forked = false;  // the hot tile pass was launched on aux_stream (launch_finish joins)
+  // programmatic dependent launch on the step's same-stream kernel edges (RS_PDL=0: off)
+  bool pdl = true;
+  bool pdl_now = false;
+  // rs_step_checksum: f64 sum of the gathered rows, fused into the gather
+  double* csum_dst = nullptr;
+  bool csum_done = false;
+  double* csum_part = nullptr;         // per-tile partials
+  unsigned int* csum_ticket = nullptr;  // tiles done (the last one sums, then zeroes it)  // set while step_enqueue issues the unbounded fast step
   bool graph_fork = true;  // hot-id finish as a forked branch inside captured graphs (RS_GRAPH_FORK=0: linear)
   uint64_t max_tokens = 0;
   uint64_t S = 0;  // scratch hash capacity (power of two)

@@ -105,6 +105,12 @@ __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+// Programmatic dependent launch: a kernel launched with launch_pdl may start
+// while its same-stream predecessor drains; pdl_wait() (first statement of
+// such a kernel, before any global access) blocks until the predecessor grid
+// completed and its writes are visible.  Both are no-ops for plain launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -132,6 +138,24 @@ bool debug_sync();  // RS_DEBUG_SYNC=1: synchronize after every launch (debuggin
     if (_e == cudaSuccess && ::rs::debug_sync()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess) return ::rs::cuda_fail(_e, name); \
   } while (0)
+
+// <<<g, b, smem, s>>> with the programmatic-serialization attribute when pdl
+// (the kernel must start with pdl_wait()).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), unsigned g, unsigned b, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(g);
+  cfg.blockDim = dim3(b);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
 
 inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 148u * 32u) {
   uint64_t g = (work + per_block - 1) / per_block;

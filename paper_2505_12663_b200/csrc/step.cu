@@ -114,6 +114,7 @@ __device__ __forceinline__ uint32_t local_insert(const LocalTable& lt, uint64_t 
 __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetDev S,
                          uint32_t* __restrict__ slot_of, uint64_t* __restrict__ unique,
                          uint32_t* __restrict__ ctr, const uint32_t* __restrict__ d_n) {
+  pdl_trigger();  // KB may get resident (it waits for this grid)
   const uint32_t n = d_n ? *d_n : n_host;
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
@@ -197,6 +198,8 @@ struct FTableArgs {
 constexpr unsigned kGroups = 32;  // 8-lane groups per 256-thread block
 
 __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
+  pdl_wait();
+  pdl_trigger();
   TableDev* td = a.td;
   const TableDesc d = td->d;
   const unsigned long long free_n0 = td->c.free_n;
@@ -341,6 +344,11 @@ struct TileArgs {
   const uint32_t* pos_map;  // CSR value per token (null: token index)
   bool stage;               // hot ids possible: stage the tile's gradient rows
   rs_dist_sync sync;        // sharded step: wait for the peers' rows before gathering
+  // f64 sum of every gathered value (run_workload's emb_checksum), fused into
+  // the gather: per-tile partials, the last tile sums them in tile order
+  double* csum_out = nullptr;
+  double* csum_part = nullptr;
+  unsigned int* csum_ticket = nullptr;
 };
 
 // MODE kTileFull: gather + CSR placement + hot-id tile partials (one pass);
@@ -350,6 +358,8 @@ enum : int { kTileFull = 0, kTileGatherCsr = 1, kTileHot = 2 };
 
 template <int VEC, int CH, int LPR, int MODE>
 __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? 4 : 3) k_ftile(TileArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t NW = TT >> 5;
@@ -434,6 +444,8 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? 4 : 3) k_ftile(T
     const uint32_t sub = lane / LPR, l = lane % LPR;
     const uint32_t wb = warp * 32;
     const uint32_t cnt = rows > wb ? min(32u, rows - wb) : 0u;
+    const bool csum = a.csum_out != nullptr;
+    double cs = 0.0;
 #pragma unroll
     for (int b0 = 0; b0 < ITERS; b0 += BATCH) {
       uint32_t rr[BATCH];
@@ -451,7 +463,39 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? 4 : 3) k_ftile(T
 #pragma unroll
         for (int k = 0; k < BATCH; ++k) {
           const uint32_t tok = (b0 + k) * RPI + sub;
-          if (tok < cnt && j < D4) __stcs(o4 + (size_t)(t0 + wb + tok) * D4 + j, v[k]);
+          if (tok < cnt && j < D4) {
+            __stcs(o4 + (size_t)(t0 + wb + tok) * D4 + j, v[k]);
+            if (csum) cs += (double)v[k].x + (double)v[k].y + (double)v[k].z + (double)v[k].w;
+          }
+        }
+      }
+    }
+    if (csum) {  // fixed reduction tree: the result does not depend on timing
+      __shared__ double s_cs[32];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(kFull, cs, o);
+      if (lane == 0) s_cs[warp] = cs;
+      __syncthreads();
+      if (warp == 0) {
+        double x = lane < NW ? s_cs[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        unsigned last = 0;
+        if (lane == 0) {
+          a.csum_part[tile] = x;
+          __threadfence();
+          last = atomicAdd(a.csum_ticket, 1u) == gridDim.x - 1;
+        }
+        if (__shfl_sync(kFull, last, 0)) {
+          __threadfence();
+          double y = 0.0;
+          for (uint32_t b = lane; b < gridDim.x; b += 32) y += __ldcg(a.csum_part + b);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(kFull, y, o);
+          if (lane == 0) {
+            *a.csum_out = y;
+            *a.csum_ticket = 0;
+          }
         }
       }
     }
@@ -685,6 +729,7 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 // in position order (the reference's accumulate order) -> bit-exact sums.
 template <int G>
 __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) {
+  pdl_wait();
   constexpr int PPT = (int)(kCsrMax / G);  // positions held per thread
   __shared__ uint32_t order_s[(256 / G) * kCsrMax];
   const TableDesc d = a.td->d;
@@ -827,6 +872,7 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
 //                   (sparse_update.cpp:49-54), so these sums are bit-exact
 template <int VEC, int CH>
 __global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint32_t hot_blocks) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem2[];
   const uint32_t NW = blockDim.x >> 5;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
@@ -1259,6 +1305,12 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.pbuf = ws->pbuf;
   a.ptile = ws->ptile;
   a.csr_pos = ws->csr_pos;
+  if (ws->csum_dst && !dopt && d_out && D % 4 == 0) {
+    a.csum_out = ws->csum_dst;
+    a.csum_part = ws->csum_part;
+    a.csum_ticket = ws->csum_ticket;
+    ws->csum_done = true;
+  }
   if (d_out && D % 4 != 0) {
     k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, a.use, t->dev,
                                                             (uint32_t)n, ws->inverse, d_out);
@@ -1308,9 +1360,11 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
 #define RS_TILE(V, C, LP)                                                     \
   if (sh.vec == V && sh.ch == C && lpr == LP) {                               \
     if (split)                                                                \
-      k_ftile<V, C, LP, kTileGatherCsr><<<ntiles, TT, 16, s>>>(a);            \
+      RS_CUDA(launch_pdl(ws->pdl_now, k_ftile<V, C, LP, kTileGatherCsr>,      \
+                         ntiles, TT, 16, s, a));                              \
     else                                                                      \
-      k_ftile<V, C, LP, kTileFull><<<ntiles, TT, smem, s>>>(a);               \
+      RS_CUDA(launch_pdl(ws->pdl_now, k_ftile<V, C, LP, kTileFull>, ntiles,   \
+                         TT, smem, s, a));                                    \
     RS_LAUNCH_CHECK("k_ftile");                                               \
     return RS_OK;                                                             \
   }
@@ -1364,8 +1418,10 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
   cudaStream_t hs = s;
   bool fork = G > 0 && ws->fork && !(dopt && dopt->no_hot);
+  bool split_fork = false;  // the hot finish follows the hot tile pass on aux_stream
   if (ws->kc_forked) {  // the hot tile pass already runs on the aux stream
     ws->kc_forked = false;
+    split_fork = G > 0;
     if (G > 0) {
       hs = ws->aux_stream;
       fork = true;
@@ -1380,6 +1436,8 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
     hs = ws->aux_stream;
   }
   const Shape sh = shape_for(D);
+  // programmatic edges only where the same-stream predecessor is our tile kernel
+  const bool pdl_hot = ws->pdl_now && split_fork;
   bool launched = G > 0 && dopt && dopt->no_hot;  // owner side: no hot ids possible
   const unsigned eg = G > 0 ? grid_for(n * (uint64_t)G, 256, 148 * 16) : 0;
   if (dopt) {  // the blocks of both finish kernels arrive on one counter
@@ -1388,7 +1446,8 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   }
 #define RS_FIN(V, C)                                                   \
   if (!launched && sh.vec == V && sh.ch == C) {                        \
-    k_finish<V, C><<<grid, 256, smem, hs>>>(a, o, hot_blocks);         \
+    RS_CUDA(launch_pdl(pdl_hot, k_finish<V, C>, grid, 256, smem, hs, a, o, \
+                       hot_blocks));                                   \
     RS_LAUNCH_CHECK("k_finish");                                       \
     launched = true;                                                   \
   }
@@ -1401,7 +1460,8 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   if (G > 0) {
 #define RS_CSR(GG)                                      \
   if (G == GG) {                                        \
-    k_finish_csr<GG><<<eg, 256, 0, s>>>(a, o);          \
+    RS_CUDA(launch_pdl(ws->pdl_now, k_finish_csr<GG>,   \
+                       eg, 256, 0, s, a, o));           \
     RS_LAUNCH_CHECK("k_finish_csr");                    \
   }
     RS_CSR(32) RS_CSR(16) RS_CSR(8) RS_CSR(4) RS_CSR(2)
@@ -1515,6 +1575,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   if (const char* e = getenv("RS_NO_FORK")) ws->fork = e[0] == '0';
   if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] != '0';
   if (const char* e = getenv("RS_SPLIT_KC")) ws->split_kc = e[0] != '0';
+  if (const char* e = getenv("RS_PDL")) ws->pdl = e[0] != '0';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;
@@ -1531,7 +1592,9 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
        A(&ws->u_ntile, N * 4) && A(&ws->u_poff, N * 4) && A(&ws->u_ticket, N * 4) &&
        A(&ws->urow, N * 4) && A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) &&
        A(&ws->porder, N * 4) && A(&ws->hot_list, (N / 32 + 64) * 4) && A(&ws->u_cnt, N * 4) && A(&ws->csr_pos, N * 4) &&
-       A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64);
+       A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64) &&
+       A(&ws->csum_part, (N / 32 + 2) * 8) && A(&ws->csum_ticket, 16) &&
+       cudaMemset(ws->csum_ticket, 0, 16) == cudaSuccess;
   if (!ok) {
     rs_workspace_destroy(ws);
     return cuda_fail(cudaGetLastError(), "rs_workspace_create: cudaMalloc");
@@ -1569,7 +1632,8 @@ int rs_workspace_destroy(rs_workspace* ws) {
   }
   void* ptrs[] = {ws->slot_of, ws->inverse, ws->unique, ws->u_ntile,  ws->u_poff,
                   ws->u_ticket, ws->urow,   ws->urow64, ws->ptile,    ws->porder,
-                  ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list, ws->u_cnt, ws->csr_pos};
+                  ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list, ws->u_cnt, ws->csr_pos,
+                  ws->csum_part, ws->csum_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : ws->graphs)
@@ -1704,20 +1768,48 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
   } else {
     if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
     if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
-    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
+    ws->pdl_now = ws->pdl && !ev;  // eager profiling keeps plain launches
+    RS_CUDA(launch_pdl(ws->pdl_now, k_ftable, grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s,
+                       ftable_args(ws, t, use)));
     RS_LAUNCH_CHECK("k_ftable");
   }
   if (ev) RS_CUDA(cudaEventRecord(ev[2], s));
   if ((st = launch_tile(ws, t, use, n, d_out, d_grads, true, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[3], s));
   if ((st = launch_finish(ws, t, use, n, d_grads, o, nullptr, s))) return st;
+  ws->pdl_now = false;
   if (ev) RS_CUDA(cudaEventRecord(ev[4], s));
   return table_mirror_copy(t, mirror, s);
 }
 
+static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream);
+
 int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
             const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream) {
   if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_step: null handle");
+  ws->csum_dst = nullptr;
+  return step_call(ws, t, d_ids, n, d_grads, d_out, opt, stream);
+}
+
+// rs_step + run_workload's emb_checksum of the gathered rows (workload.cpp:
+// 547-549) into d_checksum (device f64), summed inside the gather kernel.
+int rs_step_checksum(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, float* d_out, const rs_optimizer_params* opt,
+                     double* d_checksum, void* stream) {
+  if (!ws || !t || !d_checksum) return fail(RS_ERR_CONFIG, "rs_step_checksum: null argument");
+  // the gather kernel sums the rows it writes when D % 4 == 0; otherwise a
+  // separate reduction over d_out
+  const bool fused = n > 0 && t->desc.dim % 4 == 0;
+  ws->csum_dst = fused ? d_checksum : nullptr;
+  int st = step_call(ws, t, d_ids, n, d_grads, d_out, opt, stream);
+  ws->csum_dst = nullptr;
+  if (st || fused) return st;
+  return rs_checksum(d_out, n * t->desc.dim, d_checksum, stream);
+}
+
+static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                     const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream) {
   if (n == 0) {
     int st = rs_forward(ws, t, d_ids, n, d_out, stream);
     if (st) return st;
@@ -1759,6 +1851,7 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
     rs_graph_entry* hit = nullptr;
     for (auto& g : ws->graphs) {
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
+          g.csum == ws->csum_dst &&
           g.mirror == mirror && g.set == use && g.pbuf == ws->pbuf && g.tcap == t->capacity &&
           g.tgen == t->buf_gen &&
           std::memcmp(g.opt, &o, sizeof(o)) == 0) {
@@ -1780,6 +1873,7 @@ int rs_step(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
       e.ids = d_ids;
       e.grads = d_grads;
       e.out = d_out;
+      e.csum = ws->csum_dst;
       e.n = n;
       e.mirror = mirror;
       e.set = use;

@@ -283,6 +283,17 @@ class SparseStep:
                               _ptr(out), C.byref(self.params.c()), _stream()), "step")
         return out
 
+    def step_checksum(self, ids: torch.Tensor, grads: torch.Tensor, out: torch.Tensor,
+                      checksum: torch.Tensor) -> torch.Tensor:
+        """step() + checksum[0] (device float64) = sum of every value written to
+        out (run_workload's emb_checksum, workload.cpp:547-549), summed in the
+        gather kernel."""
+        assert checksum.dtype == torch.float64 and checksum.is_cuda
+        check(L.lib().rs_step_checksum(self.ws.handle, self.table.handle, _ptr(ids), ids.numel(), _ptr(grads),
+                                       _ptr(out), C.byref(self.params.c()), _ptr(checksum), _stream()),
+              "step_checksum")
+        return out
+
     def last_unique(self) -> torch.Tensor:
         """unique ids of the last forward, indexed like accumulate()'s rows."""
         n = C.c_uint64()

@@ -441,6 +441,41 @@ def test_pseudo_grads_jagged_equals_per_token(cuda, oracle):
     torch.testing.assert_close(c, b, rtol=0, atol=0)
 
 
+@pytest.mark.parametrize("dim", [64, 6])
+def test_step_checksum_fused(cuda, dim):
+    # rs_step_checksum == rs_step (bit-exact outputs and table), its checksum ==
+    # the f64 sum of the outputs, and it does not depend on timing (repeatable)
+    tabs = [_gpu_table(1 << 12, dim, opt="adagrad") for _ in range(2)]
+    steps = [P.SparseStep(t, 40000, P.AdagradParams(lr=0.05)) for t in tabs]
+    rng = np.random.default_rng(5)
+    cs = torch.zeros(1, dtype=torch.float64, device="cuda")
+    for k in range(5):
+        n = int(rng.integers(1, 40000))
+        ids = P.as_keys(rng.zipf(1.2, n).astype(np.uint64) % 3000)
+        g = torch.randn((n, dim), device="cuda")
+        o1, o2 = torch.empty((n, dim), device="cuda"), torch.empty((n, dim), device="cuda")
+        steps[0].step_checksum(ids, g, o1, cs)
+        steps[1].step(ids, g, o2)
+        torch.testing.assert_close(o1, o2, rtol=0, atol=0)
+        want = float(o2.double().sum())
+        assert float(cs[0]) == pytest.approx(want, rel=1e-12, abs=1e-9)
+    a, b = tabs[0].export(), tabs[1].export()
+    for fld in ("keys", "emb", "v", "step"):
+        np.testing.assert_array_equal(a[fld], b[fld], err_msg=fld)
+    # same inputs, same table state -> bit-identical checksum
+    t3 = [_gpu_table(1 << 12, dim, opt="adagrad") for _ in range(2)]
+    s3 = [P.SparseStep(t, 40000, P.AdagradParams(lr=0.05)) for t in t3]
+    ids = P.as_keys(rng.zipf(1.2, 30000).astype(np.uint64) % 3000)
+    g = torch.randn((30000, dim), device="cuda")
+    res = []
+    for st in s3:
+        o = torch.empty((30000, dim), device="cuda")
+        c = torch.zeros(1, dtype=torch.float64, device="cuda")
+        st.step_checksum(ids, g, o, c)
+        res.append(float(c[0]))
+    assert res[0] == res[1]
+
+
 def test_feeder_step_matches_device_step(cuda):
     # rs_feeder_step (host ids + lengths -> device grads -> rs_step -> checksum)
     # equals the same step driven from device buffers, checksum included
