@@ -87,7 +87,7 @@ int rs_feeder_destroy(rs_feeder* f) {
 float* rs_feeder_out(rs_feeder* f, int which) { return f ? f->out[which & 1] : nullptr; }
 
 static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const uint64_t* h_lengths,
-                        uint64_t n_seq, cudaStream_t s, int* set) {
+                        uint64_t n_seq, uint64_t first_sample_id, uint64_t step, cudaStream_t s, int* set) {
   if (n > f->max_tokens || n_seq > f->max_seqs)
     return fail(RS_ERR_CONFIG, "rs_feeder_step: batch exceeds the feeder's capacity");
   const int b = (int)(f->k & 1);
@@ -112,23 +112,41 @@ static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const u
   f->h_offs[b][n_seq] = run;
   f->n_chunks[b] = nc;
   if (run != n) return fail(RS_ERR_CONFIG, "rs_feeder_step: sum of lengths != number of ids");
-  static const int skip = getenv("RS_FEED_SKIP") ? atoi(getenv("RS_FEED_SKIP")) : 0;  // profiling only
-  if (!(skip & 1) || f->k < 2) {
-    RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
-    RS_CUDA(cudaMemcpyAsync(f->chunks[b], f->h_chunks[b], (size_t)nc * 12, cudaMemcpyHostToDevice, f->copy));
-  }
+  RS_CUDA(cudaMemcpyAsync(f->ids[b], h_ids, n * 8, cudaMemcpyHostToDevice, f->copy));
+  RS_CUDA(cudaMemcpyAsync(f->chunks[b], f->h_chunks[b], (size_t)nc * 12, cudaMemcpyHostToDevice, f->copy));
+  // the batch's gradients are data of the batch: generated on the copy stream
+  // too, so they overlap the previous step instead of preceding this one
+  int st = rs_pseudo_grads_chunks(f->chunks[b], nc, first_sample_id, step, f->dim, f->grads[b], f->copy);
+  if (st) return st;
   RS_CUDA(cudaEventRecord(f->landed[b], f->copy));
   RS_CUDA(cudaStreamWaitEvent(s, f->landed[b], 0));
   *set = b;
   return RS_OK;
 }
 
+// Where the step's checksum goes: straight into h_checksum when it is mapped
+// pinned memory (UVA: cudaMallocHost / pinned torch tensors) -- the kernel's
+// 8-byte store crosses PCIe, no copy on the stream -- else the device slot
+// of the buffer set, copied back by feeder_finish.
+static double* checksum_dst(rs_feeder* f, int b, double* h_checksum, bool* direct) {
+  *direct = false;
+  if (!h_checksum) return f->sum[b];
+  cudaPointerAttributes pa;
+  if (cudaPointerGetAttributes(&pa, h_checksum) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+      pa.devicePointer) {
+    *direct = true;
+    return static_cast<double*>(pa.devicePointer);
+  }
+  (void)cudaGetLastError();
+  return f->sum[b];
+}
+
 static int feeder_finish(rs_feeder* f, int b, uint64_t n, double* h_checksum, cudaStream_t s,
-                         bool summed) {
-  int st = summed ? RS_OK : rs_checksum(f->out[b], n * f->dim, f->sum[b], s);
+                         bool summed, double* dst, bool direct) {
+  int st = summed ? RS_OK : rs_checksum(f->out[b], n * f->dim, dst, s);
   if (st) return st;
   RS_CUDA(cudaEventRecord(f->in_free[b], s));
-  if (h_checksum) RS_CUDA(cudaMemcpyAsync(h_checksum, f->sum[b], 8, cudaMemcpyDeviceToHost, s));
+  if (h_checksum && !direct) RS_CUDA(cudaMemcpyAsync(h_checksum, dst, 8, cudaMemcpyDeviceToHost, s));
   f->k++;
   return RS_OK;
 }
@@ -142,12 +160,11 @@ int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* 
   if (t->desc.dim != f->dim) return fail(RS_ERR_CONFIG, "rs_feeder_step: table dim != feeder dim");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
-  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
-  static const int skip = getenv("RS_FEED_SKIP") ? atoi(getenv("RS_FEED_SKIP")) : 0;  // profiling only
-  if (!st && (!(skip & 2) || f->k < 2))
-    st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
-  if (!st) st = rs_step_checksum(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, f->sum[b], stream);
-  if (!st) st = feeder_finish(f, b, n, h_checksum, s, true);
+  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, first_sample_id, step, s, &b);
+  bool direct = false;
+  double* dst = checksum_dst(f, b, h_checksum, &direct);
+  if (!st) st = rs_step_checksum(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, dst, stream);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s, true, dst, direct);
   return st;
 }
 
@@ -159,10 +176,11 @@ int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_
   if (shard->desc.dim != f->dim) return fail(RS_ERR_CONFIG, "rs_feeder_dist_step: table dim != feeder dim");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
-  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, s, &b);
-  if (!st) st = rs_pseudo_grads_chunks(f->chunks[b], f->n_chunks[b], first_sample_id, step, f->dim, f->grads[b], stream);
+  int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, first_sample_id, step, s, &b);
   if (!st) st = rs_dist_step(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
-  if (!st) st = feeder_finish(f, b, n, h_checksum, s, false);
+  bool direct = false;
+  double* dst = checksum_dst(f, b, h_checksum, &direct);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s, false, dst, direct);
   return st;
 }
 
