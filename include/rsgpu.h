@@ -211,6 +211,11 @@ int rs_dist_backward(rs_comm* c, rs_table* shard, const float* d_grads, uint64_t
  * were before this step's update (distributed_lookup semantics). */
 int rs_dist_step(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t n,
                  const float* d_grads, float* d_out, const rs_optimizer_params* opt, void* stream);
+/* rs_dist_step plus this rank's emb_checksum (the f64 sum of every value
+ * written to d_out, computed inside the gather kernel) into *d_checksum. */
+int rs_dist_step_checksum(rs_comm* c, rs_table* shard, const uint64_t* d_ids, uint64_t n,
+                          const float* d_grads, float* d_out, const rs_optimizer_params* opt,
+                          double* d_checksum, void* stream);
 /* This rank's ExchangeTrace row (exchange_sim.hpp:37-59) for the last step:
  * ids_sent[W] (to each owner), embs_sent[W] (vectors this owner sent back to
  * each requester), lookups, ids_requested, ids_received.  Synchronizes. */

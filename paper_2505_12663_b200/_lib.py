@@ -127,6 +127,7 @@ _SIGS = {
     "rs_dist_forward": (C.c_int, [vp, vp, vp, u64, vp, vp]),
     "rs_dist_backward": (C.c_int, [vp, vp, vp, u64, C.POINTER(rs_optimizer_params), vp]),
     "rs_dist_step": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp]),
+    "rs_dist_step_checksum": (C.c_int, [vp, vp, vp, u64, vp, vp, C.POINTER(rs_optimizer_params), vp, vp]),
     "rs_comm_set_profiling": (C.c_int, [vp, C.c_int]),
     "rs_comm_barrier": (C.c_int, [vp, vp]),
     "rs_comm_phase_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int, C.POINTER(u64)]),

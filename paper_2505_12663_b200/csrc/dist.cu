@@ -279,6 +279,7 @@ struct DistGraph {
   uint64_t n;
   int mirror, ru, ou, par;
   const void* pbuf;
+  double* csum;
   unsigned char opt[256];
   cudaGraphExec_t exec;
   uint64_t last_use, launches;
@@ -322,6 +323,7 @@ struct rs_comm {
   // CUDA graphs of rs_dist_step
   bool use_graphs = true;
   bool graph_fork = true;
+  double* csum_dst = nullptr;  // rs_dist_step_checksum: sum of the gathered rows (fused in the gather)
   bool one_stream = false;          // RS_DIST_ONE_STREAM=1: both roles on the caller's stream
   cudaStream_t cap_stream = nullptr;
   cudaStream_t own_stream = nullptr;  // owner role runs here, concurrently with the requester's
@@ -485,6 +487,7 @@ static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSet
     rs_dist_opts o;
     o.gather_view = c->view;
     o.sync = wait_sync(c, c->own_sig_emb, kRequester);  // the owners' rows landed
+    o.csum = c->csum_dst;
     RS_TRY(step_tile(c->ws_req, t, ss.ru, n, d_out, nullptr, true, s, &o));
   }
   RS_TRY(prof_end(c, kPhGather, s));
@@ -533,6 +536,7 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
     rs_dist_opts o;
     o.gather_view = c->view;
     o.sync = wait_sync(c, c->own_sig_emb, kRequester);  // the owners' rows landed
+    o.csum = c->csum_dst;
     RS_TRY(step_tile(wr, t, ss.ru, n, d_out, d_grads, true, s, &o));
     rs_dist_opts f;
     f.peer_dst = c->d_peer_grad[ss.par];
@@ -872,7 +876,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     for (auto& g : c->graphs)
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
           g.mirror == mirror && g.ru == ss.ru && g.ou == ss.ou && g.par == ss.par &&
-          g.pbuf == c->ws_req->pbuf && std::memcmp(g.opt, ob, sizeof(ob)) == 0) {
+          g.pbuf == c->ws_req->pbuf && g.csum == c->csum_dst && std::memcmp(g.opt, ob, sizeof(ob)) == 0) {
         hit = &g;
         break;
       }
@@ -896,6 +900,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
       e.ou = ss.ou;
       e.par = ss.par;
       e.pbuf = c->ws_req->pbuf;
+      e.csum = c->csum_dst;
       std::memcpy(e.opt, ob, sizeof(ob));
       // hot-id finish as a forked graph branch (RS_DIST_GRAPH_FORK=0: linear)
       const bool f0 = c->ws_req->fork, f1 = c->ws_own->fork;
@@ -930,6 +935,21 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
   t->applies++;
   c->have_forward = false;
   return prof_step_done(c);
+}
+
+// rs_dist_step + the f64 sum of this rank's gathered rows (run_workload's
+// emb_checksum, workload.cpp:547-549) into d_checksum, summed inside the
+// gather kernel (D % 4 == 0; else a separate reduction over d_out).
+int rs_dist_step_checksum(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
+                          const float* d_grads, float* d_out, const rs_optimizer_params* opt,
+                          double* d_checksum, void* stream) {
+  if (!c || !t || !d_checksum) return fail(RS_ERR_CONFIG, "rs_dist_step_checksum: null argument");
+  const bool fused = n > 0 && t->desc.dim % 4 == 0;
+  c->csum_dst = fused ? d_checksum : nullptr;
+  const int st = rs_dist_step(c, t, d_ids, n, d_grads, d_out, opt, stream);
+  c->csum_dst = nullptr;
+  if (st || fused) return st;
+  return rs_checksum(d_out, n * t->desc.dim, d_checksum, stream);
 }
 
 // Device-side barrier over the group on `stream` (every rank must call it):

@@ -177,10 +177,10 @@ int rs_feeder_dist_step(rs_feeder* f, rs_comm* c, rs_table* shard, const uint64_
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   int b = 0;
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, first_sample_id, step, s, &b);
-  if (!st) st = rs_dist_step(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, stream);
   bool direct = false;
   double* dst = checksum_dst(f, b, h_checksum, &direct);
-  if (!st) st = feeder_finish(f, b, n, h_checksum, s, false, dst, direct);
+  if (!st) st = rs_dist_step_checksum(c, shard, f->ids[b], n, f->grads[b], f->out[b], opt, dst, stream);
+  if (!st) st = feeder_finish(f, b, n, h_checksum, s, true, dst, direct);
   return st;
 }
 

@@ -183,6 +183,7 @@ struct rs_dist_opts {
   float* const* peer_dst = nullptr;     // device [W] peer gradient receive bases
   const uint32_t* send_pos = nullptr;   // per unique id: owner * cap + position
   uint32_t cap = 0, rank = 0;
+  double* csum = nullptr;               // gather: f64 sum of the gathered rows (host token count only)
 };
 
 namespace rs {

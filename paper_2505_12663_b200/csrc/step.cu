@@ -1305,8 +1305,9 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.pbuf = ws->pbuf;
   a.ptile = ws->ptile;
   a.csr_pos = ws->csr_pos;
-  if (ws->csum_dst && !dopt && d_out && D % 4 == 0) {
-    a.csum_out = ws->csum_dst;
+  double* csum = dopt ? (dopt->d_n ? nullptr : dopt->csum) : ws->csum_dst;
+  if (csum && d_out && D % 4 == 0) {
+    a.csum_out = csum;
     a.csum_part = ws->csum_part;
     a.csum_ticket = ws->csum_ticket;
     ws->csum_done = true;

@@ -69,12 +69,21 @@ class ShardedTable:
         check(L.lib().rs_dist_backward(self._c, self.shard.handle, _ptr(g), g.shape[0], C.byref(params.c()),
                                        _stream()), "rs_dist_backward")
 
-    def step(self, ids, grads: torch.Tensor, params, out: torch.Tensor | None = None) -> torch.Tensor:
-        """forward + backward in one call (rs_dist_step); returns the gathered rows."""
+    def step(self, ids, grads: torch.Tensor, params, out: torch.Tensor | None = None,
+             checksum: torch.Tensor | None = None) -> torch.Tensor:
+        """forward + backward in one call (rs_dist_step); returns the gathered rows.
+        checksum (float64, device or pinned host): receives the f64 sum of the
+        rows (rs_dist_step_checksum, summed inside the gather kernel)."""
         k = as_keys(ids)
         g = grads.contiguous()
         if out is None:
             out = torch.empty((k.numel(), self.dim), dtype=torch.float32, device="cuda")
+        if checksum is not None:
+            assert checksum.dtype == torch.float64
+            check(L.lib().rs_dist_step_checksum(self._c, self.shard.handle, _ptr(k), k.numel(), _ptr(g), _ptr(out),
+                                                C.byref(params.c()), _ptr(checksum), _stream()),
+                  "rs_dist_step_checksum")
+            return out
         check(L.lib().rs_dist_step(self._c, self.shard.handle, _ptr(k), k.numel(), _ptr(g), _ptr(out),
                                    C.byref(params.c()), _stream()), "rs_dist_step")
         return out

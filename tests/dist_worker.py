@@ -76,6 +76,12 @@ def main():
         if step % 2 == 0:  # the split API (distributed_lookup, then accumulate/apply) ...
             out = st.forward(ids_t)
             st.backward(g_t, params)
+        elif step == 3:  # ... the fused step with the gather's checksum ...
+            cs = torch.full((1,), -1.0, dtype=torch.float64, device="cuda")
+            out = st.step(ids_t, g_t, params, checksum=cs)
+            assert float(cs[0]) == float(out.double().sum()) or \
+                abs(float(cs[0]) - float(out.double().sum())) <= 1e-9 * max(1.0, float(out.double().abs().sum())), \
+                (float(cs[0]), float(out.double().sum()))
         else:  # ... and the fused step must give identical results
             out = st.step(ids_t, g_t, params)
         tr = st.trace()
