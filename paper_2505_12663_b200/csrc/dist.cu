@@ -228,12 +228,32 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
     }
     if (row == kNoRow) continue;  // table error (reported through the counters)
     const float4* e = reinterpret_cast<const float4*>(d.emb) + (size_t)row * D4;
-    for (uint32_t k = 0; k < cnt; ++k) {
-      const uint32_t origin = __ldg(a.origins + (size_t)slot * c.world + k);
-      const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
-      float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
-                    ((size_t)c.rank * c.cap + jj) * D4;
-      for (uint32_t q = g; q < D4; q += kBucket) dst[q] = __ldg(e + q);
+    // the group's origins (<= world) in one parallel load, then each lane's
+    // part of the row (held in registers) goes to every requester
+    const uint32_t my_origin = g < cnt ? __ldg(a.origins + (size_t)slot * c.world + g) : 0u;
+    if (D4 <= 4 * kBucket) {
+      float4 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (g + j * kBucket < D4) v[j] = __ldg(e + g + j * kBucket);
+      for (uint32_t k = 0; k < cnt; ++k) {
+        const uint32_t origin = k < kBucket ? __shfl_sync(gmask, my_origin, k, kBucket)
+                                            : __ldg(a.origins + (size_t)slot * c.world + k);
+        const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
+        float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
+                      ((size_t)c.rank * c.cap + jj) * D4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (g + j * kBucket < D4) dst[g + j * kBucket] = v[j];
+      }
+    } else {
+      for (uint32_t k = 0; k < cnt; ++k) {
+        const uint32_t origin = __ldg(a.origins + (size_t)slot * c.world + k);
+        const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
+        float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
+                      ((size_t)c.rank * c.cap + jj) * D4;
+        for (uint32_t q = g; q < D4; q += kBucket) dst[q] = __ldg(e + q);
+      }
     }
   }
   __syncthreads();

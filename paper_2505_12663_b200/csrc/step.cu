@@ -759,11 +759,13 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     // issue the row loads early: independent of the gradient sum
     float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), vv = wv, mv = wv;
     size_t roff = 0;
+    uint32_t st0 = 0;  // the row's step counter, also loaded early
     if (!sums && row != kNoRow) {
       roff = (size_t)row * d.dim + 4 * gl;
       wv = *reinterpret_cast<const float4*>(d.emb + roff);
       vv = *reinterpret_cast<const float4*>(d.s2 + roff);
       if (d.s1) mv = *reinterpret_cast<const float4*>(d.s1 + roff);
+      if (gl == 0) st0 = d.step[row];
     }
     uint32_t p[PPT], r[PPT];
 #pragma unroll
@@ -829,7 +831,7 @@ __global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) 
     if (row == kNoRow) continue;
     uint32_t st = 0;
     if (gl == 0) {
-      st = d.step[row] + 1;
+      st = st0 + 1;
       d.step[row] = st;
     }
     st = __shfl_sync(gmask, st, 0, G);
@@ -1440,7 +1442,8 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   // programmatic edges only where the same-stream predecessor is our tile kernel
   const bool pdl_hot = ws->pdl_now && split_fork;
   bool launched = G > 0 && dopt && dopt->no_hot;  // owner side: no hot ids possible
-  const unsigned eg = G > 0 ? grid_for(n * (uint64_t)G, 256, 148 * 16) : 0;
+  static const unsigned csr_cap = getenv("RS_CSR_GRID") ? (unsigned)atoi(getenv("RS_CSR_GRID")) : 148u * 16u;
+  const unsigned eg = G > 0 ? grid_for(n * (uint64_t)G, 256, csr_cap) : 0;
   if (dopt) {  // the blocks of both finish kernels arrive on one counter
     a.sync = dopt->sync;
     a.sync.sig_total = (launched ? 0u : grid) + eg;
