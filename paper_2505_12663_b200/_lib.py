@@ -12,7 +12,8 @@ import subprocess
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "librsgpu.so")
+# RS_LIB_PATH: load another build (kernel-variant experiments)
+LIB_PATH = os.environ.get("RS_LIB_PATH") or os.path.join(HERE, "_lib", "librsgpu.so")
 CSRC = os.path.join(HERE, "csrc")
 
 RS_OK, RS_ERR_CONFIG, RS_ERR_INVARIANT, RS_ERR_IO, RS_ERR_CUDA, RS_ERR_CAPACITY, RS_ERR_RANGE = range(7)

@@ -728,7 +728,10 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 // group (shuffles), written sorted to smem, and the gradient rows are summed
 // in position order (the reference's accumulate order) -> bit-exact sums.
 template <int G>
-__global__ void __launch_bounds__(256, 4) k_finish_csr(FinishArgs a, OptArgs o) {
+#ifndef RS_CSR_MINB
+#define RS_CSR_MINB 4
+#endif
+__global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, OptArgs o) {
   pdl_wait();
   constexpr int PPT = (int)(kCsrMax / G);  // positions held per thread
   __shared__ uint32_t order_s[(256 / G) * kCsrMax];
