@@ -356,8 +356,11 @@ struct TileArgs {
 // per SM); kTileHot: hot-id tile partials only (runs beside the CSR finish)
 enum : int { kTileFull = 0, kTileGatherCsr = 1, kTileHot = 2 };
 
+#ifndef RS_KC1_MINB
+#define RS_KC1_MINB 4
+#endif
 template <int VEC, int CH, int LPR, int MODE>
-__global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? 4 : 3) k_ftile(TileArgs a) {
+__global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3) k_ftile(TileArgs a) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ __align__(128) unsigned char smem[];
@@ -729,7 +732,7 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 // in position order (the reference's accumulate order) -> bit-exact sums.
 template <int G>
 #ifndef RS_CSR_MINB
-#define RS_CSR_MINB 4
+#define RS_CSR_MINB 5  // measured: 5 (48 regs) beats 4 / 6 / 8 at config 1
 #endif
 __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, OptArgs o) {
   pdl_wait();
@@ -875,8 +878,11 @@ __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, O
 //                   sorted and the gradient rows summed in position order --
 //                   exactly the reference's accumulate order
 //                   (sparse_update.cpp:49-54), so these sums are bit-exact
+#ifndef RS_FIN_MINB
+#define RS_FIN_MINB 3
+#endif
 template <int VEC, int CH>
-__global__ void __launch_bounds__(256, 3) k_finish(FinishArgs a, OptArgs o, uint32_t hot_blocks) {
+__global__ void __launch_bounds__(256, RS_FIN_MINB) k_finish(FinishArgs a, OptArgs o, uint32_t hot_blocks) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem2[];
   const uint32_t NW = blockDim.x >> 5;
