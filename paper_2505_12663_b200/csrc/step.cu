@@ -232,6 +232,11 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       nt = a.use.sntile[slot];
       cnt = a.use.sfirstx[slot];
     }
+    // the probe depends only on the key: issue it before the metadata work
+    // so its slot loads overlap the scratch loads above
+    uint32_t row = kNoRow;
+    if (a.do_table && active)
+      row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins, &s_reuse);
     const bool hot = cnt > kCsrMax;
     // segments: CSR of the id's token positions (exact-order path) or its
     // per-tile partial sums (hot path); warp-aggregated allocation
@@ -277,8 +282,6 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       }
     }
     if (!a.do_table || !active) continue;
-    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0,
-                                              &s_ins, &s_reuse);
     if (g == 0) {
       a.urow[i] = row;
       a.urow64[i] = row == kNoRow ? -1 : (int64_t)row;
@@ -434,6 +437,12 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
     u = __ldcg(a.use.suidx + s);
     r = __ldcg(a.use.srow + s);
   }
+  // the id's CSR metadata, issued with the gather's row loads
+  uint32_t nt = 0, upoff = 0;
+  if (red && valid) {
+    nt = __ldg(a.u_ntile + u);
+    if (MODE != kTileHot) upoff = __ldg(a.u_poff + u);
+  }
 
   // ---- gather: warp w copies the rows of tokens [32w, 32w + 32)
   if (MODE != kTileHot && a.out) {
@@ -507,8 +516,6 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
 
   // ---- ids with <= kCsrMax occurrences: place the token position into the
   // id's CSR segment (warp-aggregated cursor; the finish kernel sorts it)
-  uint32_t nt = 0;
-  if (valid) nt = __ldg(a.u_ntile + u);
   const bool csr_tok = valid && nt == 0;
   if (MODE != kTileHot) {
     const uint32_t key = csr_tok ? u : (0xFFFF0000u | lane);
@@ -518,7 +525,7 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
     if (csr_tok && lane == leader) base = atomicAdd(a.u_ticket + u, (uint32_t)__popc(mm0));
     base = __shfl_sync(kFull, base, leader);
     if (csr_tok)
-      a.csr_pos[__ldg(a.u_poff + u) + base + __popc(mm0 & lanemask_lt())] =
+      a.csr_pos[upoff + base + __popc(mm0 & lanemask_lt())] =
           a.pos_map ? __ldg(a.pos_map + t0 + tid) : t0 + tid;
   }
   const bool hotv = valid && nt > 0;
@@ -751,17 +758,19 @@ __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, O
   dist_wait(a.sync);
   const uint32_t nu = *a.n_unique;
   const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grads);
+  const bool sums = a.sums_out || a.peer_dst;
   for (uint32_t uu = gid; uu < nu; uu += ngroups) {
-    if (__ldg(a.u_ntile + uu) != 0) continue;  // hot path (group-uniform)
+    // the id's metadata in one round trip (the hot test must not serialize it)
+    const uint32_t nt = __ldg(a.u_ntile + uu);
     const uint32_t c = __ldg(a.u_cnt + uu), off = __ldg(a.u_poff + uu);
+    const uint32_t row = sums ? 0u : __ldg(a.urow + uu);
+    if (nt != 0) continue;  // hot path (group-uniform)
 #ifdef RS_BOUNDS
     if (c > kCsrMax || off + c > a.dbg_ncsr) {
       if (gl == 0) printf("k_finish_csr: uu %u c %u off %u ncsr %llu\n", uu, c, off, (unsigned long long)a.dbg_ncsr);
       continue;
     }
 #endif
-    const bool sums = a.sums_out || a.peer_dst;
-    const uint32_t row = sums ? 0u : __ldg(a.urow + uu);
     // issue the row loads early: independent of the gradient sum
     float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), vv = wv, mv = wv;
     size_t roff = 0;
