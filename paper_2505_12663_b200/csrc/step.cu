@@ -214,12 +214,14 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
   const unsigned gbase = lane & ~(kBucket - 1);
   const unsigned gmask = 0xFFu << gbase;
   __shared__ unsigned long long s_ins, s_reuse;
+  __shared__ uint32_t s_wc[8], s_wp[8], s_bc, s_bp;
   if (threadIdx.x == 0) {
     s_ins = 0;
     s_reuse = 0;
   }
   __syncthreads();
-  // every warp runs the same trip count (shuffles below are warp-wide)
+  // every warp runs the same trip count (shuffles below are warp-wide, the
+  // allocation block-wide)
   const uint32_t per_iter = gridDim.x * kGroups;
   for (uint32_t base = 0; base < nu; base += per_iter) {
     const uint32_t i = base + blockIdx.x * kGroups + (threadIdx.x >> 3);
@@ -252,12 +254,30 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
         ip += yp;
       }
     }
+    // block-aggregated allocation: one atomic per block and counter (the
+    // counters are single addresses every block hits)
     const uint32_t tc = __shfl_sync(kFull, ic, 31), tp = __shfl_sync(kFull, ip, 31);
-    uint32_t bc = 0, bp = 0;
-    if (lane == 0 && tc) bc = atomicAdd(&a.ctr[kCtrCsrAlloc], tc);
-    if (lane == 0 && tp) bp = atomicAdd(&a.ctr[kCtrPartAlloc], tp);
-    bc = __shfl_sync(kFull, bc, 0);
-    bp = __shfl_sync(kFull, bp, 0);
+    const uint32_t warp = threadIdx.x >> 5;
+    if (lane == 0) {
+      s_wc[warp] = tc;
+      s_wp[warp] = tp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t rc = 0, rp = 0;
+      for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+        const uint32_t xc = s_wc[w], xp = s_wp[w];
+        s_wc[w] = rc;
+        s_wp[w] = rp;
+        rc += xc;
+        rp += xp;
+      }
+      s_bc = rc ? atomicAdd(&a.ctr[kCtrCsrAlloc], rc) : 0u;
+      s_bp = rp ? atomicAdd(&a.ctr[kCtrPartAlloc], rp) : 0u;
+    }
+    __syncthreads();
+    const uint32_t bc = s_bc + s_wc[warp], bp = s_bp + s_wp[warp];
+    __syncthreads();  // s_w* / s_b* are rewritten by the next trip
     if (active && g == 0) {
       a.u_cnt[i] = cnt;
       a.u_ntile[i] = hot ? nt : 0u;  // 0 marks the CSR path
