@@ -215,10 +215,12 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
   const unsigned gmask = 0xFFu << gbase;
   __shared__ unsigned long long s_ins, s_reuse;
   __shared__ uint32_t s_wc[8], s_wp[8], s_bc, s_bp;
+  __shared__ uint32_t s_ocnt[64], s_obase[64];  // sharded send: per-owner block counts (world <= 64)
   if (threadIdx.x == 0) {
     s_ins = 0;
     s_reuse = 0;
   }
+  for (uint32_t r = threadIdx.x; r < 64; r += blockDim.x) s_ocnt[r] = 0;
   __syncthreads();
   // every warp runs the same trip count (shuffles below are warp-wide, the
   // allocation block-wide)
@@ -286,15 +288,21 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       if (hot) a.hot_list[atomicAdd(&a.ctr[kCtrNHot], 1u)] = i;
     }
     if (a.send.peers) {  // owner partition: one lane per group holds the id
+      // positions: block-local counters per owner, then one global atomic per
+      // (block, owner) -- the per-owner counters are hot single addresses
       const bool mine = active && g == 0;
       const uint32_t o = mine ? (uint32_t)(hash64(key) % a.send.world) : 0u;
-      const unsigned mm = __match_any_sync(kFull, mine ? o : (0xFFFF0000u | lane));
-      const uint32_t leader = __ffs(mm) - 1;
-      uint32_t j0 = 0;
-      if (mine && lane == leader) j0 = atomicAdd(&a.send.send_cnt[o], (uint32_t)__popc(mm));
-      j0 = __shfl_sync(kFull, j0, leader);
+      uint32_t jl = 0;
+      if (mine) jl = atomicAdd(&s_ocnt[o], 1u);
+      __syncthreads();
+      for (uint32_t r = threadIdx.x; r < a.send.world; r += blockDim.x) {
+        const uint32_t c = s_ocnt[r];
+        s_obase[r] = c ? atomicAdd(&a.send.send_cnt[r], c) : 0u;
+        s_ocnt[r] = 0;
+      }
+      __syncthreads();
       if (mine) {
-        const uint32_t j = j0 + __popc(mm & lanemask_lt());
+        const uint32_t j = s_obase[o] + jl;
         reinterpret_cast<uint64_t*>(a.send.peers[o] + a.send.off_ids)[(size_t)a.send.rank * a.send.cap + j] = key;
         const uint32_t sp = o * a.send.cap + j;
         a.send.send_pos[i] = sp;
