@@ -163,11 +163,23 @@ __global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t
     const uint32_t k = atomicAdd(&S.sntile[gs], 1u);  // origins so far (<= W)
     origins[gs * c.world + k] = src * c.cap + j;
   }
-  // unique numbering of the fresh ids: one atomic per warp
+  // unique numbering of the fresh ids: one atomic per block
+  __shared__ uint32_t s_w[32], s_base;
   const unsigned fm = __ballot_sync(0xFFFFFFFFu, fresh);
-  uint32_t base = 0;
-  if (lane_id() == 0 && fm) base = atomicAdd(S.cnt, (uint32_t)__popc(fm));
-  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  const uint32_t warp = threadIdx.x >> 5;
+  if (lane_id() == 0) s_w[warp] = __popc(fm);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+      const uint32_t x = s_w[w];
+      s_w[w] = run;
+      run += x;
+    }
+    s_base = run ? atomicAdd(S.cnt, run) : 0u;
+  }
+  __syncthreads();
+  const uint32_t base = s_base + s_w[warp];
   if (fresh) {
     const uint32_t u = base + __popc(fm & lanemask_lt());
     S.u_slot[u] = (uint32_t)gs;
