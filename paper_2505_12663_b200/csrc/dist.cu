@@ -535,8 +535,10 @@ static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhReqReduce, s));
   if (n) {
-    rs_dist_opts one_pass;  // (a dopt: the one-pass KC -- the split measured slower here)
-    RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, &one_pass));
+    // one-pass KC (the split KC measured slower here; RS_DIST_SPLIT_KC=1 for experiments)
+    static const bool split = getenv("RS_DIST_SPLIT_KC") && getenv("RS_DIST_SPLIT_KC")[0] == '1';
+    rs_dist_opts one_pass;
+    RS_TRY(step_tile(wr, t, ss.ru, n, nullptr, d_grads, false, s, split ? nullptr : &one_pass));
     rs_dist_opts o;
     o.peer_dst = c->d_peer_grad[ss.par];
     o.send_pos = c->send_pos;

@@ -43,6 +43,17 @@ __device__ __forceinline__ uint64_t scratch_insert(const SetDev& S, uint64_t id,
   }
   uint64_t gs = h & S.smask;
   for (;;) {
+    // plain L2 read first: ids repeated across tiles find their slot without
+    // an atomic (hot ids would otherwise serialize every tile on one address)
+    const unsigned long long cur = __ldcg(&S.skey[gs]);
+    if (cur == id) {
+      *fresh = false;
+      return gs;
+    }
+    if (cur != kEmptyKey) {
+      gs = (gs + 1) & S.smask;
+      continue;
+    }
     const unsigned long long prev = atomicCAS(&S.skey[gs], kEmptyKey, (unsigned long long)id);
     if (prev == kEmptyKey) {
       *fresh = true;
