@@ -765,11 +765,12 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 // chunk of the row.  The id's <= kCsrMax token positions are ranked within the
 // group (shuffles), written sorted to smem, and the gradient rows are summed
 // in position order (the reference's accumulate order) -> bit-exact sums.
-template <int G>
+template <int G, int NV>
 #ifndef RS_CSR_MINB
-#define RS_CSR_MINB 5  // measured: 5 (48 regs) beats 4 / 6 / 8 at config 1
+#define RS_CSR_MINB 5  // measured: 5 (48 regs) beats 4 / 6 / 8 at config 1 (G = 16, NV = 1)
 #endif
-__global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, OptArgs o) {
+__global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(FinishArgs a, OptArgs o) {
+  // G lanes per id, each owning NV float4 chunks of the row (chunk gl + j*G)
   pdl_wait();
   constexpr int PPT = (int)(kCsrMax / G);  // positions held per thread
   __shared__ uint32_t order_s[(256 / G) * kCsrMax];
@@ -800,16 +801,22 @@ __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, O
     }
 #endif
     // issue the row loads early: independent of the gradient sum
-    float4 wv = make_float4(0.f, 0.f, 0.f, 0.f), vv = wv, mv = wv;
-    size_t roff = 0;
+    float4 wv[NV], vv[NV], mv[NV];
+    float4* rw = reinterpret_cast<float4*>(d.emb);
+    float4* rv = reinterpret_cast<float4*>(d.s2);
+    float4* rm = reinterpret_cast<float4*>(d.s1);
+    const size_t rbase = (size_t)row * D4 + gl;
     uint32_t st0 = 0;  // the row's step counter, also loaded early
-    if (!sums && row != kNoRow) {
-      roff = (size_t)row * d.dim + 4 * gl;
-      wv = *reinterpret_cast<const float4*>(d.emb + roff);
-      vv = *reinterpret_cast<const float4*>(d.s2 + roff);
-      if (d.s1) mv = *reinterpret_cast<const float4*>(d.s1 + roff);
-      if (gl == 0) st0 = d.step[row];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      wv[j] = vv[j] = mv[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!sums && row != kNoRow) {
+        wv[j] = rw[rbase + j * G];
+        vv[j] = rv[rbase + j * G];
+        if (rm) mv[j] = rm[rbase + j * G];
+      }
     }
+    if (!sums && row != kNoRow && gl == 0) st0 = d.step[row];
     uint32_t p[PPT], r[PPT];
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -844,31 +851,43 @@ __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, O
       }
     }
 #endif
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    // gradient rows summed in token order (the reference's accumulate order)
+    float4 acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int B = NV == 1 ? 4 : 2;  // rows in flight per step of the loop
     uint32_t k = 0;
-    for (; k + 4 <= c; k += 4) {
-      float4 x[4];
+    for (; k + B <= c; k += B) {
+      float4 x[B][NV];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) x[q] = g4[(size_t)order[k + q] * D4 + gl];
+      for (int q = 0; q < B; ++q)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc.x += x[q].x;
-        acc.y += x[q].y;
-        acc.z += x[q].z;
-        acc.w += x[q].w;
-      }
+        for (int j = 0; j < NV; ++j) x[q][j] = g4[(size_t)order[k + q] * D4 + gl + j * G];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          acc[j].x += x[q][j].x;
+          acc[j].y += x[q][j].y;
+          acc[j].z += x[q][j].z;
+          acc[j].w += x[q][j].w;
+        }
     }
     for (; k < c; ++k) {
-      const float4 x = g4[(size_t)order[k] * D4 + gl];
-      acc.x += x.x;
-      acc.y += x.y;
-      acc.z += x.z;
-      acc.w += x.w;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const float4 x = g4[(size_t)order[k] * D4 + gl + j * G];
+        acc[j].x += x.x;
+        acc[j].y += x.y;
+        acc[j].z += x.z;
+        acc[j].w += x.w;
+      }
     }
     __syncwarp(gmask);
     if (gl == 0) a.u_ticket[uu] = 0;
     if (float* dst = sum_dst(a, uu, d.dim)) {
-      reinterpret_cast<float4*>(dst)[gl] = acc;
+#pragma unroll
+      for (int j = 0; j < NV; ++j) reinterpret_cast<float4*>(dst)[gl + j * G] = acc[j];
       continue;
     }
     if (row == kNoRow) continue;
@@ -888,20 +907,23 @@ __global__ void __launch_bounds__(256, RS_CSR_MINB) k_finish_csr(FinishArgs a, O
         bc2 = 1.0 - pow(o.b2, (double)st);
       }
     }
-    float* wp = reinterpret_cast<float*>(&wv);
-    float* vp = reinterpret_cast<float*>(&vv);
-    float* mp = reinterpret_cast<float*>(&mv);
-    const float* gp = reinterpret_cast<const float*>(&acc);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (o.kind == RS_OPT_ADAM)
-        adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
-      else
-        adagrad_elem(wp[e], vp[e], gp[e], o);
+    for (int j = 0; j < NV; ++j) {
+      float* wp = reinterpret_cast<float*>(&wv[j]);
+      float* vp = reinterpret_cast<float*>(&vv[j]);
+      float* mp = reinterpret_cast<float*>(&mv[j]);
+      const float* gp = reinterpret_cast<const float*>(&acc[j]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (o.kind == RS_OPT_ADAM)
+          adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
+        else
+          adagrad_elem(wp[e], vp[e], gp[e], o);
+      }
+      rw[rbase + j * G] = wv[j];
+      rv[rbase + j * G] = vv[j];
+      if (rm) rm[rbase + j * G] = mv[j];
     }
-    *reinterpret_cast<float4*>(d.emb + roff) = wv;
-    *reinterpret_cast<float4*>(d.s2 + roff) = vv;
-    if (d.s1) *reinterpret_cast<float4*>(d.s1 + roff) = mv;
   }
   dist_arrive(a.sync);
 }
@@ -1463,6 +1485,12 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
                                        (size_t)2 * a.bw * 4 + 16 + (size_t)8 * D * 4 + 16);
   const uint32_t g4 = D % 4 == 0 ? D / 4 : 0;
   const int G = (g4 >= 2 && g4 <= 32 && !(g4 & (g4 - 1))) ? (int)g4 : 0;
+  // CSR finish shape: G lanes x 1 float4 per id; RS_CSR_NV=2 runs G/2 lanes
+  // x 2 float4 (twice the ids in flight per SM -- measured ~1 % slower at
+  // config 1, kept for other shapes' experiments)
+  static const int nv_env = getenv("RS_CSR_NV") ? atoi(getenv("RS_CSR_NV")) : 1;
+  const int NVc = (nv_env == 2 && G >= 4) ? 2 : 1;
+  const int Gc = G / NVc;
   // G > 0: CSR ids on s, hot ids concurrently on the forked aux stream
   const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
   cudaStream_t hs = s;
@@ -1489,7 +1517,7 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   const bool pdl_hot = ws->pdl_now && split_fork;
   bool launched = G > 0 && dopt && dopt->no_hot;  // owner side: no hot ids possible
   static const unsigned csr_cap = getenv("RS_CSR_GRID") ? (unsigned)atoi(getenv("RS_CSR_GRID")) : 148u * 16u;
-  const unsigned eg = G > 0 ? grid_for(n * (uint64_t)G, 256, csr_cap) : 0;
+  const unsigned eg = G > 0 ? grid_for(n * (uint64_t)Gc, 256, csr_cap) : 0;
   if (dopt) {  // the blocks of both finish kernels arrive on one counter
     a.sync = dopt->sync;
     a.sync.sig_total = (launched ? 0u : grid) + eg;
@@ -1508,13 +1536,14 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
 #undef RS_FIN
   if (!launched) return fail(RS_ERR_CONFIG, "embedding_dim " + std::to_string(D) + " unsupported");
   if (G > 0) {
-#define RS_CSR(GG)                                      \
-  if (G == GG) {                                        \
-    RS_CUDA(launch_pdl(ws->pdl_now, k_finish_csr<GG>,   \
-                       eg, 256, 0, s, a, o));           \
-    RS_LAUNCH_CHECK("k_finish_csr");                    \
+#define RS_CSR(GG, NN)                                      \
+  if (Gc == GG && NVc == NN) {                              \
+    RS_CUDA(launch_pdl(ws->pdl_now, k_finish_csr<GG, NN>,   \
+                       eg, 256, 0, s, a, o));               \
+    RS_LAUNCH_CHECK("k_finish_csr");                        \
   }
-    RS_CSR(32) RS_CSR(16) RS_CSR(8) RS_CSR(4) RS_CSR(2)
+    RS_CSR(32, 1) RS_CSR(16, 1) RS_CSR(8, 1) RS_CSR(4, 1) RS_CSR(2, 1)
+    RS_CSR(16, 2) RS_CSR(8, 2) RS_CSR(4, 2) RS_CSR(2, 2)
 #undef RS_CSR
     if (fork) {
       RS_CUDA(cudaEventRecord(ws->ev_join, ws->aux_stream));
