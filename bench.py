@@ -217,14 +217,16 @@ def run_ours(args, cfg):
         "finish_update": 16 * D * U_avg + 8 * U_avg,
     }
     dom = max(phases, key=lambda k: phases[k])
-    traffic = None
+    traffic = traffic_ctx = None
     try:  # dram bytes of the same kernel from the committed ncu --set full capture
         import glob
         tf = sorted(glob.glob(os.path.join(ROOT, "profiles", "traffic_r*.json")))[-1]
         with open(tf) as f:
-            traffic = json.load(f).get(dom)
+            tj = json.load(f)
+        traffic = tj.get(dom)
+        traffic_ctx = tj.get("in_context", {}).get(dom)  # --cache-control none: the step's real L2 state
     except Exception:
-        traffic = None
+        traffic = traffic_ctx = None
     ach = algo[dom] / (phases[dom] / 1e3) / 1e9 if phases.get(dom) else None
     step_bytes = 12 * T_avg + 24 * U_avg + 8 * D * T_avg + 20 * D * U_avg
     res = {
@@ -253,7 +255,7 @@ def run_ours(args, cfg):
         "kernel_gbs": {k: (algo[k] / (phases[k] / 1e3) / 1e9 if phases[k] else None) for k in algo},
         "roofline": {"bound": "hbm", "kernel": dom,
                      "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if ach else None,
-                     "traffic": traffic, "peak_source": how,
+                     "traffic": traffic, "traffic_in_context": traffic_ctx, "peak_source": how,
                      "algorithmic_bytes_per_launch": algo[dom]},
         "e2e": e2e,
         "gpu_launches": int(launches),
