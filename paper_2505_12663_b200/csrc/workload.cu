@@ -291,32 +291,44 @@ int rs_pseudo_grads_jagged(const uint64_t* d_lengths, uint64_t n_seq, uint64_t f
   if (n_tokens == 0 || n_seq == 0) return RS_OK;
   if (dim % 4) return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: dim % 4 != 0");
   cudaStream_t s = (cudaStream_t)stream;
-  // scratch kept across calls (one caller stream at a time; grows only)
-  static uint64_t* offs = nullptr;
-  static float* rows = nullptr;
-  static uint64_t cap_seq = 0, cap_rows = 0, cap_tok = 0;
-  static uint32_t* sample_of = nullptr;
-  if (cap_tok < n_tokens) {
-    if (sample_of) RS_CUDA(cudaFree(sample_of));
-    RS_CUDA(cudaMalloc(&sample_of, n_tokens * 4));
-    cap_tok = n_tokens;
+  if (n_tokens * (uint64_t)dim >= (1ull << 32) || n_seq >= (1ull << 32))
+    return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: batch too large");
+  // per-device scratch kept across calls (one caller stream per device at a
+  // time; grows only)
+  struct Scratch {
+    uint64_t* offs = nullptr;
+    float* rows = nullptr;
+    uint32_t* sample_of = nullptr;
+    uint64_t cap_seq = 0, cap_rows = 0, cap_tok = 0;
+  };
+  constexpr int kMaxDev = 64;
+  static Scratch scr[kMaxDev];
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: device ordinal out of range");
+  Scratch& x = scr[dev];
+  if (x.cap_tok < n_tokens) {
+    if (x.sample_of) RS_CUDA(cudaFree(x.sample_of));
+    RS_CUDA(cudaMalloc(&x.sample_of, n_tokens * 4));
+    x.cap_tok = n_tokens;
   }
-  if (cap_seq < n_seq + 1) {
-    if (offs) RS_CUDA(cudaFree(offs));
-    RS_CUDA(cudaMalloc(&offs, (n_seq + 1) * 8));
-    cap_seq = n_seq + 1;
+  if (x.cap_seq < n_seq + 1) {
+    if (x.offs) RS_CUDA(cudaFree(x.offs));
+    RS_CUDA(cudaMalloc(&x.offs, (n_seq + 1) * 8));
+    x.cap_seq = n_seq + 1;
   }
-  if (cap_rows < n_seq * dim) {
-    if (rows) RS_CUDA(cudaFree(rows));
-    RS_CUDA(cudaMalloc(&rows, n_seq * dim * 4));
-    cap_rows = n_seq * dim;
+  if (x.cap_rows < n_seq * dim) {
+    if (x.rows) RS_CUDA(cudaFree(x.rows));
+    RS_CUDA(cudaMalloc(&x.rows, n_seq * dim * 4));
+    x.cap_rows = n_seq * dim;
   }
+  uint64_t* offs = x.offs;
+  float* rows = x.rows;
+  uint32_t* sample_of = x.sample_of;
   k_seq_offsets<<<1, 1024, 0, s>>>(d_lengths, n_seq, offs);
   RS_LAUNCH_CHECK("k_seq_offsets");
   k_sample_rows<<<grid_for(n_seq * dim, 256, 148 * 8), 256, 0, s>>>(n_seq, first_sample_id, step, dim, rows);
   RS_LAUNCH_CHECK("k_sample_rows");
-  if (n_tokens * (uint64_t)dim >= (1ull << 32) || n_seq >= (1ull << 32))
-    return fail(RS_ERR_CONFIG, "rs_pseudo_grads_jagged: batch too large");
   k_fill_sample<<<(unsigned)n_seq, 256, 0, s>>>(offs, sample_of);
   RS_LAUNCH_CHECK("k_fill_sample");
   k_broadcast_rows<<<grid_for(n_tokens * dim / 16, 256, 148 * 8), 256, 0, s>>>(sample_of, rows, dim,
@@ -357,14 +369,19 @@ int rs_checksum(const float* d_x, uint64_t n, double* d_out, void* stream) {
   using namespace rs;
   cudaStream_t s = (cudaStream_t)stream;
   const unsigned nb = 148 * 4;
-  static double* part = nullptr;  // kept across calls (one stream at a time)
-  static unsigned int* done = nullptr;
-  if (!part) {
-    RS_CUDA(cudaMalloc(&part, nb * 8));
-    RS_CUDA(cudaMalloc(&done, 4));
-    RS_CUDA(cudaMemset(done, 0, 4));
+  // per-device partials, kept across calls (one stream per device at a time)
+  constexpr int kMaxDev = 64;
+  static double* part[kMaxDev] = {};
+  static unsigned int* done[kMaxDev] = {};
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDev) return fail(RS_ERR_CONFIG, "rs_checksum: device ordinal out of range");
+  if (!part[dev]) {
+    RS_CUDA(cudaMalloc(&part[dev], nb * 8));
+    RS_CUDA(cudaMalloc(&done[dev], 4));
+    RS_CUDA(cudaMemset(done[dev], 0, 4));
   }
-  k_sum_partials<<<nb, 256, 0, s>>>(d_x, n, part, done, d_out);
+  k_sum_partials<<<nb, 256, 0, s>>>(d_x, n, part[dev], done[dev], d_out);
   RS_LAUNCH_CHECK("k_sum_partials");
   return RS_OK;
 }
