@@ -441,17 +441,21 @@ def test_pseudo_grads_jagged_equals_per_token(cuda, oracle):
     torch.testing.assert_close(c, b, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("dim", [64, 6])
-def test_step_checksum_fused(cuda, dim):
+@pytest.mark.parametrize("dim,bound", [(64, 0), (6, 0), (64, 2000)])
+def test_step_checksum_fused(cuda, dim, bound):
     # rs_step_checksum == rs_step (bit-exact outputs and table), its checksum ==
-    # the f64 sum of the outputs, and it does not depend on timing (repeatable)
-    tabs = [_gpu_table(1 << 12, dim, opt="adagrad") for _ in range(2)]
+    # the f64 sum of the outputs, and it does not depend on timing (repeatable);
+    # bound > 0: a bounded table (device eviction inside the step)
+    kw = {"max_keys": bound} if bound else {}
+    tabs = [_gpu_table(1 << 12, dim, opt="adagrad", **kw) for _ in range(2)]
     steps = [P.SparseStep(t, 40000, P.AdagradParams(lr=0.05)) for t in tabs]
     rng = np.random.default_rng(5)
     cs = torch.zeros(1, dtype=torch.float64, device="cuda")
     for k in range(5):
         n = int(rng.integers(1, 40000))
-        ids = P.as_keys(rng.zipf(1.2, n).astype(np.uint64) % 3000)
+        raw = rng.zipf(1.2, n).astype(np.uint64)
+        # bounded: <= 1500 distinct per batch, a sliding window -> evictions
+        ids = P.as_keys(raw % 1500 + np.uint64(700 * k) if bound else raw % 3000)
         g = torch.randn((n, dim), device="cuda")
         o1, o2 = torch.empty((n, dim), device="cuda"), torch.empty((n, dim), device="cuda")
         steps[0].step_checksum(ids, g, o1, cs)
@@ -463,9 +467,9 @@ def test_step_checksum_fused(cuda, dim):
     for fld in ("keys", "emb", "v", "step"):
         np.testing.assert_array_equal(a[fld], b[fld], err_msg=fld)
     # same inputs, same table state -> bit-identical checksum
-    t3 = [_gpu_table(1 << 12, dim, opt="adagrad") for _ in range(2)]
+    t3 = [_gpu_table(1 << 12, dim, opt="adagrad", **kw) for _ in range(2)]
     s3 = [P.SparseStep(t, 40000, P.AdagradParams(lr=0.05)) for t in t3]
-    ids = P.as_keys(rng.zipf(1.2, 30000).astype(np.uint64) % 3000)
+    ids = P.as_keys(rng.zipf(1.2, 30000).astype(np.uint64) % 1500)
     g = torch.randn((30000, dim), device="cuda")
     res = []
     for st in s3:
