@@ -1380,7 +1380,6 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     a.csum_out = csum;
     a.csum_part = ws->csum_part;
     a.csum_ticket = ws->csum_ticket;
-    ws->csum_done = true;
   }
   if (d_out && D % 4 != 0) {
     k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, a.use, t->dev,
@@ -1830,6 +1829,11 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
                         const float* d_grads, float* d_out, const OptArgs& o, int use,
                         int mirror, cudaStream_t s, cudaEvent_t* ev) {
   int st;
+  struct PdlOff {  // programmatic edges only inside this call, also on error returns
+    rs_workspace* w;
+    ~PdlOff() { w->pdl_now = false; }
+  } pdl_off{ws};
+  ws->pdl_now = false;
   if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
   if (t->cfg.max_keys) {  // bounded: dedup + metadata, then probe / evict / insert on the device
     k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
@@ -1856,7 +1860,7 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
   if ((st = launch_tile(ws, t, use, n, d_out, d_grads, true, s))) return st;
   if (ev) RS_CUDA(cudaEventRecord(ev[3], s));
   if ((st = launch_finish(ws, t, use, n, d_grads, o, nullptr, s))) return st;
-  ws->pdl_now = false;
+  ws->pdl_now = false;  // (the mirror copy below is not a kernel)
   if (ev) RS_CUDA(cudaEventRecord(ev[4], s));
   return table_mirror_copy(t, mirror, s);
 }
