@@ -856,7 +856,24 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(F
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     constexpr int B = NV == 1 ? 4 : 2;  // rows in flight per step of the loop
+    constexpr int B2 = 2 * B;           // long lists: twice as many in flight
     uint32_t k = 0;
+    for (; k + B2 <= c; k += B2) {
+      float4 x[B2][NV];
+#pragma unroll
+      for (int q = 0; q < B2; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) x[q][j] = g4[(size_t)order[k + q] * D4 + gl + j * G];
+#pragma unroll
+      for (int q = 0; q < B2; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          acc[j].x += x[q][j].x;
+          acc[j].y += x[q][j].y;
+          acc[j].z += x[q][j].z;
+          acc[j].w += x[q][j].w;
+        }
+    }
     for (; k + B <= c; k += B) {
       float4 x[B][NV];
 #pragma unroll
