@@ -35,17 +35,22 @@ __device__ __forceinline__ void clean_set(const SetDev& c, uint64_t gtid, uint64
 
 // Probe the global scratch for `id` (linear probing on the low hash bits),
 // claiming an empty slot.  Returns the slot; *fresh = slot newly claimed.
+// first0: the key at slot h & smask if the caller already read it (an
+// early, possibly stale read -- keys never change within a step, so a
+// matching or foreign key is final and an empty one is re-checked by the CAS).
 __device__ __forceinline__ uint64_t scratch_insert(const SetDev& S, uint64_t id, uint64_t h,
-                                                   bool* fresh) {
+                                                   bool* fresh, const unsigned long long* first0 = nullptr) {
   if (id == kEmptyKey) {
     *fresh = atomicCAS(&S.skey[S.spare], kEmptyKey, 0ull) == kEmptyKey;
     return S.spare;
   }
   uint64_t gs = h & S.smask;
+  bool use0 = first0 != nullptr;
   for (;;) {
     // plain L2 read first: ids repeated across tiles find their slot without
     // an atomic (hot ids would otherwise serialize every tile on one address)
-    const unsigned long long cur = __ldcg(&S.skey[gs]);
+    const unsigned long long cur = use0 ? *first0 : __ldcg(&S.skey[gs]);
+    use0 = false;
     if (cur == id) {
       *fresh = false;
       return gs;

@@ -145,16 +145,19 @@ __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetD
   uint64_t id = 0, h = 0;
   uint32_t p = 0;
   bool rep = false;
+  unsigned long long first0 = kEmptyKey;
   if (valid) {
     id = ids[t];
     h = hash64(id);
+    // the global slot's key, read now: overlaps the tile-local dedup below
+    if (id != kEmptyKey) first0 = __ldcg(&S.skey[h & S.smask]);
     p = local_insert(lt, id, h, tid, false, &rep);
     atomicAdd(&lcnt[p], 1u);
   }
   __syncthreads();
   if (rep) {
     bool fresh = false;
-    const uint64_t gs = scratch_insert(S, id, h, &fresh);
+    const uint64_t gs = scratch_insert(S, id, h, &fresh, &first0);
     atomicAdd(&S.sntile[gs], 1u);
     atomicAdd(&S.sfirstx[gs], lcnt[p]);  // occurrence count
     lt.gslot[p] = (uint32_t)gs;
