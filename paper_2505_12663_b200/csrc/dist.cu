@@ -739,10 +739,18 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   if (const char* e = getenv("RS_DIST_GRAPH_FORK")) c->graph_fork = e[0] != '0';
   if (const char* e = getenv("RS_DIST_ONE_STREAM")) c->one_stream = e[0] == '1';
   RS_CUDA(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-  RS_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+  // stream priorities (experiment knobs): RS_DIST_PRIO = "<owner><gather>",
+  // each 'h' (high), 'l' (low) or 'n' (default)
+  int prio_lo = 0, prio_hi = 0;
+  RS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const char* pe = getenv("RS_DIST_PRIO");
+  auto prio_of = [&](char ch) { return ch == 'h' ? prio_hi : (ch == 'l' ? prio_lo : 0); };
+  const int own_prio = pe && pe[0] ? prio_of(pe[0]) : 0;
+  const int gat_prio = pe && pe[0] && pe[1] ? prio_of(pe[1]) : 0;
+  RS_CUDA(cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, own_prio));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-  RS_CUDA(cudaStreamCreateWithFlags(&c->gather_stream, cudaStreamNonBlocking));
+  RS_CUDA(cudaStreamCreateWithPriority(&c->gather_stream, cudaStreamNonBlocking, gat_prio));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
   c->h_peers[rank] = c->arena;
