@@ -119,9 +119,17 @@ __global__ void __launch_bounds__(256) k_jagged_grads_chunks(const GradChunk* __
   }
   __syncthreads();
   const uint32_t d4 = dim >> 2;
-  const uint64_t total = (uint64_t)(w.t1 - w.t0) * d4;
   float4* dst = reinterpret_cast<float4*>(out) + (uint64_t)w.t0 * d4;
-  for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) __stcs(dst + i, srow4c[i % d4]);
+  const uint32_t ntok = w.t1 - w.t0;
+  if (d4 <= blockDim.x && blockDim.x % d4 == 0) {
+    // fixed column per thread: one smem read, then only streaming stores
+    const uint32_t c = threadIdx.x % d4, rstep = blockDim.x / d4;
+    const float4 v = srow4c[c];
+    for (uint32_t r = threadIdx.x / d4; r < ntok; r += rstep) __stcs(dst + (uint64_t)r * d4 + c, v);
+  } else {
+    const uint64_t total = (uint64_t)ntok * d4;
+    for (uint64_t i = threadIdx.x; i < total; i += blockDim.x) __stcs(dst + i, srow4c[i % d4]);
+  }
 }
 
 // sample index of every token: block s fills [offs[s], offs[s+1])
