@@ -90,6 +90,8 @@ struct rs_workspace {
   bool pdl_now = false;
   // rs_step_checksum: f64 sum of the gathered rows, fused into the gather
   double* csum_dst = nullptr;
+  uint32_t* tok_rank = nullptr;  // per token: rank among its id's occurrences (KA -> KC)
+  bool tok_rank_ok = false;      // the last KA of this workspace produced tok_rank
   double* csum_part = nullptr;         // per-tile partials
   unsigned int* csum_ticket = nullptr;  // tiles done (the last one sums, then zeroes it)  // set while step_enqueue issues the unbounded fast step
   bool graph_fork = true;  // hot-id finish as a forked branch inside captured graphs (RS_GRAPH_FORK=0: linear)

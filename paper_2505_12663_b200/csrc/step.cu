@@ -113,7 +113,8 @@ __device__ __forceinline__ uint32_t local_insert(const LocalTable& lt, uint64_t 
 // KA: fast dedup tile.  blockDim.x == TT.
 __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetDev S,
                          uint32_t* __restrict__ slot_of, uint64_t* __restrict__ unique,
-                         uint32_t* __restrict__ ctr, const uint32_t* __restrict__ d_n) {
+                         uint32_t* __restrict__ ctr, const uint32_t* __restrict__ d_n,
+                         uint32_t* __restrict__ tok_rank) {
   pdl_trigger();  // KB may get resident (it waits for this grid)
   const uint32_t n = d_n ? *d_n : n_host;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -146,20 +147,24 @@ __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetD
   uint32_t p = 0;
   bool rep = false;
   unsigned long long first0 = kEmptyKey;
+  uint32_t lr = 0;
   if (valid) {
     id = ids[t];
     h = hash64(id);
     // the global slot's key, read now: overlaps the tile-local dedup below
     if (id != kEmptyKey) first0 = __ldcg(&S.skey[h & S.smask]);
     p = local_insert(lt, id, h, tid, false, &rep);
-    atomicAdd(&lcnt[p], 1u);
+    lr = atomicAdd(&lcnt[p], 1u);  // rank within the tile (any order: KD sorts)
   }
   __syncthreads();
   if (rep) {
     bool fresh = false;
     const uint64_t gs = scratch_insert(S, id, h, &fresh, &first0);
     atomicAdd(&S.sntile[gs], 1u);
-    atomicAdd(&S.sfirstx[gs], lcnt[p]);  // occurrence count
+    if (tok_rank)  // the tile's base within the id's occurrences (lt.first is free here)
+      lt.first[p] = atomicAdd(&S.sfirstx[gs], lcnt[p]);
+    else
+      atomicAdd(&S.sfirstx[gs], lcnt[p]);  // occurrence count
     lt.gslot[p] = (uint32_t)gs;
     if (fresh) lnew[p] = atomicAdd(&s_nnew, 1u) + 1;
   }
@@ -173,7 +178,12 @@ __global__ void k_fdedup(const uint64_t* __restrict__ ids, uint32_t n_host, SetD
     S.u_slot[u] = gs;
     unique[u] = id;
   }
-  if (valid) slot_of[t] = lt.gslot[p];
+  if (valid) {
+    slot_of[t] = lt.gslot[p];
+    // the token's rank among all occurrences of its id: KC places its CSR
+    // position there without an atomic
+    if (tok_rank) tok_rank[t] = lt.first[p] + lr;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -376,6 +386,7 @@ struct TileArgs {
   uint32_t* csr_pos;
   const uint32_t* d_n;      // device token count (null: n)
   const uint32_t* pos_map;  // CSR value per token (null: token index)
+  const uint32_t* tok_rank; // rank of the token among its id's occurrences (null: atomic placement)
   bool stage;               // hot ids possible: stage the tile's gradient rows
   rs_dist_sync sync;        // sharded step: wait for the peers' rows before gathering
   // f64 sum of every gathered value (run_workload's emb_checksum), fused into
@@ -462,9 +473,10 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
 
   // ---- resolve every token: slot -> (unique id, table row)
   const bool valid = tid < rows;
-  uint32_t u = kFull, r = 0;
+  uint32_t u = kFull, r = 0, trank = 0;
   if (valid) {
     const uint32_t s = __ldg(a.slot_of + t0 + tid);
+    if (MODE != kTileHot && a.tok_rank) trank = __ldg(a.tok_rank + t0 + tid);
     u = __ldcg(a.use.suidx + s);
     r = __ldcg(a.use.srow + s);
   }
@@ -548,7 +560,9 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
   // ---- ids with <= kCsrMax occurrences: place the token position into the
   // id's CSR segment (warp-aggregated cursor; the finish kernel sorts it)
   const bool csr_tok = valid && nt == 0;
-  if (MODE != kTileHot) {
+  if (MODE != kTileHot && a.tok_rank) {
+    if (csr_tok) a.csr_pos[upoff + trank] = t0 + tid;
+  } else if (MODE != kTileHot) {
     const uint32_t key = csr_tok ? u : (0xFFFF0000u | lane);
     const unsigned mm0 = __match_any_sync(kFull, key);
     const uint32_t leader = __ffs(mm0) - 1;
@@ -1337,20 +1351,21 @@ static FTableArgs ftable_args(rs_workspace* ws, rs_table* t, int use) {
 }
 
 static int launch_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use,
-                         cudaStream_t s, const uint32_t* d_n = nullptr) {
+                         cudaStream_t s, const uint32_t* d_n = nullptr, bool ranks = false) {
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4 + 4);
   k_fdedup<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, set_dev(ws, use), ws->slot_of, ws->unique,
-                                  ws->ctr, d_n);
+                                  ws->ctr, d_n, ranks ? ws->tok_rank : nullptr);
   RS_LAUNCH_CHECK("k_fdedup");
+  ws->tok_rank_ok = ranks;
   return RS_OK;
 }
 
 // KA + KB of the fast step on set `use`, cleaning set `use ^ 1`.
 static int fast_dedup_table(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
                             int use, cudaStream_t s) {
-  int st = launch_fdedup(ws, d_ids, n, use, s);
+  int st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true);
   if (st) return st;
   k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
   RS_LAUNCH_CHECK("k_ftable");
@@ -1395,6 +1410,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.pbuf = ws->pbuf;
   a.ptile = ws->ptile;
   a.csr_pos = ws->csr_pos;
+  a.tok_rank = (!dopt && ws->tok_rank_ok) ? ws->tok_rank : nullptr;
   double* csum = dopt ? (dopt->d_n ? nullptr : dopt->csum) : ws->csum_dst;
   if (csum && d_out && D % 4 == 0) {
     a.csum_out = csum;
@@ -1605,7 +1621,7 @@ static int forward_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids,
   if (t->cfg.max_keys) {
     k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
     RS_LAUNCH_CHECK("k_clean");
-    if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
+    if ((st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true))) return st;
     FTableArgs a = ftable_args(ws, t, use);
     a.do_clean = false;
     a.do_table = false;
@@ -1691,7 +1707,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
        A(&ws->urow, N * 4) && A(&ws->urow64, N * 8) && A(&ws->ptile, N * 4) &&
        A(&ws->porder, N * 4) && A(&ws->hot_list, (N / 32 + 64) * 4) && A(&ws->u_cnt, N * 4) && A(&ws->csr_pos, N * 4) &&
        A(&ws->scan_status, ((N + kScanTile - 1) / kScanTile + 1) * 8) && A(&ws->ctr, 64) &&
-       A(&ws->csum_part, (N / 32 + 2) * 8) && A(&ws->csum_ticket, 16) &&
+       A(&ws->csum_part, (N / 32 + 2) * 8) && A(&ws->csum_ticket, 16) && A(&ws->tok_rank, N * 4) &&
        cudaMemset(ws->csum_ticket, 0, 16) == cudaSuccess;
   if (!ok) {
     rs_workspace_destroy(ws);
@@ -1731,7 +1747,7 @@ int rs_workspace_destroy(rs_workspace* ws) {
   void* ptrs[] = {ws->slot_of, ws->inverse, ws->unique, ws->u_ntile,  ws->u_poff,
                   ws->u_ticket, ws->urow,   ws->urow64, ws->ptile,    ws->porder,
                   ws->pbuf,    ws->scan_status, ws->ctr, ws->hot_list, ws->u_cnt, ws->csr_pos,
-                  ws->csum_part, ws->csum_ticket};
+                  ws->csum_part, ws->csum_ticket, ws->tok_rank};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : ws->graphs)
@@ -1858,7 +1874,7 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
   if (t->cfg.max_keys) {  // bounded: dedup + metadata, then probe / evict / insert on the device
     k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
     RS_LAUNCH_CHECK("k_clean");
-    if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
+    if ((st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true))) return st;
     if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
     FTableArgs a = ftable_args(ws, t, use);
     a.do_clean = false;
@@ -1869,7 +1885,7 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
                                     ws->set[use].u_slot, ws->set[use].srow, s)))
       return st;
   } else {
-    if ((st = launch_fdedup(ws, d_ids, n, use, s))) return st;
+    if ((st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true))) return st;
     if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
     ws->pdl_now = ws->pdl && !ev;  // eager profiling keeps plain launches
     RS_CUDA(launch_pdl(ws->pdl_now, k_ftable, grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s,
