@@ -1410,7 +1410,8 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
   a.pbuf = ws->pbuf;
   a.ptile = ws->ptile;
   a.csr_pos = ws->csr_pos;
-  a.tok_rank = (!dopt && ws->tok_rank_ok) ? ws->tok_rank : nullptr;
+  // token ranks from this workspace's KA (not for the owner's received lists)
+  a.tok_rank = (d_grads && ws->tok_rank_ok && !(dopt && (dopt->pos_map || dopt->d_n))) ? ws->tok_rank : nullptr;
   double* csum = dopt ? (dopt->d_n ? nullptr : dopt->csum) : ws->csum_dst;
   if (csum && d_out && D % 4 == 0) {
     a.csum_out = csum;
@@ -1639,7 +1640,7 @@ static int forward_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids,
 int step_set_smem_attrs() { return set_smem_attrs(); }
 int step_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
                 const uint32_t* d_n) {
-  return launch_fdedup(ws, d_ids, n, use, s, d_n);
+  return launch_fdedup(ws, d_ids, n, use, s, d_n, d_n == nullptr);  // host n: token ranks too
 }
 int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_table,
                 bool do_clean, cudaStream_t s, const rs_dist_send* send) {
