@@ -249,11 +249,12 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       nt = a.use.sntile[slot];
       cnt = a.use.sfirstx[slot];
     }
-    // the probe depends only on the key: issue it before the metadata work
-    // so its slot loads overlap the scratch loads above
-    uint32_t row = kNoRow;
-    if (a.do_table && active)
-      row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins, &s_reuse);
+    // the probe's first slot window depends only on the key: prefetch it into
+    // L2 now (overlaps the scratch loads and the block-wide allocation below)
+    if (a.do_table && active && g == 0) {
+      const uint64_t b = (hash64(key) >> 32) & d.nb_mask;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(d.slots + b * kBucket));
+    }
     const bool hot = cnt > kCsrMax;
     // segments: CSR of the id's token positions (exact-order path) or its
     // per-tile partial sums (hot path); warp-aggregated allocation
@@ -323,6 +324,8 @@ __global__ void __launch_bounds__(256, 8) k_ftable(FTableArgs a) {
       }
     }
     if (!a.do_table || !active) continue;
+    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0,
+                                              &s_ins, &s_reuse);
     if (g == 0) {
       a.urow[i] = row;
       a.urow64[i] = row == kNoRow ? -1 : (int64_t)row;
