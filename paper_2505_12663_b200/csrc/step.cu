@@ -848,7 +848,9 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(F
 #pragma unroll
     for (int jq = 0; jq < PPT; ++jq) {
       if ((uint32_t)(jq * G) >= c) break;
-      for (uint32_t src = 0; src < (uint32_t)G; ++src) {
+      // lanes >= c hold the kFull sentinel, which ranks nothing: skip them
+      const uint32_t lim = min((uint32_t)G, c - (uint32_t)(jq * G));
+      for (uint32_t src = 0; src < lim; ++src) {
         const uint32_t q = __shfl_sync(gmask, p[jq], src, G);
 #pragma unroll
         for (int j = 0; j < PPT; ++j) r[j] += q < p[j];
@@ -920,8 +922,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(F
         acc[j].w += x.w;
       }
     }
-    __syncwarp(gmask);
-    if (gl == 0) a.u_ticket[uu] = 0;
+    __syncwarp(gmask);  // (u_ticket needs no reset: KB / k_own_table zero it every step)
     if (float* dst = sum_dst(a, uu, d.dim)) {
 #pragma unroll
       for (int j = 0; j < NV; ++j) reinterpret_cast<float4*>(dst)[gl + j * G] = acc[j];
