@@ -785,10 +785,10 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 // chunk of the row.  The id's <= kCsrMax token positions are ranked within the
 // group (shuffles), written sorted to smem, and the gradient rows are summed
 // in position order (the reference's accumulate order) -> bit-exact sums.
-template <int G, int NV>
 #ifndef RS_CSR_MINB
 #define RS_CSR_MINB 5  // measured: 5 (48 regs) beats 4 / 6 / 8 at config 1 (G = 16, NV = 1)
 #endif
+template <int G, int NV>
 __global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(FinishArgs a, OptArgs o) {
   // G lanes per id, each owning NV float4 chunks of the row (chunk gl + j*G)
   pdl_wait();
