@@ -397,6 +397,7 @@ struct TileArgs {
   double* csum_out = nullptr;
   double* csum_part = nullptr;
   unsigned int* csum_ticket = nullptr;
+  uint32_t persist_tiles = 0;  // kTileHot: > 0 = number of tiles walked by a smaller grid
 };
 
 // MODE kTileFull: gather + CSR placement + hot-id tile partials (one pass);
@@ -407,10 +408,10 @@ enum : int { kTileFull = 0, kTileGatherCsr = 1, kTileHot = 2 };
 #ifndef RS_KC1_MINB
 #define RS_KC1_MINB 4
 #endif
+// One tile of KC (`iter`: how many tiles this block processed before -- the
+// TMA barrier's phase parity).
 template <int VEC, int CH, int LPR, int MODE>
-__global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3) k_ftile(TileArgs a) {
-  pdl_wait();
-  pdl_trigger();
+__device__ __forceinline__ void ftile_body(const TileArgs& a, const uint32_t tile, const uint32_t iter) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t TT = blockDim.x;
   const uint32_t NW = TT >> 5;
@@ -434,7 +435,6 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
   uint16_t* csr = wcnt + (size_t)NW * TT;                    // [TT]
 
   const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
-  const uint32_t tile = blockIdx.x;
   const uint32_t t0 = tile * TT;
   const uint32_t nn = a.d_n ? *a.d_n : a.n;
   if (a.clean_cnt && tile == 0 && tid == 0) *a.clean_cnt = 0;
@@ -450,8 +450,11 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
     for (uint32_t i = tid; i < NW * TT; i += TT) wcnt[i] = 0;
     if (a.tma) {
       if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (iter == 0) {
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        // the previous tile's generic-proxy reads of sg happen before these async writes
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t bytes = rows * D * 4u;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
@@ -578,6 +581,7 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
   }
   const bool hotv = valid && nt > 0;
   if (MODE == kTileGatherCsr || !a.stage) return;  // no hot part here / none possible
+  __syncthreads();  // lkey / lfirst / wcnt initialised by all threads above
 
   // ---- hot ids: group the tile's tokens by unique id (first occurrence)
   uint32_t ps = 0;
@@ -661,8 +665,8 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
   if (a.tma) {
     asm volatile(
         "{\n\t.reg .pred P;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n\t"
-        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar))
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(iter & 1u)
         : "memory");
   }
   __syncthreads();
@@ -699,6 +703,23 @@ __global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3)
       a.pbuf[(size_t)gdst[g] * D + e] = sg[(size_t)csr[goff[g]] * D + e];
     }
   }
+}
+
+template <int VEC, int CH, int LPR, int MODE>
+__global__ void __launch_bounds__(256, MODE == kTileGatherCsr ? RS_KC1_MINB : 3) k_ftile(TileArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  if (MODE == kTileHot && a.persist_tiles) {
+    // persistent hot pass: fewer resident blocks, each walking tiles, so the
+    // concurrent main branch (gather + CSR finish) keeps most of the SMs
+    uint32_t iter = 0;
+    for (uint32_t tile = blockIdx.x; tile < a.persist_tiles; tile += gridDim.x, ++iter) {
+      ftile_body<VEC, CH, LPR, MODE>(a, tile, iter);
+      __syncthreads();
+    }
+    return;
+  }
+  ftile_body<VEC, CH, LPR, MODE>(a, blockIdx.x, 0);
 }
 
 // scalar gather for D % 4 != 0 (the reduce part of KC handles any D)
@@ -1448,6 +1469,14 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     TileArgs a2 = a;
     a2.out = nullptr;
     a2.clean_cnt = nullptr;
+    a2.csum_out = nullptr;
+    // RS_KC2_PER_SM: resident hot-pass blocks per SM (0: one block per tile)
+    static const unsigned kc2_per_sm = getenv("RS_KC2_PER_SM") ? (unsigned)atoi(getenv("RS_KC2_PER_SM")) : 0u;
+    unsigned hot_grid = ntiles;
+    if (kc2_per_sm && !a.d_n && ntiles > 148u * kc2_per_sm) {
+      hot_grid = 148u * kc2_per_sm;
+      a2.persist_tiles = ntiles;
+    }
     cudaStream_t hs = s;
     if (ws->fork) {
       RS_CUDA(cudaEventRecord(ws->ev_fork, s));
@@ -1458,7 +1487,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     bool kc2 = false;
 #define RS_HOT(V, C)                                                           \
   if (!kc2 && sh.vec == V && sh.ch == C) {                                     \
-    k_ftile<V, C, 1, kTileHot><<<ntiles, TT, smem, hs>>>(a2);                  \
+    k_ftile<V, C, 1, kTileHot><<<hot_grid, TT, smem, hs>>>(a2);                \
     RS_LAUNCH_CHECK("k_ftile(hot)");                                           \
     kc2 = true;                                                                \
   }
