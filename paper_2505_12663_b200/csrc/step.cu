@@ -1846,7 +1846,10 @@ int rs_forward(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
   ws->last_n = n;
   ws->last_tile = tile_tokens_for_dim(t->desc.dim);
   ws->last_table = t;
-  if (n == 0) return RS_OK;
+  if (n == 0) {  // an empty batch is a forward too: its (no-op) backward may follow
+    ws->have_forward = true;
+    return RS_OK;
+  }
   int st = set_smem_attrs();
   if (st) return st;
   if (!t->cfg.max_keys && (st = table_prepare(t, n, s))) return st;
@@ -1865,7 +1868,10 @@ int rs_backward(rs_workspace* ws, rs_table* t, const float* d_grads, uint64_t n,
   if (!ws || !t) return fail(RS_ERR_CONFIG, "rs_backward: null handle");
   if (!ws->have_forward || ws->last_table != t || ws->last_n != n)
     return fail(RS_ERR_CONFIG, "rs_backward: must follow rs_forward on the same table and batch");
-  if (n == 0) return RS_OK;
+  if (n == 0) {
+    ws->have_forward = false;
+    return RS_OK;
+  }
   cudaStream_t s = S(stream);
   OptArgs o;
   int st = opt_args(t, opt, &o, s);

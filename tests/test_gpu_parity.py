@@ -239,6 +239,46 @@ def test_step_vs_oracle(cuda, oracle, dim, opt):
         _compare_contents(g, ot, ("keys", "emb", "v", "step") + (("m",) if opt == "adam" else ()))
 
 
+@pytest.mark.parametrize("opt", ["adagrad", "adam"])
+def test_step_edge_batches(cuda, oracle, opt):
+    """Ragged edge cases through the fused step (rs_step): an empty batch is a
+    no-op, single-token and duplicate-only batches update exactly like the
+    reference's accumulate + apply (sparse_update.cpp:45-83), and an id with
+    65 occurrences (past the sequential-sum limit) stays within the tolerance."""
+    dim, vocab = 16, 300
+    _, _, g, ot = _c1_like(5, 4, vocab, dim, opt)
+    params = P.AdagradParams() if opt == "adagrad" else P.AdamParams()
+    st = P.SparseStep(g, 4096, params)
+    batches = [np.zeros(0, np.uint64),
+               np.array([7], np.uint64) + np.uint64(TAG1),
+               np.array([9, 9, 9, 4, 9], np.uint64) + np.uint64(TAG1),
+               np.array([vocab + 5], np.uint64) + np.uint64(TAG1),  # new id: vivified zero row
+               np.concatenate([np.full(65, 11, np.uint64), np.arange(20, dtype=np.uint64)]) + np.uint64(TAG1)]
+    for s, batch in enumerate(batches):
+        n = len(batch)
+        rng = np.random.default_rng(s)
+        grads = torch.from_numpy(rng.uniform(-0.05, 0.05, (max(n, 1), dim)).astype(np.float32)).cuda()[:n]
+        out = torch.empty((max(n, 1), dim), device="cuda")[:n]
+        want_out = np.zeros((n, dim), np.float32)
+        if n:
+            oracle.table_lookup_batch(ot.h, batch, n, want_out.reshape(-1))
+        st.step(P.as_keys(batch), grads.contiguous(), out)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out.cpu().numpy(), want_out)
+        if n:
+            ids_acc, sums_ref = oracle.accumulate_np(batch, grads.cpu().numpy(), dim)
+            oracle.apply(ot.h, ids_acc, np.ascontiguousarray(sums_ref.astype(np.float32)).reshape(-1),
+                         len(ids_acc), 1 if opt == "adagrad" else 0, params.lr, getattr(params, "beta1", 0.9),
+                         getattr(params, "beta2", 0.999), params.eps)
+        a, b = g.export(), ot.export()
+        np.testing.assert_array_equal(a["keys"], b["keys"].astype(a["keys"].dtype))
+        np.testing.assert_array_equal(a["step"], b["step"].astype(a["step"].dtype))
+        if s < 4:  # every id summed in token order: bit-exact
+            np.testing.assert_array_equal(a["emb"], b["emb"])
+        else:  # the 65-occurrence id: tolerance on its updated row
+            np.testing.assert_allclose(a["emb"], b["emb"], rtol=1e-5, atol=1e-6)
+
+
 def test_step_deterministic(cuda):
     dim = 64
     lengths, ids = W.generate(4, 128, 128.0, 4096, 1.0, 1.1, [50000])
