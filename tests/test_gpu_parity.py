@@ -277,6 +277,16 @@ def test_step_edge_batches(cuda, oracle, opt):
             np.testing.assert_array_equal(a["emb"], b["emb"])
         else:  # the 65-occurrence id: tolerance on its updated row
             np.testing.assert_allclose(a["emb"], b["emb"], rtol=1e-5, atol=1e-6)
+    # empty batch through the checksum variant: checksum 0, table untouched
+    before = g.export()
+    cs = torch.full((1,), 123.0, dtype=torch.float64, device="cuda")
+    empty = torch.empty((1, dim), device="cuda")[:0]
+    st.step_checksum(P.as_keys(np.zeros(0, np.uint64)), empty, empty, cs)
+    torch.cuda.synchronize()
+    assert float(cs[0]) == 0.0
+    after = g.export()
+    for f in ("keys", "emb", "v", "step"):
+        np.testing.assert_array_equal(before[f], after[f], err_msg=f)
 
 
 def test_step_deterministic(cuda):
@@ -529,8 +539,12 @@ def test_feeder_step_matches_device_step(cuda):
     steps = [P.SparseStep(t, 5000, P.AdagradParams(lr=0.05)) for t in tabs]
     f = Feeder(5000, 64, dim)
     rng = np.random.default_rng(12)
-    for k in range(4):
+    for k in range(5):
         lengths = rng.integers(1, 120, 40).astype(np.uint64)
+        if k == 2:  # ragged: empty sequences inside the batch
+            lengths[::3] = 0
+        if k == 3:  # every sequence empty: a no-op step, checksum 0
+            lengths[:] = 0
         ids = rng.integers(0, 900, int(lengths.sum())).astype(np.uint64)
         h_ids = torch.from_numpy(ids.view(np.int64)).pin_memory()
         h_len = torch.from_numpy(lengths.view(np.int64)).pin_memory()
