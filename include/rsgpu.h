@@ -231,6 +231,27 @@ int rs_comm_barrier(rs_comm* c, void* stream);
 int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count);
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received);
+/* A group of `world` logical ranks on the current GPU (one process): the
+ * SimCluster of the reference (exchange_sim.hpp:63-75 -- W shards in one
+ * process, exchange_sim.cpp:117-233) on the sharded step's own kernels, arena
+ * layout and flag protocol, with each other's arenas as plain device
+ * pointers.  comms_out[world] in rank order; destroy each with
+ * rs_comm_destroy.  Drive it only with rs_dist_group_*, which enqueue every
+ * phase rank by rank on one stream in data-flow order (no kernel waits on a
+ * kernel that has not run). */
+int rs_comm_create_local(int world, uint64_t max_tokens, uint32_t dim, rs_comm** comms_out);
+/* rs_dist_forward / rs_dist_backward / rs_dist_step for all ranks of a local
+ * group: arrays of `world` per-rank arguments (shards[r] owns the keys with
+ * hash64 % world == r). */
+int rs_dist_group_forward(rs_comm* const* comms, rs_table* const* shards, int world,
+                          const uint64_t* const* d_ids, const uint64_t* n, float* const* d_out,
+                          void* stream);
+int rs_dist_group_backward(rs_comm* const* comms, rs_table* const* shards, int world,
+                           const float* const* d_grads, const uint64_t* n,
+                           const rs_optimizer_params* opt, void* stream);
+int rs_dist_group_step(rs_comm* const* comms, rs_table* const* shards, int world,
+                       const uint64_t* const* d_ids, const uint64_t* n, const float* const* d_grads,
+                       float* const* d_out, const rs_optimizer_params* opt, void* stream);
 
 /* ---- table merging (merge_registry.cpp:23-176) ---------------------------- */
 /* encode_tagged_id on device (merge_registry.cpp:23-33); synchronizes,

@@ -319,6 +319,7 @@ struct DistGraph {
 
 struct rs_comm {
   int rank = 0, world = 1;
+  bool local = false;  // rs_comm_create_local: the peers are arenas of this process
   uint64_t cap = 0;
   uint32_t dim = 0;
   char* arena = nullptr;
@@ -766,16 +767,10 @@ int rs_comm_ipc_handle(rs_comm* c, void* handle_out /* 64 bytes */) {
   return RS_OK;
 }
 
-int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order */) {
-  if (!c || !handles) return fail(RS_ERR_CONFIG, "rs_comm_open: null argument");
-  for (int r = 0; r < c->world; ++r) {
-    if (r == c->rank) continue;
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
-    void* p = nullptr;
-    RS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-    c->h_peers[r] = static_cast<char*>(p);
-  }
+}  // extern "C"
+
+// Device copies of the peer tables once h_peers[] holds every rank's arena.
+static int link_peers(rs_comm* c) {
   RS_CUDA(cudaMemcpy(c->d_peers, c->h_peers, kMaxWorld * sizeof(char*), cudaMemcpyHostToDevice));
   {
     std::vector<unsigned long long*> f(kMaxWorld, nullptr);
@@ -798,11 +793,57 @@ int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order
   return RS_OK;
 }
 
+extern "C" {
+
+int rs_comm_open(rs_comm* c, const void* handles /* world x 64 bytes, rank order */) {
+  if (!c || !handles) return fail(RS_ERR_CONFIG, "rs_comm_open: null argument");
+  if (c->local) return fail(RS_ERR_CONFIG, "rs_comm_open: a local group is already linked");
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    RS_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->h_peers[r] = static_cast<char*>(p);
+  }
+  return link_peers(c);
+}
+
+// W logical ranks on the current device (one process): every rank's arena is
+// a plain allocation and the peers are each other's device pointers.  The
+// kernels, arena layout and flag protocol are the ones of the multi-GPU step;
+// only the transport is local HBM instead of NVLink.  Drive the group with
+// rs_dist_group_* (never with per-rank rs_dist_* calls on concurrent streams:
+// the ranks' wait kernels would depend on each other).
+int rs_comm_create_local(int world, uint64_t max_tokens, uint32_t dim, rs_comm** comms_out) {
+  if (!comms_out || world < 1 || world > kMaxWorld)
+    return fail(RS_ERR_CONFIG, "rs_comm_create_local: bad world / null output");
+  std::vector<rs_comm*> cs(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    const int st = rs_comm_create(r, world, max_tokens, dim, &cs[r]);
+    if (st) {
+      for (auto* c : cs) rs_comm_destroy(c);
+      return st;
+    }
+    cs[r]->local = true;
+  }
+  for (int r = 0; r < world; ++r) {
+    for (int q = 0; q < world; ++q) cs[r]->h_peers[q] = cs[q]->arena;
+    const int st = link_peers(cs[r]);
+    if (st) {
+      for (auto* c : cs) rs_comm_destroy(c);
+      return st;
+    }
+  }
+  for (int r = 0; r < world; ++r) comms_out[r] = cs[r];
+  return RS_OK;
+}
+
 int rs_comm_destroy(rs_comm* c) {
   if (!c) return RS_OK;
   cudaDeviceSynchronize();
   for (int r = 0; r < c->world; ++r)
-    if (r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
+    if (!c->local && r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
   void* ps[] = {c->arena, c->d_peers, c->d_peer_grad[0], c->d_peer_grad[1], c->trace, c->done,
                 c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch, c->d_sig_grad_ptrs,
                 c->d_sig_ids_ptrs, c->d_cnt_ptrs};
@@ -1037,6 +1078,103 @@ int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t*
   if (lookups) *lookups = h[kTrLookups];
   if (ids_requested) *ids_requested = h[kTrRequested];
   if (ids_received) *ids_received = h[kTrReceived];
+  return RS_OK;
+}
+
+
+// ---- the group of local ranks (rs_comm_create_local) --------------------------
+// Every phase of one sharded step, rank by rank, on ONE stream in data-flow
+// order: when a rank's wait kernel runs, the flags it waits for were raised
+// by kernels earlier in the same stream, so no kernel ever waits on a kernel
+// that has not run yet.  Same kernels, arena traffic and flag protocol as the
+// multi-GPU step.
+struct alignas(16) OptBuf {
+  unsigned char b[256] = {0};
+};
+
+static int group_check(rs_comm* const* cs, rs_table* const* ts, int world, const uint64_t* n,
+                       const char* who) {
+  if (!cs || !ts || !n || world < 1) return fail(RS_ERR_CONFIG, std::string(who) + ": null argument");
+  for (int r = 0; r < world; ++r) {
+    if (!cs[r] || !cs[r]->local || cs[r]->world != world || cs[r]->rank != r)
+      return fail(RS_ERR_CONFIG, std::string(who) + ": comms must be a local group in rank order");
+    RS_TRY(check_call(cs[r], ts[r], n[r], who));
+  }
+  return RS_OK;
+}
+
+int rs_dist_group_forward(rs_comm* const* cs, rs_table* const* ts, int world, const uint64_t* const* d_ids,
+                          const uint64_t* n, float* const* d_out, void* stream) {
+  RS_TRY(group_check(cs, ts, world, n, "rs_dist_group_forward"));
+  cudaStream_t s = S(stream);
+  std::vector<StepSets> ss(world);
+  for (int r = 0; r < world; ++r) {
+    RS_TRY(prepare_step(cs[r], ts[r], 0, s));
+    ss[r] = begin_step(cs[r]);
+  }
+  for (int r = 0; r < world; ++r) RS_TRY(req_front(cs[r], ts[r], d_ids[r], n[r], ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    RS_TRY(owner_lookup(cs[r], ts[r], ss[r], s));
+    RS_TRY(table_after_op(ts[r], s));
+  }
+  for (int r = 0; r < world; ++r) RS_TRY(req_gather(cs[r], ts[r], n[r], d_out[r], ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    end_step(cs[r], ss[r]);
+    cs[r]->last_n = n[r];
+    cs[r]->last_table = ts[r];
+    cs[r]->have_forward = true;
+  }
+  return RS_OK;
+}
+
+int rs_dist_group_backward(rs_comm* const* cs, rs_table* const* ts, int world, const float* const* d_grads,
+                           const uint64_t* n, const rs_optimizer_params* opt, void* stream) {
+  if (!cs || !ts || !n || world < 1) return fail(RS_ERR_CONFIG, "rs_dist_group_backward: null argument");
+  cudaStream_t s = S(stream);
+  std::vector<OptBuf> obs(world);
+  for (int r = 0; r < world; ++r) {
+    rs_comm* c = cs[r];
+    if (!c || !c->local || !c->have_forward || c->last_table != ts[r] || c->last_n != n[r])
+      return fail(RS_ERR_CONFIG, "rs_dist_group_backward: must follow rs_dist_group_forward on the same batches");
+    RS_TRY(step_opt_args(ts[r], opt, obs[r].b, s));
+    if (n[r]) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n[r], s));
+  }
+  for (int r = 0; r < world; ++r) RS_TRY(req_reduce(cs[r], ts[r], d_grads[r], n[r], cs[r]->last_sets, s));
+  for (int r = 0; r < world; ++r) RS_TRY(owner_update(cs[r], ts[r], obs[r].b, cs[r]->last_sets, s));
+  for (int r = 0; r < world; ++r) {
+    ts[r]->applies++;
+    cs[r]->have_forward = false;
+  }
+  return RS_OK;
+}
+
+// forward + backward of one step of the group (rs_dist_step's data flow:
+// the owners answer with the rows as they were before this step's update).
+int rs_dist_group_step(rs_comm* const* cs, rs_table* const* ts, int world, const uint64_t* const* d_ids,
+                       const uint64_t* n, const float* const* d_grads, float* const* d_out,
+                       const rs_optimizer_params* opt, void* stream) {
+  RS_TRY(group_check(cs, ts, world, n, "rs_dist_group_step"));
+  cudaStream_t s = S(stream);
+  std::vector<OptBuf> obs(world);
+  std::vector<StepSets> ss(world);
+  for (int r = 0; r < world; ++r) {
+    RS_TRY(step_opt_args(ts[r], opt, obs[r].b, s));
+    RS_TRY(prepare_step(cs[r], ts[r], n[r], s));
+    ss[r] = begin_step(cs[r]);
+  }
+  for (int r = 0; r < world; ++r) RS_TRY(req_front(cs[r], ts[r], d_ids[r], n[r], ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    RS_TRY(owner_lookup(cs[r], ts[r], ss[r], s));
+    RS_TRY(table_after_op(ts[r], s));
+  }
+  for (int r = 0; r < world; ++r) RS_TRY(req_reduce(cs[r], ts[r], d_grads[r], n[r], ss[r], s));
+  for (int r = 0; r < world; ++r) RS_TRY(req_gather(cs[r], ts[r], n[r], d_out[r], ss[r], s));
+  for (int r = 0; r < world; ++r) RS_TRY(owner_update(cs[r], ts[r], obs[r].b, ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    end_step(cs[r], ss[r]);
+    ts[r]->applies++;
+    cs[r]->have_forward = false;
+  }
   return RS_OK;
 }
 

@@ -128,3 +128,91 @@ class ShardedTable:
         if self._c:
             L.lib().rs_comm_destroy(self._c)
             self._c = C.c_void_p()
+
+
+class LocalShardGroup:
+    """W logical ranks of the sharded step on the current GPU (one process).
+
+    The reference's SimCluster (exchange_sim.hpp:63-75: W shards in one
+    process, distributed_lookup exchange_sim.cpp:117-233) run on the sharded
+    step's own kernels, arena layout and flag protocol
+    (rs_comm_create_local / rs_dist_group_*): every rank's phases are enqueued
+    on one stream in data-flow order, so the W-rank data path -- owner
+    routing, stage-2 dedup, find-or-insert at the owner, the embedding and
+    gradient exchanges, the owner's ordered update -- is exercised on one GPU.
+    shards[r] owns the keys with hash64(key) % W == r."""
+
+    def __init__(self, config: TableConfig, world: int, max_tokens: int):
+        self.world, self.dim, self.max_tokens = world, config.embedding_dim, max_tokens
+        self.shards = [EmbedTable(config) for _ in range(world)]
+        self._cs = (C.c_void_p * world)()
+        check(L.lib().rs_comm_create_local(world, max_tokens, self.dim, self._cs), "rs_comm_create_local")
+        self._ts = (C.c_void_p * world)(*[s.handle for s in self.shards])
+
+    def insert_all(self, keys, emb: torch.Tensor) -> None:
+        """Insert every row into the shard that owns its key."""
+        k = as_keys(keys)
+        own = shard_of_batch(k, self.world)
+        e = emb.to("cuda")
+        for r in range(self.world):
+            sel = torch.nonzero(own == r).flatten()
+            if sel.numel():
+                self.shards[r].insert(k[sel], e[sel])
+
+    def _arrays(self, ids):
+        ks = [as_keys(i) for i in ids]
+        n = (C.c_uint64 * self.world)(*[k.numel() for k in ks])
+        return ks, n
+
+    def forward(self, ids: list) -> list:
+        ks, n = self._arrays(ids)
+        outs = [torch.empty((k.numel(), self.dim), dtype=torch.float32, device="cuda") for k in ks]
+        pi = (C.c_void_p * self.world)(*[_ptr(k) for k in ks])
+        po = (C.c_void_p * self.world)(*[_ptr(o) for o in outs])
+        check(L.lib().rs_dist_group_forward(self._cs, self._ts, self.world, pi, n, po, _stream()),
+              "rs_dist_group_forward")
+        self._keep = ks
+        return outs
+
+    def backward(self, grads: list, params) -> None:
+        gs = [g.to("cuda", torch.float32).contiguous() for g in grads]
+        n = (C.c_uint64 * self.world)(*[g.shape[0] for g in gs])
+        pg = (C.c_void_p * self.world)(*[_ptr(g) for g in gs])
+        check(L.lib().rs_dist_group_backward(self._cs, self._ts, self.world, pg, n, C.byref(params.c()), _stream()),
+              "rs_dist_group_backward")
+        torch.cuda.current_stream().synchronize()  # keeps gs alive until the kernels read them
+
+    def step(self, ids: list, grads: list, params) -> list:
+        ks, n = self._arrays(ids)
+        gs = [g.to("cuda", torch.float32).contiguous() for g in grads]
+        outs = [torch.empty((k.numel(), self.dim), dtype=torch.float32, device="cuda") for k in ks]
+        pi = (C.c_void_p * self.world)(*[_ptr(k) for k in ks])
+        pg = (C.c_void_p * self.world)(*[_ptr(g) for g in gs])
+        po = (C.c_void_p * self.world)(*[_ptr(o) for o in outs])
+        check(L.lib().rs_dist_group_step(self._cs, self._ts, self.world, pi, n, pg, po, C.byref(params.c()),
+                                         _stream()), "rs_dist_group_step")
+        torch.cuda.current_stream().synchronize()
+        return outs
+
+    def trace(self) -> dict:
+        """ExchangeTrace of the last step (rows = src), as ShardedTable.trace()."""
+        rows = []
+        for r in range(self.world):
+            ids = np.zeros(self.world, np.uint64)
+            embs = np.zeros(self.world, np.uint64)
+            lk, rq, rv = C.c_uint64(), C.c_uint64(), C.c_uint64()
+            check(L.lib().rs_comm_trace(self._cs[r], ids.ctypes.data, embs.ctypes.data, C.byref(lk), C.byref(rq),
+                                        C.byref(rv)), "rs_comm_trace")
+            rows.append(dict(ids_sent=ids, embs_sent=embs, lookups=lk.value, ids_requested=rq.value,
+                             ids_received=rv.value))
+        return dict(ids_sent=np.stack([r["ids_sent"] for r in rows]),
+                    embs_sent=np.stack([r["embs_sent"] for r in rows]),
+                    lookups=np.array([r["lookups"] for r in rows], np.uint64),
+                    ids_requested=sum(r["ids_requested"] for r in rows),
+                    ids_received=sum(r["ids_received"] for r in rows))
+
+    def close(self):
+        for r in range(self.world):
+            if self._cs[r]:
+                L.lib().rs_comm_destroy(self._cs[r])
+                self._cs[r] = None

@@ -59,10 +59,11 @@ def test_shard_of_matches_oracle(oracle):
 @pytest.mark.gpu
 @pytest.mark.parametrize("opt,dim", [("adam", 32), ("adagrad", 64), ("adam", 128)])
 def test_sharded_step_vs_oracle(opt, dim):
+    # one process per GPU over CUDA IPC + NVLink; on a 1-GPU box the same worker
+    # runs at W = 1 (the bootstrap and the arena mapped as its own peer).  The
+    # W-rank data path on one GPU is tests/test_dist_local.py.
     n = torch.cuda.device_count()
-    if n < 2:
-        pytest.skip("sharded step needs >= 2 GPUs (run under gpurun --gpus 2)")
-    w = min(n, 4)
+    w = min(n, 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={w}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "dist_worker.py"), opt, str(dim)]
