@@ -115,6 +115,28 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def n_batches(warmup):
+    """Distinct batches both arms cycle through (step k uses batch k % nb): even,
+    so each batch always meets the same scratch parity (one captured graph
+    each), at most 6, and every one of them runs during the W warm-up steps --
+    no graph is ever captured inside the timed region."""
+    return max(2, min(6, warmup - warmup % 2))
+
+
+def batch_seed(cfg, rank, b):
+    return cfg["seed"] + 1000 * rank + b
+
+
+def bench_config(cfg, world, nb, sharded):
+    """The `config` object, identical in both arms (--impl ours / reference)."""
+    c = {"workload": cfg["workload"] + ("; row-sharded over the ranks (owner = hash64 % N), per-rank batch"
+                                        if sharded else ""),
+         "embedding_dim": cfg["dim"], "table_keys": cfg["vocab"], "optimizer": "adagrad (lr 0.01, eps 1e-8)",
+         "batches": nb, "batch_seeds": f"{cfg['seed']} + 1000*rank + b, b < {nb}",
+         "parallelism": f"row-sharded x{world}" if sharded else "single"}
+    return c
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args, cfg):
     import torch
@@ -138,10 +160,10 @@ def run_ours(args, cfg):
         table.insert(raw + int(TAG1), W.pseudo_grads(raw, 0, dim))
     del raw
     # distinct batches (weak scaling: each rank its own seed stream)
-    nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
+    nb = n_batches(args.warmup)
     batches = []
     for b in range(nb):
-        lengths, ids = W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"],
+        lengths, ids = W.generate(batch_seed(cfg, rank, b), cfg["seqs"], cfg["mean"], cfg["max_len"],
                                   cfg["sigma"], cfg["zipf"], [vocab])
         batches.append((lengths, ids))
     max_t = max(len(i) for _, i in batches)
@@ -159,9 +181,8 @@ def run_ours(args, cfg):
         d_ids, d_g, out = dev[b % nb]
         step.step(d_ids, d_g, out)
 
-    # warm-up: at least W steps and every batch once (one CUDA graph per
-    # batch buffer set is captured on first use -- never inside the timed region)
-    args.warmup = max(args.warmup, nb)
+    # warm-up: W steps, every batch at least once (one CUDA graph per batch
+    # buffer set is captured on first use -- never inside the timed region)
     for w in range(args.warmup):
         one(w)
     torch.cuda.synchronize()
@@ -174,6 +195,7 @@ def run_ours(args, cfg):
     uniq_per_batch = [int(np.unique(ids).size) for _, ids in batches]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.rs_kernel_launches()
+    syncs0 = table.info().host_syncs
     with Clocks(local) as clk:
         h0 = time.perf_counter()
         for k in range(args.steps):
@@ -184,6 +206,7 @@ def run_ours(args, cfg):
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host enqueue time per step
         torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
+    syncs = table.info().host_syncs - syncs0
     times = [a.elapsed_time(b) for a, b in evs]
     uniq = sum(uniq_per_batch[(args.warmup + k) % nb] for k in range(args.steps))
     toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
@@ -243,10 +266,10 @@ def run_ours(args, cfg):
         "dtype": "f32 rows, f64 optimizer math, u64 ids",
         "data": "synthetic: the reference's generator (mt19937_64, truncated lognormal lengths, Zipf 1.1 ids), "
                 "pseudo_sparse_grad gradients",
-        "config": {"workload": cfg["workload"], "tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg,
-                   "embedding_dim": D, "table_keys": vocab, "optimizer": "adagrad",
-                   "parallelism": "replicas" if world > 1 else "single",
-                   "l2": "flushed (512 MiB write) between timed steps"},
+        "config": bench_config(cfg, world, nb, False),
+        "shape": {"tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg},
+        "l2": "flushed (512 MiB write) between timed steps",
+        "table_host_syncs_in_timed_region": int(syncs),
         "tokens_per_s": toks_job / t_job,
         "host_enqueue_ms_per_step": host_ms,
         "step_hbm_gbs": step_bytes * world / (t_job / args.steps) / 1e9,
@@ -292,7 +315,7 @@ def run_sharded(args, cfg):
     os.environ.setdefault("WORLD_SIZE", "1")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dim, vocab = cfg["dim"], cfg["vocab"]
-    nb = 6  # distinct batches; even, so each batch always meets the same scratch parity (one graph each)
+    nb = n_batches(args.warmup)
     balance = None
     if cfg.get("pooled"):
         # config 5: one pool of sequences per step, every rank computes the same
@@ -313,7 +336,7 @@ def run_sharded(args, cfg):
         balance = {"policy": args.balance, "token_spread_mean": float(np.mean(spreads)),
                    "cost_spread_mean": float(np.mean(cost_spreads))}
     else:
-        batches = [W.generate(cfg["seed"] + 1000 * rank + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
+        batches = [W.generate(batch_seed(cfg, rank, b), cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
                               cfg["zipf"], [vocab]) for b in range(nb)]
     mt = torch.tensor([max(len(i) for _, i in batches)], dtype=torch.int64, device="cuda")
     dist.all_reduce(mt, op=dist.ReduceOp.MAX)  # the arena layout must agree on every rank
@@ -342,8 +365,7 @@ def run_sharded(args, cfg):
         d_ids, d_g, out = dev[b % nb]
         st.step(d_ids, d_g, params, out)
 
-    args.warmup = max(args.warmup, nb)  # every batch's graph captured before timing
-    for w in range(args.warmup):
+    for w in range(args.warmup):  # every batch's graph captured before timing (W >= nb)
         one(w)
     torch.cuda.synchronize()
     dist.barrier()
@@ -409,12 +431,12 @@ def run_sharded(args, cfg):
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32 rows, f64 optimizer math, u64 ids",
-        "data": "synthetic: the reference's generator per rank (seed + 1000*rank), pseudo_sparse_grad gradients",
-        "config": {"workload": cfg["workload"] + "; row-sharded over the ranks (owner = hash64 % N), per-rank batch",
-                   "tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg, "embedding_dim": D,
-                   "table_keys": vocab, "optimizer": "adagrad", "parallelism": f"row-sharded x{world}",
-                   "exchange": "NVLink peer stores from the producing kernels (CUDA IPC arena)",
-                   "l2": "flushed (512 MiB write) between timed steps, then a device barrier of all ranks"},
+        "data": "synthetic: the reference's generator (mt19937_64, truncated lognormal lengths, Zipf 1.1 ids), "
+                "pseudo_sparse_grad gradients",
+        "config": bench_config(cfg, world, nb, True),
+        "shape": {"tokens_per_step_per_rank": T_avg, "unique_per_step_per_rank": U_avg},
+        "exchange": "NVLink peer stores from the producing kernels (CUDA IPC arena)",
+        "l2": "flushed (512 MiB write) between timed steps, then a device barrier of all ranks",
         "tokens_per_s": toks_job / t_job,
         "kernel_ms_rank0": phases,
         "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
@@ -867,22 +889,114 @@ def cpu_baseline(cfg, batches, budget_s=15.0):
 
 
 def run_reference(args, cfg):
+    """The reference arm: the reference's own CPU implementation of the path
+    (oracle/_ref/librsref.so, compiled from the reference sources; else the C
+    restatement) on this host's cores, on our arm's config / metric / batches
+    (the reference's own generator, same seeds) and the same K/W step schedule.
+    N = 1: ref_c1_step (distributed_lookup on SimCluster(1) + accumulate +
+    apply); N > 1: ref_dist_step (distributed_lookup over N simulated workers,
+    per-owner accumulate + apply, as run_workload, workload.cpp:506-581) on the
+    N ranks' batches of each step.  Under torchrun only rank 0 runs.  Nothing
+    of the product (librsgpu) is loaded in this process."""
+    import ctypes as C
     rank, world, local = dist_env()
     if rank != 0:
         return
     os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    from paper_2505_12663_b200 import workload as W  # host-side generator (same ids as the reference's)
-    nb = max(1, min(args.steps + args.warmup, 4))
-    batches = [W.generate(cfg["seed"] + b, cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"], cfg["zipf"],
-                          [cfg["vocab"]]) for b in range(nb)]
-    cb = cpu_baseline(cfg, batches, budget_s=args.cpu_seconds)
-    res = {"metric": "unique-ID lookups+updates/sec", "value": cb["value"], "unit": "unique-ids/s", "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32 rows, f64 optimizer math, u64 ids",
-           "data": "synthetic: the reference's generator", "config": {"workload": cfg["workload"]},
-           "impl": "reference", "cpu_baseline": cb,
-           "e2e": {"value": cb["value"], "unit": "unique-ids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    from oracle import bind
+    kind = "reference" if bind.ref_available() else "port"
+    o = bind.Oracle("ref" if kind == "reference" else "oracle")
+    dim, vocab = cfg["dim"], cfg["vocab"]
+    nb = n_batches(args.warmup)
+    batches = []  # [b][r] = (ids, grads) of rank r's batch b
+    for b in range(nb):
+        per = []
+        for r in range(world):
+            lengths, ids = o.generate(batch_seed(cfg, r, b), cfg["seqs"], cfg["mean"], cfg["max_len"], cfg["sigma"],
+                                      cfg["zipf"], [vocab])
+            per.append((ids, o.token_grads(lengths, b, dim)))
+        batches.append(per)
+    h = C.c_void_p()
+    assert o.cluster_create(world, max(cfg["capacity"] // (2 * world), 1 << 16), dim, 1, 0.75, 1 << 16, 3,
+                            C.byref(h)) == 0
+    keys = np.arange(vocab, dtype=np.uint64) + TAG1
+    row = np.zeros(dim, np.float32)
+    shards = [bind.Table(o, 0, dim, handle=o.cluster_shard(h, s)) for s in range(world)]
+    for t in shards:
+        t.owned = False
+    for r in range(vocab):
+        o.pseudo_sparse_grad(r, 0, row, dim)
+        shards[int(o.shard_of(int(keys[r]), world)) if world > 1 else 0].insert(int(keys[r]), row)
+    uniq_b = [sum(len(np.unique(ids)) for ids, _ in per) for per in batches]
+
+    def one(b):
+        per = batches[b]
+        if world == 1 and kind == "reference":
+            ids, g = per[0]
+            return o.c1_step(h, ids, g.reshape(-1), len(ids), 1, 0.01, 1e-8, None)
+        if kind == "reference":
+            flat = np.ascontiguousarray(np.concatenate([ids for ids, _ in per]))
+            cnt = np.array([len(ids) for ids, _ in per], np.uint64)
+            g = np.ascontiguousarray(np.concatenate([g for _, g in per]).reshape(-1))
+            return o.dist_step(h, flat, cnt, g, 1, 0.01, 1e-8)
+        t0 = time.perf_counter()  # the C restatement: same sequence of reference operations
+        flat = np.ascontiguousarray(np.concatenate([ids for ids, _ in per]))
+        cnt = np.array([len(ids) for ids, _ in per], np.uint64)
+        out = np.zeros(len(flat) * dim, np.float32)
+        z = np.zeros(world * world, np.uint64)
+        o.distributed_lookup(h, flat, cnt, out, z, z.copy(), np.zeros(world, np.uint64), np.zeros(2, np.uint64))
+        g = np.concatenate([g for _, g in per])
+        own = np.array([o.shard_of(int(k), world) for k in flat]) if world > 1 else np.zeros(len(flat), int)
+        for s_ in range(world):
+            sel = np.nonzero(own == s_)[0]
+            if len(sel):
+                ia, sa = o.accumulate_np(flat[sel], g[sel], dim)
+                o.apply(o.cluster_shard(h, s_), ia, sa.reshape(-1), len(ia), 1, 0.01, 0.9, 0.999, 1e-8)
+        return time.perf_counter() - t0
+
+    for k in range(args.warmup):
+        one(k % nb)
+    times, uniq = [], 0
+    for k in range(args.warmup, args.warmup + args.steps):
+        times.append(one(k % nb))
+        uniq += uniq_b[k % nb]
+    o.cluster_destroy(h)
+    t = sum(times)
+    cpu = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            cpu = next(l.split(":", 1)[1].strip() for l in f if l.startswith("model name"))
+    except Exception:
+        pass
+    cores = o.omp_max_threads() if kind == "reference" else 1
+    value = uniq / t
+    sample = (f"{args.steps} timed steps after {args.warmup} warm-up steps over the {nb} batches of every rank "
+              f"({'ref_c1_step: distributed_lookup W=1' if world == 1 else f'ref_dist_step: distributed_lookup W={world} (single-threaded simulation)'}"
+              f" + accumulate + apply, OpenMP rows), {cpu}, nproc={os.cpu_count()}")
+    res = {"metric": "unique-ID lookups+updates/sec", "value": value, "unit": "unique-ids/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / len(times) * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32 rows, f64 optimizer math, u64 ids",
+           "data": "synthetic: the reference's generator (mt19937_64, truncated lognormal lengths, Zipf 1.1 ids), "
+                   "pseudo_sparse_grad gradients",
+           "config": bench_config(cfg, world, nb, world > 1),
+           "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": "unique-ids/s", "cores": cores, "kind": kind, "sample": sample},
+           "e2e": {"value": value, "unit": "unique-ids/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(res), flush=True)
+
+
+def self_launch(args):
+    """--gpus N without a torchrun environment: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -900,11 +1014,20 @@ def main():
     ap.add_argument("--balance", default="lpt", choices=["lpt", "rr"], help="config 5 rank assignment")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)  # does not return
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}; "
+              "n_gpus reports WORLD_SIZE", file=sys.stderr)
     if args.config == "c2" and args.impl == "ours":
         run_c2(args, C2)
     elif args.config == "c3" and args.impl == "ours":
         run_c3(args, C3)
     elif args.impl == "reference":
+        if args.config != "c1":
+            print(json.dumps({"impl": "reference", "unavailable": f"the reference arm is timed on config 1 only "
+                              f"(--config {args.config} is a parity/extra config of this repo)"}))
+            return
         run_reference(args, C1)
     elif args.config == "c5":
         run_sharded(args, C5)

@@ -111,6 +111,7 @@ class Oracle:
               C.c_double, C.c_double, C.c_double, C.c_int)
             f("c1_step", C.c_double, vp, u64p, f32p, C.c_uint64, C.c_int, C.c_double, C.c_double,
               vp)
+            f("dist_step", C.c_double, vp, u64p, u64p, f32p, C.c_int, C.c_double, C.c_double)
             f("omp_max_threads", C.c_int)
         else:
             f("table_export", C.c_size_t, vp, vp, vp, vp, vp, vp, vp)

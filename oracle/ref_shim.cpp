@@ -459,6 +459,32 @@ void ref_pseudo_sparse_grad(uint64_t sample_id, uint64_t step, float* out, uint3
 // then GradAccumulator::accumulate + apply (OpenMP rows).  Adam is the
 // reference's; optimizer=1 (Adagrad) has no reference and runs the frozen
 // restatement of oracle.c on the reference's table rows.  Returns seconds.
+// Adagrad has no reference: the frozen restatement of oracle.c on the
+// reference's rows (ascending id, ensure per id, OpenMP rows like apply).
+static void adagrad_apply(EmbedTable& t, const GradAccumulator& acc, double lr, double eps) {
+  const uint32_t dim = t.embedding_dim();
+  std::vector<RowHandle> hs;
+  std::vector<const std::vector<float>*> gs;
+  for (const auto& [id, g] : acc.pending()) {
+    hs.push_back(t.ensure(id));
+    gs.push_back(&g);
+  }
+  const int64_t m = static_cast<int64_t>(hs.size());
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < m; ++i) {
+    auto w = t.embedding(hs[i]);
+    auto a = t.opt_v(hs[i]);
+    t.opt_step(hs[i]) += 1;
+    const std::vector<float>& g = *gs[i];
+    for (uint32_t e = 0; e < dim; ++e) {
+      const double gd = g[e];
+      const double an = a[e] + gd * gd;
+      a[e] = static_cast<float>(an);
+      w[e] = static_cast<float>(w[e] - lr * gd / (std::sqrt(an) + eps));
+    }
+  }
+}
+
 double ref_c1_step(void* cluster, const uint64_t* ids, const float* grads, uint64_t n,
                    int optimizer, double lr, double eps, float* out) {
   auto* c = static_cast<SimCluster*>(cluster);
@@ -468,34 +494,59 @@ double ref_c1_step(void* cluster, const uint64_t* ids, const float* grads, uint6
   LookupResult r = distributed_lookup(*c, req);
   GradAccumulator acc(dim, 1);
   acc.accumulate(req[0], std::span<const float>(grads, n * dim));
-  if (optimizer == 0) {
+  if (optimizer == 0)
     acc.apply(c->shards[0], AdamParams{lr, 0.9, 0.999, eps});
-  } else {
-    EmbedTable& t = c->shards[0];
-    std::vector<RowHandle> hs;
-    std::vector<const std::vector<float>*> gs;
-    for (const auto& [id, g] : acc.pending()) {
-      hs.push_back(t.ensure(id));
-      gs.push_back(&g);
-    }
-    const int64_t m = static_cast<int64_t>(hs.size());
-#pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < m; ++i) {
-      auto w = t.embedding(hs[i]);
-      auto a = t.opt_v(hs[i]);
-      t.opt_step(hs[i]) += 1;
-      const std::vector<float>& g = *gs[i];
-      for (uint32_t e = 0; e < dim; ++e) {
-        const double gd = g[e];
-        const double an = a[e] + gd * gd;
-        a[e] = static_cast<float>(an);
-        w[e] = static_cast<float>(w[e] - lr * gd / (std::sqrt(an) + eps));
-      }
-    }
-  }
+  else
+    adagrad_apply(c->shards[0], acc, lr, eps);
   const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (out) std::memcpy(out, r.outputs[0].data(), r.outputs[0].size() * 4);
   return sec;
+}
+
+// One W-worker step exactly as run_workload drives it (workload.cpp:506-581):
+// distributed_lookup over the W workers' token lists, every token's gradient
+// routed to its owner in (worker, token) order (workload.cpp:519-526), one
+// GradAccumulator per owner shard (:565-569), then apply (:573-581).  The
+// simulation is single-threaded by the reference's design; the row updates
+// inside apply use OpenMP.  requests = the W lists concatenated, counts[W].
+// Returns seconds.
+double ref_dist_step(void* cluster, const uint64_t* requests, const uint64_t* counts, const float* grads,
+                     int optimizer, double lr, double eps) {
+  auto* c = static_cast<SimCluster*>(cluster);
+  const uint64_t W = c->world_size;
+  const uint32_t dim = c->shards[0].embedding_dim();
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::vector<uint64_t>> req(W);
+  uint64_t off = 0;
+  for (uint64_t w = 0; w < W; ++w) {
+    req[w].assign(requests + off, requests + off + counts[w]);
+    off += counts[w];
+  }
+  LookupResult r = distributed_lookup(*c, req);
+  (void)r;
+  std::vector<std::vector<uint64_t>> gid(W);
+  std::vector<std::vector<float>> grow(W);
+  off = 0;
+  for (uint64_t w = 0; w < W; ++w) {
+    for (uint64_t j = 0; j < counts[w]; ++j) {
+      const uint64_t id = requests[off + j];
+      const size_t s = SimCluster::shard_of(id, W);
+      gid[s].push_back(id);
+      grow[s].insert(grow[s].end(), grads + (off + j) * dim, grads + (off + j + 1) * dim);
+    }
+    off += counts[w];
+  }
+  std::vector<GradAccumulator> acc;
+  for (uint64_t s = 0; s < W; ++s) acc.emplace_back(dim, 1);
+  for (uint64_t s = 0; s < W; ++s)
+    if (!gid[s].empty()) acc[s].accumulate(gid[s], grow[s]);
+  for (uint64_t s = 0; s < W; ++s) {
+    if (optimizer == 0)
+      acc[s].apply(c->shards[s], AdamParams{lr, 0.9, 0.999, eps});
+    else
+      adagrad_apply(c->shards[s], acc[s], lr, eps);
+  }
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 int ref_omp_max_threads() { return omp_get_max_threads(); }
 
