@@ -902,7 +902,8 @@ def run_reference(args, cfg):
     rank, world, local = dist_env()
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+    # every host core (torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 is the only worker here)
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     from oracle import bind
     kind = "reference" if bind.ref_available() else "port"
     o = bind.Oracle("ref" if kind == "reference" else "oracle")
