@@ -116,6 +116,7 @@ _SIGS = {
     "rs_sparse_update": (C.c_int, [vp, vp, vp, u64, vp, C.POINTER(rs_optimizer_params), vp]),
     "rs_workspace_results": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)]),
     "rs_workspace_set_profiling": (C.c_int, [vp, C.c_int]),
+    "rs_workspace_trace": (C.c_int, [vp, vp, u64, C.POINTER(u64)]),
     "rs_workspace_phase_ms": (C.c_int, [vp, vp, u32, C.POINTER(u64)]),
     "rs_workspace_unique": (C.c_int, [vp, vp, u64, C.POINTER(u64)]),
     "rs_workspace_n_unique": (C.c_int, [vp, C.POINTER(u64)]),

@@ -65,6 +65,7 @@ struct rs_graph_entry {
   cudaGraphExec_t exec = nullptr;
   uint64_t last_use = 0;
   uint64_t launches = 0;  // rsgpu kernels inside the graph
+  bool fast = false;      // the step_fast.cu graph
 };
 
 // One dedup scratch hash set (SoA, S+1 slots; slot S holds the id equal to
@@ -81,7 +82,39 @@ struct rs_scratch {
   uint32_t* cnt = nullptr;      // device [0] = unique ids in the set
 };
 
+// Scratch of the single-GPU fast step (step_fast.cu), allocated on the first
+// rs_step: two alternating sets of 16-byte records {key, count, row} (each
+// step cleans the other set from its dirty list), plus per-slot unique /
+// hot indices, token positions (64 per slot) and the hot-id partial lists.
+struct rs_fast_set {
+  void* rec = nullptr;           // [S + 1] records
+  uint32_t* u_slot = nullptr;    // slot of each unique id (dirty list)
+  uint32_t* cnt = nullptr;       // device [0] unique ids
+};
+struct rs_fast {
+  bool ready = false;
+  rs_fast_set set[2];
+  int cur = 0;                   // set the next fast step uses
+  int last = 0;                  // set of the last fast step
+  uint32_t* uidx = nullptr;      // [S + 1]
+  uint32_t* hidx = nullptr;      // [S + 1] hot index (~0 between steps)
+  uint32_t* pos = nullptr;       // [(S + 1) x 64] token positions
+  uint32_t* hot_slot = nullptr;  // [max_hot]
+  uint32_t* hlist = nullptr;     // [max_hot x ntiles]
+  uint32_t* ctr = nullptr;       // [0] hot ids [1] partials [2] error bits
+  double* tokcs = nullptr;       // [max_tokens] per-token row sums (rs_step_checksum)
+  unsigned long long* trace = nullptr;  // RS_TRACE=1: per (kernel, block) start / end timeline
+  uint64_t ntiles = 0, max_hot = 0;
+  uint32_t hot_min = 64;         // ids with more occurrences take the hot path (RS_HOT_MIN)
+  cudaStream_t aux2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_j1 = nullptr, ev_j2 = nullptr;
+};
+
 struct rs_workspace {
+  rs_fast fast;
+  bool use_fast = true;     // rs_step on unbounded tables: step_fast.cu (RS_FAST_STEP=0: the split kernels)
+  bool last_fast = false;   // the last op was a fast step (its unique count lives in fast.set[fast.last])
+  bool last_exact = false;  // the last op was rs_dedup (first-occurrence numbering)
   // KC split (RS_SPLIT_KC=0: one pass): the hot-id pass is launched by the finish
   bool split_kc = true;
   bool kc_forked = false;  // the hot tile pass was launched on aux_stream (launch_finish joins)
@@ -227,4 +260,10 @@ int step_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, const float*
                 const void* opt_args, float* sums_out, cudaStream_t s, const rs_dist_opts* dopt);
 int step_opt_args(rs_table* t, const rs_optimizer_params* p, void* out, cudaStream_t s);
 int step_reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s);
+// step_fast.cu
+bool fast_step_supported(const rs_table* t);
+int fast_prepare(rs_workspace* ws);
+void fast_free(rs_workspace* ws);
+int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
+                 float* d_out, const void* opt_args, int use, cudaStream_t s, cudaEvent_t* ev, bool fork);
 }  // namespace rs

@@ -1724,6 +1724,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
   if (const char* e = getenv("RS_GRAPH_FORK")) ws->graph_fork = e[0] != '0';
   if (const char* e = getenv("RS_SPLIT_KC")) ws->split_kc = e[0] != '0';
   if (const char* e = getenv("RS_PDL")) ws->pdl = e[0] != '0';
+  if (const char* e = getenv("RS_FAST_STEP")) ws->use_fast = e[0] != '0';
   uint64_t S_ = 1024;
   while (S_ < 2 * max_tokens) S_ <<= 1;
   ws->S = S_;
@@ -1773,6 +1774,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
 int rs_workspace_destroy(rs_workspace* ws) {
   if (!ws) return RS_OK;
   cudaDeviceSynchronize();
+  fast_free(ws);
   for (auto& x : ws->set) {
     void* ps[] = {x.skey, x.sfirstx, x.sntile, x.suidx, x.srow, x.u_slot, x.cnt};
     for (void* p : ps)
@@ -1813,6 +1815,9 @@ int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_un
     RS_CUDA(cudaMemsetAsync(ws->set[use].cnt, 0, 4, s));
     RS_CUDA(cudaMemsetAsync(sc.cnt, 0, 4, s));
     if (d_n_unique) RS_CUDA(cudaMemsetAsync(d_n_unique, 0, sizeof(uint32_t), s));
+    ws->last_set = use;
+    ws->last_fast = false;
+    ws->last_exact = true;
     ws->cur ^= 1;
     return RS_OK;
   }
@@ -1832,6 +1837,8 @@ int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_un
   k_copy_unique<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->unique, su.cnt, d_unique, d_n_unique);
   RS_LAUNCH_CHECK("k_copy_unique");
   ws->last_set = use;
+  ws->last_fast = false;
+  ws->last_exact = true;
   ws->cur ^= 1;
   ws->last_n = n;
   return RS_OK;
@@ -1858,6 +1865,8 @@ int rs_forward(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n,
   if (st) return st;
   if (!t->cfg.max_keys && (st = table_after_op(t, s))) return st;
   ws->last_set = use;
+  ws->last_fast = false;
+  ws->last_exact = false;
   ws->cur ^= 1;
   ws->have_forward = true;
   return RS_OK;
@@ -1986,14 +1995,21 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   ws->last_tile = tile_tokens_for_dim(t->desc.dim);
   if ((st = reduce_prepare(ws, t->desc.dim, n, s))) return st;
   const int mirror = t->mirror_next;
-  const int use = ws->cur;
+  // unbounded tables: the fast step (step_fast.cu) on its own scratch sets
+  const bool fast = ws->use_fast && d_grads && ((uintptr_t)d_grads & 15u) == 0 && fast_step_supported(t);
+  if (fast && (st = fast_prepare(ws))) return st;
+  const int use = fast ? ws->fast.cur : ws->cur;
+  auto enqueue = [&](cudaStream_t q, cudaEvent_t* ev) -> int {
+    if (!fast) return step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, q, ev);
+    const int e = fast_enqueue(ws, t, d_ids, n, d_grads, d_out, &o, use, q, ev, ws->fork);
+    return e ? e : table_mirror_copy(t, mirror, q);
+  };
   if (ws->profiling || !ws->use_graphs) {
     // profiling runs the kernels one after another (no fork) so that every
     // phase's events bracket only its own kernels
     const bool f0 = ws->fork;
     if (ws->profiling) ws->fork = false;
-    st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, s,
-                      ws->profiling ? ws->prof_ev : nullptr);
+    st = enqueue(s, ws->profiling ? ws->prof_ev : nullptr);
     ws->fork = f0;
     if (st) return st;
     if (ws->profiling) {
@@ -2011,7 +2027,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
     for (auto& g : ws->graphs) {
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
           g.csum == ws->csum_dst &&
-          g.mirror == mirror && g.set == use && g.pbuf == ws->pbuf && g.tcap == t->capacity &&
+          g.mirror == mirror && g.set == use && g.fast == fast && g.pbuf == ws->pbuf && g.tcap == t->capacity &&
           g.tgen == t->buf_gen &&
           std::memcmp(g.opt, &o, sizeof(o)) == 0) {
         hit = &g;
@@ -2036,6 +2052,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
       e.n = n;
       e.mirror = mirror;
       e.set = use;
+      e.fast = fast;
       e.pbuf = ws->pbuf;
       e.tcap = t->capacity;
       e.tgen = t->buf_gen;
@@ -2046,7 +2063,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
       // a forked branch inside the captured graph measured slower: linear graph
       const bool fork = ws->fork;
       ws->fork = ws->fork && ws->graph_fork;
-      st = step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, cs, nullptr);
+      st = enqueue(cs, nullptr);
       ws->fork = fork;
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(cs, &g);
@@ -2069,8 +2086,16 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   }
   ws->last_n = n;
   ws->last_table = t;
-  ws->last_set = use;
-  ws->cur ^= 1;
+  ws->last_exact = false;
+  if (fast) {
+    ws->fast.last = use;
+    ws->fast.cur ^= 1;
+    ws->last_fast = true;
+  } else {
+    ws->last_set = use;
+    ws->cur ^= 1;
+    ws->last_fast = false;
+  }
   ws->have_forward = false;
   t->applies++;
   return table_mirror_commit(t, mirror, s);
@@ -2099,17 +2124,26 @@ int rs_sparse_update(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   if ((st = launch_finish(ws, t, use, n, d_grads, o, nullptr, s))) return st;
   if (!t->cfg.max_keys && (st = table_after_op(t, s))) return st;
   ws->last_set = use;
+  ws->last_fast = false;
+  ws->last_exact = false;
   ws->cur ^= 1;
   t->applies++;
   return RS_OK;
 }
 
+static const uint32_t* last_count(const rs_workspace* ws) {
+  return ws->last_fast ? ws->fast.set[ws->fast.last].cnt : ws->set[ws->last_set].cnt;
+}
+
 int rs_workspace_results(rs_workspace* ws, const uint64_t** d_unique, const int32_t** d_inverse,
                          const uint32_t** d_n_unique, const int64_t** d_rows) {
   if (!ws) return fail(RS_ERR_CONFIG, "rs_workspace_results: null workspace");
+  if (!ws->last_exact)
+    return fail(RS_ERR_CONFIG, "rs_workspace_results: the unique ids of rs_forward / rs_step are numbered in "
+                               "unspecified order; rs_dedup gives stage1_dedup's first-occurrence order");
   if (d_unique) *d_unique = ws->unique;
   if (d_inverse) *d_inverse = ws->inverse;
-  if (d_n_unique) *d_n_unique = ws->set[ws->last_set].cnt;
+  if (d_n_unique) *d_n_unique = last_count(ws);
   if (d_rows) *d_rows = ws->urow64;
   return RS_OK;
 }
@@ -2118,7 +2152,7 @@ int rs_workspace_unique(rs_workspace* ws, uint64_t* d_out, uint64_t cap, uint64_
   if (!ws || !n_out) return fail(RS_ERR_CONFIG, "rs_workspace_unique: null argument");
   RS_CUDA(cudaDeviceSynchronize());
   uint32_t n = 0;
-  RS_CUDA(cudaMemcpy(&n, ws->set[ws->last_set].cnt, 4, cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(&n, last_count(ws), 4, cudaMemcpyDeviceToHost));
   *n_out = n;
   if (d_out) {
     if (cap < n) return fail(RS_ERR_CONFIG, "rs_workspace_unique: buffer too small");
@@ -2149,7 +2183,7 @@ int rs_workspace_n_unique(rs_workspace* ws, uint64_t* out) {
   if (!ws || !out) return fail(RS_ERR_CONFIG, "rs_workspace_n_unique: null argument");
   RS_CUDA(cudaDeviceSynchronize());
   uint32_t n = 0;
-  RS_CUDA(cudaMemcpy(&n, ws->set[ws->last_set].cnt, 4, cudaMemcpyDeviceToHost));
+  RS_CUDA(cudaMemcpy(&n, last_count(ws), 4, cudaMemcpyDeviceToHost));
   *out = n;
   return RS_OK;
 }

@@ -1,0 +1,1111 @@
+// step_fast.cu -- the single-GPU training step (rs_step / rs_step_checksum on
+// an unbounded table): one dedup + probe kernel, then two concurrent
+// branches that each own a disjoint set of ids (and so of table rows).
+//
+// Reference caller: run_workload (workload.cpp:506-581) with
+// distributed_lookup at W = 1 (stage1_dedup + ensure + inverse expand,
+// exchange_sim.cpp:117-233), then GradAccumulator::accumulate + apply
+// (sparse_update.cpp:45-83).
+//
+//   KA  k_fa   per 256-token tile: tile-local dedup in smem, one scratch
+//              insert per (tile, id) into 16-byte records {key, count, row};
+//              each token's position stored at pos[slot * 64 + rank] (rank
+//              = tile base from the count atomic + rank in the tile, any
+//              order: KD sorts); the tile that claims an id numbers it and
+//              resolves its table row right away (find-or-insert-zero,
+//              grouped bucket probing); cleans the other scratch set; the
+//              last block folds the table counters.
+//   then, forked (both need only KA):
+//   KD  k_fc   per unique id with <= 64 occurrences (G = D/4 lanes): loads
+//              its row, writes it to each of its tokens (the forward
+//              gather), ranks its positions in registers, sums its gradient
+//              rows in token order (the reference's accumulate order:
+//              bit-exact), optimizer
+//   KH  k_fh   per tile: tokens of hot ids (> 64 occurrences) grouped by id;
+//              each group's row to its tokens (the forward), its (tile, id)
+//              partial summed in token order straight from the gradient rows
+//   KF  k_fhf  per hot id: its tile partials in tile order, optimizer
+//              (KH -> KF on one branch: KF updates a hot row after KH read it)
+//   KS  k_fcs  rs_step_checksum only: the f64 sum of the forward rows
+// Every token's row is written once and every gradient row read once; the
+// pre-update rows of an id are read by the same branch that updates them.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "opt_dev.cuh"
+#include "rs_host.hpp"
+#include "table_dev.cuh"
+
+namespace rs {
+namespace {
+
+using namespace odev;
+using namespace tdev;
+
+constexpr uint32_t kPosMax = 64;  // exact-order (CSR) path limit == step.cu kCsrMax
+constexpr uint32_t kTT = 256;     // tokens per tile
+constexpr uint32_t kHotNone = 0xFFFFFFFFu, kHotClaim = 0xFFFFFFFEu;
+
+struct __align__(16) Rec {
+  unsigned long long key;
+  uint32_t cnt;  // occurrences of the id in the batch
+  uint32_t row;  // table row
+};
+
+struct FSet {
+  Rec* rec;         // [S + 1]; slot S holds the id equal to the empty sentinel
+  uint32_t* u_slot; // slot of each unique id (the set's dirty list)
+  uint32_t* cnt;    // [0] unique ids in the set
+  uint64_t smask, spare;
+};
+
+struct FShared {
+  uint32_t* uidx;      // [S + 1] unique index of a slot (written before read each step)
+  uint32_t* hidx;      // [S + 1] hot index of a slot (kHotNone between steps)
+  uint32_t* pos;       // [(S + 1) * 64] token positions per slot
+  uint32_t* hot_slot;  // [max_hot]
+  uint32_t* hlist;     // [max_hot * ntiles] partial index + 1 of (hot id, tile), 0 = none
+  float* part;         // partial rows
+  uint32_t* ctr;       // [0] hot ids [1] partials [2] error bits [3] clean blocks
+  uint32_t ntiles;
+  uint32_t hot_min;    // ids with more occurrences take the hot (tile partial) path, <= 64
+  unsigned long long* trace;  // diagnostics timeline or null
+};
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+// Device-side timeline (rs_workspace_trace, diagnostics): per (kernel, block)
+// the first warp start and the last warp end (%globaltimer, ns).
+constexpr uint32_t kTraceBlocks = 4096;
+// phase mark of a block (thread 0): kernel slot kid, end time = now
+__device__ __forceinline__ void trace_mark(unsigned long long* base, uint32_t kid) {
+  if (base && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned long long* p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
+    atomicMin(p, t);
+    atomicMax(p + 1, t);
+  }
+}
+struct WarpTrace {
+  unsigned long long* p = nullptr;
+  __device__ __forceinline__ WarpTrace(unsigned long long* base, uint32_t kid) {
+    if (base && (threadIdx.x & 31) == 0 && blockIdx.x < kTraceBlocks) {
+      p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMin(p, t);
+    }
+  }
+  __device__ __forceinline__ ~WarpTrace() {
+    if (p) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p + 1, t);
+    }
+  }
+};
+
+// Global scratch insert (linear probing on the low hash bits) into the
+// 16-byte records.  first0: the start record's key read early by the caller.
+__device__ __forceinline__ uint64_t rec_insert(const FSet& S, uint64_t id, uint64_t h, bool* fresh,
+                                               unsigned long long first0) {
+  if (id == kEmptyKey) {
+    *fresh = atomicCAS(&S.rec[S.spare].key, kEmptyKey, 0ull) == kEmptyKey;
+    return S.spare;
+  }
+  uint64_t gs = h & S.smask;
+  bool use0 = true;
+  for (;;) {
+    const unsigned long long cur = use0 ? first0 : __ldcg(&S.rec[gs].key);
+    use0 = false;
+    if (cur == id) {
+      *fresh = false;
+      return gs;
+    }
+    if (cur != kEmptyKey) {
+      gs = (gs + 1) & S.smask;
+      continue;
+    }
+    const unsigned long long prev = atomicCAS(&S.rec[gs].key, kEmptyKey, (unsigned long long)id);
+    if (prev == kEmptyKey) {
+      *fresh = true;
+      return gs;
+    }
+    if (prev == id) {
+      *fresh = false;
+      return gs;
+    }
+    gs = (gs + 1) & S.smask;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KA: dedup + positions + probe of the ids this tile claims.  blockDim == kTT.
+struct FaArgs {
+  const uint64_t* ids;
+  uint32_t n;
+  FSet use, clean;
+  FShared sh;
+  TableDev* td;
+  uint32_t* slot_of;
+  uint64_t* unique;
+  uint32_t* urow;
+  int64_t* urow64;
+};
+
+__global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
+  WarpTrace wt_(a.sh.trace, 0);
+  constexpr uint32_t L = 2 * kTT;
+  __shared__ unsigned long long lkey[L + 1];
+  __shared__ uint32_t lbase[L + 1], lslot[L + 1], lnew[L + 1], lcnt[L + 1];
+  __shared__ unsigned long long fid[kTT];
+  __shared__ uint32_t fslot[kTT], fu[kTT];
+  __shared__ uint32_t s_nnew, s_base;
+  __shared__ unsigned long long s_ins, s_reuse;
+  TableDev* td = a.td;
+  const TableDesc d = td->d;
+  const unsigned long long free_n0 = td->c.free_n;
+  const unsigned long long fresh0 = td->c.fresh_next;
+  const uint32_t tick_now = td->c.tick + 1;
+  const uint32_t tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) {  // this step's hot-id / partial counters (KH, KF follow KA)
+    a.sh.ctr[0] = 0;
+    a.sh.ctr[1] = 0;
+  }
+  for (uint32_t i = tid; i <= L; i += kTT) {
+    lkey[i] = kEmptyKey;
+    lnew[i] = 0;
+    lcnt[i] = 0;
+  }
+  if (tid == 0) {
+    s_nnew = 0;
+    s_ins = 0;
+    s_reuse = 0;
+  }
+  __syncthreads();
+  const uint32_t t = blockIdx.x * kTT + tid;
+  const bool valid = t < a.n;
+  uint64_t id = 0, h = 0;
+  uint32_t p = 0, lr = 0;
+  bool rep = false;
+  unsigned long long first0 = kEmptyKey;
+  if (valid) {
+    id = a.ids[t];
+    h = hash64(id);
+    // the start record's key, read now: overlaps the tile-local dedup below
+    if (id != kEmptyKey) first0 = __ldcg(&a.use.rec[h & a.use.smask].key);
+    if (id == kEmptyKey) {
+      p = L;
+      rep = atomicCAS(&lkey[p], kEmptyKey, 0ull) == kEmptyKey;
+    } else {
+      p = (uint32_t)(h >> 40) & (L - 1);
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&lkey[p], kEmptyKey, (unsigned long long)id);
+        if (prev == kEmptyKey) {
+          rep = true;
+          break;
+        }
+        if (prev == id) break;
+        p = (p + 1) & (L - 1);
+      }
+    }
+    lr = atomicAdd(&lcnt[p], 1u);  // rank within the tile (any order: KD sorts)
+  }
+  __syncthreads();
+  if (rep) {
+    bool fresh = false;
+    const uint64_t gs = rec_insert(a.use, id, h, &fresh, first0);
+    lbase[p] = atomicAdd(&a.use.rec[gs].cnt, lcnt[p]);  // the tile's base among the id's occurrences
+    lslot[p] = (uint32_t)gs;
+    if (fresh) {
+      // the probe below starts at this bucket: fetch it into L2 now (overlaps
+      // the numbering barriers)
+      if (id != kEmptyKey && id != kTombKey)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(d.slots + ((h >> 32) & d.nb_mask) * kBucket));
+      const uint32_t k = atomicAdd(&s_nnew, 1u);
+      lnew[p] = k + 1;
+      fid[k] = id;
+      fslot[k] = (uint32_t)gs;
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && s_nnew) s_base = atomicAdd(a.use.cnt, s_nnew);
+  __syncthreads();
+  const uint32_t nnew = s_nnew;
+  if (rep && lnew[p]) {
+    const uint32_t k = lnew[p] - 1, u = s_base + k;
+    const uint32_t gs = lslot[p];
+    fu[k] = u;
+    a.sh.uidx[gs] = u;
+    a.use.u_slot[u] = gs;
+    a.unique[u] = id;
+  }
+  if (valid) {
+    const uint32_t gs = lslot[p];
+    a.slot_of[t] = gs;
+    const uint32_t rank = lbase[p] + lr;
+    if (rank < kPosMax) a.sh.pos[(size_t)gs * kPosMax + rank] = t;
+  }
+  __syncthreads();
+  // the ids this tile claimed: find-or-insert-zero in the table, 8 lanes per id
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  for (uint32_t k = tid >> 3; k < nnew; k += kTT / kBucket) {
+    const uint64_t key = fid[k];
+    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins,
+                                              &s_reuse);
+    if (g == 0) {
+      a.use.rec[fslot[k]].row = row;
+      a.urow[fu[k]] = row;
+      a.urow64[fu[k]] = row == kNoRow ? -1 : (int64_t)row;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_ins) atomicAdd(&td->c.inserted, s_ins);
+    if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
+  }
+  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  // (launch_epilogue's last block has folded the counters; every block ran it)
+}
+
+// The previous step's scratch set goes back to empty records (its dirty
+// list), off the critical path beside KD / KH; the last block zeroes its
+// count (the next step's KA inserts into it).
+__global__ void __launch_bounds__(256) k_fclean(FSet c, unsigned int* done, unsigned long long* trace) {
+  WarpTrace wt_(trace, 4);
+  const uint32_t prev = *c.cnt;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= prev;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t sl = i < prev ? c.u_slot[i] : c.spare;
+    c.rec[sl] = Rec{kEmptyKey, 0u, kNoRow};
+  }
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    *c.cnt = 0;
+    *done = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KS (rs_step_checksum only): run_workload's emb_checksum (workload.cpp:
+// 547-549) = the f64 sum of every gathered value.  KD / KH store each token's
+// row sum (fixed lane tree); here per tile a fixed tree, then the last block
+// sums the tile partials in tile order -- deterministic.
+__global__ void __launch_bounds__(kTT) k_fcs(const double* __restrict__ tokcs, uint32_t n, double* out,
+                                             double* part, unsigned int* ticket) {
+  constexpr uint32_t NW = kTT / 32;
+  __shared__ double s_cs[NW];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const uint32_t t = blockIdx.x * kTT + tid;
+  double cs = t < n ? tokcs[t] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cs += __shfl_xor_sync(kFull, cs, o);
+  if (lane == 0) s_cs[warp] = cs;
+  __syncthreads();
+  if (warp == 0) {
+    double x = lane < NW ? s_cs[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    unsigned last = 0;
+    if (lane == 0) {
+      part[blockIdx.x] = x;
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    if (__shfl_sync(kFull, last, 0)) {
+      __threadfence();
+      double y = 0.0;
+      for (uint32_t b = lane; b < gridDim.x; b += 32) y += __ldcg(part + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(kFull, y, o);
+      if (lane == 0) {
+        *out = y;
+        *ticket = 0;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KD: ids with <= 64 occurrences.  G lanes per id, each owning NV float4
+// chunks of the row (chunk gl + j*G).  Positions ranked within the group
+// (shuffles), written sorted to smem, gradient rows summed in position order
+// = the reference's accumulate order (sparse_update.cpp:49-54) -> bit-exact.
+struct FcArgs {
+  const TableDev* td;
+  FSet use;
+  FShared sh;
+  const float* grads;
+  float* out;        // forward rows [n x D]
+  int32_t* inverse;  // [n]
+  double* tokcs;     // per-token row sums (checksum) or null
+  const uint32_t* urow;  // table row per unique id (KA)
+  uint32_t exp;          // timing experiments (RS_FC_EXP bits, wrong results): 1 no optimizer, 2 no grads, 4 no forward
+};
+
+#ifndef RS_FC_MINB
+#define RS_FC_MINB 5
+#endif
+template <int G, int NV>
+__global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, OptArgs o) {
+  WarpTrace wt_(a.sh.trace, 1);
+  constexpr int PPT = (int)(kPosMax / G);  // positions held per thread
+  __shared__ uint32_t order_s[(256 / G) * kPosMax];
+  const TableDesc d = a.td->d;
+  const uint32_t D4 = d.dim >> 2;
+  const uint32_t lane = lane_id();
+  const uint32_t gl = lane & (G - 1);
+  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (lane & ~(G - 1));
+  const uint32_t gpb = blockDim.x / G;
+  uint32_t* order = order_s + (threadIdx.x / G) * kPosMax;
+  const uint32_t gid = blockIdx.x * gpb + threadIdx.x / G;
+  const uint32_t ngroups = gridDim.x * gpb;
+  const uint32_t nu = *a.use.cnt;
+  const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grads);
+  float4* rw = reinterpret_cast<float4*>(d.emb);
+  float4* rv = reinterpret_cast<float4*>(d.s2);
+  float4* rm = reinterpret_cast<float4*>(d.s1);
+  for (uint32_t uu = gid; uu < nu; uu += ngroups) {
+    // slot and row in one round trip (KA's claiming tile wrote both), then the
+    // count, the positions (speculatively, all 64) and the row's state together
+    const uint32_t gs = __ldg(a.use.u_slot + uu);
+    const uint32_t row = __ldg(a.urow + uu);
+    if (row == kNoRow) continue;  // table error (reported through the counters)
+    const uint32_t c = __ldcg(&a.use.rec[gs].cnt);
+    uint32_t p[PPT], r[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      p[j] = __ldcg(a.sh.pos + (size_t)gs * kPosMax + gl + j * G);
+      r[j] = 0;
+    }
+    float4 wv[NV], vv[NV], mv[NV];
+    const size_t rbase = (size_t)row * D4 + gl;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      wv[j] = rw[rbase + j * G];
+      vv[j] = rv[rbase + j * G];
+      mv[j] = rm ? rm[rbase + j * G] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    uint32_t st0 = 0;
+    if (gl == 0) st0 = d.step[row];
+    if (c > a.sh.hot_min) continue;  // hot path (group-uniform)
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+      if (gl + j * G >= c) p[j] = kFull;
+    // rank every held position against all c positions of the id
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq) {
+      if ((uint32_t)(jq * G) >= c) break;
+      const uint32_t lim = min((uint32_t)G, c - (uint32_t)(jq * G));
+      for (uint32_t src = 0; src < lim; ++src) {
+        const uint32_t q = __shfl_sync(gmask, p[jq], src, G);
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) r[j] += q < p[j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PPT; ++j)
+      if (gl + j * G < c) order[r[j]] = p[j];
+    __syncwarp(gmask);
+    // the forward for this id: its pre-update row to each of its tokens
+    // (distributed_lookup's inverse expand, exchange_sim.cpp:211-230)
+    if (!(a.exp & 4)) {
+      float4* o4 = reinterpret_cast<float4*>(a.out);
+      for (uint32_t k = 0; k < c; ++k) {
+        const size_t ob = (size_t)order[k] * D4 + gl;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) __stcs(o4 + ob + j * G, wv[j]);
+      }
+      for (uint32_t k = gl; k < c; k += G) a.inverse[order[k]] = (int32_t)uu;
+      if (a.tokcs) {
+        double rs = 0.0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) rs += ((double)wv[j].x + (double)wv[j].y) + ((double)wv[j].z + (double)wv[j].w);
+#pragma unroll
+        for (int o2 = G / 2; o2 > 0; o2 >>= 1) rs += __shfl_xor_sync(gmask, rs, o2, G);
+        for (uint32_t k = gl; k < c; k += G) a.tokcs[order[k]] = rs;
+      }
+    }
+    float4 acc[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int B = NV == 1 ? 4 : 2;
+    constexpr int B2 = 2 * B;
+    uint32_t k = (a.exp & 2) ? c : 0;
+    for (; k + B2 <= c; k += B2) {
+      float4 x[B2][NV];
+#pragma unroll
+      for (int q = 0; q < B2; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) x[q][j] = g4[(size_t)order[k + q] * D4 + gl + j * G];
+#pragma unroll
+      for (int q = 0; q < B2; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          acc[j].x += x[q][j].x;
+          acc[j].y += x[q][j].y;
+          acc[j].z += x[q][j].z;
+          acc[j].w += x[q][j].w;
+        }
+    }
+    for (; k + B <= c; k += B) {
+      float4 x[B][NV];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) x[q][j] = g4[(size_t)order[k + q] * D4 + gl + j * G];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          acc[j].x += x[q][j].x;
+          acc[j].y += x[q][j].y;
+          acc[j].z += x[q][j].z;
+          acc[j].w += x[q][j].w;
+        }
+    }
+    for (; k < c; ++k) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        const float4 x = g4[(size_t)order[k] * D4 + gl + j * G];
+        acc[j].x += x.x;
+        acc[j].y += x.y;
+        acc[j].z += x.z;
+        acc[j].w += x.w;
+      }
+    }
+    __syncwarp(gmask);
+    uint32_t st = 0;
+    if (gl == 0) {
+      st = st0 + 1;
+      d.step[row] = st;
+    }
+    st = __shfl_sync(gmask, st, 0, G);
+    double bc1 = 1.0, bc2 = 1.0;
+    if (o.kind == RS_OPT_ADAM) {
+      if (st < o.bc_len) {
+        bc1 = o.bc[st];
+        bc2 = o.bc[o.bc_len + st];
+      } else {
+        bc1 = 1.0 - pow(o.b1, (double)st);
+        bc2 = 1.0 - pow(o.b2, (double)st);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      float* wp = reinterpret_cast<float*>(&wv[j]);
+      float* vp = reinterpret_cast<float*>(&vv[j]);
+      float* mp = reinterpret_cast<float*>(&mv[j]);
+      const float* gp = reinterpret_cast<const float*>(&acc[j]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (a.exp & 1)
+          wp[e] += gp[e];
+        else if (o.kind == RS_OPT_ADAM)
+          adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
+        else
+          adagrad_elem(wp[e], vp[e], gp[e], o);
+      }
+      rw[rbase + j * G] = wv[j];
+      rv[rbase + j * G] = vv[j];
+      if (rm) rm[rbase + j * G] = mv[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KH: per tile, the tokens of hot ids grouped by id (first occurrence
+// order), each group's gradient rows summed in token order straight from
+// global memory by one warp; the (tile, id) partial goes to part[], its
+// index to the id's tile list.
+struct FhArgs {
+  FSet use;
+  FShared sh;
+  const uint32_t* slot_of;
+  uint32_t n;
+  const float* grads;
+  uint32_t dim;
+  const float* emb;  // table rows (hot rows are not updated before KF)
+  float* out;
+  int32_t* inverse;
+  double* tokcs;
+};
+
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+template <int VEC, int CH>
+__global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
+  WarpTrace wt_(a.sh.trace, 2);
+  constexpr uint32_t L = 2 * kTT, NW = kTT / 32;
+  const uint32_t D = a.dim;
+  __shared__ uint32_t lkey[L], lfirst[L], lgroup[L];
+  __shared__ uint32_t gcnt[kTT], goff[kTT], gslot[kTT], grow[kTT], gpidx[kTT];
+  __shared__ uint16_t wcnt[NW * kTT];
+  __shared__ uint16_t csr[kTT];
+  __shared__ uint32_t wsum[32], s_ng, s_pbase, s_nhot;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const uint32_t tile = blockIdx.x, t0 = tile * kTT;
+  const uint32_t rows = min(kTT, a.n - t0);
+  for (uint32_t i = tid; i < L; i += kTT) {
+    lkey[i] = kFull;
+    lfirst[i] = kFull;
+  }
+  for (uint32_t i = tid; i < NW * kTT; i += kTT) wcnt[i] = 0;
+  const bool valid = tid < rows;
+  uint32_t gs = 0, row = kNoRow;
+  bool hot = false;
+  if (valid) {  // the token's record (count, row) and unique index in one round trip
+    gs = __ldg(a.slot_of + t0 + tid);
+    const uint2 cr = __ldcg(reinterpret_cast<const uint2*>(&a.use.rec[gs].cnt));
+    const uint32_t ux = __ldcg(a.sh.uidx + gs);
+    hot = cr.x > a.sh.hot_min;
+    row = cr.y;
+    if (hot) a.inverse[t0 + tid] = (int32_t)ux;
+  }
+  // the hot tokens' rank in the tile (block scan of the hot flags)
+  const unsigned hbal = __ballot_sync(kFull, hot);
+  if (lane == 0) wsum[warp] = __popc(hbal);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < NW ? wsum[lane] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o2);
+      if (lane >= (unsigned)o2) x += y;
+    }
+    if (lane < NW) wsum[lane] = x - v;
+    if (lane == 31) s_nhot = x;
+  }
+  __syncthreads();
+  const uint32_t nhot = s_nhot;
+  if (nhot == 0) return;  // no hot token in this tile (block-uniform)
+  trace_mark(a.sh.trace, 5);
+  uint32_t ps = 0;
+  if (hot) {
+    ps = hash32(gs) & (L - 1);
+    for (;;) {
+      const uint32_t prev = atomicCAS(&lkey[ps], kFull, gs);
+      if (prev == kFull || prev == gs) break;
+      ps = (ps + 1) & (L - 1);
+    }
+    atomicMin(&lfirst[ps], tid);
+  }
+  __syncthreads();
+  const bool head = hot && lfirst[ps] == tid;
+  const unsigned hb = __ballot_sync(kFull, head);
+  __syncthreads();  // wsum is reused
+  if (lane == 0) wsum[warp] = __popc(hb);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t v = lane < NW ? wsum[lane] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o2);
+      if (lane >= (unsigned)o2) x += y;
+    }
+    if (lane < NW) wsum[lane] = x - v;
+    if (lane == 31) s_ng = x;
+  }
+  __syncthreads();
+  const uint32_t ng = s_ng;
+  if (head) {
+    const uint32_t lg = wsum[warp] + __popc(hb & lanemask_lt());
+    lgroup[ps] = lg;
+    gslot[lg] = gs;
+    grow[lg] = row;
+  }
+  if (tid == 0) s_pbase = atomicAdd(&a.sh.ctr[1], ng);  // the tile's partial slots: one atomic
+  __syncthreads();
+  // per-warp counts of each group, then each token's place in its group (token order)
+  const uint32_t mylg = hot ? lgroup[ps] : (0xFFFF0000u | lane);
+  const unsigned mm = __match_any_sync(kFull, mylg);
+  const uint32_t rw = __popc(mm & lanemask_lt());
+  if (hot && rw == 0) wcnt[warp * kTT + mylg] = (uint16_t)__popc(mm);
+  __syncthreads();
+  if (tid < ng) {
+    uint32_t run = 0;
+    for (uint32_t w = 0; w < NW; ++w) {
+      const uint32_t c = wcnt[w * kTT + tid];
+      wcnt[w * kTT + tid] = (uint16_t)run;
+      run += c;
+    }
+    gcnt[tid] = run;
+    // the group's hot index (claimed by the first tile that gets here; the
+    // claimer waits on nothing) and its partial slot in the id's tile list
+    const uint32_t sl = gslot[tid];
+    uint32_t h = __ldcg(&a.sh.hidx[sl]);
+    if (h == kHotNone) {
+      const uint32_t old = atomicCAS(&a.sh.hidx[sl], kHotNone, kHotClaim);
+      if (old == kHotNone) {
+        h = atomicAdd(&a.sh.ctr[0], 1u);
+        a.sh.hot_slot[h] = sl;
+        __threadfence();
+        atomicExch(&a.sh.hidx[sl], h);
+      } else {
+        h = old;
+      }
+    }
+    // bounded spin: a broken protocol reports an error instead of hanging the GPU
+    for (uint32_t spin = 0; h == kHotClaim; ++spin) {
+      if (spin > (1u << 22)) {
+        atomicOr(&a.sh.ctr[2], 1u);
+        break;
+      }
+      __nanosleep(32);
+      h = atomicAdd(&a.sh.hidx[sl], 0u);
+    }
+    if (h < kHotClaim) {
+      gpidx[tid] = s_pbase + tid;
+      a.sh.hlist[(size_t)h * a.sh.ntiles + tile] = s_pbase + tid + 1;
+    } else {
+      gpidx[tid] = kFull;
+    }
+  }
+  __syncthreads();
+  {  // exclusive scan of gcnt[0, ng) -> goff
+    const uint32_t v = tid < ng ? gcnt[tid] : 0;
+    uint32_t x = v;
+#pragma unroll
+    for (int o2 = 1; o2 < 32; o2 <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o2);
+      if (lane >= (unsigned)o2) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t wv = lane < NW ? wsum[lane] : 0;
+      uint32_t z = wv;
+#pragma unroll
+      for (int o2 = 1; o2 < 32; o2 <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, z, o2);
+        if (lane >= (unsigned)o2) z += y;
+      }
+      if (lane < NW) wsum[lane] = z - wv;
+    }
+    __syncthreads();
+    if (tid < ng) goff[tid] = wsum[warp] + x - v;
+  }
+  __syncthreads();
+  if (hot) csr[goff[mylg] + wcnt[warp * kTT + mylg] + rw] = (uint16_t)tid;
+  trace_mark(a.sh.trace, 6);
+  trace_mark(a.sh.trace, 7);
+  // one warp per group: the id's row and its gradient rows issued together;
+  // the row to each of the group's tokens (the forward), the gradient rows
+  // summed in token order
+  constexpr int PF = (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+  for (uint32_t gq = warp; gq < ng; gq += NW) {
+    const uint32_t c = gcnt[gq], base = goff[gq], grw = grow[gq];
+    float w[CH][VEC], acc[CH][VEC];
+    if (grw != kNoRow) load_vec<VEC, CH>(a.emb + (size_t)grw * D, D, w, false);
+    zero_acc<VEC, CH>(acc);
+    for (uint32_t k0 = 0; k0 < c; k0 += PF) {
+      float x[PF][CH][VEC];
+#pragma unroll
+      for (int q = 0; q < PF; ++q) {
+        if (k0 + q < c) load_vec<VEC, CH>(a.grads + (size_t)(t0 + csr[base + k0 + q]) * D, D, x[q], false);
+      }
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (k0 + q < c) add_acc<VEC, CH>(acc, x[q]);
+    }
+    if (grw != kNoRow) {
+      for (uint32_t k = 0; k < c; ++k) store_vec<VEC, CH>(a.out + (size_t)(t0 + csr[base + k]) * D, D, w);
+      if (a.tokcs) {
+        double rs = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+          for (int j = 0; j < VEC; ++j) rs += (double)w[c2][j];
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) rs += __shfl_xor_sync(kFull, rs, o2);
+        for (uint32_t k = lane; k < c; k += 32) a.tokcs[t0 + csr[base + k]] = rs;
+      }
+    }
+    const uint32_t pidx = gpidx[gq];
+    if (pidx != kFull) store_vec<VEC, CH>(a.sh.part + (size_t)pidx * D, D, acc);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// KF: per hot id (block of NWF warps): its partials in tile order, split over
+// the warps in fixed contiguous chunks, warp sums combined in warp order
+// (deterministic), then the optimizer.  Resets the id's tile list and hot
+// index for the next step.
+constexpr uint32_t NWF = 16;
+struct FfArgs {
+  TableDev* td;
+  FSet use;
+  FShared sh;
+};
+
+template <int VEC, int CH>
+__global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
+  WarpTrace wt_(a.sh.trace, 3);
+  extern __shared__ __align__(16) unsigned char smf[];
+  uint32_t* list = reinterpret_cast<uint32_t*>(smf);                        // [ntiles]
+  float* wpart = reinterpret_cast<float*>(list + ((a.sh.ntiles + 3) & ~3u));  // [NWF x D]
+  __shared__ uint32_t s_w[NWF + 1];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const TableDesc d = a.td->d;
+  const uint32_t D = d.dim;
+  const uint32_t nh = *reinterpret_cast<volatile uint32_t*>(&a.sh.ctr[0]);
+  const uint32_t NT = a.sh.ntiles;
+  for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const uint32_t gs = a.sh.hot_slot[h];
+    uint32_t* hl = a.sh.hlist + (size_t)h * NT;
+    if (warp == NWF - 1) {  // the row's optimizer state: into L2 while the partials are summed
+      const uint32_t row = __ldcg(&a.use.rec[gs].row);
+      if (row != kNoRow && lane * 32u < D * 4u) {
+        const char* w = reinterpret_cast<const char*>(d.emb + (size_t)row * D) + lane * 32;
+        const char* v = reinterpret_cast<const char*>(d.s2 + (size_t)row * D) + lane * 32;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(w));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(v));
+        if (d.s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(d.s1 + (size_t)row * D) + lane * 32));
+      }
+    }
+    // compaction of the present partials, in tile order
+    uint32_t m = 0;
+    for (uint32_t b = 0; b < NT; b += NWF * 32) {
+      const uint32_t i = b + tid;
+      const uint32_t v = i < NT ? hl[i] : 0u;
+      if (v) hl[i] = 0;
+      const unsigned bal = __ballot_sync(kFull, v != 0);
+      if (lane == 0) s_w[warp] = __popc(bal);
+      __syncthreads();
+      if (tid == 0) {
+        uint32_t run = 0;
+        for (uint32_t w = 0; w < NWF; ++w) {
+          const uint32_t x = s_w[w];
+          s_w[w] = run;
+          run += x;
+        }
+        s_w[NWF] = run;
+      }
+      __syncthreads();
+      if (v) list[m + s_w[warp] + __popc(bal & lanemask_lt())] = v - 1;
+      m += s_w[NWF];
+      __syncthreads();
+    }
+    const uint32_t per = (m + NWF - 1) / NWF;
+    const uint32_t r0 = min(warp * per, m), r1 = min(r0 + per, m);
+    float acc[CH][VEC];
+    zero_acc<VEC, CH>(acc);
+    constexpr int PF = (CH * VEC <= 2) ? 16 : (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+    for (uint32_t k0 = r0; k0 < r1; k0 += PF) {
+      float x[PF][CH][VEC];
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (k0 + q < r1) load_vec<VEC, CH>(a.sh.part + (size_t)list[k0 + q] * D, D, x[q], true);
+#pragma unroll
+      for (int q = 0; q < PF; ++q)
+        if (k0 + q < r1) add_acc<VEC, CH>(acc, x[q]);
+    }
+    store_vec<VEC, CH>(wpart + (size_t)warp * D, D, acc);
+    __syncthreads();
+    if (warp == 0) {
+      float tot[CH][VEC];
+      zero_acc<VEC, CH>(tot);
+      for (uint32_t w = 0; w < NWF; ++w) {
+        float x[CH][VEC];
+        load_vec<VEC, CH>(wpart + (size_t)w * D, D, x, false);
+        add_acc<VEC, CH>(tot, x);
+      }
+      const uint32_t row = __ldcg(&a.use.rec[gs].row);
+      apply_row<VEC, CH>(d, row, tot, o);
+      if (lane == 0) a.sh.hidx[gs] = kHotNone;
+    }
+    __syncthreads();
+  }
+}
+
+struct Shape {
+  int vec, ch;
+};
+Shape shape_of(uint32_t D) {
+  if (D % 128 == 0 && D / 128 <= 4) return {4, (int)(D / 128)};
+  if (D % 64 == 0 && D / 64 <= 2) return {2, (int)(D / 64)};
+  return {1, (int)((D + 31) / 32)};
+}
+
+}  // namespace
+
+// ---- host side ---------------------------------------------------------------
+bool fast_step_supported(const rs_table* t) {
+  const uint32_t D = t->desc.dim;
+  if (t->cfg.max_keys || D % 4) return false;
+  const Shape sh = shape_of(D);
+  const uint32_t D4 = D / 4;
+  const bool g_ok = D4 == 4 || D4 == 8 || D4 == 16 || D4 == 32 || D4 == 64;
+  const bool s_ok = (sh.vec == 4 && sh.ch <= 2) || (sh.vec == 2 && sh.ch <= 2) || (sh.vec == 1 && sh.ch <= 2);
+  return g_ok && s_ok;
+}
+
+static cudaError_t fast_trace_reset(rs_workspace* ws) {
+  // [kernel][block] = {start = ~0, end = 0}
+  std::vector<unsigned long long> h(8 * kTraceBlocks * 2);
+  for (size_t i = 0; i < h.size(); i += 2) {
+    h[i] = ~0ull;
+    h[i + 1] = 0;
+  }
+  return cudaMemcpy(ws->fast.trace, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+}
+
+static int fast_alloc(rs_workspace* ws) {
+  rs_fast& f = ws->fast;
+  if (f.ready) return RS_OK;
+  const uint64_t S = ws->S, N = ws->max_tokens;
+  f.ntiles = (N + kTT - 1) / kTT;
+  f.hot_min = kPosMax;
+  if (const char* e = getenv("RS_HOT_MIN")) f.hot_min = std::min<uint32_t>(kPosMax, std::max(1, atoi(e)));
+  f.max_hot = N / (f.hot_min + 1) + 1;
+  auto A = [&](auto** p, size_t bytes) {
+    return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16)) == cudaSuccess;
+  };
+  bool ok = true;
+  for (auto& x : f.set) ok = ok && A(&x.rec, (S + 1) * sizeof(Rec)) && A(&x.u_slot, N * 4) && A(&x.cnt, 16);
+  ok = ok && A(&f.uidx, (S + 1) * 4) && A(&f.hidx, (S + 1) * 4) && A(&f.pos, (S + 1) * kPosMax * 4) &&
+       A(&f.hot_slot, f.max_hot * 4) && A(&f.hlist, f.max_hot * f.ntiles * 4) && A(&f.ctr, 64) &&
+       A(&f.tokcs, N * 8);
+  if (!ok) return cuda_fail(cudaGetLastError(), "fast step: cudaMalloc");
+  // empty records (key ~0, count 0, row ~0): all-ones then zero counts
+  for (auto& x : f.set) {
+    RS_CUDA(cudaMemset(x.rec, 0xFF, (S + 1) * sizeof(Rec)));
+    RS_CUDA(cudaMemset2D(reinterpret_cast<char*>(x.rec) + 8, sizeof(Rec), 0, 4, S + 1));
+    RS_CUDA(cudaMemset(x.cnt, 0, 16));
+  }
+  RS_CUDA(cudaMemset(f.hidx, 0xFF, (S + 1) * 4));
+  RS_CUDA(cudaMemset(f.hlist, 0, f.max_hot * f.ntiles * 4));
+  RS_CUDA(cudaMemset(f.ctr, 0, 64));
+  if (getenv("RS_TRACE") && getenv("RS_TRACE")[0] == '1') {
+    RS_CUDA(cudaMalloc(&f.trace, 8 * kTraceBlocks * 2 * sizeof(unsigned long long)));
+    RS_CUDA(fast_trace_reset(ws));
+  }
+  {  // the hot branch (KH -> KF) at the highest priority: KF's blocks go ahead of the CSR kernel's pending ones
+    int lo = 0, hi = 0;
+    RS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    static const bool prio = !(getenv("RS_FAST_PRIO") && getenv("RS_FAST_PRIO")[0] == '0');
+    RS_CUDA(cudaStreamCreateWithPriority(&f.aux2, cudaStreamNonBlocking, prio ? hi : 0));
+  }
+  RS_CUDA(cudaEventCreateWithFlags(&f.ev_fork, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&f.ev_j1, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&f.ev_j2, cudaEventDisableTiming));
+  RS_CUDA(cudaDeviceSynchronize());
+  f.ready = true;
+  return RS_OK;
+}
+
+void fast_free(rs_workspace* ws) {
+  rs_fast& f = ws->fast;
+  for (auto& x : f.set) {
+    void* ps[] = {x.rec, x.u_slot, x.cnt};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  }
+  void* ps[] = {f.uidx, f.hidx, f.pos, f.hot_slot, f.hlist, f.ctr, f.tokcs, f.trace};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  if (f.aux2) cudaStreamDestroy(f.aux2);
+  cudaEvent_t es[] = {f.ev_fork, f.ev_j1, f.ev_j2};
+  for (auto e : es)
+    if (e) cudaEventDestroy(e);
+  f = rs_fast{};
+}
+
+int fast_prepare(rs_workspace* ws) { return fast_alloc(ws); }
+
+static FSet fset(rs_workspace* ws, int k) {
+  rs_fast_set& x = ws->fast.set[k];
+  FSet s;
+  s.rec = reinterpret_cast<Rec*>(x.rec);
+  s.u_slot = x.u_slot;
+  s.cnt = x.cnt;
+  s.smask = ws->S - 1;
+  s.spare = ws->S;
+  return s;
+}
+static FShared fshared(rs_workspace* ws) {
+  rs_fast& f = ws->fast;
+  FShared s;
+  s.uidx = f.uidx;
+  s.hidx = f.hidx;
+  s.pos = f.pos;
+  s.hot_slot = f.hot_slot;
+  s.hlist = f.hlist;
+  s.part = ws->pbuf;
+  s.ctr = f.ctr;
+  s.ntiles = (uint32_t)f.ntiles;
+  s.hot_min = f.hot_min;
+  s.trace = f.trace;
+  return s;
+}
+
+// Enqueue-only (capturable).  ev != null: eager profiling -- the kernels run
+// one after another with events ev[0..4] around KA, KG, KD, KH+KF.
+int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
+                 float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork) {
+  const OptArgs& o = *static_cast<const OptArgs*>(opt);
+  const uint32_t D = t->desc.dim;
+  const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
+  const FShared sh = fshared(ws);
+  if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
+  FaArgs fa;
+  fa.ids = d_ids;
+  fa.n = (uint32_t)n;
+  fa.use = fset(ws, use);
+  fa.clean = fset(ws, use ^ 1);
+  fa.sh = sh;
+  fa.td = t->dev;
+  fa.slot_of = ws->slot_of;
+  fa.unique = ws->unique;
+  fa.urow = ws->urow;
+  fa.urow64 = ws->urow64;
+  k_fa<<<ntiles, kTT, 0, s>>>(fa);
+  RS_LAUNCH_CHECK("k_fa");
+  if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
+  rs_fast& f = ws->fast;
+  cudaStream_t sd = s, sh2 = s;
+  if (fork && !ev) {
+    RS_CUDA(cudaEventRecord(f.ev_fork, s));
+    RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, f.ev_fork, 0));
+    RS_CUDA(cudaStreamWaitEvent(f.aux2, f.ev_fork, 0));
+    sd = ws->aux_stream;
+    sh2 = f.aux2;
+  }
+  const Shape shp = shape_of(D);
+  // hot branch first (longest chain): KH -> KF
+  auto hot = [&](cudaStream_t q) -> int {
+    FhArgs h;
+    h.use = fa.use;
+    h.sh = sh;
+    h.slot_of = ws->slot_of;
+    h.n = (uint32_t)n;
+    h.grads = d_grads;
+    h.dim = D;
+    h.emb = t->desc.emb;
+    h.out = d_out;
+    h.inverse = ws->inverse;
+    h.tokcs = ws->csum_dst ? f.tokcs : nullptr;
+    FfArgs ff;
+    ff.td = t->dev;
+    ff.use = fa.use;
+    ff.sh = sh;
+    const size_t fsm = ((f.ntiles + 3) & ~3ull) * 4 + (size_t)NWF * D * 4;
+    const unsigned fgrid = (unsigned)std::min<uint64_t>(f.max_hot, 148 * 2);
+#define RS_FH(V, C)                                                                        \
+  if (shp.vec == V && shp.ch == C) {                                                       \
+    k_fh<V, C><<<ntiles, kTT, 0, q>>>(h);                                                  \
+    RS_LAUNCH_CHECK("k_fh");                                                               \
+    if (fsm > 48 * 1024)                                                                   \
+      RS_CUDA(cudaFuncSetAttribute(k_fhf<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)fsm));                                             \
+    k_fhf<V, C><<<fgrid, NWF * 32, fsm, q>>>(ff, o);                                       \
+    RS_LAUNCH_CHECK("k_fhf");                                                              \
+    return RS_OK;                                                                          \
+  }
+    RS_FH(4, 1) RS_FH(4, 2) RS_FH(2, 1) RS_FH(2, 2) RS_FH(1, 1) RS_FH(1, 2)
+#undef RS_FH
+    return fail(RS_ERR_INVARIANT, "fast step: no hot kernel for this dim");
+  };
+  auto csr = [&](cudaStream_t q) -> int {
+    FcArgs c;
+    c.td = t->dev;
+    c.use = fa.use;
+    c.sh = sh;
+    c.grads = d_grads;
+    c.urow = ws->urow;
+    static const uint32_t fexp = getenv("RS_FC_EXP") ? (uint32_t)atoi(getenv("RS_FC_EXP")) : 0u;
+    c.exp = fexp;
+    c.out = d_out;
+    c.inverse = ws->inverse;
+    c.tokcs = ws->csum_dst ? f.tokcs : nullptr;
+    const uint32_t D4 = D / 4;
+    const uint32_t G = D4 >= 32 ? 32 : D4;
+    const uint32_t gpb = 256 / G;
+    static const unsigned cap_blocks = getenv("RS_FC_GRID") ? (unsigned)atoi(getenv("RS_FC_GRID")) : 148u * 16u;
+    const unsigned grid = grid_for(n, gpb, cap_blocks);
+    static const int g8 = getenv("RS_FC_G8") ? atoi(getenv("RS_FC_G8")) : 0;  // experiment: 8 lanes x 2 chunks
+    if (D4 == 4) k_fc<4, 1><<<grid, 256, 0, q>>>(c, o);
+    else if (D4 == 8) k_fc<8, 1><<<grid, 256, 0, q>>>(c, o);
+    else if (D4 == 16 && g8) k_fc<8, 2><<<grid_for(n, 32, cap_blocks), 256, 0, q>>>(c, o);
+    else if (D4 == 16) k_fc<16, 1><<<grid, 256, 0, q>>>(c, o);
+    else if (D4 == 32) k_fc<32, 1><<<grid, 256, 0, q>>>(c, o);
+    else k_fc<32, 2><<<grid, 256, 0, q>>>(c, o);
+    RS_LAUNCH_CHECK("k_fc");
+    return RS_OK;
+  };
+  auto checksum = [&](cudaStream_t q) -> int {
+    if (!ws->csum_dst) return RS_OK;
+    k_fcs<<<ntiles, kTT, 0, q>>>(f.tokcs, (uint32_t)n, ws->csum_dst, ws->csum_part, ws->csum_ticket);
+    RS_LAUNCH_CHECK("k_fcs");
+    return RS_OK;
+  };
+  int st;
+  if (ev) {  // eager, serial: KA (+ clean) | KD | KH + KF | KS
+    k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace);
+    RS_LAUNCH_CHECK("k_fclean");
+    if ((st = csr(s))) return st;
+    RS_CUDA(cudaEventRecord(ev[2], s));
+    if ((st = hot(s))) return st;
+    RS_CUDA(cudaEventRecord(ev[3], s));
+    if ((st = checksum(s))) return st;
+    RS_CUDA(cudaEventRecord(ev[4], s));
+    return RS_OK;
+  }
+  // RS_FAST_SKIP (timing experiments only, wrong results): 1 = no hot branch, 2 = no CSR branch
+  static const int skip = getenv("RS_FAST_SKIP") ? atoi(getenv("RS_FAST_SKIP")) : 0;
+  if (skip != 1 && (st = hot(sh2))) return st;
+  if (skip != 2 && (st = csr(sd))) return st;
+  k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace);
+  RS_LAUNCH_CHECK("k_fclean");
+  if (sd != s) {
+    RS_CUDA(cudaEventRecord(f.ev_j1, sd));
+    RS_CUDA(cudaStreamWaitEvent(s, f.ev_j1, 0));
+    RS_CUDA(cudaEventRecord(f.ev_j2, sh2));
+    RS_CUDA(cudaStreamWaitEvent(s, f.ev_j2, 0));
+  }
+  return checksum(s);
+}
+
+}  // namespace rs
+
+extern "C" int rs_workspace_trace(rs_workspace* ws, uint64_t* out, uint64_t cap, uint64_t* n_out) {
+  using namespace rs;
+  if (!ws || !n_out) return fail(RS_ERR_CONFIG, "rs_workspace_trace: null argument");
+  *n_out = 0;
+  if (!ws->fast.trace) return RS_OK;  // RS_TRACE=1 at the first rs_step enables it
+  const uint64_t n = 8ull * kTraceBlocks * 2;
+  *n_out = n;
+  if (!out) return RS_OK;
+  if (cap < n) return fail(RS_ERR_CONFIG, "rs_workspace_trace: buffer too small");
+  RS_CUDA(cudaDeviceSynchronize());
+  RS_CUDA(cudaMemcpy(out, ws->fast.trace, n * 8, cudaMemcpyDeviceToHost));
+  RS_CUDA(fast_trace_reset(ws));
+  return RS_OK;
+}
