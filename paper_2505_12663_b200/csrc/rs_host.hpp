@@ -12,6 +12,7 @@
 // (DESIGN.md §4 "sync-free capacity management").
 struct rs_mirror {
   rs::TableCounters* pinned = nullptr;
+  rs::TableCounters* dev_ptr = nullptr;  // the same pinned buffer as seen by kernels (mapped)
   cudaEvent_t ev = nullptr;
   uint64_t requested_at_copy = 0;  // cumulative keys requested when the copy was enqueued
   bool valid = false;
@@ -265,5 +266,6 @@ bool fast_step_supported(const rs_table* t);
 int fast_prepare(rs_workspace* ws);
 void fast_free(rs_workspace* ws);
 int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
-                 float* d_out, const void* opt_args, int use, cudaStream_t s, cudaEvent_t* ev, bool fork);
+                 float* d_out, const void* opt_args, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,
+                 rs::TableCounters* mirror_out);
 }  // namespace rs

@@ -2001,8 +2001,11 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   const int use = fast ? ws->fast.cur : ws->cur;
   auto enqueue = [&](cudaStream_t q, cudaEvent_t* ev) -> int {
     if (!fast) return step_enqueue(ws, t, d_ids, n, d_grads, d_out, o, use, mirror, q, ev);
-    const int e = fast_enqueue(ws, t, d_ids, n, d_grads, d_out, &o, use, q, ev, ws->fork);
-    return e ? e : table_mirror_copy(t, mirror, q);
+    // the counters reach the pinned mirror from inside the step (mapped store,
+    // k_fclean) when the mirror is mapped; else a copy after the step
+    TableCounters* mo = t->mirror[mirror].dev_ptr;
+    const int e = fast_enqueue(ws, t, d_ids, n, d_grads, d_out, &o, use, q, ev, ws->fork, mo);
+    return e ? e : (mo ? RS_OK : table_mirror_copy(t, mirror, q));
   };
   if (ws->profiling || !ws->use_graphs) {
     // profiling runs the kernels one after another (no fork) so that every

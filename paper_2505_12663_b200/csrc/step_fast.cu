@@ -286,7 +286,8 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
 // The previous step's scratch set goes back to empty records (its dirty
 // list), off the critical path beside KD / KH; the last block zeroes its
 // count (the next step's KA inserts into it).
-__global__ void __launch_bounds__(256) k_fclean(FSet c, unsigned int* done, unsigned long long* trace) {
+__global__ void __launch_bounds__(256) k_fclean(FSet c, unsigned int* done, unsigned long long* trace,
+                                                const TableDev* td, TableCounters* mirror_out) {
   WarpTrace wt_(trace, 4);
   const uint32_t prev = *c.cnt;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i <= prev;
@@ -305,6 +306,15 @@ __global__ void __launch_bounds__(256) k_fclean(FSet c, unsigned int* done, unsi
     __threadfence();
     *c.cnt = 0;
     *done = 0;
+  }
+  // the table counters (final since KA's epilogue) into the host's pinned
+  // mirror (mapped memory): the sync-free capacity bookkeeping of the next
+  // batches, without a copy node on the step's critical path
+  if (last && mirror_out) {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(&td->c);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(mirror_out);
+    for (uint32_t i = threadIdx.x; i < sizeof(TableCounters) / 4; i += blockDim.x) dst[i] = __ldcg(src + i);
+    __threadfence_system();
   }
 }
 
@@ -363,6 +373,7 @@ struct FcArgs {
   double* tokcs;     // per-token row sums (checksum) or null
   const uint32_t* urow;  // table row per unique id (KA)
   uint32_t exp;          // timing experiments (RS_FC_EXP bits, wrong results): 1 no optimizer, 2 no grads, 4 no forward
+  uint32_t heavy_first;  // > 0: two passes, ids with more occurrences first (RS_FC_HEAVY)
 };
 
 #ifndef RS_FC_MINB
@@ -387,7 +398,14 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
   float4* rw = reinterpret_cast<float4*>(d.emb);
   float4* rv = reinterpret_cast<float4*>(d.s2);
   float4* rm = reinterpret_cast<float4*>(d.s1);
-  for (uint32_t uu = gid; uu < nu; uu += ngroups) {
+  // two passes over the group's ids when a.heavy_first > 0: ids with more
+  // than heavy_first occurrences first (their long ordered sums start at once
+  // instead of in a late wave), then the rest
+  const uint32_t npass = a.heavy_first ? 2u : 1u;
+  for (uint32_t it = 0; it < npass * ((nu + ngroups - 1) / ngroups); ++it) {
+    const uint32_t pass = a.heavy_first ? it / ((nu + ngroups - 1) / ngroups) : 1u;
+    const uint32_t uu = gid + (it - (pass == 1 && a.heavy_first ? (nu + ngroups - 1) / ngroups : 0u)) * ngroups;
+    if (uu >= nu) continue;
     // slot and row in one round trip (KA's claiming tile wrote both), then the
     // count, the positions (speculatively, all 64) and the row's state together
     const uint32_t gs = __ldg(a.use.u_slot + uu);
@@ -411,6 +429,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
     uint32_t st0 = 0;
     if (gl == 0) st0 = d.step[row];
     if (c > a.sh.hot_min) continue;  // hot path (group-uniform)
+    if (a.heavy_first && ((pass == 0) != (c > a.heavy_first))) continue;
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
       if (gl + j * G >= c) p[j] = kFull;
@@ -758,14 +777,13 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
 // the warps in fixed contiguous chunks, warp sums combined in warp order
 // (deterministic), then the optimizer.  Resets the id's tile list and hot
 // index for the next step.
-constexpr uint32_t NWF = 16;
 struct FfArgs {
   TableDev* td;
   FSet use;
   FShared sh;
 };
 
-template <int VEC, int CH>
+template <int VEC, int CH, int NWF>
 __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
   WarpTrace wt_(a.sh.trace, 3);
   extern __shared__ __align__(16) unsigned char smf[];
@@ -817,7 +835,7 @@ __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
     const uint32_t r0 = min(warp * per, m), r1 = min(r0 + per, m);
     float acc[CH][VEC];
     zero_acc<VEC, CH>(acc);
-    constexpr int PF = (CH * VEC <= 2) ? 16 : (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+    constexpr int PF = (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
     for (uint32_t k0 = r0; k0 < r1; k0 += PF) {
       float x[PF][CH][VEC];
 #pragma unroll
@@ -969,7 +987,8 @@ static FShared fshared(rs_workspace* ws) {
 // Enqueue-only (capturable).  ev != null: eager profiling -- the kernels run
 // one after another with events ev[0..4] around KA, KG, KD, KH+KF.
 int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
-                 float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork) {
+                 float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,
+                 TableCounters* mirror_out) {
   const OptArgs& o = *static_cast<const OptArgs*>(opt);
   const uint32_t D = t->desc.dim;
   const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
@@ -1016,21 +1035,29 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     ff.td = t->dev;
     ff.use = fa.use;
     ff.sh = sh;
-    const size_t fsm = ((f.ntiles + 3) & ~3ull) * 4 + (size_t)NWF * D * 4;
-    const unsigned fgrid = (unsigned)std::min<uint64_t>(f.max_hot, 148 * 2);
+    // hot finish: a block of kf_warps warps per hot id (small blocks fit beside the CSR kernel's)
+    static const int kfw = getenv("RS_KF_WARPS") ? atoi(getenv("RS_KF_WARPS")) : 8;
+    const int nwf = kfw == 4 || kfw == 16 ? kfw : 8;
+    const size_t fsm = ((f.ntiles + 3) & ~3ull) * 4 + (size_t)nwf * D * 4;
+    const unsigned fgrid = (unsigned)std::min<uint64_t>(f.max_hot, 148 * 4);
+#define RS_KF(V, C, NWV)                                                                     \
+  if (nwf == NWV) {                                                                          \
+    if (fsm > 48 * 1024)                                                                     \
+      RS_CUDA(cudaFuncSetAttribute(k_fhf<V, C, NWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                   (int)fsm));                                               \
+    k_fhf<V, C, NWV><<<fgrid, NWV * 32, fsm, q>>>(ff, o);                                    \
+  }
 #define RS_FH(V, C)                                                                        \
   if (shp.vec == V && shp.ch == C) {                                                       \
     k_fh<V, C><<<ntiles, kTT, 0, q>>>(h);                                                  \
     RS_LAUNCH_CHECK("k_fh");                                                               \
-    if (fsm > 48 * 1024)                                                                   \
-      RS_CUDA(cudaFuncSetAttribute(k_fhf<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                   (int)fsm));                                             \
-    k_fhf<V, C><<<fgrid, NWF * 32, fsm, q>>>(ff, o);                                       \
+    RS_KF(V, C, 4) RS_KF(V, C, 8) RS_KF(V, C, 16)                                          \
     RS_LAUNCH_CHECK("k_fhf");                                                              \
     return RS_OK;                                                                          \
   }
     RS_FH(4, 1) RS_FH(4, 2) RS_FH(2, 1) RS_FH(2, 2) RS_FH(1, 1) RS_FH(1, 2)
 #undef RS_FH
+#undef RS_KF
     return fail(RS_ERR_INVARIANT, "fast step: no hot kernel for this dim");
   };
   auto csr = [&](cudaStream_t q) -> int {
@@ -1042,6 +1069,8 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     c.urow = ws->urow;
     static const uint32_t fexp = getenv("RS_FC_EXP") ? (uint32_t)atoi(getenv("RS_FC_EXP")) : 0u;
     c.exp = fexp;
+    static const uint32_t heavy = getenv("RS_FC_HEAVY") ? (uint32_t)atoi(getenv("RS_FC_HEAVY")) : 0u;
+    c.heavy_first = heavy;
     c.out = d_out;
     c.inverse = ws->inverse;
     c.tokcs = ws->csum_dst ? f.tokcs : nullptr;
@@ -1068,7 +1097,8 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   };
   int st;
   if (ev) {  // eager, serial: KA (+ clean) | KD | KH + KF | KS
-    k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace);
+    k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
+                                                            t->dev, mirror_out);
     RS_LAUNCH_CHECK("k_fclean");
     if ((st = csr(s))) return st;
     RS_CUDA(cudaEventRecord(ev[2], s));
@@ -1082,7 +1112,8 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   static const int skip = getenv("RS_FAST_SKIP") ? atoi(getenv("RS_FAST_SKIP")) : 0;
   if (skip != 1 && (st = hot(sh2))) return st;
   if (skip != 2 && (st = csr(sd))) return st;
-  k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace);
+  k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
+                                                            t->dev, mirror_out);
   RS_LAUNCH_CHECK("k_fclean");
   if (sd != s) {
     RS_CUDA(cudaEventRecord(f.ev_j1, sd));

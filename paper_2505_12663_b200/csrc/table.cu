@@ -678,6 +678,11 @@ int rs_table_create(const rs_table_config* cfg, rs_table** out) {
     if (cudaMallocHost(&m.pinned, sizeof(TableCounters)) != cudaSuccess ||
         cudaEventCreateWithFlags(&m.ev, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(cuda_fail(cudaGetLastError(), "mirror alloc"));
+    // kernels may store the counters straight into it (mapped pinned memory)
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&m.dev_ptr), m.pinned, 0) != cudaSuccess) {
+      cudaGetLastError();
+      m.dev_ptr = nullptr;
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess)
     return cleanup(cuda_fail(cudaGetLastError(), "rs_table_create"));

@@ -1,3 +1,3 @@
-for cfg in "RS_FAST_SKIP=1" "RS_FAST_SKIP=1 RS_FC_EXP=1" "RS_FAST_SKIP=1 RS_FC_EXP=2" "RS_FAST_SKIP=1 RS_FC_EXP=4" "RS_FAST_SKIP=1 RS_FC_EXP=7" "RS_FAST_SKIP=3"; do
+for cfg in "RS_FAST_STEP=0" "RS_FAST_STEP=1" "RS_FAST_STEP=0" "RS_FAST_STEP=1"; do
   echo "$cfg $(env $cfg timeout 300 python tools/exp_flush.py 30 2>/dev/null | python -c 'import json,sys; d=json.load(sys.stdin); print([round(x["median_ms"]*1e3,1) for x in d["dirty"]+d["clean"]])')"
 done
