@@ -259,7 +259,7 @@ int rs_dist_group_step(rs_comm* const* comms, rs_table* const* shards, int world
                        const uint64_t* const* d_ids, const uint64_t* n, const float* const* d_grads,
                        float* const* d_out, const rs_optimizer_params* opt, void* stream);
 
-/* ---- table merging (merge_registry.cpp:23-176) ---------------------------- */
+/* ---- table merging (merge_registry.cpp:23-175) ---------------------------- */
 /* encode_tagged_id on device (merge_registry.cpp:23-33); synchronizes,
  * RS_ERR_RANGE if an index or raw id is out of range. */
 int rs_encode_ids(const uint64_t* d_raw, uint64_t n, uint32_t k_bits, uint32_t table_index,

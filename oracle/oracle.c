@@ -790,7 +790,7 @@ void or_adagrad_row(float* w, float* acc, uint64_t* step, const float* grad, uin
 
 size_t or_apply(or_table* t, const uint64_t* ids, const float* sums, size_t n, int optimizer,
                 double lr, double beta1, double beta2, double eps) {
-  /* GradAccumulator::apply_serial, sparse_update.cpp:157-170 */
+  /* GradAccumulator::apply_serial, sparse_update.cpp:85-98 */
   for (size_t i = 0; i < n; ++i) {
     int64_t r = or_table_ensure(t, ids[i]);
     const float* g = sums + i * t->dim;

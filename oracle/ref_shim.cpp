@@ -3,8 +3,8 @@
 // in place together with this file into oracle/_ref/librsref.so.  Nothing of
 // the reference is copied into this repository; this file only calls its
 // public API (proj/include/recsparse/*.hpp).  Used by tests (to pin the C
-// restatement in oracle.c), by tests/golden/make_golden.py, and by bench.py's
-// reference arm (CPU baseline, kind "reference").
+// restatement in oracle.c and as the reference of GPU parity tests) and by
+// bench.py's reference arm (CPU baseline, kind "reference").
 #include <omp.h>
 
 #include <chrono>

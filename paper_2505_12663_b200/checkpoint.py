@@ -4,7 +4,7 @@
 the reference's names and file format (checkpoint.hpp:25-54); ``save_cluster``
 / ``load_cluster`` operate on one process's ``ShardedTable`` (every rank
 saves / loads its own shard; load_cluster's modulo file selection and
-ownership refilter, checkpoint.cpp:211-276).
+ownership refilter, checkpoint.cpp:194-254).
 """
 from __future__ import annotations
 

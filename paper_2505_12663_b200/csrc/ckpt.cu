@@ -12,7 +12,7 @@
 // and save -> load -> save is byte-identical.  Loading ignores the stored
 // slot and re-inserts (the reference restores exact slots only at an
 // unchanged world size, checkpoint.cpp:181-207).  Elastic reload follows
-// load_cluster (checkpoint.cpp:211-276): worker r' reads file r' mod W when
+// load_cluster (checkpoint.cpp:194-254): worker r' reads file r' mod W when
 // growing, every file f with f mod W' == r' when shrinking, keeps the
 // entries it owns under hash64(id) % W', and fast-forwards its tick to the
 // newest timestamp.  Host code over rs_table_export / rs_table_import.
@@ -177,7 +177,7 @@ int rs_ckpt_read_header(const char* path, rs_ckpt_header* out) {
   return RS_OK;
 }
 
-// load_cluster (checkpoint.cpp:211-276) for worker `rank` of `new_world`,
+// load_cluster (checkpoint.cpp:194-254) for worker `rank` of `new_world`,
 // into the (empty) device shard t.  Synchronizes.
 int rs_ckpt_load_shard(rs_table* t, const char* dir, uint32_t saved_world, uint32_t new_world,
                        uint32_t rank) {

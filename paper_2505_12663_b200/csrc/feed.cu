@@ -96,6 +96,15 @@ static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const u
   // the loader's lengths -> token offsets (host, a few thousand adds); the
   // staging buffer of this set is free once its previous copy completed
   RS_CUDA(cudaEventSynchronize(f->landed[b]));
+  {  // validate before touching the pinned staging buffers
+    uint64_t tot = 0, chunks = 0;
+    for (uint64_t i = 0; i < n_seq; ++i) {
+      tot += h_lengths[i];
+      chunks += (h_lengths[i] + kChunkTok - 1) / kChunkTok;
+    }
+    if (tot != n) return fail(RS_ERR_CONFIG, "rs_feeder_step: sum of lengths != number of ids");
+    if (chunks > f->max_seqs + f->max_tokens / kChunkTok + 1) return fail(RS_ERR_CONFIG, "rs_feeder_step: batch exceeds the feeder's capacity");
+  }
   uint64_t run = 0;
   uint32_t nc = 0;
   for (uint64_t i = 0; i < n_seq; ++i) {

@@ -73,7 +73,10 @@ __global__ void k_pool(const int64_t* __restrict__ rows, uint64_t n, uint32_t L,
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (uint32_t r = 0; r < L; ++r) {
           const int64_t row = __ldg(rows + (uint64_t)r * n + t);
-          const float4 v = __ldg(reinterpret_cast<const float4*>(tab.emb[r] + (size_t)row * D) + j);
+          // row < 0: the ensure failed (table full / row pool; reported by its
+          // error counters) -- pool zeros instead of reading outside the pool
+          const float4 v = row < 0 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                   : __ldg(reinterpret_cast<const float4*>(tab.emb[r] + (size_t)row * D) + j);
           if (mode == RS_POOL_NONE) {
             acc = v;
           } else {
@@ -96,7 +99,7 @@ __global__ void k_pool(const int64_t* __restrict__ rows, uint64_t n, uint32_t L,
         float acc = 0.f;
         for (uint32_t r = 0; r < L; ++r) {
           const int64_t row = __ldg(rows + (uint64_t)r * n + t);
-          const float v = __ldg(tab.emb[r] + (size_t)row * D + j);
+          const float v = row < 0 ? 0.f : __ldg(tab.emb[r] + (size_t)row * D + j);
           acc = mode == RS_POOL_NONE ? v : __fadd_rn(acc, v);
         }
         if (mode == RS_POOL_MEAN) acc = __fmul_rn(acc, inv);
@@ -369,7 +372,7 @@ int rs_merge_plan_find(const rs_merge_plan* p, const char* table, uint32_t* grou
   return RS_OK;
 }
 
-// HashTableCollection (merge_registry.cpp:160-176): one physical table per
+// HashTableCollection (merge_registry.cpp:160-175): one physical table per
 // group, the prototype config with the group's embedding dim.
 int rs_collection_create(const rs_merge_plan* p, const rs_table_config* prototype,
                          rs_collection** out) {

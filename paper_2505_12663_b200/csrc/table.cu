@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <unordered_map>
 #include <vector>
 
 #include "rs_host.hpp"
@@ -338,6 +339,31 @@ __global__ void k_set_ticks(TableDev* __restrict__ td, const uint64_t* __restric
     const Probe p = probe_group<false>(d.slots, d.nb_mask, keys[i], g, gbase, gmask);
     if (p.found && g == 0) d.slots[p.slot].tick = (uint32_t)ticks[i];
   }
+}
+
+// Batched insert with duplicate keys: the reference inserts one key at a time,
+// so the LAST occurrence's row wins (embed_table.cpp:193-227).  A temporary
+// open-addressed set keyed by the key keeps the highest index + 1 of each key
+// (slot `mask + 1` holds the key equal to the empty sentinel); the selection
+// then lists the winning indices for one upsert launch.
+__device__ __forceinline__ uint64_t last_slot(unsigned long long* hkey, uint64_t mask, uint64_t key, bool claim) {
+  if (key == kEmptyKey) return mask + 1;
+  uint64_t h = hash64(key) & mask;
+  for (;;) {
+    const unsigned long long cur = claim ? atomicCAS(&hkey[h], kEmptyKey, (unsigned long long)key) : hkey[h];
+    if (cur == key || (claim && cur == kEmptyKey)) return h;
+    h = (h + 1) & mask;
+  }
+}
+__global__ void k_last_of_key(const uint64_t* __restrict__ keys, uint64_t n, unsigned long long* hkey,
+                              uint32_t* hidx, uint64_t mask) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicMax(&hidx[last_slot(hkey, mask, keys[i], true)], (uint32_t)(i + 1));
+}
+__global__ void k_select_last(const uint64_t* __restrict__ keys, uint64_t n, unsigned long long* hkey,
+                              const uint32_t* hidx, uint64_t mask, uint32_t* sel, uint32_t* cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    if (hidx[last_slot(hkey, mask, keys[i], false)] == i + 1) sel[atomicAdd(cnt, 1u)] = (uint32_t)i;
 }
 
 __global__ void k_hash64(const uint64_t* __restrict__ k, uint64_t n, uint64_t* __restrict__ out) {
@@ -742,9 +768,27 @@ int rs_table_insert(rs_table* t, const uint64_t* d_keys, uint64_t n, const float
   cudaStream_t s = S(stream);
   int st = table_prepare(t, n, s);
   if (st) return st;
+  // duplicate keys in the batch: the last occurrence wins (one upsert per key)
+  uint64_t S_ = 16;
+  while (S_ < 2 * n) S_ <<= 1;
+  unsigned long long* hkey = nullptr;
+  uint32_t *hidx = nullptr, *sel = nullptr;
+  RS_CUDA(cudaMallocAsync(&hkey, (S_ + 2) * 8, s));
+  RS_CUDA(cudaMallocAsync(&hidx, (S_ + 2) * 4 + n * 4 + 16, s));
+  sel = hidx + S_ + 2;
+  uint32_t* cnt = sel + n;
+  RS_CUDA(cudaMemsetAsync(hkey, 0xFF, (S_ + 2) * 8, s));
+  RS_CUDA(cudaMemsetAsync(hidx, 0, (S_ + 2) * 4, s));
+  RS_CUDA(cudaMemsetAsync(cnt, 0, 4, s));
+  k_last_of_key<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_keys, n, hkey, hidx, S_ - 1);
+  RS_LAUNCH_CHECK("k_last_of_key");
+  k_select_last<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(d_keys, n, hkey, hidx, S_ - 1, sel, cnt);
+  RS_LAUNCH_CHECK("k_select_last");
   k_table_upsert<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
-      t->dev, d_keys, nullptr, (uint32_t)n, d_emb, 1, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+      t->dev, d_keys, cnt, (uint32_t)n, d_emb, 1, nullptr, nullptr, nullptr, nullptr, nullptr, sel);
   RS_LAUNCH_CHECK("k_table_upsert(insert)");
+  RS_CUDA(cudaFreeAsync(hkey, s));
+  RS_CUDA(cudaFreeAsync(hidx, s));
   return table_after_op(t, s);
 }
 
@@ -885,6 +929,46 @@ int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* 
   if (!t) return fail(RS_ERR_CONFIG, "rs_table_import: null table");
   if (n == 0) return RS_OK;
   const size_t D = t->desc.dim;
+  // the device keeps step counters and ticks in 32 bits
+  uint64_t max_step = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if ((step && step[i] >> 32) || (ts && ts[i] >> 32))
+      return fail(RS_ERR_CONFIG, "rs_table_import: step / ts values >= 2^32 are not representable");
+    if (step) max_step = std::max(max_step, step[i]);
+  }
+  // duplicate keys: the last occurrence wins (insert one at a time, embed_table.cpp:193-227)
+  {
+    std::unordered_map<uint64_t, uint64_t> last;
+    last.reserve(n * 2);
+    for (uint64_t i = 0; i < n; ++i) last[keys[i]] = i;
+    if (last.size() != n) {
+      std::vector<uint64_t> idx;
+      idx.reserve(last.size());
+      for (uint64_t i = 0; i < n; ++i)
+        if (last[keys[i]] == i) idx.push_back(i);
+      const uint64_t u = idx.size();
+      std::vector<uint64_t> k2(u), s2, t2;
+      std::vector<float> e2, m2, v2;
+      if (emb) e2.resize(u * D);
+      if (m) m2.resize(u * D);
+      if (v) v2.resize(u * D);
+      if (step) s2.resize(u);
+      if (ts) t2.resize(u);
+      for (uint64_t j = 0; j < u; ++j) {
+        const uint64_t i = idx[j];
+        k2[j] = keys[i];
+        if (emb) std::copy(emb + i * D, emb + (i + 1) * D, e2.begin() + j * D);
+        if (m) std::copy(m + i * D, m + (i + 1) * D, m2.begin() + j * D);
+        if (v) std::copy(v + i * D, v + (i + 1) * D, v2.begin() + j * D);
+        if (step) s2[j] = step[i];
+        if (ts) t2[j] = ts[i];
+      }
+      return rs_table_import(t, u, k2.data(), emb ? e2.data() : nullptr, m ? m2.data() : nullptr,
+                             v ? v2.data() : nullptr, step ? s2.data() : nullptr, ts ? t2.data() : nullptr);
+    }
+  }
+  // Adam's bias-correction table covers every imported step (host-libm bits)
+  t->applies = std::max<uint64_t>(t->applies, max_step);
   uint64_t *dk = nullptr, *dstep = nullptr, *dts = nullptr;
   float *de = nullptr, *dm = nullptr, *dv = nullptr;
   int64_t* drows = nullptr;

@@ -278,7 +278,21 @@ class SparseStep:
         check(L.lib().rs_backward(self.ws.handle, self.table.handle, _ptr(g), n, C.byref(self.params.c()),
                                   _stream()), "backward")
 
+    def _check(self, ids, grads, out):
+        """The C-ABI reads raw device pointers: reject anything it would misread."""
+        d = self.table.dim
+        ok = (isinstance(ids, torch.Tensor) and ids.is_cuda and ids.dtype in (torch.int64, torch.uint64)
+              and ids.is_contiguous() and ids.dim() == 1)
+        n = ids.numel() if ok else -1
+        for t in (grads, out):
+            ok = ok and (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                         and tuple(t.shape) == (n, d))
+        if not ok:
+            raise L.ConfigError("SparseStep: ids must be a contiguous 1-D int64 CUDA tensor of n keys (as_keys), "
+                              "grads / out contiguous float32 CUDA tensors of shape (n, embedding_dim)")
+
     def step(self, ids: torch.Tensor, grads: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        self._check(ids, grads, out)
         check(L.lib().rs_step(self.ws.handle, self.table.handle, _ptr(ids), ids.numel(), _ptr(grads),
                               _ptr(out), C.byref(self.params.c()), _stream()), "step")
         return out
@@ -289,6 +303,7 @@ class SparseStep:
         out (run_workload's emb_checksum, workload.cpp:547-549), summed in the
         gather kernel."""
         assert checksum.dtype == torch.float64 and checksum.is_cuda
+        self._check(ids, grads, out)
         check(L.lib().rs_step_checksum(self.ws.handle, self.table.handle, _ptr(ids), ids.numel(), _ptr(grads),
                                        _ptr(out), C.byref(self.params.c()), _ptr(checksum), _stream()),
               "step_checksum")

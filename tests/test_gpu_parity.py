@@ -95,6 +95,36 @@ def _compare_contents(gpu, ora, fields=("keys", "emb", "m", "v", "step")):
         np.testing.assert_array_equal(a[f], b[f].astype(a[f].dtype), err_msg=f)
 
 
+def test_insert_and_import_duplicate_keys_last_wins(cuda, oracle):
+    # the reference inserts one key at a time (embed_table.cpp:193-227): within
+    # one batch the LAST occurrence of a key determines its row
+    rng = np.random.default_rng(17)
+    dim = 8
+    g = _gpu_table(64, dim)
+    o = Table(oracle, 64, dim, chunk_rows=64)
+    for it in range(6):
+        keys = rng.integers(0, 40, 300).astype(np.uint64)  # many duplicates per batch
+        keys[:3] = np.array([2**64 - 1, 2**64 - 2, 2**64 - 1], np.uint64)  # sentinel bit patterns, duplicated
+        emb = rng.standard_normal((len(keys), dim)).astype(np.float32)
+        g.insert(keys, torch.from_numpy(emb))
+        for k, e in zip(keys, emb):
+            o.insert(int(k), e)
+        _compare_contents(g, o, ("keys", "emb", "step"))
+    # import (host arrays): the same rule
+    h = _gpu_table(64, dim)
+    keys = rng.integers(0, 30, 200).astype(np.uint64)
+    emb = rng.standard_normal((len(keys), dim)).astype(np.float32)
+    h.import_entries(keys, emb, step=np.arange(len(keys), dtype=np.uint64))
+    got = h.export()
+    last = {int(k): i for i, k in enumerate(keys)}
+    assert sorted(last) == [int(k) for k in got["keys"]]
+    for j, k in enumerate(got["keys"]):
+        np.testing.assert_array_equal(got["emb"][j], emb[last[int(k)]])
+        assert int(got["step"][j]) == last[int(k)]
+    with pytest.raises(P.ConfigError):  # 32-bit device step counters
+        h.import_entries(np.array([5], np.uint64), emb[:1], step=np.array([1 << 33], np.uint64))
+
+
 def test_table_model_vs_oracle(cuda, oracle):
     rng = np.random.default_rng(99)
     dim = 4
