@@ -2,7 +2,7 @@
  * rsgpu.h -- C-ABI of the B200-native (sm_100a) sparse-embedding hot path.
  *
  * Drop-in boundary for the reference's table/lookup API
- * (/root/reference/proj/include/recsparse/*.hpp).  Plain pointers and sizes,
+ * (/root/reference/proj/include/recsparse/ *.hpp).  Plain pointers and sizes,
  * no C++ or torch types.  Every entry point names the reference interface it
  * replaces.  Pointers prefixed d_ are device pointers; `stream` is a
  * cudaStream_t (NULL = legacy default stream).  All calls are asynchronous on
@@ -80,6 +80,12 @@ const char* rs_status_string(int status);
 const char* rs_last_error(void);
 /* number of rsgpu kernel launches issued so far by this process (evidence) */
 uint64_t rs_kernel_launches(void);
+/* Device buffers and synchronous copies for C / C++ callers without a CUDA
+ * runtime of their own (the C++ shim include/recsparse_gpu uses them). */
+int rs_buffer_alloc(uint64_t bytes, void** out);
+int rs_buffer_free(void* d);
+int rs_copy_to_device(void* d, const void* h, uint64_t bytes);
+int rs_copy_to_host(void* h, const void* d, uint64_t bytes);
 
 /* ---- primitives (hash.hpp) --------------------------------------------- */
 /* hash64_batch (hash.hpp:38, hash.cpp:21-30) */
@@ -124,6 +130,18 @@ int rs_table_gather_rows(rs_table* t, const int64_t* d_rows, uint64_t n, float* 
  * max_entries = 0 to query the count.  Synchronizes. */
 int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* emb, float* m,
                     float* v, uint64_t* step, uint64_t* ts, uint64_t* count);
+/* bump_tick (embed_table.hpp:159-161): fast-forward the batch tick. */
+int rs_table_bump_tick(rs_table* t, uint64_t to);
+/* Deep copy (EmbedTable's copy constructor, embed_table.cpp:47-97): same
+ * slots, row ids, state, counters and tick.  Synchronizes. */
+int rs_table_clone(rs_table* src, rs_table** out);
+/* Row state of host keys (the row accessors embedding(h) / opt_m / opt_v /
+ * opt_step / row_timestamp of embed_table.hpp:123-132, batched, no side
+ * effects): rows[n] = row id or -1; emb/m/v [n x dim], step[n], ts[n] (the
+ * key's batch tick); zeros for absent keys.  Any output may be NULL.
+ * Synchronizes. */
+int rs_table_read_entries(rs_table* t, const uint64_t* keys, uint64_t n, int64_t* rows, float* emb,
+                          float* m, float* v, uint64_t* step, uint64_t* ts);
 /* Host import of full entries (restore path, checkpoint.cpp:238-249: keys are
  * re-inserted, slots are not portable).  m/v/step/ts may be NULL. */
 int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* emb,

@@ -54,4 +54,25 @@ const char* rs_last_error(void) { return rs::g_last_error.c_str(); }
 
 uint64_t rs_kernel_launches(void) { return rs::launches(); }
 
+// Device buffers and copies for C / C++ callers without a CUDA runtime of
+// their own (the C++ shim, include/recsparse_gpu): synchronous, legacy stream.
+int rs_buffer_alloc(uint64_t bytes, void** out) {
+  if (!out) return rs::fail(RS_ERR_CONFIG, "rs_buffer_alloc: null out");
+  *out = nullptr;
+  RS_CUDA(cudaMalloc(out, bytes ? bytes : 16));
+  return RS_OK;
+}
+int rs_buffer_free(void* d) {
+  if (d) RS_CUDA(cudaFree(d));
+  return RS_OK;
+}
+int rs_copy_to_device(void* d, const void* h, uint64_t bytes) {
+  if (bytes) RS_CUDA(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+  return RS_OK;
+}
+int rs_copy_to_host(void* h, const void* d, uint64_t bytes) {
+  if (bytes) RS_CUDA(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost));
+  return RS_OK;
+}
+
 }  // extern "C"

@@ -204,6 +204,47 @@ __global__ void __launch_bounds__(kProbeThreads)
   }
 }
 
+// Row state of given keys (no side effects): row id or -1, emb / m / v rows,
+// step counter and tick; zeros for absent keys.  8-lane group per key.
+__global__ void __launch_bounds__(kProbeThreads)
+    k_read_entries(const TableDev* __restrict__ td, const uint64_t* __restrict__ keys, uint64_t n,
+                   int64_t* rows64, float* emb, float* m, float* v, uint64_t* step, uint64_t* ts) {
+  const TableDesc d = td->d;
+  const unsigned lane = lane_id();
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint64_t group = (uint64_t)blockIdx.x * kGroupsPerBlock + (threadIdx.x >> 3);
+  const uint64_t ngroups = (uint64_t)gridDim.x * kGroupsPerBlock;
+  for (uint64_t i = group; i < n; i += ngroups) {
+    const uint64_t key = keys[i];
+    uint32_t row = kNoRow, tick = 0;
+    const int sp = special_index(key);
+    if (sp >= 0) {
+      row = td->c.special_row[sp];
+      tick = td->c.special_tick[sp];
+    } else {
+      const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
+      if (p.found) {
+        row = p.row;
+        tick = p.tick;
+      }
+    }
+    const uint64_t D = d.dim;
+    for (uint32_t e = g; e < D; e += kBucket) {
+      const bool live = row != kNoRow;
+      emb[i * D + e] = live ? d.emb[(uint64_t)row * D + e] : 0.f;
+      m[i * D + e] = live && d.s1 ? d.s1[(uint64_t)row * D + e] : 0.f;
+      v[i * D + e] = live && d.s2 ? d.s2[(uint64_t)row * D + e] : 0.f;
+    }
+    if (g == 0) {
+      rows64[i] = row == kNoRow ? -1 : (int64_t)row;
+      step[i] = row == kNoRow ? 0 : d.step[row];
+      ts[i] = tick;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kProbeThreads)
     k_table_remove(TableDev* __restrict__ td, const uint64_t* __restrict__ keys, uint64_t n,
                    uint8_t* removed) {
@@ -241,7 +282,7 @@ __global__ void __launch_bounds__(kProbeThreads)
       if (removed) removed[i] = row != kNoRow;
     }
   }
-  launch_epilogue(td, free_n0, fresh0, true, td->c.tick + 1);
+  launch_epilogue(td, free_n0, fresh0, 2, td->c.tick + 1);
 }
 
 // Rehash every occupied slot of `old` into the (empty) new key structure.
@@ -674,7 +715,7 @@ int rs_table_create(const rs_table_config* cfg, rs_table** out) {
   if (c.optimizer > RS_OPT_ADAGRAD) return fail(RS_ERR_CONFIG, "TableConfig: unknown optimizer");
   rs_table* t = new rs_table();
   t->cfg = c;
-  t->capacity = std::max<uint64_t>(c.capacity, 2 * kBucket);
+  t->capacity = std::max<uint64_t>(c.capacity, kBucket);  // >= one bucket
   t->desc.dim = c.embedding_dim;
   t->desc.opt = c.optimizer;
   cudaStream_t s = nullptr;
@@ -864,6 +905,99 @@ int rs_table_evict(rs_table* t, uint64_t k, uint64_t* evicted, void* stream) {
   if (!st) st = evict_device(t, nullptr, 0, k, s);
   if (!st) st = table_after_op(t, s);
   if (!st) st = evict_count(t, evicted, s);  // synchronizes
+  return st;
+}
+
+// EmbedTable's copy constructor (embed_table.cpp:47-97): a device-side deep
+// copy -- same key slots, row ids, row pool, free stack, counters and tick --
+// so handles, contents and every later operation behave identically.
+int rs_table_clone(rs_table* src, rs_table** out) {
+  if (!src || !out) return fail(RS_ERR_CONFIG, "rs_table_clone: null argument");
+  RS_CUDA(cudaDeviceSynchronize());
+  rs_table_config c = src->cfg;
+  c.capacity = src->capacity;
+  c.initial_rows = src->desc.row_cap;
+  rs_table* t = nullptr;
+  int st = rs_table_create(&c, &t);
+  if (st) return st;
+  auto cp = [&](void* d, const void* s_, size_t b) {
+    return b && d && s_ ? cudaMemcpy(d, s_, b, cudaMemcpyDeviceToDevice) : cudaSuccess;
+  };
+  const TableDesc& a = src->desc;
+  TableDesc& b = t->desc;
+  const size_t D = a.dim, R = a.row_cap;
+  cudaError_t e = cp(b.slots, a.slots, src->capacity * sizeof(Slot));
+  if (e == cudaSuccess) e = cp(b.emb, a.emb, R * D * 4);
+  if (e == cudaSuccess) e = cp(b.s1, a.s1, R * D * 4);
+  if (e == cudaSuccess) e = cp(b.s2, a.s2, R * D * 4);
+  if (e == cudaSuccess) e = cp(b.step, a.step, R * 4);
+  if (e == cudaSuccess) e = cp(b.free_stack, a.free_stack, R * 4);
+  if (e == cudaSuccess) e = cp(&t->dev->c, &src->dev->c, sizeof(TableCounters));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    rs_table_destroy(t);
+    return cuda_fail(e, "rs_table_clone");
+  }
+  t->cfg = src->cfg;
+  t->requested_total = src->requested_total;
+  t->exact_occ = src->exact_occ;
+  t->exact_tomb = src->exact_tomb;
+  t->exact_rows = src->exact_rows;
+  t->exact_requested = src->exact_requested;
+  t->applies = src->applies;
+  t->host_tick = src->host_tick;
+  *out = t;
+  return RS_OK;
+}
+
+// EmbedTable::bump_tick (embed_table.hpp:159-161): the batch tick never moves backwards.
+int rs_table_bump_tick(rs_table* t, uint64_t to) {
+  if (!t) return fail(RS_ERR_CONFIG, "rs_table_bump_tick: null table");
+  if (to >> 32) return fail(RS_ERR_CONFIG, "rs_table_bump_tick: the device tick is 32 bits");
+  RS_CUDA(cudaDeviceSynchronize());
+  uint32_t cur = 0;
+  RS_CUDA(cudaMemcpy(&cur, &t->dev->c.tick, 4, cudaMemcpyDeviceToHost));
+  if (to > cur) {
+    const uint32_t v = (uint32_t)to;
+    RS_CUDA(cudaMemcpy(&t->dev->c.tick, &v, 4, cudaMemcpyHostToDevice));
+  }
+  return RS_OK;
+}
+
+int rs_table_read_entries(rs_table* t, const uint64_t* keys, uint64_t n, int64_t* rows, float* emb,
+                          float* m, float* v, uint64_t* step, uint64_t* ts) {
+  if (!t || (n && !keys)) return fail(RS_ERR_CONFIG, "rs_table_read_entries: null argument");
+  if (n == 0) return RS_OK;
+  const uint64_t D = t->desc.dim;
+  // one device block: keys | rows | step | ts | emb | m | v
+  const size_t bytes = n * (8 + 8 + 8 + 8) + 3 * n * D * 4;
+  char* dbuf = nullptr;
+  RS_CUDA(cudaMalloc(&dbuf, bytes));
+  uint64_t* dk = reinterpret_cast<uint64_t*>(dbuf);
+  int64_t* dr = reinterpret_cast<int64_t*>(dk + n);
+  uint64_t* ds = reinterpret_cast<uint64_t*>(dr + n);
+  uint64_t* dt = ds + n;
+  float* de = reinterpret_cast<float*>(dt + n);
+  float* dm = de + n * D;
+  float* dv = dm + n * D;
+  int st = RS_OK;
+  cudaError_t e = cudaMemcpy(dk, keys, n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_read_entries<<<grid_for(n, kGroupsPerBlock, 148 * 8), kProbeThreads>>>(t->dev, dk, n, dr, de, dm, dv, ds, dt);
+    count_launch();
+    e = cudaGetLastError();
+  }
+  auto back = [&](void* h, const void* d, size_t b) {
+    if (h && e == cudaSuccess) e = cudaMemcpy(h, d, b, cudaMemcpyDeviceToHost);
+  };
+  back(rows, dr, n * 8);
+  back(emb, de, n * D * 4);
+  back(m, dm, n * D * 4);
+  back(v, dv, n * D * 4);
+  back(step, ds, n * 8);
+  back(ts, dt, n * 8);
+  if (e != cudaSuccess) st = cuda_fail(e, "rs_table_read_entries");
+  cudaFree(dbuf);
   return st;
 }
 

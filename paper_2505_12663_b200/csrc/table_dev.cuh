@@ -211,8 +211,11 @@ __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const Tab
 
 // Last-block epilogue: folds this launch's per-launch counters into the
 // table counters (the "fix-up" of the lock-free row allocator).
+// bump_tick: 0 keep the tick, 1 advance it, 2 advance it iff this launch
+// removed a key (remove of absent keys leaves the table identical,
+// embed_table.cpp:250-260)
 __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
-                                                unsigned long long fresh0, bool bump_tick,
+                                                unsigned long long fresh0, int bump_tick,
                                                 uint32_t tick_now) {
   __syncthreads();
   __shared__ bool s_last;
@@ -238,6 +241,7 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     c.free_n += c.returned;
     c.returned = 0;
     // removals push rows above free_n0 (remove kernel); fold them in
+    const bool any_removed = c.removed != 0;
     c.free_n += c.removed;
     c.occupied = c.occupied + c.inserted - c.removed;
     c.tombstones = c.tombstones - c.reused + c.removed;
@@ -245,7 +249,7 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     c.inserted = 0;
     c.reused = 0;
     c.removed = 0;
-    if (bump_tick) c.tick = tick_now;
+    if (bump_tick == 1 || (bump_tick == 2 && any_removed)) c.tick = tick_now;
     c.blocks_done = 0;
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
