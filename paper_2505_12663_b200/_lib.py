@@ -91,6 +91,13 @@ _SIGS = {
     "rs_status_string": (C.c_char_p, [C.c_int]),
     "rs_last_error": (C.c_char_p, []),
     "rs_kernel_launches": (u64, []),
+    "rs_buffer_alloc": (C.c_int, [u64, C.POINTER(vp)]),
+    "rs_buffer_free": (C.c_int, [vp]),
+    "rs_copy_to_device": (C.c_int, [vp, vp, u64]),
+    "rs_copy_to_host": (C.c_int, [vp, vp, u64]),
+    "rs_table_bump_tick": (C.c_int, [vp, u64]),
+    "rs_table_clone": (C.c_int, [vp, C.POINTER(vp)]),
+    "rs_table_read_entries": (C.c_int, [vp, vp, u64, vp, vp, vp, vp, vp, vp]),
     "rs_hash64_batch": (C.c_int, [vp, u64, vp, vp]),
     "rs_shard_of_batch": (C.c_int, [vp, u64, u32, vp, vp]),
     "rs_table_create": (C.c_int, [C.POINTER(rs_table_config), C.POINTER(vp)]),
