@@ -264,6 +264,7 @@ int step_reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s
 // step_fast.cu
 bool fast_step_supported(const rs_table* t);
 int fast_prepare(rs_workspace* ws);
+int fast_check_errors(rs_workspace* ws, cudaStream_t s);
 void fast_free(rs_workspace* ws);
 int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
                  float* d_out, const void* opt_args, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,

@@ -2091,6 +2091,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   ws->last_table = t;
   ws->last_exact = false;
   if (fast) {
+    if ((st = fast_check_errors(ws, s))) return st;
     ws->fast.last = use;
     ws->fast.cur ^= 1;
     ws->last_fast = true;

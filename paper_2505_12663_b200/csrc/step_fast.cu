@@ -74,6 +74,8 @@ struct FShared {
   uint32_t ntiles;
   uint32_t hot_min;    // ids with more occurrences take the hot (tile partial) path, <= 64
   unsigned long long* trace;  // diagnostics timeline or null
+  uint64_t n_slots;    // S + 1 (checked builds)
+  uint32_t max_tokens, max_hot;
 };
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -84,6 +86,17 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
   x ^= x >> 16;
   return x;
 }
+
+// Checked builds (-DRS_BOUNDS, `make EXTRA=-DRS_BOUNDS OUT=...`): every
+// computed index is range-checked before use; a violation sets error bit 2
+// of ctr[2] (rs_step then fails with RS_ERR_INVARIANT) and skips the access.
+// compute-sanitizer is not available on this pool; this is the substitute.
+#ifdef RS_BOUNDS
+#define RS_IDX_OK(cond, ctr) \
+  ((cond) ? true : (atomicOr((ctr) + 2, 2u), printf("step_fast bounds: %s (%s:%d)\n", #cond, __FILE__, __LINE__), false))
+#else
+#define RS_IDX_OK(cond, ctr) true
+#endif
 
 // Device-side timeline (rs_workspace_trace, diagnostics): per (kernel, block)
 // the first warp start and the last warp end (%globaltimer, ns).
@@ -248,15 +261,17 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     const uint32_t k = lnew[p] - 1, u = s_base + k;
     const uint32_t gs = lslot[p];
     fu[k] = u;
-    a.sh.uidx[gs] = u;
-    a.use.u_slot[u] = gs;
-    a.unique[u] = id;
+    if (RS_IDX_OK(gs < a.sh.n_slots && u < a.sh.max_tokens, a.sh.ctr)) {
+      a.sh.uidx[gs] = u;
+      a.use.u_slot[u] = gs;
+      a.unique[u] = id;
+    }
   }
   if (valid) {
     const uint32_t gs = lslot[p];
     a.slot_of[t] = gs;
     const uint32_t rank = lbase[p] + lr;
-    if (rank < kPosMax) a.sh.pos[(size_t)gs * kPosMax + rank] = t;
+    if (rank < kPosMax && RS_IDX_OK(gs < a.sh.n_slots, a.sh.ctr)) a.sh.pos[(size_t)gs * kPosMax + rank] = t;
   }
   __syncthreads();
   // the ids this tile claimed: find-or-insert-zero in the table, 8 lanes per id
@@ -374,6 +389,7 @@ struct FcArgs {
   const uint32_t* urow;  // table row per unique id (KA)
   uint32_t exp;          // timing experiments (RS_FC_EXP bits, wrong results): 1 no optimizer, 2 no grads, 4 no forward
   uint32_t heavy_first;  // > 0: two passes, ids with more occurrences first (RS_FC_HEAVY)
+  uint32_t n_tokens;
 };
 
 #ifndef RS_FC_MINB
@@ -411,6 +427,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
     const uint32_t gs = __ldg(a.use.u_slot + uu);
     const uint32_t row = __ldg(a.urow + uu);
     if (row == kNoRow) continue;  // table error (reported through the counters)
+    if (!RS_IDX_OK(gs < a.sh.n_slots && row < d.row_cap, a.sh.ctr)) continue;
     const uint32_t c = __ldcg(&a.use.rec[gs].cnt);
     uint32_t p[PPT], r[PPT];
 #pragma unroll
@@ -446,7 +463,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
     }
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
-      if (gl + j * G < c) order[r[j]] = p[j];
+      if (gl + j * G < c && RS_IDX_OK(r[j] < c && p[j] < a.n_tokens, a.sh.ctr)) order[r[j]] = p[j];
     __syncwarp(gmask);
     // the forward for this id: its pre-update row to each of its tokens
     // (distributed_lookup's inverse expand, exchange_sim.cpp:211-230)
@@ -684,7 +701,7 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
       const uint32_t old = atomicCAS(&a.sh.hidx[sl], kHotNone, kHotClaim);
       if (old == kHotNone) {
         h = atomicAdd(&a.sh.ctr[0], 1u);
-        a.sh.hot_slot[h] = sl;
+        if (RS_IDX_OK(h < a.sh.max_hot, a.sh.ctr)) a.sh.hot_slot[h] = sl;
         __threadfence();
         atomicExch(&a.sh.hidx[sl], h);
       } else {
@@ -700,7 +717,7 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
       __nanosleep(32);
       h = atomicAdd(&a.sh.hidx[sl], 0u);
     }
-    if (h < kHotClaim) {
+    if (h < kHotClaim && RS_IDX_OK(h < a.sh.max_hot && tile < a.sh.ntiles && s_pbase + tid < a.n, a.sh.ctr)) {
       gpidx[tid] = s_pbase + tid;
       a.sh.hlist[(size_t)h * a.sh.ntiles + tile] = s_pbase + tid + 1;
     } else {
@@ -796,6 +813,7 @@ __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
   const uint32_t nh = *reinterpret_cast<volatile uint32_t*>(&a.sh.ctr[0]);
   const uint32_t NT = a.sh.ntiles;
   for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    if (!RS_IDX_OK(h < a.sh.max_hot, a.sh.ctr)) break;
     const uint32_t gs = a.sh.hot_slot[h];
     uint32_t* hl = a.sh.hlist + (size_t)h * NT;
     if (warp == NWF - 1) {  // the row's optimizer state: into L2 while the partials are summed
@@ -840,7 +858,8 @@ __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
       float x[PF][CH][VEC];
 #pragma unroll
       for (int q = 0; q < PF; ++q)
-        if (k0 + q < r1) load_vec<VEC, CH>(a.sh.part + (size_t)list[k0 + q] * D, D, x[q], true);
+        if (k0 + q < r1 && RS_IDX_OK(list[k0 + q] < a.sh.max_tokens, a.sh.ctr))
+          load_vec<VEC, CH>(a.sh.part + (size_t)list[k0 + q] * D, D, x[q], true);
 #pragma unroll
       for (int q = 0; q < PF; ++q)
         if (k0 + q < r1) add_acc<VEC, CH>(acc, x[q]);
@@ -958,6 +977,21 @@ void fast_free(rs_workspace* ws) {
 
 int fast_prepare(rs_workspace* ws) { return fast_alloc(ws); }
 
+// Checked builds: the step's device error bits (bounds violations, a hot-index
+// claim that never resolved) fail the call.  No-op otherwise (no sync).
+int fast_check_errors(rs_workspace* ws, cudaStream_t s) {
+#ifdef RS_BOUNDS
+  uint32_t bits = 0;
+  RS_CUDA(cudaStreamSynchronize(s));
+  RS_CUDA(cudaMemcpy(&bits, ws->fast.ctr + 2, 4, cudaMemcpyDeviceToHost));
+  if (bits) return fail(RS_ERR_INVARIANT, "fast step: device error bits " + std::to_string(bits));
+#else
+  (void)ws;
+  (void)s;
+#endif
+  return RS_OK;
+}
+
 static FSet fset(rs_workspace* ws, int k) {
   rs_fast_set& x = ws->fast.set[k];
   FSet s;
@@ -981,6 +1015,9 @@ static FShared fshared(rs_workspace* ws) {
   s.ntiles = (uint32_t)f.ntiles;
   s.hot_min = f.hot_min;
   s.trace = f.trace;
+  s.n_slots = ws->S + 1;
+  s.max_tokens = (uint32_t)ws->max_tokens;
+  s.max_hot = (uint32_t)f.max_hot;
   return s;
 }
 
@@ -1066,6 +1103,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     c.use = fa.use;
     c.sh = sh;
     c.grads = d_grads;
+    c.n_tokens = (uint32_t)n;
     c.urow = ws->urow;
     static const uint32_t fexp = getenv("RS_FC_EXP") ? (uint32_t)atoi(getenv("RS_FC_EXP")) : 0u;
     c.exp = fexp;
