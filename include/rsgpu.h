@@ -405,6 +405,15 @@ int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len,
                          double sigma, double zipf, uint32_t tables, const uint64_t* vocab,
                          uint64_t* lengths, uint64_t* ids, uint64_t max_tokens,
                          uint64_t* n_tokens);
+/* generate_workload_file (workload.cpp:280-315): the same workload written in
+ * the reference's text format (header line, then "sid<TAB>label<TAB>ids"). */
+int rs_workload_write(const char* path, uint64_t seed, uint64_t num_sequences, double mean_len,
+                      uint64_t max_len, double sigma, double zipf, uint32_t tables, const uint64_t* vocab);
+/* read_workload_file (workload.cpp:317-339): host arrays sample_ids/labels/
+ * lengths [cap_seq], ids [cap_tok] (any may be NULL); zero capacities return
+ * the counts only.  RS_ERR_IO on open failure, "bad record", "empty sequence". */
+int rs_workload_read(const char* path, uint64_t cap_seq, uint64_t cap_tok, uint64_t* sample_ids,
+                     double* labels, uint64_t* lengths, uint64_t* ids, uint64_t* n_seq, uint64_t* n_tok);
 /* pseudo_sparse_grad per token on device: d_out[t] = g(sample_of_token[t], step) */
 int rs_pseudo_grads(const uint64_t* d_sample_of_token, uint64_t n, uint64_t step, uint32_t dim,
                     float* d_out, void* stream);

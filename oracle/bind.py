@@ -112,6 +112,10 @@ class Oracle:
             f("c1_step", C.c_double, vp, u64p, f32p, C.c_uint64, C.c_int, C.c_double, C.c_double,
               vp)
             f("dist_step", C.c_double, vp, u64p, u64p, f32p, C.c_int, C.c_double, C.c_double)
+            f("write_workload_file", C.c_int, C.c_char_p, C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+              C.c_double, C.c_double, C.c_uint32, u64p)
+            f("read_workload_file", C.c_int64, C.c_char_p, u64p, np.ctypeslib.ndpointer(np.float64), u64p, u64p,
+              C.c_uint64, C.POINTER(C.c_uint64))
             f("omp_max_threads", C.c_int)
         else:
             f("table_export", C.c_size_t, vp, vp, vp, vp, vp, vp, vp)

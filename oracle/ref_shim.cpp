@@ -449,6 +449,47 @@ int64_t ref_generate_workload(uint64_t seed, uint64_t num_sequences, double mean
     return -1;
   }
 }
+// generate_workload_file / read_workload_file (workload.cpp:309-339) as they are.
+int ref_write_workload_file(const char* path, uint64_t seed, uint64_t num_sequences, double mean_len,
+                            uint64_t max_len, double sigma, double zipf, uint32_t tables, const uint64_t* vocab) {
+  try {
+    WorkloadSpec spec;
+    spec.seed = seed;
+    spec.num_sequences = num_sequences;
+    spec.length.mean = mean_len;
+    spec.length.max_len = max_len;
+    spec.length.sigma = sigma;
+    spec.zipf_exponent = zipf;
+    for (uint32_t t = 0; t < tables; ++t) {
+      const std::string name = "t" + std::to_string(t);
+      spec.features.push_back({"f" + std::to_string(t), 1, {name}, Pooling::kNone});
+      spec.table_vocab[name] = vocab[t];
+    }
+    generate_workload_file(spec, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+// -> number of samples (tokens in *n_tok), or -status on an exception
+int64_t ref_read_workload_file(const char* path, uint64_t* sample_ids, double* labels, uint64_t* lengths,
+                               uint64_t* ids, uint64_t cap_tok, uint64_t* n_tok) {
+  try {
+    const std::vector<SequenceSample> s = read_workload_file(path);
+    uint64_t tok = 0;
+    for (size_t i = 0; i < s.size(); ++i) {
+      sample_ids[i] = s[i].sample_id;
+      labels[i] = s[i].label;
+      lengths[i] = s[i].feature_ids.size();
+      for (uint64_t id : s[i].feature_ids)
+        if (tok < cap_tok) ids[tok++] = id;
+    }
+    *n_tok = tok;
+    return static_cast<int64_t>(s.size());
+  } catch (const std::exception& e) {
+    return -status_of(e);
+  }
+}
 void ref_pseudo_sparse_grad(uint64_t sample_id, uint64_t step, float* out, uint32_t dim) {
   pseudo_sparse_grad(sample_id, step, std::span<float>(out, dim));
 }

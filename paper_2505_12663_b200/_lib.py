@@ -185,6 +185,8 @@ _SIGS = {
     "rs_workload_generate": (C.c_int, [u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp, vp, vp,
                                        u64, C.POINTER(u64)]),
     "rs_pseudo_grads": (C.c_int, [vp, u64, u64, u32, vp, vp]),
+    "rs_workload_write": (C.c_int, [C.c_char_p, u64, u64, C.c_double, u64, C.c_double, C.c_double, u32, vp]),
+    "rs_workload_read": (C.c_int, [C.c_char_p, u64, u64, vp, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)]),
 }
 
 _lock = threading.Lock()

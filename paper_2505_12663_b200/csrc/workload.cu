@@ -10,6 +10,10 @@
 #include <cmath>
 #include <random>
 #include <vector>
+#include <string>
+#include <cstdio>
+#include <sstream>
+#include <fstream>
 
 #include "rs_internal.cuh"
 
@@ -214,6 +218,9 @@ __global__ void __launch_bounds__(256) k_sum_partials(const float* __restrict__ 
 }
 
 }  // namespace
+int generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len, double sigma,
+             double zipf, uint32_t tables, const uint64_t* vocab, uint64_t* lengths, uint64_t* ids,
+             uint64_t max_tokens, uint64_t* n_tokens, double* labels);
 }  // namespace rs
 
 extern "C" {
@@ -222,7 +229,16 @@ int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len,
                          double sigma, double zipf, uint32_t tables, const uint64_t* vocab,
                          uint64_t* lengths, uint64_t* ids, uint64_t max_tokens,
                          uint64_t* n_tokens) {
-  using namespace rs;
+  return rs::generate(seed, num_sequences, mean_len, max_len, sigma, zipf, tables, vocab, lengths, ids,
+                      max_tokens, n_tokens, nullptr);
+}
+
+}  // extern "C"
+
+namespace rs {
+int generate(uint64_t seed, uint64_t num_sequences, double mean_len, uint64_t max_len, double sigma,
+             double zipf, uint32_t tables, const uint64_t* vocab, uint64_t* lengths, uint64_t* ids,
+             uint64_t max_tokens, uint64_t* n_tokens, double* labels) {
   if (!(sigma > 0) || max_len < 2 || !(mean_len > 1.0) || mean_len >= (double)max_len ||
       tables == 0 || zipf < 0)
     return fail(RS_ERR_CONFIG, "workload: bad length/zipf config");
@@ -264,7 +280,8 @@ int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len,
       len = std::max<uint64_t>(1, std::min(nn, max_len));
       break;
     }
-    (void)rng.unit();  // label
+    const double label = rng.unit();
+    if (labels) labels[sid - 1] = label;
     lengths[sid - 1] = len;
     for (uint64_t t = 0; t < len; ++t) {
       const uint32_t ord = static_cast<uint32_t>(1 + t % tables);
@@ -277,6 +294,80 @@ int rs_workload_generate(uint64_t seed, uint64_t num_sequences, double mean_len,
     }
   }
   *n_tokens = tok;
+  return RS_OK;
+}
+}  // namespace rs
+
+extern "C" {
+
+// generate_workload_file (workload.cpp:280-315): the reference's text format
+// -- a "# recsparse-workload v1" header, then one line per sequence:
+// sample id, TAB, label (%.4f), TAB, the catalog-tagged ids space-separated.
+int rs_workload_write(const char* path, uint64_t seed, uint64_t num_sequences, double mean_len,
+                      uint64_t max_len, double sigma, double zipf, uint32_t tables, const uint64_t* vocab) {
+  using namespace rs;
+  if (!path) return fail(RS_ERR_CONFIG, "rs_workload_write: null path");
+  std::vector<uint64_t> lengths(num_sequences);
+  std::vector<double> labels(num_sequences);
+  std::vector<uint64_t> ids(std::max<uint64_t>(1, num_sequences * max_len));
+  uint64_t n = 0;
+  int st = generate(seed, num_sequences, mean_len, max_len, sigma, zipf, tables, vocab, lengths.data(),
+                    ids.data(), ids.size(), &n, labels.data());
+  if (st) return st;
+  FILE* f = std::fopen(path, "w");
+  if (!f) return fail(RS_ERR_IO, std::string("cannot open workload file for writing: ") + path);
+  bool ok = std::fprintf(f, "# recsparse-workload v1 seed=%llu sequences=%llu tables=%u\n",
+                         (unsigned long long)seed, (unsigned long long)num_sequences, tables) > 0;
+  uint64_t tok = 0;
+  for (uint64_t s = 0; ok && s < num_sequences; ++s) {
+    ok = std::fprintf(f, "%llu\t%.4f\t", (unsigned long long)(s + 1), labels[s]) > 0;
+    for (uint64_t t = 0; ok && t < lengths[s]; ++t)
+      ok = std::fprintf(f, t ? " %llu" : "%llu", (unsigned long long)ids[tok++]) > 0;
+    ok = ok && std::fputc('\n', f) != EOF;
+  }
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) return fail(RS_ERR_IO, std::string("write failed: ") + path);
+  return RS_OK;
+}
+
+// read_workload_file (workload.cpp:317-339): blank and '#' lines skipped;
+// each record is "sample_id label id id ..."; a record without an id or
+// without both leading fields is an IoError naming path:line.  Pass zero
+// capacities to get the counts only.
+int rs_workload_read(const char* path, uint64_t cap_seq, uint64_t cap_tok, uint64_t* sample_ids,
+                     double* labels, uint64_t* lengths, uint64_t* ids, uint64_t* n_seq, uint64_t* n_tok) {
+  using namespace rs;
+  if (!path || !n_seq || !n_tok) return fail(RS_ERR_CONFIG, "rs_workload_read: null argument");
+  std::ifstream is(path);
+  if (!is) return fail(RS_ERR_IO, std::string("cannot open workload file: ") + path);
+  std::string line;
+  uint64_t lineno = 0, s = 0, tok = 0;
+  const bool fill = cap_seq && cap_tok;
+  while (std::getline(is, line)) {
+    ++lineno;
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ls(line);
+    uint64_t sid = 0;
+    double label = 0;
+    if (!(ls >> sid >> label))
+      return fail(RS_ERR_IO, std::string(path) + ":" + std::to_string(lineno) + ": bad record");
+    uint64_t id, len = 0;
+    while (ls >> id) {
+      if (fill && tok < cap_tok) ids[tok] = id;
+      ++tok;
+      ++len;
+    }
+    if (len == 0) return fail(RS_ERR_IO, std::string(path) + ":" + std::to_string(lineno) + ": empty sequence");
+    if (fill && s < cap_seq) {
+      if (sample_ids) sample_ids[s] = sid;
+      if (labels) labels[s] = label;
+      if (lengths) lengths[s] = len;
+    }
+    ++s;
+  }
+  *n_seq = s;
+  *n_tok = tok;
+  if (fill && (s > cap_seq || tok > cap_tok)) return fail(RS_ERR_CONFIG, "rs_workload_read: buffers too small");
   return RS_OK;
 }
 

@@ -34,6 +34,29 @@ def generate(seed: int, num_sequences: int, mean_len: float, max_len: int, sigma
         cap = min(cap * 2, num_sequences * max_len)
 
 
+def write_workload_file(path: str, seed: int, num_sequences: int, mean_len: float, max_len: int, sigma: float,
+                        zipf: float, vocab) -> None:
+    """generate_workload_file (workload.cpp:280-315): the reference's text format."""
+    vocab = np.ascontiguousarray(np.atleast_1d(np.asarray(vocab, dtype=np.uint64)))
+    check(L.lib().rs_workload_write(str(path).encode(), seed, num_sequences, mean_len, max_len, sigma, zipf,
+                                    len(vocab), vocab.ctypes.data), "write_workload_file")
+
+
+def read_workload_file(path: str) -> tuple[np.ndarray, np.ndarray, np.ndarray, np.ndarray]:
+    """read_workload_file (workload.cpp:317-339) -> (sample_ids u64, labels f64,
+    lengths u64, ids u64 concatenated in file order); IoError on a bad file."""
+    ns, nt = C.c_uint64(), C.c_uint64()
+    p = str(path).encode()
+    check(L.lib().rs_workload_read(p, 0, 0, None, None, None, None, C.byref(ns), C.byref(nt)), "read_workload_file")
+    sid = np.zeros(max(ns.value, 1), np.uint64)
+    lab = np.zeros(max(ns.value, 1), np.float64)
+    ln = np.zeros(max(ns.value, 1), np.uint64)
+    ids = np.zeros(max(nt.value, 1), np.uint64)
+    check(L.lib().rs_workload_read(p, len(sid), len(ids), sid.ctypes.data, lab.ctypes.data, ln.ctypes.data,
+                                   ids.ctypes.data, C.byref(ns), C.byref(nt)), "read_workload_file")
+    return sid[: ns.value], lab[: ns.value], ln[: ns.value], ids[: nt.value]
+
+
 def sample_of_tokens(lengths, first_sample_id: int = 1) -> np.ndarray:
     lengths = np.asarray(lengths, np.int64)
     return np.repeat(np.arange(first_sample_id, first_sample_id + len(lengths), dtype=np.uint64), lengths)
