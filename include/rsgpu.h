@@ -194,7 +194,7 @@ int rs_workspace_set_profiling(rs_workspace* ws, int on);
  * at the workspace's first rs_step): out[(kernel * 4096 + block) * 2 + {0,1}]
  * = first warp start / last warp end (%globaltimer ns) of each block of the
  * steps since the last call; kernels 0 dedup+probe, 1 CSR finish, 2 hot
- * tiles, 3 hot finish, 4 scratch clean.  *n_out = 0 when tracing is off. */
+ * tiles, 3 hot finish, 4 scratch clean, 5 heavy CSR ids.  *n_out = 0 when tracing is off. */
 int rs_workspace_trace(rs_workspace* ws, uint64_t* out, uint64_t cap, uint64_t* n_out);
 int rs_workspace_phase_ms(rs_workspace* ws, double* ms, uint32_t nphases, uint64_t* count);
 /* n_unique of the last dedup on this workspace (host value).  Synchronizes. */

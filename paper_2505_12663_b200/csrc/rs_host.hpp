@@ -107,8 +107,10 @@ struct rs_fast {
   unsigned long long* trace = nullptr;  // RS_TRACE=1: per (kernel, block) start / end timeline
   uint64_t ntiles = 0, max_hot = 0;
   uint32_t hot_min = 64;         // ids with more occurrences take the hot path (RS_HOT_MIN)
-  cudaStream_t aux2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_j1 = nullptr, ev_j2 = nullptr;
+  uint32_t light_max = 8;        // CSR ids with more occurrences: the heavy CSR kernel (RS_LIGHT_MAX)
+  uint32_t* heavy = nullptr;     // [max_tokens] slots of the heavy CSR ids
+  cudaStream_t aux2 = nullptr, aux3 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_j1 = nullptr, ev_j2 = nullptr, ev_j3 = nullptr;
 };
 
 struct rs_workspace {

@@ -74,6 +74,8 @@ struct FShared {
   uint32_t ntiles;
   uint32_t hot_min;    // ids with more occurrences take the hot (tile partial) path, <= 64
   unsigned long long* trace;  // diagnostics timeline or null
+  uint32_t* heavy;     // [max_tokens] slots of ids with > light_max occurrences (KA)
+  uint32_t light_max;  // CSR ids up to this many occurrences: the light kernel; above: the heavy one
   uint64_t n_slots;    // S + 1 (checked builds)
   uint32_t max_tokens, max_hot;
 };
@@ -169,6 +171,7 @@ __device__ __forceinline__ uint64_t rec_insert(const FSet& S, uint64_t id, uint6
 struct FaArgs {
   const uint64_t* ids;
   uint32_t n;
+  uint32_t set;  // scratch set parity of this step
   FSet use, clean;
   FShared sh;
   TableDev* td;
@@ -197,6 +200,10 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     a.sh.ctr[0] = 0;
     a.sh.ctr[1] = 0;
   }
+  // heavy-list counts alternate with the scratch set (ctr[5 + set]): KA's
+  // blocks append to this set's (zeroed by the previous step), block 0 zeroes
+  // the other one for the next step
+  if (blockIdx.x == 0 && tid == 0) a.sh.ctr[5 + (a.set ^ 1)] = 0;
   for (uint32_t i = tid; i <= L; i += kTT) {
     lkey[i] = kEmptyKey;
     lnew[i] = 0;
@@ -240,8 +247,15 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   if (rep) {
     bool fresh = false;
     const uint64_t gs = rec_insert(a.use, id, h, &fresh, first0);
-    lbase[p] = atomicAdd(&a.use.rec[gs].cnt, lcnt[p]);  // the tile's base among the id's occurrences
+    const uint32_t base = atomicAdd(&a.use.rec[gs].cnt, lcnt[p]);  // the tile's base among the id's occurrences
+    lbase[p] = base;
     lslot[p] = (uint32_t)gs;
+    // the tile whose occurrences carry the id past light_max lists it (once) for
+    // the heavy CSR kernel; past hot_min it is a hot id and that kernel skips it
+    if (base <= a.sh.light_max && base + lcnt[p] > a.sh.light_max) {
+      const uint32_t k = atomicAdd(&a.sh.ctr[5 + a.set], 1u);
+      if (RS_IDX_OK(k < a.sh.max_tokens, a.sh.ctr)) a.sh.heavy[k] = (uint32_t)gs;
+    }
     if (fresh) {
       // the probe below starts at this bucket: fetch it into L2 now (overlaps
       // the numbering barriers)
@@ -388,51 +402,60 @@ struct FcArgs {
   double* tokcs;     // per-token row sums (checksum) or null
   const uint32_t* urow;  // table row per unique id (KA)
   uint32_t exp;          // timing experiments (RS_FC_EXP bits, wrong results): 1 no optimizer, 2 no grads, 4 no forward
-  uint32_t heavy_first;  // > 0: two passes, ids with more occurrences first (RS_FC_HEAVY)
   uint32_t n_tokens;
+  const uint32_t* list;    // null: every unique id; else slots (KA's heavy list) ...
+  const uint32_t* list_n;  // ... and their count
+  uint32_t c_min, c_max;   // ids with c_min < occurrences <= c_max
 };
 
 #ifndef RS_FC_MINB
 #define RS_FC_MINB 5
 #endif
-template <int G, int NV>
+template <int G, int NV, int PMAX>
 __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, OptArgs o) {
-  WarpTrace wt_(a.sh.trace, 1);
-  constexpr int PPT = (int)(kPosMax / G);  // positions held per thread
-  __shared__ uint32_t order_s[(256 / G) * kPosMax];
+  WarpTrace wt_(a.sh.trace, a.list ? 5 : 1);
+  constexpr int PPT = (PMAX + G - 1) / G;  // positions held per thread
+  __shared__ uint32_t order_s[(256 / G) * PMAX];
   const TableDesc d = a.td->d;
   const uint32_t D4 = d.dim >> 2;
   const uint32_t lane = lane_id();
   const uint32_t gl = lane & (G - 1);
   const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (lane & ~(G - 1));
   const uint32_t gpb = blockDim.x / G;
-  uint32_t* order = order_s + (threadIdx.x / G) * kPosMax;
+  uint32_t* order = order_s + (threadIdx.x / G) * PMAX;
   const uint32_t gid = blockIdx.x * gpb + threadIdx.x / G;
   const uint32_t ngroups = gridDim.x * gpb;
-  const uint32_t nu = *a.use.cnt;
+  // the ids: every unique id (light kernel: c <= c_max), or KA's list of the
+  // heavy ones (c_min < c <= c_max)
+  const uint32_t nitems = a.list ? *a.list_n : *a.use.cnt;
   const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grads);
   float4* rw = reinterpret_cast<float4*>(d.emb);
   float4* rv = reinterpret_cast<float4*>(d.s2);
   float4* rm = reinterpret_cast<float4*>(d.s1);
-  // two passes over the group's ids when a.heavy_first > 0: ids with more
-  // than heavy_first occurrences first (their long ordered sums start at once
-  // instead of in a late wave), then the rest
-  const uint32_t npass = a.heavy_first ? 2u : 1u;
-  for (uint32_t it = 0; it < npass * ((nu + ngroups - 1) / ngroups); ++it) {
-    const uint32_t pass = a.heavy_first ? it / ((nu + ngroups - 1) / ngroups) : 1u;
-    const uint32_t uu = gid + (it - (pass == 1 && a.heavy_first ? (nu + ngroups - 1) / ngroups : 0u)) * ngroups;
-    if (uu >= nu) continue;
-    // slot and row in one round trip (KA's claiming tile wrote both), then the
-    // count, the positions (speculatively, all 64) and the row's state together
-    const uint32_t gs = __ldg(a.use.u_slot + uu);
-    const uint32_t row = __ldg(a.urow + uu);
+  for (uint32_t it = gid; it < nitems; it += ngroups) {
+    // slot and row in one round trip (KA's claiming tile wrote both; list
+    // mode: the slot's record), then the count, the positions (speculatively)
+    // and the row's state together
+    uint32_t gs, row, uu, c;
+    if (a.list) {
+      gs = __ldg(a.list + it);
+      const uint2 cr = __ldcg(reinterpret_cast<const uint2*>(&a.use.rec[gs].cnt));
+      c = cr.x;
+      row = cr.y;
+      uu = __ldcg(a.sh.uidx + gs);
+    } else {
+      uu = it;
+      gs = __ldg(a.use.u_slot + uu);
+      row = __ldg(a.urow + uu);
+      c = 0;
+    }
     if (row == kNoRow) continue;  // table error (reported through the counters)
     if (!RS_IDX_OK(gs < a.sh.n_slots && row < d.row_cap, a.sh.ctr)) continue;
-    const uint32_t c = __ldcg(&a.use.rec[gs].cnt);
+    if (!a.list) c = __ldcg(&a.use.rec[gs].cnt);
     uint32_t p[PPT], r[PPT];
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      p[j] = __ldcg(a.sh.pos + (size_t)gs * kPosMax + gl + j * G);
+      p[j] = gl + j * G < PMAX ? __ldcg(a.sh.pos + (size_t)gs * kPosMax + gl + j * G) : kFull;
       r[j] = 0;
     }
     float4 wv[NV], vv[NV], mv[NV];
@@ -445,8 +468,7 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
     }
     uint32_t st0 = 0;
     if (gl == 0) st0 = d.step[row];
-    if (c > a.sh.hot_min) continue;  // hot path (group-uniform)
-    if (a.heavy_first && ((pass == 0) != (c > a.heavy_first))) continue;
+    if (c > a.c_max || c <= a.c_min) continue;  // another kernel's id (group-uniform)
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
       if (gl + j * G >= c) p[j] = kFull;
@@ -587,6 +609,7 @@ struct FhArgs {
   float* out;
   int32_t* inverse;
   double* tokcs;
+  uint32_t exp;  // timing experiments (RS_FH_EXP bits, wrong results): 1 no forward stores, 2 no gradient sums
 };
 
 
@@ -594,11 +617,14 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+constexpr uint32_t kRowStage = 8;  // group rows per warp staged in smem (more: read from global)
+
 template <int VEC, int CH>
 __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
   WarpTrace wt_(a.sh.trace, 2);
   constexpr uint32_t L = 2 * kTT, NW = kTT / 32;
   const uint32_t D = a.dim;
+  extern __shared__ __align__(16) float srow[];  // [kRowStage * NW x D] the first groups' rows
   __shared__ uint32_t lkey[L], lfirst[L], lgroup[L];
   __shared__ uint32_t gcnt[kTT], goff[kTT], gslot[kTT], grow[kTT], gpidx[kTT];
   __shared__ uint16_t wcnt[NW * kTT];
@@ -641,7 +667,6 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
   __syncthreads();
   const uint32_t nhot = s_nhot;
   if (nhot == 0) return;  // no hot token in this tile (block-uniform)
-  trace_mark(a.sh.trace, 5);
   uint32_t ps = 0;
   if (hot) {
     ps = hash32(gs) & (L - 1);
@@ -750,43 +775,86 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
   }
   __syncthreads();
   if (hot) csr[goff[mylg] + wcnt[warp * kTT + mylg] + rw] = (uint16_t)tid;
-  trace_mark(a.sh.trace, 6);
-  trace_mark(a.sh.trace, 7);
-  // one warp per group: the id's row and its gradient rows issued together;
-  // the row to each of the group's tokens (the forward), the gradient rows
-  // summed in token order
-  constexpr int PF = (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
-  for (uint32_t gq = warp; gq < ng; gq += NW) {
-    const uint32_t c = gcnt[gq], base = goff[gq], grw = grow[gq];
-    float w[CH][VEC], acc[CH][VEC];
-    if (grw != kNoRow) load_vec<VEC, CH>(a.emb + (size_t)grw * D, D, w, false);
-    zero_acc<VEC, CH>(acc);
-    for (uint32_t k0 = 0; k0 < c; k0 += PF) {
-      float x[PF][CH][VEC];
+  // Warp w takes a contiguous range of groups holding ~1/NW of the tile's hot
+  // tokens and streams them as one list: PF gradient rows in flight across
+  // group boundaries (no per-group round trip), the sums in token order per
+  // group, each group's partial stored after its last token; the groups'
+  // table rows are fetched up front into smem (one round trip for all) and
+  // stored to each token (the forward).
+  const uint32_t nhot_t = ng ? goff[ng - 1] + gcnt[ng - 1] : 0u;
+  auto first_group = [&](uint32_t wq) -> uint32_t {  // groups starting before token wq * nhot / NW
+    const uint64_t lim = (uint64_t)wq * nhot_t;
+    uint32_t cnt = 0;
+    for (uint32_t g = lane; g < ng; g += 32) cnt += (uint64_t)goff[g] * NW < lim;
 #pragma unroll
-      for (int q = 0; q < PF; ++q) {
-        if (k0 + q < c) load_vec<VEC, CH>(a.grads + (size_t)(t0 + csr[base + k0 + q]) * D, D, x[q], false);
-      }
+    for (int o2 = 16; o2 > 0; o2 >>= 1) cnt += __shfl_xor_sync(kFull, cnt, o2);
+    return cnt;
+  };
+  const uint32_t gb = warp == 0 ? 0u : first_group(warp);
+  const uint32_t ge = warp == NW - 1 ? ng : first_group(warp + 1);
+  if (!(a.exp & 4)) {  // the tile's first kRowStage * NW group rows -> smem, warp w fetching
+     // groups w, w + NW, ...: every load issued before the first store
+    float wr[kRowStage][CH][VEC];
 #pragma unroll
-      for (int q = 0; q < PF; ++q)
-        if (k0 + q < c) add_acc<VEC, CH>(acc, x[q]);
+    for (uint32_t k = 0; k < kRowStage; ++k) {
+      const uint32_t gg = warp + k * NW;
+      if (gg < ng && grow[gg] != kNoRow) load_vec<VEC, CH>(a.emb + (size_t)grow[gg] * D, D, wr[k], false);
     }
-    if (grw != kNoRow) {
-      for (uint32_t k = 0; k < c; ++k) store_vec<VEC, CH>(a.out + (size_t)(t0 + csr[base + k]) * D, D, w);
-      if (a.tokcs) {
-        double rs = 0.0;
 #pragma unroll
-        for (int c2 = 0; c2 < CH; ++c2)
-#pragma unroll
-          for (int j = 0; j < VEC; ++j) rs += (double)w[c2][j];
-#pragma unroll
-        for (int o2 = 16; o2 > 0; o2 >>= 1) rs += __shfl_xor_sync(kFull, rs, o2);
-        for (uint32_t k = lane; k < c; k += 32) a.tokcs[t0 + csr[base + k]] = rs;
-      }
+    for (uint32_t k = 0; k < kRowStage; ++k) {
+      const uint32_t gg = warp + k * NW;
+      if (gg < ng && grow[gg] != kNoRow) store_vec<VEC, CH>(srow + (size_t)gg * D, D, wr[k]);
     }
-    const uint32_t pidx = gpidx[gq];
-    if (pidx != kFull) store_vec<VEC, CH>(a.sh.part + (size_t)pidx * D, D, acc);
   }
+  __syncthreads();
+  constexpr int PF = (CH * VEC <= 4) ? 8 : (CH * VEC <= 8) ? 4 : 2;
+  const uint32_t tb = gb < ng ? goff[gb] : nhot_t, te = ge < ng ? goff[ge] : nhot_t;
+  uint32_t g = gb, gend = gb < ge ? goff[gb] + gcnt[gb] : 0u;
+  float w[CH][VEC], acc[CH][VEC];
+  zero_acc<VEC, CH>(acc);
+  auto row_of = [&](uint32_t gg, float (&r)[CH][VEC]) {
+    if (grow[gg] == kNoRow) return;
+    if (gg < kRowStage * NW)
+      load_vec<VEC, CH>(srow + (size_t)gg * D, D, r, false);
+    else
+      load_vec<VEC, CH>(a.emb + (size_t)grow[gg] * D, D, r, false);
+  };
+  auto finish_group = [&](uint32_t gg) {
+    const uint32_t pidx = gpidx[gg];
+    if (pidx != kFull) store_vec<VEC, CH>(a.sh.part + (size_t)pidx * D, D, acc);
+    if (a.tokcs && grow[gg] != kNoRow) {
+      double rs = 0.0;
+#pragma unroll
+      for (int c2 = 0; c2 < CH; ++c2)
+#pragma unroll
+        for (int j = 0; j < VEC; ++j) rs += (double)w[c2][j];
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) rs += __shfl_xor_sync(kFull, rs, o2);
+      for (uint32_t k = lane; k < gcnt[gg]; k += 32) a.tokcs[t0 + csr[goff[gg] + k]] = rs;
+    }
+  };
+  if (gb < ge) row_of(gb, w);
+  for (uint32_t i0 = tb; i0 < ((a.exp & 8) ? tb : te); i0 += PF) {
+    float x[PF][CH][VEC];
+#pragma unroll
+    for (int q = 0; q < PF; ++q)
+      if (i0 + q < te && !(a.exp & 2)) load_vec<VEC, CH>(a.grads + (size_t)(t0 + csr[i0 + q]) * D, D, x[q], false);
+#pragma unroll
+    for (int q = 0; q < PF; ++q) {
+      const uint32_t i = i0 + q;
+      if (i >= te) break;
+      while (i >= gend) {  // the previous group is complete
+        finish_group(g);
+        zero_acc<VEC, CH>(acc);
+        ++g;
+        gend = goff[g] + gcnt[g];
+        row_of(g, w);
+      }
+      if (!(a.exp & 2)) add_acc<VEC, CH>(acc, x[q]);
+      if (grow[g] != kNoRow && !(a.exp & 1)) store_vec<VEC, CH>(a.out + (size_t)(t0 + csr[i]) * D, D, w);
+    }
+  }
+  if (gb < ge && !(a.exp & 8)) finish_group(g);
 }
 
 // ---------------------------------------------------------------------------
@@ -922,6 +990,8 @@ static int fast_alloc(rs_workspace* ws) {
   f.hot_min = kPosMax;
   if (const char* e = getenv("RS_HOT_MIN")) f.hot_min = std::min<uint32_t>(kPosMax, std::max(1, atoi(e)));
   f.max_hot = N / (f.hot_min + 1) + 1;
+  f.light_max = std::min<uint32_t>(f.hot_min, 8);  // <= the light kernel's 8 positions
+  if (const char* e = getenv("RS_LIGHT_MAX")) f.light_max = std::min<uint32_t>(f.light_max, std::max(1, atoi(e)));
   auto A = [&](auto** p, size_t bytes) {
     return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 16)) == cudaSuccess;
   };
@@ -929,7 +999,7 @@ static int fast_alloc(rs_workspace* ws) {
   for (auto& x : f.set) ok = ok && A(&x.rec, (S + 1) * sizeof(Rec)) && A(&x.u_slot, N * 4) && A(&x.cnt, 16);
   ok = ok && A(&f.uidx, (S + 1) * 4) && A(&f.hidx, (S + 1) * 4) && A(&f.pos, (S + 1) * kPosMax * 4) &&
        A(&f.hot_slot, f.max_hot * 4) && A(&f.hlist, f.max_hot * f.ntiles * 4) && A(&f.ctr, 64) &&
-       A(&f.tokcs, N * 8);
+       A(&f.tokcs, N * 8) && A(&f.heavy, N * 4);
   if (!ok) return cuda_fail(cudaGetLastError(), "fast step: cudaMalloc");
   // empty records (key ~0, count 0, row ~0): all-ones then zero counts
   for (auto& x : f.set) {
@@ -947,12 +1017,16 @@ static int fast_alloc(rs_workspace* ws) {
   {  // the hot branch (KH -> KF) at the highest priority: KF's blocks go ahead of the CSR kernel's pending ones
     int lo = 0, hi = 0;
     RS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    static const bool prio = !(getenv("RS_FAST_PRIO") && getenv("RS_FAST_PRIO")[0] == '0');
-    RS_CUDA(cudaStreamCreateWithPriority(&f.aux2, cudaStreamNonBlocking, prio ? hi : 0));
+    // RS_FAST_PRIO = "<hot branch><heavy CSR>", each 'h' (high) or 'n' (default)
+    const char* pe = getenv("RS_FAST_PRIO");
+    const bool p_hot = !pe || pe[0] != 'n', p_heavy = !pe || !pe[0] || pe[1] != 'n';
+    RS_CUDA(cudaStreamCreateWithPriority(&f.aux2, cudaStreamNonBlocking, p_hot ? hi : 0));
+    RS_CUDA(cudaStreamCreateWithPriority(&f.aux3, cudaStreamNonBlocking, p_heavy ? hi : 0));
   }
   RS_CUDA(cudaEventCreateWithFlags(&f.ev_fork, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&f.ev_j1, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&f.ev_j2, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&f.ev_j3, cudaEventDisableTiming));
   RS_CUDA(cudaDeviceSynchronize());
   f.ready = true;
   return RS_OK;
@@ -965,11 +1039,12 @@ void fast_free(rs_workspace* ws) {
     for (void* p : ps)
       if (p) cudaFree(p);
   }
-  void* ps[] = {f.uidx, f.hidx, f.pos, f.hot_slot, f.hlist, f.ctr, f.tokcs, f.trace};
+  void* ps[] = {f.uidx, f.hidx, f.pos, f.hot_slot, f.hlist, f.ctr, f.tokcs, f.trace, f.heavy};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (f.aux2) cudaStreamDestroy(f.aux2);
-  cudaEvent_t es[] = {f.ev_fork, f.ev_j1, f.ev_j2};
+  if (f.aux3) cudaStreamDestroy(f.aux3);
+  cudaEvent_t es[] = {f.ev_fork, f.ev_j1, f.ev_j2, f.ev_j3};
   for (auto e : es)
     if (e) cudaEventDestroy(e);
   f = rs_fast{};
@@ -1015,6 +1090,8 @@ static FShared fshared(rs_workspace* ws) {
   s.ntiles = (uint32_t)f.ntiles;
   s.hot_min = f.hot_min;
   s.trace = f.trace;
+  s.heavy = f.heavy;
+  s.light_max = f.light_max;
   s.n_slots = ws->S + 1;
   s.max_tokens = (uint32_t)ws->max_tokens;
   s.max_hot = (uint32_t)f.max_hot;
@@ -1034,6 +1111,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   FaArgs fa;
   fa.ids = d_ids;
   fa.n = (uint32_t)n;
+  fa.set = (uint32_t)use;
   fa.use = fset(ws, use);
   fa.clean = fset(ws, use ^ 1);
   fa.sh = sh;
@@ -1046,13 +1124,15 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   RS_LAUNCH_CHECK("k_fa");
   if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
   rs_fast& f = ws->fast;
-  cudaStream_t sd = s, sh2 = s;
+  cudaStream_t sd = s, sh2 = s, sd3 = s;
   if (fork && !ev) {
     RS_CUDA(cudaEventRecord(f.ev_fork, s));
     RS_CUDA(cudaStreamWaitEvent(ws->aux_stream, f.ev_fork, 0));
     RS_CUDA(cudaStreamWaitEvent(f.aux2, f.ev_fork, 0));
+    RS_CUDA(cudaStreamWaitEvent(f.aux3, f.ev_fork, 0));
     sd = ws->aux_stream;
     sh2 = f.aux2;
+    sd3 = f.aux3;
   }
   const Shape shp = shape_of(D);
   // hot branch first (longest chain): KH -> KF
@@ -1068,6 +1148,8 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     h.out = d_out;
     h.inverse = ws->inverse;
     h.tokcs = ws->csum_dst ? f.tokcs : nullptr;
+    static const uint32_t hexp = getenv("RS_FH_EXP") ? (uint32_t)atoi(getenv("RS_FH_EXP")) : 0u;
+    h.exp = hexp;
     FfArgs ff;
     ff.td = t->dev;
     ff.use = fa.use;
@@ -1086,7 +1168,10 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   }
 #define RS_FH(V, C)                                                                        \
   if (shp.vec == V && shp.ch == C) {                                                       \
-    k_fh<V, C><<<ntiles, kTT, 0, q>>>(h);                                                  \
+    if ((kTT / 32) * kRowStage * D * 4 > 48 * 1024)                                         \
+      RS_CUDA(cudaFuncSetAttribute(k_fh<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                   (int)((kTT / 32) * kRowStage * D * 4)));                  \
+    k_fh<V, C><<<ntiles, kTT, (kTT / 32) * kRowStage * D * 4, q>>>(h);                      \
     RS_LAUNCH_CHECK("k_fh");                                                               \
     RS_KF(V, C, 4) RS_KF(V, C, 8) RS_KF(V, C, 16)                                          \
     RS_LAUNCH_CHECK("k_fhf");                                                              \
@@ -1097,7 +1182,10 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
 #undef RS_KF
     return fail(RS_ERR_INVARIANT, "fast step: no hot kernel for this dim");
   };
-  auto csr = [&](cudaStream_t q) -> int {
+  // CSR ids: the light kernel over every unique id (c <= light_max: short
+  // ordered sums, 8 lanes per id) and the heavy kernel over KA's list
+  // (light_max < c <= hot_min: 16 lanes, 64 positions), on two streams
+  auto csr = [&](cudaStream_t ql, cudaStream_t qh) -> int {
     FcArgs c;
     c.td = t->dev;
     c.use = fa.use;
@@ -1107,24 +1195,41 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     c.urow = ws->urow;
     static const uint32_t fexp = getenv("RS_FC_EXP") ? (uint32_t)atoi(getenv("RS_FC_EXP")) : 0u;
     c.exp = fexp;
-    static const uint32_t heavy = getenv("RS_FC_HEAVY") ? (uint32_t)atoi(getenv("RS_FC_HEAVY")) : 0u;
-    c.heavy_first = heavy;
     c.out = d_out;
     c.inverse = ws->inverse;
     c.tokcs = ws->csum_dst ? f.tokcs : nullptr;
     const uint32_t D4 = D / 4;
-    const uint32_t G = D4 >= 32 ? 32 : D4;
-    const uint32_t gpb = 256 / G;
     static const unsigned cap_blocks = getenv("RS_FC_GRID") ? (unsigned)atoi(getenv("RS_FC_GRID")) : 148u * 16u;
-    const unsigned grid = grid_for(n, gpb, cap_blocks);
-    static const int g8 = getenv("RS_FC_G8") ? atoi(getenv("RS_FC_G8")) : 0;  // experiment: 8 lanes x 2 chunks
-    if (D4 == 4) k_fc<4, 1><<<grid, 256, 0, q>>>(c, o);
-    else if (D4 == 8) k_fc<8, 1><<<grid, 256, 0, q>>>(c, o);
-    else if (D4 == 16 && g8) k_fc<8, 2><<<grid_for(n, 32, cap_blocks), 256, 0, q>>>(c, o);
-    else if (D4 == 16) k_fc<16, 1><<<grid, 256, 0, q>>>(c, o);
-    else if (D4 == 32) k_fc<32, 1><<<grid, 256, 0, q>>>(c, o);
-    else k_fc<32, 2><<<grid, 256, 0, q>>>(c, o);
-    RS_LAUNCH_CHECK("k_fc");
+    // heavy (first: its ids start at once on their stream)
+    FcArgs ch = c;
+    ch.list = f.heavy;
+    ch.list_n = sh.ctr + 5 + use;
+    ch.c_min = f.light_max;
+    ch.c_max = f.hot_min;
+    const uint64_t max_heavy = n / (f.light_max + 1) + 1;
+#define RS_FC(GG, NVV, PM, args, q, items)                                                  \
+  k_fc<GG, NVV, PM><<<grid_for(items, 256 / GG, cap_blocks), 256, 0, q>>>(args, o);
+    // a grid-stride grid: the heavy ids are ~1-2% of the unique ids
+    static const uint64_t hcap = getenv("RS_FCH_ITEMS") ? (uint64_t)atoll(getenv("RS_FCH_ITEMS")) : 148ull * 16;
+    const uint64_t hitems = std::min<uint64_t>(max_heavy, hcap);
+    if (D4 == 4) { RS_FC(4, 1, 64, ch, qh, hitems) }
+    else if (D4 == 8) { RS_FC(8, 1, 64, ch, qh, hitems) }
+    else if (D4 == 16) { RS_FC(16, 1, 64, ch, qh, hitems) }
+    else if (D4 == 32) { RS_FC(16, 2, 64, ch, qh, hitems) }
+    else { RS_FC(16, 4, 64, ch, qh, hitems) }
+    RS_LAUNCH_CHECK("k_fc(heavy)");
+    FcArgs cl = c;
+    cl.list = nullptr;
+    cl.list_n = nullptr;
+    cl.c_min = 0;
+    cl.c_max = f.light_max;
+    if (D4 == 4) { RS_FC(4, 1, 8, cl, ql, n) }
+    else if (D4 == 8) { RS_FC(8, 1, 8, cl, ql, n) }
+    else if (D4 == 16) { RS_FC(8, 2, 8, cl, ql, n) }
+    else if (D4 == 32) { RS_FC(8, 4, 8, cl, ql, n) }
+    else { RS_FC(16, 4, 8, cl, ql, n) }
+#undef RS_FC
+    RS_LAUNCH_CHECK("k_fc(light)");
     return RS_OK;
   };
   auto checksum = [&](cudaStream_t q) -> int {
@@ -1138,7 +1243,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
                                                             t->dev, mirror_out);
     RS_LAUNCH_CHECK("k_fclean");
-    if ((st = csr(s))) return st;
+    if ((st = csr(s, s))) return st;
     RS_CUDA(cudaEventRecord(ev[2], s));
     if ((st = hot(s))) return st;
     RS_CUDA(cudaEventRecord(ev[3], s));
@@ -1149,7 +1254,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   // RS_FAST_SKIP (timing experiments only, wrong results): 1 = no hot branch, 2 = no CSR branch
   static const int skip = getenv("RS_FAST_SKIP") ? atoi(getenv("RS_FAST_SKIP")) : 0;
   if (skip != 1 && (st = hot(sh2))) return st;
-  if (skip != 2 && (st = csr(sd))) return st;
+  if (skip != 2 && (st = csr(sd, sd3))) return st;
   k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
                                                             t->dev, mirror_out);
   RS_LAUNCH_CHECK("k_fclean");
@@ -1158,6 +1263,8 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     RS_CUDA(cudaStreamWaitEvent(s, f.ev_j1, 0));
     RS_CUDA(cudaEventRecord(f.ev_j2, sh2));
     RS_CUDA(cudaStreamWaitEvent(s, f.ev_j2, 0));
+    RS_CUDA(cudaEventRecord(f.ev_j3, sd3));
+    RS_CUDA(cudaStreamWaitEvent(s, f.ev_j3, 0));
   }
   return checksum(s);
 }

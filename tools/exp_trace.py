@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 import paper_2505_12663_b200 as P  # noqa: E402
 from paper_2505_12663_b200 import workload as W  # noqa: E402
 
-NAMES = ["dedup_probe", "csr_finish", "hot_tiles", "hot_finish", "clean", "kh_loaded", "kh_grouped", "kh_staged"]
+NAMES = ["dedup_probe", "csr_light", "hot_tiles", "hot_finish", "clean", "csr_heavy"]
 
 
 def main():
