@@ -207,6 +207,14 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
     launches = lib.rs_kernel_launches() - launches0
     syncs = table.info().host_syncs - syncs0
+    # host time to issue the step alone (no flush launch, no event records): the
+    # timed loop's host time also covers the 512 MiB flush kernel and 2 events
+    torch.cuda.synchronize()
+    h1 = time.perf_counter()
+    for k in range(args.steps):
+        one(args.warmup + k)
+    host_step_ms = (time.perf_counter() - h1) * 1e3 / args.steps
+    torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in evs]
     uniq = sum(uniq_per_batch[(args.warmup + k) % nb] for k in range(args.steps))
     toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
@@ -224,6 +232,9 @@ def run_ours(args, cfg):
 
     # ---- per-kernel shares (separate pass with phase events, same inputs)
     phases = phase_times(step, dev, nb, args, flush, P)
+    # ---- in-graph kernel spans (device %globaltimer per block, a separate
+    # workspace with the timeline on)
+    in_graph = graph_timeline(table, dev, nb, flush, P, max_t)
 
     # ---- end to end through the public API with HOST buffers
     e2e = e2e_pass(args, cfg, batches, step, P, W, rank)
@@ -233,13 +244,23 @@ def run_ours(args, cfg):
     hbm, how = peaks()
     D = dim
     T_avg, U_avg = toks / args.steps, uniq / args.steps
+    # tokens / ids of the CSR path (<= 64 occurrences) and of the hot path
+    T_hot = U_hot = 0.0
+    for k in range(args.steps):
+        _, cnt = np.unique(batches[(args.warmup + k) % nb][1], return_counts=True)
+        T_hot += float(cnt[cnt > 64].sum()) / args.steps
+        U_hot += float((cnt > 64).sum()) / args.steps
+    T_csr, U_csr = T_avg - T_hot, U_avg - U_hot
+    # SURVEY §8(d) per-phase compulsory bytes: ids 8T + dedup out 8U + 4T +
+    # slot probe 16U; per id: gather read 4D + Adagrad state r/w 16D; per
+    # token: forward write 4D + gradient read 4D
     algo = {
-        "dedup": 12 * T_avg + 8 * U_avg,
-        "table": 16 * U_avg,
-        "gather_reduce": 8 * D * T_avg + 4 * D * U_avg,
-        "finish_update": 16 * D * U_avg + 8 * U_avg,
+        "dedup_probe": 12 * T_avg + 24 * U_avg,
+        "csr_update": 8 * D * T_csr + 20 * D * U_csr,
+        "hot_update": 8 * D * T_hot + 20 * D * U_hot,
+        "checksum": 0.0,
     }
-    dom = max(phases, key=lambda k: phases[k])
+    dom = max(algo, key=lambda k: phases.get(k) or 0.0)
     traffic = traffic_ctx = None
     try:  # dram bytes of the same kernel from the committed ncu --set full capture
         import glob
@@ -272,10 +293,16 @@ def run_ours(args, cfg):
         "table_host_syncs_in_timed_region": int(syncs),
         "tokens_per_s": toks_job / t_job,
         "host_enqueue_ms_per_step": host_ms,
+        "host_issue_ms_per_step": host_step_ms,
+        "host_note": "host_enqueue = host time per timed iteration (flush launch + 2 event records + the step); "
+                     "host_issue = the step's own host time (graph launch, capacity bookkeeping, no sync); "
+                     "the device timing brackets only the step",
         "step_hbm_gbs": step_bytes * world / (t_job / args.steps) / 1e9,
         "step_roofline_frac": step_bytes / (t_job / args.steps) / 1e9 / hbm,
         "kernel_ms": phases,
-        "kernel_gbs": {k: (algo[k] / (phases[k] / 1e3) / 1e9 if phases[k] else None) for k in algo},
+        "kernel_ms_note": "eager, one kernel group after another (no graph, no concurrency), L2 flushed",
+        "kernel_gbs": {k: (algo[k] / (phases[k] / 1e3) / 1e9 if phases.get(k) else None) for k in algo},
+        "kernel_span_in_graph_us": in_graph,
         "roofline": {"bound": "hbm", "kernel": dom,
                      "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": (ach / hbm) if ach else None,
                      "traffic": traffic, "traffic_in_context": traffic_ctx, "peak_source": how,
@@ -686,7 +713,53 @@ def _n_unique(step):
     return n.value
 
 
-PHASES = ["dedup", "table", "gather_reduce", "finish_update"]
+# the fast step's eager phases (rs_workspace_phase_ms): dedup + probe (KA);
+# the CSR ids' forward + ordered reduce + Adagrad (scratch clean, heavy and
+# light kernels); the hot ids' tile partials + finish; the checksum (0 here)
+PHASES = ["dedup_probe", "csr_update", "hot_update", "checksum"]
+TRACE_NAMES = ["dedup_probe", "csr_light", "hot_tiles", "hot_finish", "scratch_clean", "csr_heavy"]
+
+
+def graph_timeline(table, dev, nb, flush, P, max_t):
+    """Kernel spans inside the step's CUDA graph: a second workspace with the
+    device timeline (RS_TRACE=1 at its first step: per block the first warp
+    start / last warp end, %globaltimer), L2 flushed before each step; per
+    kernel the median over 6 steps of start / end relative to the first
+    kernel's first block (us)."""
+    import ctypes
+    os.environ["RS_TRACE"] = "1"
+    try:
+        st = P.SparseStep(table, max_t, P.AdagradParams(lr=0.01, eps=1e-8))
+        for k in range(2 * nb):
+            st.step(*dev[k % nb])
+    finally:
+        del os.environ["RS_TRACE"]
+    lib = P.lib()
+    n = ctypes.c_uint64()
+    buf = np.zeros(8 * 4096 * 2, np.uint64)
+    rows = {name: [] for name in TRACE_NAMES}
+    for k in range(6):
+        flush.zero_()
+        import torch
+        torch.cuda.synchronize()
+        P._lib.check(lib.rs_workspace_trace(st.ws.handle, buf.ctypes.data, buf.size, ctypes.byref(n)), "trace")
+        st.step(*dev[k % nb])
+        torch.cuda.synchronize()
+        P._lib.check(lib.rs_workspace_trace(st.ws.handle, buf.ctypes.data, buf.size, ctypes.byref(n)), "trace")
+        if not n.value:
+            return None
+        t = buf.reshape(8, 4096, 2).astype(np.float64)
+        t0 = t[0, :, 0][t[0, :, 1] > 0].min()
+        for i, name in enumerate(TRACE_NAMES):
+            ok = t[i, :, 1] > 0
+            if ok.any():
+                rows[name].append(((t[i, ok, 0].min() - t0) / 1e3, (t[i, ok, 1].max() - t0) / 1e3))
+    out = {}
+    for name, v in rows.items():
+        if v:
+            a = np.array(v)
+            out[name] = {"start_us": round(float(np.median(a[:, 0])), 2), "end_us": round(float(np.median(a[:, 1])), 2)}
+    return out
 
 
 def phase_times(step, dev, nb, args, flush, P):

@@ -411,8 +411,11 @@ struct FcArgs {
 #ifndef RS_FC_MINB
 #define RS_FC_MINB 5
 #endif
-template <int G, int NV, int PMAX>
-__global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, OptArgs o) {
+// MINB: resident blocks per SM the register budget is sized for -- the light
+// kernel needs occupancy, the heavy one (few ids, long ordered sums) needs
+// registers so that its B2 gradient rows are really in flight together
+template <int G, int NV, int PMAX, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fc(FcArgs a, OptArgs o) {
   WarpTrace wt_(a.sh.trace, a.list ? 5 : 1);
   constexpr int PPT = (PMAX + G - 1) / G;  // positions held per thread
   __shared__ uint32_t order_s[(256 / G) * PMAX];
@@ -509,8 +512,11 @@ __global__ void __launch_bounds__(256, NV == 1 ? RS_FC_MINB : 4) k_fc(FcArgs a, 
     float4 acc[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // rows in flight: B2 per step of the long loop, B for the tail; a
+    // register-tight build (MINB >= 4 with 64 positions) keeps B2 = B so the
+    // loads are not serialized by spills
     constexpr int B = NV == 1 ? 4 : 2;
-    constexpr int B2 = 2 * B;
+    constexpr int B2 = (MINB >= 4 && PMAX > 8) ? B : 2 * B;
     uint32_t k = (a.exp & 2) ? c : 0;
     for (; k + B2 <= c; k += B2) {
       float4 x[B2][NV];
@@ -1207,27 +1213,31 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     ch.c_min = f.light_max;
     ch.c_max = f.hot_min;
     const uint64_t max_heavy = n / (f.light_max + 1) + 1;
-#define RS_FC(GG, NVV, PM, args, q, items)                                                  \
-  k_fc<GG, NVV, PM><<<grid_for(items, 256 / GG, cap_blocks), 256, 0, q>>>(args, o);
+#define RS_FC(GG, NVV, PM, MB, args, q, items)                                              \
+  k_fc<GG, NVV, PM, MB><<<grid_for(items, 256 / GG, cap_blocks), 256, 0, q>>>(args, o);
     // a grid-stride grid: the heavy ids are ~1-2% of the unique ids
     static const uint64_t hcap = getenv("RS_FCH_ITEMS") ? (uint64_t)atoll(getenv("RS_FCH_ITEMS")) : 148ull * 16;
     const uint64_t hitems = std::min<uint64_t>(max_heavy, hcap);
-    if (D4 == 4) { RS_FC(4, 1, 64, ch, qh, hitems) }
-    else if (D4 == 8) { RS_FC(8, 1, 64, ch, qh, hitems) }
-    else if (D4 == 16) { RS_FC(16, 1, 64, ch, qh, hitems) }
-    else if (D4 == 32) { RS_FC(16, 2, 64, ch, qh, hitems) }
-    else { RS_FC(16, 4, 64, ch, qh, hitems) }
+    static const int hminb = getenv("RS_FC_HMINB") ? atoi(getenv("RS_FC_HMINB")) : 5;  // experiment knob
+    if (D4 == 4) { RS_FC(4, 1, 64, 5, ch, qh, hitems) }
+    else if (D4 == 8) { RS_FC(8, 1, 64, 5, ch, qh, hitems) }
+    else if (D4 == 16 && hminb == 2) { RS_FC(16, 1, 64, 2, ch, qh, hitems) }
+    else if (D4 == 16) { RS_FC(16, 1, 64, 5, ch, qh, hitems) }
+    else if (D4 == 32) { RS_FC(16, 2, 64, 4, ch, qh, hitems) }
+    else { RS_FC(16, 4, 64, 3, ch, qh, hitems) }
     RS_LAUNCH_CHECK("k_fc(heavy)");
+    static const int lminb = getenv("RS_FC_LMINB") ? atoi(getenv("RS_FC_LMINB")) : 4;  // experiment knob
     FcArgs cl = c;
     cl.list = nullptr;
     cl.list_n = nullptr;
     cl.c_min = 0;
     cl.c_max = f.light_max;
-    if (D4 == 4) { RS_FC(4, 1, 8, cl, ql, n) }
-    else if (D4 == 8) { RS_FC(8, 1, 8, cl, ql, n) }
-    else if (D4 == 16) { RS_FC(8, 2, 8, cl, ql, n) }
-    else if (D4 == 32) { RS_FC(8, 4, 8, cl, ql, n) }
-    else { RS_FC(16, 4, 8, cl, ql, n) }
+    if (D4 == 4) { RS_FC(4, 1, 8, 5, cl, ql, n) }
+    else if (D4 == 8) { RS_FC(8, 1, 8, 5, cl, ql, n) }
+    else if (D4 == 16 && lminb == 3) { RS_FC(8, 2, 8, 3, cl, ql, n) }
+    else if (D4 == 16) { RS_FC(8, 2, 8, 4, cl, ql, n) }
+    else if (D4 == 32) { RS_FC(8, 4, 8, 3, cl, ql, n) }
+    else { RS_FC(16, 4, 8, 3, cl, ql, n) }
 #undef RS_FC
     RS_LAUNCH_CHECK("k_fc(light)");
     return RS_OK;
