@@ -202,6 +202,7 @@ struct OwnTableArgs {
   uint32_t* u_poff;
   uint32_t* u_ntile;
   uint32_t* u_ticket;
+  TableCounters* mirror_out;  // host's pinned counter mirror (mapped), or null
 };
 
 __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
     if (s_ins) atomicAdd(&td->c.inserted, s_ins);
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
-  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  launch_epilogue(td, free_n0, fresh0, true, tick_now, a.mirror_out);
   if (blockIdx.x == 0) {  // every source's flag was observed by k_own_dedup
     const ArenaHdr* h = hdr_of(c, c.rank);
     uint64_t tot = 0;
@@ -474,7 +475,8 @@ static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
 // owner: stage-2 dedup straight from the receive lists (KA'), then per
 // owner-unique id find-or-insert on the shard (capacity prepared by the
 // caller) and the row stored into every requester that asked for it (KB')
-static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s) {
+static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
+                        TableCounters* mirror_out = nullptr) {
   rs_workspace* wo = c->ws_own;
   const CommDev cd = comm_dev(c, ss.par, kOwner);
   const uint64_t nflat = (uint64_t)c->world * c->cap;
@@ -500,6 +502,7 @@ static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s) {
   a.u_poff = wo->u_poff;
   a.u_ntile = wo->u_ntile;
   a.u_ticket = wo->u_ticket;
+  a.mirror_out = mirror_out;
   k_own_table<<<grid_for(nflat, 32, 148 * 8), 256, 0, s>>>(cd, a);
   RS_LAUNCH_CHECK("k_own_table");
   RS_TRY(prof_end(c, kPhRespond, s));
@@ -944,8 +947,11 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     RS_CUDA(cudaEventRecord(c->ev_meta, q));
     RS_CUDA(cudaStreamWaitEvent(c->gather_stream, c->ev_meta, 0));
     RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
-    RS_TRY(owner_lookup(c, t, ss, own));
-    RS_TRY(table_mirror_copy(t, mirror, own));
+    // the counters reach the pinned mirror from k_own_table's epilogue (mapped
+    // store) instead of a copy node on the owner's critical path
+    TableCounters* mo = t->mirror[mirror].dev_ptr;
+    RS_TRY(owner_lookup(c, t, ss, own, mo));
+    if (!mo) RS_TRY(table_mirror_copy(t, mirror, own));
     RS_TRY(owner_update(c, t, ob, ss, own));
     RS_TRY(req_gather(c, t, n, d_out, ss, c->gather_stream));
     RS_CUDA(cudaEventRecord(c->ev_gjoin, c->gather_stream));

@@ -214,9 +214,11 @@ __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const Tab
 // bump_tick: 0 keep the tick, 1 advance it, 2 advance it iff this launch
 // removed a key (remove of absent keys leaves the table identical,
 // embed_table.cpp:250-260)
+// mirror_out (optional): the folded counters are also stored into the host's
+// pinned mirror (mapped memory), so no copy node follows the kernel.
 __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
                                                 unsigned long long fresh0, int bump_tick,
-                                                uint32_t tick_now) {
+                                                uint32_t tick_now, TableCounters* mirror_out = nullptr) {
   __syncthreads();
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
@@ -252,6 +254,10 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     if (bump_tick == 1 || (bump_tick == 2 && any_removed)) c.tick = tick_now;
     c.blocks_done = 0;
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (mirror_out) {
+      *mirror_out = c;
+      __threadfence_system();
+    }
   }
 }
 
