@@ -399,13 +399,16 @@ def run_sharded(args, cfg):
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = lib.rs_kernel_launches()
+    host_call = 0.0
     with Clocks(local) as clk:
         h0 = time.perf_counter()
         for k in range(args.steps):
             flush.zero_()
             st.barrier()  # device barrier: no rank's flush leaks into another rank's step bracket
             evs[k][0].record(stream)
+            h1 = time.perf_counter()
             one(args.warmup + k)
+            host_call += time.perf_counter() - h1
             evs[k][1].record(stream)
         host_ms = (time.perf_counter() - h0) * 1e3 / args.steps  # host enqueue time per step
         torch.cuda.synchronize()
@@ -413,11 +416,13 @@ def run_sharded(args, cfg):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     per_rank = [None] * world
     dist.all_gather_object(per_rank, {"sum_ms": sum(step_ms), "median_ms": statistics.median(step_ms),
-                                      "host_enqueue_ms_per_step": host_ms})
+                                      "host_enqueue_ms_per_step": host_ms,
+                                      "host_step_call_ms": host_call * 1e3 / args.steps})
     t_sum = sum(step_ms) / 1e3
     uniq = sum(uniq_b[(args.warmup + k) % nb] for k in range(args.steps))
     toks = sum(dev[(args.warmup + k) % nb][0].numel() for k in range(args.steps))
     tr = st.trace()  # last step's ExchangeTrace (all ranks)
+    timeline = dist_timeline(st, one, flush, lib, P) if os.environ.get("RS_TRACE") == "1" else None
     # per-phase device time (separate pass, CUDA events between the phases)
     st.set_profiling(True)
     for k in range(max(3, min(args.steps, 10))):
@@ -466,6 +471,7 @@ def run_sharded(args, cfg):
         "l2": "flushed (512 MiB write) between timed steps, then a device barrier of all ranks",
         "tokens_per_s": toks_job / t_job,
         "kernel_ms_rank0": phases,
+        **({"timeline_us_rank0": timeline} if timeline else {}),
         "step_ms_rank0": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
         "per_rank": per_rank,
         "balance": balance,
@@ -720,6 +726,45 @@ PHASES = ["dedup_probe", "csr_update", "hot_update", "checksum"]
 TRACE_NAMES = ["dedup_probe", "csr_light", "hot_tiles", "hot_finish", "scratch_clean", "csr_heavy"]
 
 
+DIST_TRACE_NAMES = TRACE_NAMES + ["req_gather", "req_grad_flags", "own_wait_ids", "own_dedup", "own_table_respond",
+                                   "req_wait_rows", "own_wait_grads", "own_update_done", "own_update"]
+
+
+def dist_timeline(st, one, flush, lib, P):
+    """Sharded step device timeline (diagnostics, RS_TRACE=1 for the whole
+    run): per kernel slot of this rank the median over 6 graph-replayed steps
+    of start / end relative to the requester dedup's first block (us)."""
+    import ctypes
+    import torch
+    n = ctypes.c_uint64()
+    buf = np.zeros(16 * 4096 * 2, np.uint64)
+    rows = {name: [] for name in DIST_TRACE_NAMES}
+    for k in range(6):
+        flush.zero_()
+        torch.cuda.synchronize()
+        st.barrier()
+        P._lib.check(lib.rs_comm_timeline(st._c, buf.ctypes.data, buf.size, ctypes.byref(n)), "timeline")
+        one(k)
+        torch.cuda.synchronize()
+        P._lib.check(lib.rs_comm_timeline(st._c, buf.ctypes.data, buf.size, ctypes.byref(n)), "timeline")
+        if not n.value:
+            return None
+        t = buf.reshape(16, 4096, 2).astype(np.float64)
+        t0 = t[0, :, 0][t[0, :, 1] > 0].min()
+        if os.environ.get("RS_TRACE_DUMP") and k == 5:  # raw per-block spans of the last step (us)
+            np.save(f"{os.environ['RS_TRACE_DUMP']}_rank{st.rank}.npy", np.where(t > 0, (t - t0) / 1e3, np.nan))
+        for i, name in enumerate(DIST_TRACE_NAMES):
+            ok = t[i, :, 1] > 0
+            if ok.any():
+                rows[name].append(((t[i, ok, 0].min() - t0) / 1e3, (t[i, ok, 1].max() - t0) / 1e3))
+    out = {}
+    for name, v in rows.items():
+        if v:
+            a = np.array(v)
+            out[name] = {"start_us": round(float(np.median(a[:, 0])), 2), "end_us": round(float(np.median(a[:, 1])), 2)}
+    return out
+
+
 def graph_timeline(table, dev, nb, flush, P, max_t):
     """Kernel spans inside the step's CUDA graph: a second workspace with the
     device timeline (RS_TRACE=1 at its first step: per block the first warp
@@ -736,7 +781,7 @@ def graph_timeline(table, dev, nb, flush, P, max_t):
         del os.environ["RS_TRACE"]
     lib = P.lib()
     n = ctypes.c_uint64()
-    buf = np.zeros(8 * 4096 * 2, np.uint64)
+    buf = np.zeros(16 * 4096 * 2, np.uint64)
     rows = {name: [] for name in TRACE_NAMES}
     for k in range(6):
         flush.zero_()
@@ -748,7 +793,7 @@ def graph_timeline(table, dev, nb, flush, P, max_t):
         P._lib.check(lib.rs_workspace_trace(st.ws.handle, buf.ctypes.data, buf.size, ctypes.byref(n)), "trace")
         if not n.value:
             return None
-        t = buf.reshape(8, 4096, 2).astype(np.float64)
+        t = buf.reshape(16, 4096, 2).astype(np.float64)
         t0 = t[0, :, 0][t[0, :, 1] > 0].min()
         for i, name in enumerate(TRACE_NAMES):
             ok = t[i, :, 1] > 0

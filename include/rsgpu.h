@@ -194,7 +194,10 @@ int rs_workspace_set_profiling(rs_workspace* ws, int on);
  * at the workspace's first rs_step): out[(kernel * 4096 + block) * 2 + {0,1}]
  * = first warp start / last warp end (%globaltimer ns) of each block of the
  * steps since the last call; kernels 0 dedup+probe, 1 CSR finish, 2 hot
- * tiles, 3 hot finish, 4 scratch clean, 5 heavy CSR ids.  *n_out = 0 when tracing is off. */
+ * tiles, 3 hot finish, 4 scratch clean, 5 heavy CSR ids; the sharded step
+ * (rs_comm_timeline) adds 6 requester gather, 7 gradient flags, 8 wait ids,
+ * 9 owner dedup, 10 owner table + respond, 11 wait rows, 12 wait gradients,
+ * 13 owner update done.  16 kernel slots; *n_out = 0 when tracing is off. */
 int rs_workspace_trace(rs_workspace* ws, uint64_t* out, uint64_t cap, uint64_t* n_out);
 int rs_workspace_phase_ms(rs_workspace* ws, double* ms, uint32_t nphases, uint64_t* count);
 /* n_unique of the last dedup on this workspace (host value).  Synchronizes. */
@@ -253,6 +256,8 @@ int rs_comm_set_profiling(rs_comm* c, int on);
  * enqueued after it starts once every rank reached it */
 int rs_comm_barrier(rs_comm* c, void* stream);
 int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count);
+/* rs_workspace_trace of the sharded step's requester workspace (RS_TRACE=1). */
+int rs_comm_timeline(rs_comm* c, uint64_t* out, uint64_t cap, uint64_t* n_out);
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received);
 /* A group of `world` logical ranks on the current GPU (one process): the

@@ -141,6 +141,7 @@ _SIGS = {
     "rs_comm_barrier": (C.c_int, [vp, vp]),
     "rs_comm_phase_ms": (C.c_int, [vp, C.POINTER(C.c_double), C.c_int, C.POINTER(u64)]),
     "rs_comm_trace": (C.c_int, [vp, vp, vp, vp, vp, vp]),
+    "rs_comm_timeline": (C.c_int, [vp, vp, u64, C.POINTER(u64)]),
     "rs_comm_create_local": (C.c_int, [C.c_int, u64, u32, vp]),
     "rs_dist_group_forward": (C.c_int, [vp, vp, C.c_int, vp, vp, vp, vp]),
     "rs_dist_group_backward": (C.c_int, [vp, vp, C.c_int, vp, vp, C.POINTER(rs_optimizer_params), vp]),

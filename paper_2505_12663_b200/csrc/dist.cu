@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -65,6 +67,8 @@ struct CommDev {
   unsigned long long* epoch;  // device step counter of the role (requester: bumped by KB)
   unsigned long long* trace;
   unsigned int* done;  // last-block counters [4]
+  unsigned long long* tl = nullptr;  // device timeline (RS_TRACE=1, diagnostics; slots in rs_internal.cuh)
+  uint32_t diag = 0;  // RS_DIAG_OWN timing experiments (wrong results): 1 rows to self only, 2 no row stores
 };
 
 __device__ __forceinline__ ArenaHdr* hdr_of(const CommDev& c, uint32_t r) {
@@ -128,6 +132,7 @@ __global__ void k_barrier(CommDev c, unsigned long long* bar_epoch) {
 // a 1-block waiter is what keeps a concurrently running producer on the
 // other stream of this GPU from being starved of SMs by spinning blocks.
 __global__ void k_wait(CommDev c, int phase) {
+  WarpTrace wt_(c.tl, phase == 0 ? 8 : phase == 1 ? 11 : 12);
   __shared__ unsigned long long e;
   if (threadIdx.x == 0) {
     e = *c.epoch + (phase == 0 ? 1 : 0);  // the owner's step starts here
@@ -147,6 +152,7 @@ __global__ void k_wait(CommDev c, int phase) {
 // grid (ceil(cap / 256), W): block (x, src) takes positions x*256.. of src.
 __global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t* __restrict__ origins,
                                                    uint64_t* __restrict__ unique) {
+  WarpTrace wt_(c.tl, 9);
   const ArenaHdr* h = hdr_of(c, c.rank);
   const uint32_t src = blockIdx.y;
   if (threadIdx.x == 0) spin_flag(&h->sig_ids[src], *c.epoch, c.trace + kTrError);  // src's ids landed
@@ -192,6 +198,9 @@ __global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t
 // emb_in of every requester that asked for it (one 128-bit store per lane per
 // step over NVLink).  Also the finish metadata (CSR = the slot's origin row),
 // cleaning of the other scratch set, the table epilogue and the flags.
+#ifndef RS_OWN_MINB
+#define RS_OWN_MINB 5  // 48 registers: the id-carrying blocks of k_own_table fit in one wave
+#endif
 struct OwnTableArgs {
   TableDev* td;
   SetDev use, clean;
@@ -205,7 +214,8 @@ struct OwnTableArgs {
   TableCounters* mirror_out;  // host's pinned counter mirror (mapped), or null
 };
 
-__global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
+__global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_table(CommDev c, OwnTableArgs a) {
+  WarpTrace wt_(c.tl, 10);
   TableDev* td = a.td;
   const TableDesc d = td->d;
   const unsigned long long free_n0 = td->c.free_n;
@@ -240,6 +250,7 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
       a.u_ticket[i] = 0;
     }
     if (row == kNoRow) continue;  // table error (reported through the counters)
+    if (c.diag & 2) continue;
     const float4* e = reinterpret_cast<const float4*>(d.emb) + (size_t)row * D4;
     // the group's origins (<= world) in one parallel load, then each lane's
     // part of the row (held in registers) goes to every requester
@@ -252,7 +263,7 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
       for (uint32_t k = 0; k < cnt; ++k) {
         const uint32_t origin = k < kBucket ? __shfl_sync(gmask, my_origin, k, kBucket)
                                             : __ldg(a.origins + (size_t)slot * c.world + k);
-        const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
+        const uint32_t src = (c.diag & 1) ? c.rank : origin / c.cap, jj = origin - (origin / c.cap) * c.cap;
         float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
                       ((size_t)c.rank * c.cap + jj) * D4;
 #pragma unroll
@@ -285,11 +296,18 @@ __global__ void __launch_bounds__(256) k_own_table(CommDev c, OwnTableArgs a) {
       c.trace[kTrLookups] = nu;
     }
   }
-  if (last_block_signal(c, 1, c.done + 1)) raise_flags(c, 1, c.done + 1, *c.epoch);
+  if (last_block_signal(c, 1, c.done + 1)) {
+    raise_flags(c, 1, c.done + 1, *c.epoch);
+    if (threadIdx.x == 0) *a.clean.cnt = 0;  // every block cleaned: the cleaned set starts empty
+  }
 }
 
 // Raise flag `phase` at every peer (after the kernels that stored the data).
+// timeline stamp (RS_TRACE=1 only): the stream reached this point
+__global__ void k_tl_stamp(CommDev c, int slot) { trace_mark(c.tl, slot); }
+
 __global__ void k_signal(CommDev c, int phase) {
+  WarpTrace wt_(c.tl, 7);
   if (threadIdx.x == 0) fence_sys();
   __syncthreads();
   const unsigned long long e = *c.epoch;
@@ -304,13 +322,14 @@ using namespace rs;
 
 struct StepSets {
   int ru, ou, par;  // requester / owner scratch sets, gradient-buffer parity
+  int fu = -1;      // requester on the fast kernels (step_fast.cu): its scratch set; -1: the split kernels
 };
 
 struct DistGraph {
   rs_table* t;
   const void *ids, *grads, *out;
   uint64_t n;
-  int mirror, ru, ou, par;
+  int mirror, ru, ou, par, fu;
   const void* pbuf;
   double* csum;
   unsigned char opt[256];
@@ -362,6 +381,11 @@ struct rs_comm {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t own_stream = nullptr;  // owner role runs here, concurrently with the requester's
   cudaStream_t gather_stream = nullptr;  // the requester's gather, concurrent with its reduce
+  cudaEvent_t ev_dedup = nullptr;        // owner dedup done (reduce_after_dedup)
+  bool reduce_after_dedup = false;       // RS_DIST_REDUCE_AFTER=1
+  bool host_prof = false;                // RS_HOST_PROF=1
+  double host_ns[5] = {0, 0, 0, 0, 0};
+  uint64_t host_calls = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_meta = nullptr, ev_gjoin = nullptr;
   std::vector<DistGraph> graphs;
   uint64_t graph_clock = 0;
@@ -419,6 +443,9 @@ static CommDev comm_dev(rs_comm* c, int par, Role role) {
   d.epoch = role_epoch(c, role);
   d.trace = c->trace;
   d.done = c->done;
+  d.tl = c->ws_req->fast.trace;
+  static const uint32_t diag = getenv("RS_DIAG_OWN") ? (uint32_t)atoi(getenv("RS_DIAG_OWN")) : 0u;
+  d.diag = diag;
   return d;
 }
 
@@ -476,7 +503,7 @@ static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
 // owner-unique id find-or-insert on the shard (capacity prepared by the
 // caller) and the row stored into every requester that asked for it (KB')
 static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
-                        TableCounters* mirror_out = nullptr) {
+                        TableCounters* mirror_out = nullptr, cudaEvent_t ev_dedup = nullptr) {
   rs_workspace* wo = c->ws_own;
   const CommDev cd = comm_dev(c, ss.par, kOwner);
   const uint64_t nflat = (uint64_t)c->world * c->cap;
@@ -489,6 +516,7 @@ static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
   k_own_dedup<<<dim3((unsigned)((c->cap + 255) / 256), c->world), 256, 0, s>>>(
       cd, set_dev(wo, ou), c->origins, wo->unique);
   RS_LAUNCH_CHECK("k_own_dedup");
+  if (ev_dedup) RS_CUDA(cudaEventRecord(ev_dedup, s));
   RS_TRY(prof_end(c, kPhOwnerTable, s));
   RS_TRY(prof_begin(c, kPhRespond, s));
   OwnTableArgs a;
@@ -505,9 +533,7 @@ static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
   a.mirror_out = mirror_out;
   k_own_table<<<grid_for(nflat, 32, 148 * 8), 256, 0, s>>>(cd, a);
   RS_LAUNCH_CHECK("k_own_table");
-  RS_TRY(prof_end(c, kPhRespond, s));
-  RS_CUDA(cudaMemsetAsync(wo->set[ou ^ 1].cnt, 0, 4, s));  // the cleaned set starts empty
-  return RS_OK;
+  return prof_end(c, kPhRespond, s);
 }
 
 // requester: wait for the rows, expand them to the tokens (KC gather)
@@ -591,6 +617,63 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
   return RS_OK;
 }
 
+// ---- the requester on the fast kernels (step_fast.cu) -----------------------
+// The single-GPU step's dedup (KA) with the id send folded into it, its
+// light / heavy / hot-tile segment reduce storing each unique id's sum into
+// the owner's grad_in, and a gather from the receive buffer.
+static rs_dist_send dist_send(rs_comm* c, uint64_t n) {
+  rs_dist_send snd;
+  snd.peers = c->d_peers;
+  snd.off_ids = c->off_ids;
+  snd.cap = (uint32_t)c->cap;
+  snd.world = (uint32_t)c->world;
+  snd.rank = (uint32_t)c->rank;
+  snd.send_cnt = c->send_cnt;
+  snd.send_pos = c->send_pos;
+  snd.cnt_ptrs = c->d_cnt_ptrs;
+  snd.flag_ptrs = c->d_sig_ids_ptrs;
+  snd.epoch = role_epoch(c, kRequester);
+  snd.done = c->done + 0;
+  snd.trace_ids_sent = c->trace + kTrIdsSent;
+  snd.trace_requested = c->trace + kTrRequested;
+  snd.n_tokens = n;
+  return snd;
+}
+static int req_front_fast(rs_comm* c, const uint64_t* d_ids, uint64_t n, StepSets ss, cudaStream_t s) {
+  RS_TRY(prof_begin(c, kPhReqDedup, s));
+  RS_TRY(fast_dist_front(c->ws_req, c->dim, d_ids, n, ss.fu, s, dist_send(c, n)));
+  return prof_end(c, kPhReqDedup, s);
+}
+static int req_reduce_fast(rs_comm* c, const float* d_grads, uint64_t n, StepSets ss, cudaStream_t s) {
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
+  RS_TRY(prof_begin(c, kPhReqReduce, s));
+  RS_TRY(fast_dist_reduce(c->ws_req, c->view, c->dim, n, d_grads, ss.fu, s, c->ws_req->fork,
+                          c->d_peer_grad[ss.par], (uint32_t)c->cap, (uint32_t)c->rank));
+  k_signal<<<1, 64, 0, s>>>(cd, 2);  // every branch joined: the sums are out
+  RS_LAUNCH_CHECK("k_signal(grads)");
+  return prof_end(c, kPhReqReduce, s);
+}
+static int req_gather_fast(rs_comm* c, uint64_t n, float* d_out, StepSets ss, cudaStream_t s) {
+  // One block waits for the rows first: gather blocks spinning on the flags
+  // would hold the SMs the owner's kernels need to answer them.  One block
+  // per tile (RS_DIST_GATHER_GRID=G: G persistent blocks, measured slower);
+  // RS_DIST_GATHER_SPIN=1: no waiter kernel, the gather's blocks wait.
+  static const uint32_t grid =
+      getenv("RS_DIST_GATHER_GRID") ? (uint32_t)atoi(getenv("RS_DIST_GATHER_GRID")) : 0u;
+  static const bool spin = getenv("RS_DIST_GATHER_SPIN") && getenv("RS_DIST_GATHER_SPIN")[0] == '1';
+  const CommDev cd = comm_dev(c, ss.par, kRequester);
+  if (!spin) {
+    RS_TRY(prof_begin(c, kPhWaitEmbs, s));
+    k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+    RS_LAUNCH_CHECK("k_wait(embs)");
+    RS_TRY(prof_end(c, kPhWaitEmbs, s));
+  }
+  RS_TRY(prof_begin(c, kPhGather, s));
+  RS_TRY(fast_dist_gather(c->ws_req, c->view, c->dim, n, d_out, ss.fu, s,
+                          wait_sync(c, c->own_sig_emb, kRequester), c->csum_dst, grid));
+  return prof_end(c, kPhGather, s);
+}
+
 // owner: per id sum over its origins in (source, position) order -- the
 // stage-2 origin order -- fused with the optimizer on the shard
 static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cudaStream_t s) {
@@ -607,7 +690,12 @@ static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cu
   oo.no_hot = true;
   oo.csr_pos = c->origins;
   oo.sync = wait_sync(c, c->own_sig_grad, kOwner);  // every requester's sums landed
+  oo.sync.tl = c->ws_req->fast.trace;
   RS_TRY(step_finish(wo, t, ss.ou, nflat, grad_in, ob, nullptr, s, &oo));
+  if (cd.tl) {
+    k_tl_stamp<<<1, 32, 0, s>>>(cd, 13);
+    RS_LAUNCH_CHECK("k_tl_stamp");
+  }
   RS_TRY(prof_end(c, kPhOwnerUpdate, s));
   return RS_OK;
 }
@@ -632,13 +720,27 @@ static int prepare_step(rs_comm* c, rs_table* t, uint64_t n_reduce, cudaStream_t
   if (n_reduce) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n_reduce, s));
   return RS_OK;
 }
-static StepSets begin_step(rs_comm* c) {
+// fast: the requester runs on the fast kernels (a step with gradients, n > 0)
+static int begin_step(rs_comm* c, bool fast, StepSets* out) {
+  if (fast) RS_TRY(fast_prepare(c->ws_req));
   c->epoch++;
-  return StepSets{c->ws_req->cur, c->ws_own->cur, (int)(c->epoch & 1)};
+  StepSets ss{c->ws_req->cur, c->ws_own->cur, (int)(c->epoch & 1)};
+  ss.fu = fast ? c->ws_req->fast.cur : -1;
+  *out = ss;
+  return RS_OK;
+}
+static bool fast_requester(rs_comm* c, uint64_t n, const float* d_grads) {
+  return c->ws_req->use_fast && n > 0 && d_grads && ((uintptr_t)d_grads & 15u) == 0 &&
+         fast_dim_supported(c->dim);
 }
 static void end_step(rs_comm* c, StepSets ss) {
   c->last_sets = ss;
-  c->ws_req->cur = ss.ru ^ 1;
+  if (ss.fu >= 0) {
+    c->ws_req->fast.last = ss.fu;
+    c->ws_req->fast.cur = ss.fu ^ 1;
+  } else {
+    c->ws_req->cur = ss.ru ^ 1;
+  }
   c->ws_own->cur = ss.ou ^ 1;
 }
 
@@ -661,6 +763,29 @@ static int join_owner(rs_comm* c, cudaStream_t q, cudaStream_t own) {
   RS_CUDA(cudaStreamWaitEvent(q, c->ev_join, 0));
   return RS_OK;
 }
+
+// Host-side cost of rs_dist_step by section (RS_HOST_PROF=1, diagnostics):
+// 0 args, 1 capacity / prepare, 2 graph lookup, 3 cudaGraphLaunch, 4 commit;
+// printed when the comm is destroyed.
+struct HostClock {
+  rs_comm* c;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostClock(rs_comm* c_) : c(c_) {
+    if (c->host_prof) t0 = std::chrono::steady_clock::now();
+  }
+  void mark(int k) {
+    if (!c->host_prof) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    c->host_ns[k] += (double)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+    t0 = t1;
+    if (k == 4 && ++c->host_calls % 16 == 0) {  // the last 16 calls' means, then restart
+      fprintf(stderr, "rs_dist_step host us/call (rank %d, calls to %llu): args %.1f prepare %.1f lookup %.1f launch %.1f commit %.1f\n",
+              c->rank, (unsigned long long)c->host_calls, c->host_ns[0] / 16e3, c->host_ns[1] / 16e3,
+              c->host_ns[2] / 16e3, c->host_ns[3] / 16e3, c->host_ns[4] / 16e3);
+      for (double& x : c->host_ns) x = 0;
+    }
+  }
+};
 
 // end of a step: collect the phase times recorded during it (one sync)
 static int prof_step_done(rs_comm* c) {
@@ -749,7 +874,9 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   RS_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   const char* pe = getenv("RS_DIST_PRIO");
   auto prio_of = [&](char ch) { return ch == 'h' ? prio_hi : (ch == 'l' ? prio_lo : 0); };
-  const int own_prio = pe && pe[0] ? prio_of(pe[0]) : 0;
+  // default "hn": the owner role (its dedup / table / update are the step's
+  // critical path) ahead of the requester's reduce for free SM slots
+  const int own_prio = pe && pe[0] ? prio_of(pe[0]) : prio_hi;
   const int gat_prio = pe && pe[0] && pe[1] ? prio_of(pe[1]) : 0;
   RS_CUDA(cudaStreamCreateWithPriority(&c->own_stream, cudaStreamNonBlocking, own_prio));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -757,6 +884,9 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   RS_CUDA(cudaStreamCreateWithPriority(&c->gather_stream, cudaStreamNonBlocking, gat_prio));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_meta, cudaEventDisableTiming));
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_gjoin, cudaEventDisableTiming));
+  RS_CUDA(cudaEventCreateWithFlags(&c->ev_dedup, cudaEventDisableTiming));
+  if (const char* e = getenv("RS_DIST_REDUCE_AFTER")) c->reduce_after_dedup = e[0] == '1';
+  if (const char* e = getenv("RS_HOST_PROF")) c->host_prof = e[0] == '1';
   c->h_peers[rank] = c->arena;
   *out = c;
   return RS_OK;
@@ -862,6 +992,7 @@ int rs_comm_destroy(rs_comm* c) {
   if (c->gather_stream) cudaStreamDestroy(c->gather_stream);
   if (c->ev_meta) cudaEventDestroy(c->ev_meta);
   if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
+  if (c->ev_dedup) cudaEventDestroy(c->ev_dedup);
   rs_workspace_destroy(c->ws_req);
   rs_workspace_destroy(c->ws_own);
   delete c;
@@ -876,7 +1007,8 @@ int rs_dist_forward(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, 
   RS_TRY(check_call(c, t, n, "rs_dist_forward"));
   cudaStream_t s = S(stream);
   RS_TRY(prepare_step(c, t, 0, s));
-  const StepSets ss = begin_step(c);
+  StepSets ss;
+  RS_TRY(begin_step(c, false, &ss));
   cudaStream_t own;
   RS_TRY(fork_owner(c, s, &own));
   RS_TRY(req_front(c, t, d_ids, n, ss, s));
@@ -921,15 +1053,28 @@ int rs_dist_backward(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
 // (buffers, n, parities) -- the flags' epoch lives on the device.
 int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
                  float* d_out, const rs_optimizer_params* opt, void* stream) {
+  HostClock hc(c);
   RS_TRY(check_call(c, t, n, "rs_dist_step"));
   cudaStream_t s = S(stream);
   alignas(16) unsigned char ob[256];
   std::memset(ob, 0, sizeof(ob));
   RS_TRY(step_opt_args(t, opt, ob, s));
+  hc.mark(0);
   RS_TRY(prepare_step(c, t, n, s));
-  const StepSets ss = begin_step(c);
+  hc.mark(1);
+  StepSets ss;
+  RS_TRY(begin_step(c, fast_requester(c, n, d_grads), &ss));
+  const bool fast = ss.fu >= 0;
   const int mirror = t->mirror_next;
   auto enqueue = [&](cudaStream_t q) -> int {
+    if (c->one_stream && fast) {  // both roles in one stream, data-flow order
+      RS_TRY(req_front_fast(c, d_ids, n, ss, q));
+      RS_TRY(owner_lookup(c, t, ss, q));
+      RS_TRY(table_mirror_copy(t, mirror, q));
+      RS_TRY(req_reduce_fast(c, d_grads, n, ss, q));
+      RS_TRY(req_gather_fast(c, n, d_out, ss, q));
+      return owner_update(c, t, ob, ss, q);
+    }
     if (c->one_stream) {  // both roles in one stream: fused gather + reduce pass
       RS_TRY(req_front(c, t, d_ids, n, ss, q));
       RS_TRY(owner_lookup(c, t, ss, q));
@@ -941,19 +1086,32 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     // owner on its stream: stage 2, table + answer, then the update
     cudaStream_t own;
     RS_TRY(fork_owner(c, q, &own));
-    RS_TRY(req_front(c, t, d_ids, n, ss, q));
+    if (fast) RS_TRY(req_front_fast(c, d_ids, n, ss, q));
+    else RS_TRY(req_front(c, t, d_ids, n, ss, q));
     // the gather needs only the metadata (and the rows): it runs on its own
     // stream, concurrently with the segment-reduce of the same tokens
     RS_CUDA(cudaEventRecord(c->ev_meta, q));
     RS_CUDA(cudaStreamWaitEvent(c->gather_stream, c->ev_meta, 0));
-    RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
     // the counters reach the pinned mirror from k_own_table's epilogue (mapped
     // store) instead of a copy node on the owner's critical path
     TableCounters* mo = t->mirror[mirror].dev_ptr;
-    RS_TRY(owner_lookup(c, t, ss, own, mo));
+    if (c->reduce_after_dedup) {
+      // the requester's reduce (needed only by the owners' update) waits for
+      // this rank's owner dedup: the dedup, on the critical path, then finds
+      // the SMs free instead of behind the reduce's long blocks
+      RS_TRY(owner_lookup(c, t, ss, own, mo, c->ev_dedup));
+      RS_CUDA(cudaStreamWaitEvent(q, c->ev_dedup, 0));
+      if (fast) RS_TRY(req_reduce_fast(c, d_grads, n, ss, q));
+      else RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
+    } else {
+      if (fast) RS_TRY(req_reduce_fast(c, d_grads, n, ss, q));
+      else RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
+      RS_TRY(owner_lookup(c, t, ss, own, mo));
+    }
     if (!mo) RS_TRY(table_mirror_copy(t, mirror, own));
     RS_TRY(owner_update(c, t, ob, ss, own));
-    RS_TRY(req_gather(c, t, n, d_out, ss, c->gather_stream));
+    if (fast) RS_TRY(req_gather_fast(c, n, d_out, ss, c->gather_stream));
+    else RS_TRY(req_gather(c, t, n, d_out, ss, c->gather_stream));
     RS_CUDA(cudaEventRecord(c->ev_gjoin, c->gather_stream));
     RS_CUDA(cudaStreamWaitEvent(q, c->ev_gjoin, 0));
     return join_owner(c, q, own);
@@ -964,7 +1122,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     DistGraph* hit = nullptr;
     for (auto& g : c->graphs)
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
-          g.mirror == mirror && g.ru == ss.ru && g.ou == ss.ou && g.par == ss.par &&
+          g.mirror == mirror && g.ru == ss.ru && g.ou == ss.ou && g.par == ss.par && g.fu == ss.fu &&
           g.pbuf == c->ws_req->pbuf && g.csum == c->csum_dst && std::memcmp(g.opt, ob, sizeof(ob)) == 0) {
         hit = &g;
         break;
@@ -988,6 +1146,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
       e.ru = ss.ru;
       e.ou = ss.ou;
       e.par = ss.par;
+      e.fu = ss.fu;
       e.pbuf = c->ws_req->pbuf;
       e.csum = c->csum_dst;
       std::memcpy(e.opt, ob, sizeof(ob));
@@ -1007,7 +1166,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
         return st;
       }
       if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, graph_flags());
       cudaGraphDestroy(g);
       if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
       e.launches = launches() - before;
@@ -1016,13 +1175,16 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
       hit = &c->graphs.back();
     }
     hit->last_use = ++c->graph_clock;
+    hc.mark(2);
     RS_CUDA(cudaGraphLaunch(hit->exec, s));
+    hc.mark(3);
     count_launch(hit->launches);
   }
   RS_TRY(table_mirror_commit(t, mirror, s));
   end_step(c, ss);
   t->applies++;
   c->have_forward = false;
+  hc.mark(4);
   return prof_step_done(c);
 }
 
@@ -1070,6 +1232,12 @@ int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count) {
 // This rank's ExchangeTrace row (exchange_sim.hpp:37-59): ids_sent[dst],
 // embs_sent[dst] (vectors this rank, as owner, sent to dst), lookups,
 // ids_requested, ids_received.  Synchronizes.
+// the device timeline of this rank's last step (RS_TRACE=1): rs_workspace_trace of the requester workspace
+int rs_comm_timeline(rs_comm* c, uint64_t* out, uint64_t cap, uint64_t* n_out) {
+  if (!c) return fail(RS_ERR_CONFIG, "rs_comm_timeline: null comm");
+  return rs_workspace_trace(c->ws_req, out, cap, n_out);
+}
+
 int rs_comm_trace(rs_comm* c, uint64_t* ids_sent, uint64_t* embs_sent, uint64_t* lookups,
                   uint64_t* ids_requested, uint64_t* ids_received) {
   if (!c) return fail(RS_ERR_CONFIG, "rs_comm_trace: null comm");
@@ -1116,7 +1284,7 @@ int rs_dist_group_forward(rs_comm* const* cs, rs_table* const* ts, int world, co
   std::vector<StepSets> ss(world);
   for (int r = 0; r < world; ++r) {
     RS_TRY(prepare_step(cs[r], ts[r], 0, s));
-    ss[r] = begin_step(cs[r]);
+    RS_TRY(begin_step(cs[r], false, &ss[r]));
   }
   for (int r = 0; r < world; ++r) RS_TRY(req_front(cs[r], ts[r], d_ids[r], n[r], ss[r], s));
   for (int r = 0; r < world; ++r) {
@@ -1166,15 +1334,24 @@ int rs_dist_group_step(rs_comm* const* cs, rs_table* const* ts, int world, const
   for (int r = 0; r < world; ++r) {
     RS_TRY(step_opt_args(ts[r], opt, obs[r].b, s));
     RS_TRY(prepare_step(cs[r], ts[r], n[r], s));
-    ss[r] = begin_step(cs[r]);
+    RS_TRY(begin_step(cs[r], fast_requester(cs[r], n[r], d_grads[r]), &ss[r]));
   }
-  for (int r = 0; r < world; ++r) RS_TRY(req_front(cs[r], ts[r], d_ids[r], n[r], ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    if (ss[r].fu >= 0) RS_TRY(req_front_fast(cs[r], d_ids[r], n[r], ss[r], s));
+    else RS_TRY(req_front(cs[r], ts[r], d_ids[r], n[r], ss[r], s));
+  }
   for (int r = 0; r < world; ++r) {
     RS_TRY(owner_lookup(cs[r], ts[r], ss[r], s));
     RS_TRY(table_after_op(ts[r], s));
   }
-  for (int r = 0; r < world; ++r) RS_TRY(req_reduce(cs[r], ts[r], d_grads[r], n[r], ss[r], s));
-  for (int r = 0; r < world; ++r) RS_TRY(req_gather(cs[r], ts[r], n[r], d_out[r], ss[r], s));
+  for (int r = 0; r < world; ++r) {
+    if (ss[r].fu >= 0) RS_TRY(req_reduce_fast(cs[r], d_grads[r], n[r], ss[r], s));
+    else RS_TRY(req_reduce(cs[r], ts[r], d_grads[r], n[r], ss[r], s));
+  }
+  for (int r = 0; r < world; ++r) {
+    if (ss[r].fu >= 0) RS_TRY(req_gather_fast(cs[r], n[r], d_out[r], ss[r], s));
+    else RS_TRY(req_gather(cs[r], ts[r], n[r], d_out[r], ss[r], s));
+  }
   for (int r = 0; r < world; ++r) RS_TRY(owner_update(cs[r], ts[r], obs[r].b, ss[r], s));
   for (int r = 0; r < world; ++r) {
     end_step(cs[r], ss[r]);

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "rs_internal.cuh"
@@ -188,6 +189,7 @@ struct rs_dist_sync {
   unsigned int* sig_done = nullptr;                // arrival counter of the signalling kernels
   uint32_t sig_total = 0;                          // blocks arriving (set by the launcher)
   unsigned long long* error = nullptr;             // set on a wait timeout
+  unsigned long long* tl = nullptr;                // device timeline (RS_TRACE=1): the owner update's slot
 };
 
 // The requester's id send folded into the table-metadata kernel (KB): the
@@ -224,6 +226,14 @@ struct rs_dist_opts {
 };
 
 namespace rs {
+
+// CUDA graphs run their kernel nodes at the priority of the stream each was
+// captured on (the owner / gather streams of the sharded step), not the
+// launch stream's; RS_GRAPH_PRIO=0 turns that off (experiments).
+inline unsigned long long graph_flags() {
+  static const bool off = getenv("RS_GRAPH_PRIO") && getenv("RS_GRAPH_PRIO")[0] == '0';
+  return off ? 0ull : (unsigned long long)cudaGraphInstantiateFlagUseNodePriority;
+}
 // table.cu
 int table_prepare(rs_table* t, uint64_t n, cudaStream_t s);  // room for n more keys
 int table_after_op(rs_table* t, cudaStream_t s);             // enqueue counter mirror
@@ -265,8 +275,16 @@ int step_opt_args(rs_table* t, const rs_optimizer_params* p, void* out, cudaStre
 int step_reduce_prepare(rs_workspace* ws, uint32_t D, uint64_t n, cudaStream_t s);
 // step_fast.cu
 bool fast_step_supported(const rs_table* t);
+bool fast_dim_supported(uint32_t dim);
 int fast_prepare(rs_workspace* ws);
 int fast_check_errors(rs_workspace* ws, cudaStream_t s);
+// the sharded requester on the fast kernels (step_fast.cu, used by dist.cu)
+int fast_dist_front(rs_workspace* ws, uint32_t D, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
+                    const rs_dist_send& send);
+int fast_dist_reduce(rs_workspace* ws, rs::TableDev* view, uint32_t D, uint64_t n, const float* d_grads, int use,
+                     cudaStream_t s, bool fork, float* const* peer_dst, uint32_t cap, uint32_t rank);
+int fast_dist_gather(rs_workspace* ws, const rs::TableDev* view, uint32_t D, uint64_t n, float* d_out, int use,
+                     cudaStream_t s, const rs_dist_sync& sync, double* csum, uint32_t grid);
 void fast_free(rs_workspace* ws);
 int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
                  float* d_out, const void* opt_args, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,

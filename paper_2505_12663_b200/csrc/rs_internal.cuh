@@ -164,4 +164,39 @@ inline unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap = 148u 
   return static_cast<unsigned>(g);
 }
 
+// Device-side timeline (rs_workspace_trace, diagnostics): per (kernel, block)
+// the first warp start and the last warp end (%globaltimer, ns).
+constexpr uint32_t kTraceBlocks = 4096;
+// slots: 0-5 the fast step's kernels (step_fast.cu), 6-15 the sharded
+// step's requester gather / signal and owner kernels (dist.cu)
+constexpr uint32_t kTraceSlots = 16;
+// phase mark of a block (thread 0): kernel slot kid, end time = now
+__device__ __forceinline__ void trace_mark(unsigned long long* base, uint32_t kid) {
+  if (base && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned long long* p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
+    atomicMin(p, t);
+    atomicMax(p + 1, t);
+  }
+}
+struct WarpTrace {
+  unsigned long long* p = nullptr;
+  __device__ __forceinline__ WarpTrace(unsigned long long* base, uint32_t kid) {
+    if (base && (threadIdx.x & 31) == 0 && blockIdx.x < kTraceBlocks) {
+      p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMin(p, t);
+    }
+  }
+  __device__ __forceinline__ ~WarpTrace() {
+    if (p) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMax(p + 1, t);
+    }
+  }
+};
+
 }  // namespace rs

@@ -812,6 +812,7 @@ __device__ __forceinline__ void ordered_sum(const FinishArgs& a, const uint32_t*
 template <int G, int NV>
 __global__ void __launch_bounds__(256, NV == 1 ? RS_CSR_MINB : 4) k_finish_csr(FinishArgs a, OptArgs o) {
   // G lanes per id, each owning NV float4 chunks of the row (chunk gl + j*G)
+  WarpTrace wt_(a.sync.tl, 14);
   pdl_wait();
   constexpr int PPT = (int)(kCsrMax / G);  // positions held per thread
   __shared__ uint32_t order_s[(256 / G) * kCsrMax];
@@ -1557,8 +1558,13 @@ static int launch_finish(rs_workspace* ws, rs_table* t, int use, uint64_t n, con
   // CSR finish shape: G lanes x 1 float4 per id; RS_CSR_NV=2 runs G/2 lanes
   // x 2 float4 (twice the ids in flight per SM -- measured ~1 % slower at
   // config 1, kept for other shapes' experiments)
+  // The sharded owner's update (no hot ids, <= W origins per id) runs G/2
+  // lanes x 2 float4: at 48 registers its ids then fit one wave
+  // (RS_OWN_NV=1: G lanes x 1)
   static const int nv_env = getenv("RS_CSR_NV") ? atoi(getenv("RS_CSR_NV")) : 1;
-  const int NVc = (nv_env == 2 && G >= 4) ? 2 : 1;
+  static const int nv_own = getenv("RS_OWN_NV") ? atoi(getenv("RS_OWN_NV")) : 2;
+  const bool owner = dopt && dopt->no_hot;
+  const int NVc = ((owner ? nv_own : nv_env) == 2 && G >= 4) ? 2 : 1;
   const int Gc = G / NVc;
   // G > 0: CSR ids on s, hot ids concurrently on the forked aux stream
   const unsigned grid = G > 0 ? hot_blocks : hot_blocks + grid_for(n, 8, 148 * 24);
@@ -2075,7 +2081,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
         return st;
       }
       if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+      const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, graph_flags());
       cudaGraphDestroy(g);
       if (ie != cudaSuccess) return cuda_fail(ie, "cudaGraphInstantiate");
       e.launches = launches() - before;

@@ -36,6 +36,7 @@
 #include <cstring>
 #include <vector>
 
+#include "dist_sync.cuh"
 #include "opt_dev.cuh"
 #include "rs_host.hpp"
 #include "table_dev.cuh"
@@ -100,38 +101,6 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 #define RS_IDX_OK(cond, ctr) true
 #endif
 
-// Device-side timeline (rs_workspace_trace, diagnostics): per (kernel, block)
-// the first warp start and the last warp end (%globaltimer, ns).
-constexpr uint32_t kTraceBlocks = 4096;
-// phase mark of a block (thread 0): kernel slot kid, end time = now
-__device__ __forceinline__ void trace_mark(unsigned long long* base, uint32_t kid) {
-  if (base && threadIdx.x == 0 && blockIdx.x < kTraceBlocks) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    unsigned long long* p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
-    atomicMin(p, t);
-    atomicMax(p + 1, t);
-  }
-}
-struct WarpTrace {
-  unsigned long long* p = nullptr;
-  __device__ __forceinline__ WarpTrace(unsigned long long* base, uint32_t kid) {
-    if (base && (threadIdx.x & 31) == 0 && blockIdx.x < kTraceBlocks) {
-      p = base + ((size_t)kid * kTraceBlocks + blockIdx.x) * 2;
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMin(p, t);
-    }
-  }
-  __device__ __forceinline__ ~WarpTrace() {
-    if (p) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      atomicMax(p + 1, t);
-    }
-  }
-};
-
 // Global scratch insert (linear probing on the low hash bits) into the
 // 16-byte records.  first0: the start record's key read early by the caller.
 __device__ __forceinline__ uint64_t rec_insert(const FSet& S, uint64_t id, uint64_t h, bool* fresh,
@@ -172,6 +141,9 @@ struct FaArgs {
   const uint64_t* ids;
   uint32_t n;
   uint32_t set;  // scratch set parity of this step
+  // sharded requester (send.peers != null): no table here -- the tile that
+  // claims an id sends it to its owner's receive list instead of probing
+  rs_dist_send send;
   FSet use, clean;
   FShared sh;
   TableDev* td;
@@ -180,6 +152,64 @@ struct FaArgs {
   uint32_t* urow;
   int64_t* urow64;
 };
+
+// Sharded requester: the ids this tile claimed go to their owners
+// (owner = hash64 % W, exchange_sim.cpp:82-85): positions from block-local
+// per-owner counters and one global atomic per (block, owner), each id
+// stored into the owner's ids_in[rank][j] over NVLink; the slot's record
+// row becomes the received-row index owner * cap + j (the gather reads it).
+// The last block publishes the counts and raises the ids flags (epoch e).
+__device__ __forceinline__ void fa_send(const FaArgs& a, uint32_t nnew, const unsigned long long* fid,
+                                        const uint32_t* fslot, const uint32_t* fu) {
+  const rs_dist_send& S = a.send;
+  __shared__ uint32_t s_ocnt[64], s_obase[64], fo[kTT], fj[kTT];
+  __shared__ unsigned long long s_e;
+  __shared__ bool s_last;
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t r = tid; r < 64; r += kTT) s_ocnt[r] = 0;
+  if (tid == 0) s_e = *S.epoch + 1;  // read before arriving; published by the last block
+  __syncthreads();
+  for (uint32_t k = tid; k < nnew; k += kTT) {
+    const uint32_t o = (uint32_t)(hash64(fid[k]) % S.world);
+    fo[k] = o;
+    fj[k] = atomicAdd(&s_ocnt[o], 1u);
+  }
+  __syncthreads();
+  for (uint32_t r = tid; r < S.world; r += kTT) s_obase[r] = s_ocnt[r] ? atomicAdd(&S.send_cnt[r], s_ocnt[r]) : 0u;
+  __syncthreads();
+  for (uint32_t k = tid; k < nnew; k += kTT) {
+    const uint32_t o = fo[k], j = s_obase[o] + fj[k];
+    if (!RS_IDX_OK(j < S.cap, a.sh.ctr)) continue;
+    reinterpret_cast<uint64_t*>(S.peers[o] + S.off_ids)[(size_t)S.rank * S.cap + j] = fid[k];
+    const uint32_t sp = o * S.cap + j;
+    S.send_pos[fu[k]] = sp;
+    a.urow[fu[k]] = sp;
+    a.use.rec[fslot[k]].row = sp;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(S.done) : "memory");
+    s_last = old == gridDim.x - 1;
+    if (s_last) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  __syncthreads();
+  if (!s_last) return;
+  for (uint32_t r = tid; r < S.world; r += kTT) {
+    *S.cnt_ptrs[r] = S.send_cnt[r];
+    S.trace_ids_sent[r] = S.send_cnt[r];
+  }
+  if (tid == 0) *S.trace_requested = S.n_tokens;
+  __syncthreads();
+  for (uint32_t r = tid; r < S.world; r += kTT) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(S.flag_ptrs[r]), "l"(s_e) : "memory");
+    S.send_cnt[r] = 0;
+  }
+  if (tid == 0) {
+    *S.epoch = s_e;
+    *S.done = 0;
+  }
+}
 
 __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   WarpTrace wt_(a.sh.trace, 0);
@@ -191,10 +221,11 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   __shared__ uint32_t s_nnew, s_base;
   __shared__ unsigned long long s_ins, s_reuse;
   TableDev* td = a.td;
-  const TableDesc d = td->d;
-  const unsigned long long free_n0 = td->c.free_n;
-  const unsigned long long fresh0 = td->c.fresh_next;
-  const uint32_t tick_now = td->c.tick + 1;
+  const bool sending = a.send.peers != nullptr;
+  const TableDesc d = sending ? TableDesc{} : td->d;
+  const unsigned long long free_n0 = sending ? 0ull : td->c.free_n;
+  const unsigned long long fresh0 = sending ? 0ull : td->c.fresh_next;
+  const uint32_t tick_now = sending ? 0u : td->c.tick + 1;
   const uint32_t tid = threadIdx.x;
   if (blockIdx.x == 0 && tid == 0) {  // this step's hot-id / partial counters (KH, KF follow KA)
     a.sh.ctr[0] = 0;
@@ -259,7 +290,7 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     if (fresh) {
       // the probe below starts at this bucket: fetch it into L2 now (overlaps
       // the numbering barriers)
-      if (id != kEmptyKey && id != kTombKey)
+      if (!sending && id != kEmptyKey && id != kTombKey)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(d.slots + ((h >> 32) & d.nb_mask) * kBucket));
       const uint32_t k = atomicAdd(&s_nnew, 1u);
       lnew[p] = k + 1;
@@ -288,6 +319,10 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     if (rank < kPosMax && RS_IDX_OK(gs < a.sh.n_slots, a.sh.ctr)) a.sh.pos[(size_t)gs * kPosMax + rank] = t;
   }
   __syncthreads();
+  if (sending) {  // the claimed ids to their owners (positions by block-local then global counters)
+    fa_send(a, nnew, fid, fslot, fu);
+    return;
+  }
   // the ids this tile claimed: find-or-insert-zero in the table, 8 lanes per id
   const unsigned lane = lane_id();
   const unsigned g = lane & (kBucket - 1);
@@ -406,6 +441,8 @@ struct FcArgs {
   const uint32_t* list;    // null: every unique id; else slots (KA's heavy list) ...
   const uint32_t* list_n;  // ... and their count
   uint32_t c_min, c_max;   // ids with c_min < occurrences <= c_max
+  float* const* peer_dst;  // sharded requester: sums to the owners (rows are send positions)
+  uint32_t cap, rank;
 };
 
 #ifndef RS_FC_MINB
@@ -463,14 +500,15 @@ __global__ void __launch_bounds__(256, MINB) k_fc(FcArgs a, OptArgs o) {
     }
     float4 wv[NV], vv[NV], mv[NV];
     const size_t rbase = (size_t)row * D4 + gl;
+    const bool peer = a.peer_dst != nullptr;  // sharded requester: `row` is the send position
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      wv[j] = rw[rbase + j * G];
-      vv[j] = rv[rbase + j * G];
-      mv[j] = rm ? rm[rbase + j * G] : make_float4(0.f, 0.f, 0.f, 0.f);
+      wv[j] = peer ? make_float4(0.f, 0.f, 0.f, 0.f) : rw[rbase + j * G];
+      vv[j] = peer ? make_float4(0.f, 0.f, 0.f, 0.f) : rv[rbase + j * G];
+      mv[j] = rm && !peer ? rm[rbase + j * G] : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     uint32_t st0 = 0;
-    if (gl == 0) st0 = d.step[row];
+    if (gl == 0 && !peer) st0 = d.step[row];
     if (c > a.c_max || c <= a.c_min) continue;  // another kernel's id (group-uniform)
 #pragma unroll
     for (int j = 0; j < PPT; ++j)
@@ -492,7 +530,7 @@ __global__ void __launch_bounds__(256, MINB) k_fc(FcArgs a, OptArgs o) {
     __syncwarp(gmask);
     // the forward for this id: its pre-update row to each of its tokens
     // (distributed_lookup's inverse expand, exchange_sim.cpp:211-230)
-    if (!(a.exp & 4)) {
+    if (!(a.exp & 4) && !peer) {
       float4* o4 = reinterpret_cast<float4*>(a.out);
       for (uint32_t k = 0; k < c; ++k) {
         const size_t ob = (size_t)order[k] * D4 + gl;
@@ -561,6 +599,13 @@ __global__ void __launch_bounds__(256, MINB) k_fc(FcArgs a, OptArgs o) {
       }
     }
     __syncwarp(gmask);
+    if (peer) {  // the id's sum to its owner's gradient receive buffer (NVLink store)
+      const uint32_t o = row / a.cap, jj = row - o * a.cap;
+      float4* dst = reinterpret_cast<float4*>(a.peer_dst[o] + ((size_t)a.rank * a.cap + jj) * d.dim);
+#pragma unroll
+      for (int j = 0; j < NV; ++j) dst[gl + j * G] = acc[j];
+      continue;
+    }
     uint32_t st = 0;
     if (gl == 0) {
       st = st0 + 1;
@@ -616,6 +661,7 @@ struct FhArgs {
   int32_t* inverse;
   double* tokcs;
   uint32_t exp;  // timing experiments (RS_FH_EXP bits, wrong results): 1 no forward stores, 2 no gradient sums
+  // out == nullptr: no forward (sharded requester: the rows come from the owners)
 };
 
 
@@ -804,12 +850,12 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
 #pragma unroll
     for (uint32_t k = 0; k < kRowStage; ++k) {
       const uint32_t gg = warp + k * NW;
-      if (gg < ng && grow[gg] != kNoRow) load_vec<VEC, CH>(a.emb + (size_t)grow[gg] * D, D, wr[k], false);
+      if (a.out && gg < ng && grow[gg] != kNoRow) load_vec<VEC, CH>(a.emb + (size_t)grow[gg] * D, D, wr[k], false);
     }
 #pragma unroll
     for (uint32_t k = 0; k < kRowStage; ++k) {
       const uint32_t gg = warp + k * NW;
-      if (gg < ng && grow[gg] != kNoRow) store_vec<VEC, CH>(srow + (size_t)gg * D, D, wr[k]);
+      if (a.out && gg < ng && grow[gg] != kNoRow) store_vec<VEC, CH>(srow + (size_t)gg * D, D, wr[k]);
     }
   }
   __syncthreads();
@@ -819,7 +865,7 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
   float w[CH][VEC], acc[CH][VEC];
   zero_acc<VEC, CH>(acc);
   auto row_of = [&](uint32_t gg, float (&r)[CH][VEC]) {
-    if (grow[gg] == kNoRow) return;
+    if (!a.out || grow[gg] == kNoRow) return;
     if (gg < kRowStage * NW)
       load_vec<VEC, CH>(srow + (size_t)gg * D, D, r, false);
     else
@@ -857,7 +903,7 @@ __global__ void __launch_bounds__(kTT, 4) k_fh(FhArgs a) {
         row_of(g, w);
       }
       if (!(a.exp & 2)) add_acc<VEC, CH>(acc, x[q]);
-      if (grow[g] != kNoRow && !(a.exp & 1)) store_vec<VEC, CH>(a.out + (size_t)(t0 + csr[i]) * D, D, w);
+      if (a.out && grow[g] != kNoRow && !(a.exp & 1)) store_vec<VEC, CH>(a.out + (size_t)(t0 + csr[i]) * D, D, w);
     }
   }
   if (gb < ge && !(a.exp & 8)) finish_group(g);
@@ -872,6 +918,8 @@ struct FfArgs {
   TableDev* td;
   FSet use;
   FShared sh;
+  float* const* peer_dst;  // sharded requester: the sums to the owners (rows are send positions)
+  uint32_t cap, rank;
 };
 
 template <int VEC, int CH, int NWF>
@@ -890,7 +938,7 @@ __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
     if (!RS_IDX_OK(h < a.sh.max_hot, a.sh.ctr)) break;
     const uint32_t gs = a.sh.hot_slot[h];
     uint32_t* hl = a.sh.hlist + (size_t)h * NT;
-    if (warp == NWF - 1) {  // the row's optimizer state: into L2 while the partials are summed
+    if (warp == NWF - 1 && !a.peer_dst) {  // the row's optimizer state: into L2 while the partials are summed
       const uint32_t row = __ldcg(&a.use.rec[gs].row);
       if (row != kNoRow && lane * 32u < D * 4u) {
         const char* w = reinterpret_cast<const char*>(d.emb + (size_t)row * D) + lane * 32;
@@ -949,7 +997,12 @@ __global__ void __launch_bounds__(NWF * 32) k_fhf(FfArgs a, OptArgs o) {
         add_acc<VEC, CH>(tot, x);
       }
       const uint32_t row = __ldcg(&a.use.rec[gs].row);
-      apply_row<VEC, CH>(d, row, tot, o);
+      if (a.peer_dst) {  // the id's sum to its owner's gradient receive buffer (NVLink store)
+        const uint32_t ow = row / a.cap, jj = row - ow * a.cap;
+        store_vec<VEC, CH>(a.peer_dst[ow] + ((size_t)a.rank * a.cap + jj) * D, D, tot);
+      } else {
+        apply_row<VEC, CH>(d, row, tot, o);
+      }
       if (lane == 0) a.sh.hidx[gs] = kHotNone;
     }
     __syncthreads();
@@ -968,9 +1021,10 @@ Shape shape_of(uint32_t D) {
 }  // namespace
 
 // ---- host side ---------------------------------------------------------------
-bool fast_step_supported(const rs_table* t) {
-  const uint32_t D = t->desc.dim;
-  if (t->cfg.max_keys || D % 4) return false;
+bool fast_step_supported(const rs_table* t) { return !t->cfg.max_keys && fast_dim_supported(t->desc.dim); }
+
+bool fast_dim_supported(uint32_t D) {
+  if (D % 4) return false;
   const Shape sh = shape_of(D);
   const uint32_t D4 = D / 4;
   const bool g_ok = D4 == 4 || D4 == 8 || D4 == 16 || D4 == 32 || D4 == 64;
@@ -980,7 +1034,7 @@ bool fast_step_supported(const rs_table* t) {
 
 static cudaError_t fast_trace_reset(rs_workspace* ws) {
   // [kernel][block] = {start = ~0, end = 0}
-  std::vector<unsigned long long> h(8 * kTraceBlocks * 2);
+  std::vector<unsigned long long> h(kTraceSlots * kTraceBlocks * 2);
   for (size_t i = 0; i < h.size(); i += 2) {
     h[i] = ~0ull;
     h[i + 1] = 0;
@@ -1017,7 +1071,7 @@ static int fast_alloc(rs_workspace* ws) {
   RS_CUDA(cudaMemset(f.hlist, 0, f.max_hot * f.ntiles * 4));
   RS_CUDA(cudaMemset(f.ctr, 0, 64));
   if (getenv("RS_TRACE") && getenv("RS_TRACE")[0] == '1') {
-    RS_CUDA(cudaMalloc(&f.trace, 8 * kTraceBlocks * 2 * sizeof(unsigned long long)));
+    RS_CUDA(cudaMalloc(&f.trace, kTraceSlots * kTraceBlocks * 2 * sizeof(unsigned long long)));
     RS_CUDA(fast_trace_reset(ws));
   }
   {  // the hot branch (KH -> KF) at the highest priority: KF's blocks go ahead of the CSR kernel's pending ones
@@ -1104,13 +1158,22 @@ static FShared fshared(rs_workspace* ws) {
   return s;
 }
 
-// Enqueue-only (capturable).  ev != null: eager profiling -- the kernels run
-// one after another with events ev[0..4] around KA, KG, KD, KH+KF.
-int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
-                 float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,
-                 TableCounters* mirror_out) {
-  const OptArgs& o = *static_cast<const OptArgs*>(opt);
-  const uint32_t D = t->desc.dim;
+// The fast step's launches.  Single GPU: t = the table, both halves.  The
+// sharded requester (dist.cu) calls the halves separately: KA with `send`
+// (ids to their owners, no table), then the reduce with `peer` (sums to the
+// owners' gradient buffers instead of the optimizer, no forward: the rows
+// come from the owners), `td` = the receive-buffer view (only its dim and
+// row bound are read).  Enqueue-only (capturable).  ev != null: eager
+// profiling -- the kernels run one after another with events ev[0..4]
+// around KA, KG, KD, KH+KF.
+struct FastPeer {
+  float* const* peer_dst;
+  uint32_t cap, rank;
+};
+static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_t D, const uint64_t* d_ids,
+                       uint64_t n, const float* d_grads, float* d_out, const OptArgs& o, int use, cudaStream_t s,
+                       cudaEvent_t* ev, bool fork, TableCounters* mirror_out, const rs_dist_send* send,
+                       const FastPeer* peer, bool do_ka, bool do_reduce) {
   const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
   const FShared sh = fshared(ws);
   if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
@@ -1121,13 +1184,17 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   fa.use = fset(ws, use);
   fa.clean = fset(ws, use ^ 1);
   fa.sh = sh;
-  fa.td = t->dev;
+  fa.td = td;
   fa.slot_of = ws->slot_of;
   fa.unique = ws->unique;
   fa.urow = ws->urow;
   fa.urow64 = ws->urow64;
-  k_fa<<<ntiles, kTT, 0, s>>>(fa);
-  RS_LAUNCH_CHECK("k_fa");
+  if (send) fa.send = *send;
+  if (do_ka) {
+    k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);  // an idle sharded rank still publishes its (empty) send
+    RS_LAUNCH_CHECK("k_fa");
+  }
+  if (!do_reduce) return RS_OK;
   if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
   rs_fast& f = ws->fast;
   cudaStream_t sd = s, sh2 = s, sd3 = s;
@@ -1150,16 +1217,19 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     h.n = (uint32_t)n;
     h.grads = d_grads;
     h.dim = D;
-    h.emb = t->desc.emb;
-    h.out = d_out;
+    h.emb = emb;
+    h.out = peer ? nullptr : d_out;
     h.inverse = ws->inverse;
-    h.tokcs = ws->csum_dst ? f.tokcs : nullptr;
+    h.tokcs = ws->csum_dst && !peer ? f.tokcs : nullptr;
     static const uint32_t hexp = getenv("RS_FH_EXP") ? (uint32_t)atoi(getenv("RS_FH_EXP")) : 0u;
     h.exp = hexp;
     FfArgs ff;
-    ff.td = t->dev;
+    ff.td = td;
     ff.use = fa.use;
     ff.sh = sh;
+    ff.peer_dst = peer ? peer->peer_dst : nullptr;
+    ff.cap = peer ? peer->cap : 0u;
+    ff.rank = peer ? peer->rank : 0u;
     // hot finish: a block of kf_warps warps per hot id (small blocks fit beside the CSR kernel's)
     static const int kfw = getenv("RS_KF_WARPS") ? atoi(getenv("RS_KF_WARPS")) : 8;
     const int nwf = kfw == 4 || kfw == 16 ? kfw : 8;
@@ -1193,17 +1263,20 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   // (light_max < c <= hot_min: 16 lanes, 64 positions), on two streams
   auto csr = [&](cudaStream_t ql, cudaStream_t qh) -> int {
     FcArgs c;
-    c.td = t->dev;
+    c.td = td;
     c.use = fa.use;
+    c.peer_dst = peer ? peer->peer_dst : nullptr;
+    c.cap = peer ? peer->cap : 0u;
+    c.rank = peer ? peer->rank : 0u;
     c.sh = sh;
     c.grads = d_grads;
     c.n_tokens = (uint32_t)n;
     c.urow = ws->urow;
     static const uint32_t fexp = getenv("RS_FC_EXP") ? (uint32_t)atoi(getenv("RS_FC_EXP")) : 0u;
     c.exp = fexp;
-    c.out = d_out;
+    c.out = peer ? nullptr : d_out;
     c.inverse = ws->inverse;
-    c.tokcs = ws->csum_dst ? f.tokcs : nullptr;
+    c.tokcs = ws->csum_dst && !peer ? f.tokcs : nullptr;
     const uint32_t D4 = D / 4;
     static const unsigned cap_blocks = getenv("RS_FC_GRID") ? (unsigned)atoi(getenv("RS_FC_GRID")) : 148u * 16u;
     // heavy (first: its ids start at once on their stream)
@@ -1243,7 +1316,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     return RS_OK;
   };
   auto checksum = [&](cudaStream_t q) -> int {
-    if (!ws->csum_dst) return RS_OK;
+    if (!ws->csum_dst || peer) return RS_OK;
     k_fcs<<<ntiles, kTT, 0, q>>>(f.tokcs, (uint32_t)n, ws->csum_dst, ws->csum_part, ws->csum_ticket);
     RS_LAUNCH_CHECK("k_fcs");
     return RS_OK;
@@ -1251,7 +1324,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   int st;
   if (ev) {  // eager, serial: KA (+ clean) | KD | KH + KF | KS
     k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
-                                                            t->dev, mirror_out);
+                                                            td, mirror_out);
     RS_LAUNCH_CHECK("k_fclean");
     if ((st = csr(s, s))) return st;
     RS_CUDA(cudaEventRecord(ev[2], s));
@@ -1266,7 +1339,7 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   if (skip != 1 && (st = hot(sh2))) return st;
   if (skip != 2 && (st = csr(sd, sd3))) return st;
   k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
-                                                            t->dev, mirror_out);
+                                                            td, mirror_out);
   RS_LAUNCH_CHECK("k_fclean");
   if (sd != s) {
     RS_CUDA(cudaEventRecord(f.ev_j1, sd));
@@ -1279,6 +1352,155 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
   return checksum(s);
 }
 
+int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
+                 float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,
+                 TableCounters* mirror_out) {
+  return fast_launch(ws, t->dev, t->desc.emb, t->desc.dim, d_ids, n, d_grads, d_out,
+                     *static_cast<const OptArgs*>(opt), use, s, ev, fork, mirror_out, nullptr, nullptr, true, true);
+}
+
+// ---- the sharded requester on the fast kernels (dist.cu) ----------------------
+int fast_dist_front(rs_workspace* ws, uint32_t D, const uint64_t* d_ids, uint64_t n, int use, cudaStream_t s,
+                    const rs_dist_send& send) {
+  OptArgs o{};
+  return fast_launch(ws, nullptr, nullptr, D, d_ids, n, nullptr, nullptr, o, use, s, nullptr, false, nullptr,
+                     &send, nullptr, true, false);
+}
+
+int fast_dist_reduce(rs_workspace* ws, TableDev* view, uint32_t D, uint64_t n, const float* d_grads, int use,
+                     cudaStream_t s, bool fork, float* const* peer_dst, uint32_t cap, uint32_t rank) {
+  OptArgs o{};
+  FastPeer p{peer_dst, cap, rank};
+  return fast_launch(ws, view, nullptr, D, nullptr, n, d_grads, nullptr, o, use, s, nullptr, fork, nullptr,
+                     nullptr, &p, false, true);
+}
+
+// The requester's forward: every token's row from the owners' answers in the
+// receive buffer (row = its id's send position), after the emb flags.
+struct FgdArgs {
+  const TableDev* view;
+  FSet use;
+  FShared sh;
+  const uint32_t* slot_of;
+  uint32_t n;
+  int32_t* inverse;
+  float* out;
+  double* csum_out;
+  double* csum_part;
+  unsigned int* csum_ticket;
+  rs_dist_sync sync;
+  unsigned long long* trace;
+};
+
+template <int LPR>
+__global__ void __launch_bounds__(kTT, 4) k_fgd(FgdArgs a) {
+  WarpTrace wt_(a.trace, 6);
+  dist_wait(a.sync);  // the owners' rows landed
+  const uint32_t tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  constexpr uint32_t NW = kTT / 32;
+  const uint32_t D4 = a.view->d.dim >> 2;
+  const float4* __restrict__ emb = reinterpret_cast<const float4*>(a.view->d.emb);
+  float4* __restrict__ o4 = reinterpret_cast<float4*>(a.out);
+  constexpr int RPI = 32 / LPR;
+  constexpr int ITERS = 32 / RPI;
+  constexpr int BATCH = ITERS < 4 ? ITERS : 4;  // 64 registers: co-resident with the owner kernels
+  const uint32_t sub = lane / LPR, l = lane % LPR;
+  const bool csum = a.csum_out != nullptr;
+  double cs = 0.0;
+  const uint32_t ntiles = (a.n + kTT - 1) / kTT;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {  // grid <= ntiles: persistent blocks
+    const uint32_t t0 = tile * kTT;
+    const uint32_t rows = min(kTT, a.n - t0);
+    uint32_t r = 0;
+    if (tid < rows) {
+      const uint32_t sl = __ldg(a.slot_of + t0 + tid);
+      r = __ldcg(&a.use.rec[sl].row);
+      a.inverse[t0 + tid] = (int32_t)__ldcg(a.sh.uidx + sl);
+    }
+    const uint32_t wb = warp * 32;
+    const uint32_t cnt = rows > wb ? min(32u, rows - wb) : 0u;
+#pragma unroll
+    for (int b0 = 0; b0 < ITERS; b0 += BATCH) {
+      uint32_t rr[BATCH];
+#pragma unroll
+      for (int k = 0; k < BATCH; ++k) rr[k] = __shfl_sync(kFull, r, (b0 + k) * RPI + sub);
+      for (uint32_t jj = 0; jj < D4; jj += LPR) {
+        const uint32_t j = jj + l;
+        float4 v[BATCH];
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+          const uint32_t tok = (b0 + k) * RPI + sub;
+          if (tok < cnt && j < D4) v[k] = __ldcg(emb + (size_t)rr[k] * D4 + j);  // written by peers this step
+        }
+#pragma unroll
+        for (int k = 0; k < BATCH; ++k) {
+          const uint32_t tok = (b0 + k) * RPI + sub;
+          if (tok < cnt && j < D4) {
+            __stcs(o4 + (size_t)(t0 + wb + tok) * D4 + j, v[k]);
+            if (csum) cs += ((double)v[k].x + (double)v[k].y) + ((double)v[k].z + (double)v[k].w);
+          }
+        }
+      }
+    }
+  }
+  if (csum) {  // fixed reduction tree, then the block partials in block order
+    __shared__ double s_cs[NW];
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) cs += __shfl_xor_sync(kFull, cs, o2);
+    if (lane == 0) s_cs[warp] = cs;
+    __syncthreads();
+    if (warp == 0) {
+      double x = lane < NW ? s_cs[lane] : 0.0;
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) x += __shfl_xor_sync(kFull, x, o2);
+      unsigned last = 0;
+      if (lane == 0) {
+        a.csum_part[blockIdx.x] = x;
+        __threadfence();
+        last = atomicAdd(a.csum_ticket, 1u) == gridDim.x - 1;
+      }
+      if (__shfl_sync(kFull, last, 0)) {
+        __threadfence();
+        double y = 0.0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) y += __ldcg(a.csum_part + b);
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) y += __shfl_xor_sync(kFull, y, o2);
+        if (lane == 0) {
+          *a.csum_out = y;
+          *a.csum_ticket = 0;
+        }
+      }
+    }
+  }
+}
+
+int fast_dist_gather(rs_workspace* ws, const TableDev* view, uint32_t D, uint64_t n, float* d_out, int use,
+                     cudaStream_t s, const rs_dist_sync& sync, double* csum, uint32_t grid) {
+  if (n == 0) return RS_OK;
+  FgdArgs g;
+  g.view = view;
+  g.use = fset(ws, use);
+  g.sh = fshared(ws);
+  g.slot_of = ws->slot_of;
+  g.n = (uint32_t)n;
+  g.inverse = ws->inverse;
+  g.out = d_out;
+  g.csum_out = csum;
+  g.csum_part = ws->csum_part;
+  g.csum_ticket = ws->csum_ticket;
+  g.sync = sync;
+  g.trace = ws->fast.trace;
+  const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
+  const uint32_t nb = grid ? std::min(grid, ntiles) : ntiles;
+  const uint32_t D4 = D / 4;
+  if (D4 >= 32) k_fgd<32><<<nb, kTT, 0, s>>>(g);
+  else if (D4 >= 16) k_fgd<16><<<nb, kTT, 0, s>>>(g);
+  else if (D4 >= 8) k_fgd<8><<<nb, kTT, 0, s>>>(g);
+  else k_fgd<4><<<nb, kTT, 0, s>>>(g);
+  RS_LAUNCH_CHECK("k_fgd");
+  return RS_OK;
+}
+
 }  // namespace rs
 
 extern "C" int rs_workspace_trace(rs_workspace* ws, uint64_t* out, uint64_t cap, uint64_t* n_out) {
@@ -1286,7 +1508,7 @@ extern "C" int rs_workspace_trace(rs_workspace* ws, uint64_t* out, uint64_t cap,
   if (!ws || !n_out) return fail(RS_ERR_CONFIG, "rs_workspace_trace: null argument");
   *n_out = 0;
   if (!ws->fast.trace) return RS_OK;  // RS_TRACE=1 at the first rs_step enables it
-  const uint64_t n = 8ull * kTraceBlocks * 2;
+  const uint64_t n = (uint64_t)kTraceSlots * kTraceBlocks * 2;
   *n_out = n;
   if (!out) return RS_OK;
   if (cap < n) return fail(RS_ERR_CONFIG, "rs_workspace_trace: buffer too small");

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -518,6 +519,19 @@ int table_prepare(rs_table* t, uint64_t n, cudaStream_t s) {
   auto rows_ub = [&]() { return t->exact_rows + (t->requested_total - t->exact_requested); };
   bool slots_ok = (double)(occ_ub() + t->exact_tomb + n) <= lf * (double)t->capacity;
   bool rows_ok = rows_ub() + n <= t->desc.row_cap;
+  if ((!slots_ok || !rows_ok) && t->exact_requested < t->requested_total) {
+    // the bound includes steps still in flight: wait for the newest committed
+    // mirror (the last op's completion -- work queued after it keeps the
+    // device busy) before draining the stream for an exact read
+    rs_mirror& m = t->mirror[t->mirror_next ^ 1];
+    if (m.valid && m.requested_at_copy > t->exact_requested) {
+      RS_CUDA(cudaEventSynchronize(m.ev));
+      t->host_syncs++;
+      refresh_from_mirror(t);
+      slots_ok = (double)(occ_ub() + t->exact_tomb + n) <= lf * (double)t->capacity;
+      rows_ok = rows_ub() + n <= t->desc.row_cap;
+    }
+  }
   if (!slots_ok || !rows_ok) {
     TableCounters c;
     int st = read_counters(t, &c, s);

@@ -36,14 +36,14 @@ def main():
     for k in range(8):
         flush.zero_()
         torch.cuda.synchronize()
-        buf = np.zeros(8 * 4096 * 2, np.uint64)
+        buf = np.zeros(16 * 4096 * 2, np.uint64)
         P._lib.check(lib.rs_workspace_trace(step.ws.handle, buf.ctypes.data, buf.size, ctypes.byref(n)), "trace")
         step.step(*dev[k % 2])
         torch.cuda.synchronize()
         P._lib.check(lib.rs_workspace_trace(step.ws.handle, buf.ctypes.data, buf.size, ctypes.byref(n)), "trace")
         if k < 4:
             continue
-        t = buf.reshape(8, 4096, 2).astype(np.float64)
+        t = buf.reshape(16, 4096, 2).astype(np.float64)
         t0 = t[0, :, 0][t[0, :, 1] > 0].min()
         row = {}
         for i, name in enumerate(NAMES):
