@@ -43,6 +43,7 @@ namespace {
 
 using namespace tdev;
 using namespace sdev;
+using namespace odev;
 
 constexpr int kMaxWorld = 64;
 
@@ -143,166 +144,285 @@ __global__ void k_wait(CommDev c, int phase) {
   if (r < c.world) spin_flag(flag_of(hdr_of(c, c.rank), phase, r), e, c.trace + kTrError);
 }
 
-// Owner KA': stage-2 dedup straight from the receive lists.  A requester
-// sends each id at most once, so an owner-unique id has at most W origins:
-// every received position (src, j) claims the id's scratch slot and appends
-// its origin src*cap + j to the slot's origin row origins[slot*W .. +W)
-// (atomic order; the finish kernel sorts them into (source, position)
-// order, the stage-2 origin order of exchange_sim.cpp:100-115).
-// grid (ceil(cap / 256), W): block (x, src) takes positions x*256.. of src.
-__global__ void __launch_bounds__(256) k_own_dedup(CommDev c, SetDev S, uint32_t* __restrict__ origins,
-                                                   uint64_t* __restrict__ unique) {
-  WarpTrace wt_(c.tl, 9);
-  const ArenaHdr* h = hdr_of(c, c.rank);
-  const uint32_t src = blockIdx.y;
-  if (threadIdx.x == 0) spin_flag(&h->sig_ids[src], *c.epoch, c.trace + kTrError);  // src's ids landed
-  __syncthreads();
-  const uint32_t cnt = h->cnt_in[src];  // ordered after the acquire by the barrier
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.x * blockDim.x >= cnt) return;  // block-uniform
-  const bool v = j < cnt;
-  bool fresh = false;
-  uint64_t id = 0, gs = 0;
-  if (v) {
-    id = reinterpret_cast<const uint64_t*>(c.peers[c.rank] + c.off_ids)[(size_t)src * c.cap + j];
-    gs = scratch_insert(S, id, hash64(id), &fresh);
-    const uint32_t k = atomicAdd(&S.sntile[gs], 1u);  // origins so far (<= W)
-    origins[gs * c.world + k] = src * c.cap + j;
-  }
-  // unique numbering of the fresh ids: one atomic per block
-  __shared__ uint32_t s_w[32], s_base;
-  const unsigned fm = __ballot_sync(0xFFFFFFFFu, fresh);
-  const uint32_t warp = threadIdx.x >> 5;
-  if (lane_id() == 0) s_w[warp] = __popc(fm);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
-      const uint32_t x = s_w[w];
-      s_w[w] = run;
-      run += x;
-    }
-    s_base = run ? atomicAdd(S.cnt, run) : 0u;
-  }
-  __syncthreads();
-  const uint32_t base = s_base + s_w[warp];
-  if (fresh) {
-    const uint32_t u = base + __popc(fm & lanemask_lt());
-    S.u_slot[u] = (uint32_t)gs;
-    unique[u] = id;
-  }
-}
-
-// Owner KB': per owner-unique id (8-lane group) find-or-insert on the shard,
-// then the "embedding all-to-all": the row is stored straight into the
-// emb_in of every requester that asked for it (one 128-bit store per lane per
-// step over NVLink).  Also the finish metadata (CSR = the slot's origin row),
-// cleaning of the other scratch set, the table epilogue and the flags.
+// Owner lookup: one pass over the received positions (src, j) of every
+// source, 8 lanes per position: find-or-insert of the id on the shard
+// (concurrent inserts of one id from several sources resolve in the table's
+// slot CAS), the position appended to the row's origin list -- row-indexed
+// scratch: row_cnt[row] origins so far, row_orig[row * W + k] = src * cap + j
+// (the stage-2 dedup of exchange_sim.cpp:100-115, keyed by row instead of a
+// second hash set), the row's first origin appends it to the touched list --
+// and the row stored straight into the requester's emb_in (the embedding
+// "all-to-all", one 128-bit NVLink store per lane per chunk).  Then the
+// table epilogue and the rows flags.
 #ifndef RS_OWN_MINB
-#define RS_OWN_MINB 5  // 48 registers: the id-carrying blocks of k_own_table fit in one wave
+#define RS_OWN_MINB 5  // 48 registers: the blocks carrying positions fit in one wave
 #endif
-struct OwnTableArgs {
+struct OwnLookupArgs {
   TableDev* td;
-  SetDev use, clean;
-  const uint32_t* origins;
-  const uint64_t* unique;
-  uint32_t* urow;
-  uint32_t* u_cnt;
-  uint32_t* u_poff;
-  uint32_t* u_ntile;
-  uint32_t* u_ticket;
+  uint32_t* row_cnt;          // [rows] origins of each row in this op (zero between ops)
+  uint32_t* row_orig;         // [rows * W] origin positions src * cap + j
+  uint32_t* touched;          // [W * cap] rows with an origin in this op
+  uint32_t* touched_cnt;      // their count (this op's parity)
+  uint32_t* touched_clr;      // the other parity's count, zeroed here
   TableCounters* mirror_out;  // host's pinned counter mirror (mapped), or null
 };
 
-__global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_table(CommDev c, OwnTableArgs a) {
+__global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_lookup(CommDev c, OwnLookupArgs a) {
   WarpTrace wt_(c.tl, 10);
   TableDev* td = a.td;
   const TableDesc d = td->d;
   const unsigned long long free_n0 = td->c.free_n;
   const unsigned long long fresh0 = td->c.fresh_next;
   const uint32_t tick_now = td->c.tick + 1;
-  clean_set(a.clean, blockIdx.x * (uint64_t)blockDim.x + threadIdx.x,
-            (uint64_t)gridDim.x * blockDim.x);
-  const uint32_t nu = *a.use.cnt;
-  const unsigned lane = lane_id();
-  const unsigned g = lane & (kBucket - 1);
-  const unsigned gbase = lane & ~(kBucket - 1);
-  const unsigned gmask = 0xFFu << gbase;
-  const uint32_t D4 = d.dim >> 2;
+  const ArenaHdr* h = hdr_of(c, c.rank);
+  __shared__ uint32_t s_off[kMaxWorld + 1];
+  __shared__ uint32_t s_w[8], s_base;
   __shared__ unsigned long long s_ins, s_reuse;
+  // every source's ids landed (k_wait passed: one cheap check per block)
+  if (threadIdx.x < c.world) spin_flag(&h->sig_ids[threadIdx.x], *c.epoch, c.trace + kTrError);
   if (threadIdx.x == 0) {
     s_ins = 0;
     s_reuse = 0;
   }
   __syncthreads();
-  constexpr unsigned kGroupsPB = 32;
-  for (uint32_t i = blockIdx.x * kGroupsPB + (threadIdx.x >> 3); i < nu; i += gridDim.x * kGroupsPB) {
-    const uint64_t key = a.unique[i];
-    const uint32_t slot = a.use.u_slot[i];
-    const uint32_t cnt = a.use.sntile[slot];
-    const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0,
-                                              fresh0, &s_ins, &s_reuse);
-    if (g == 0) {
-      a.urow[i] = row;
-      a.u_cnt[i] = cnt;
-      a.u_poff[i] = slot * c.world;
-      a.u_ntile[i] = 0;  // CSR path of the finish kernel
-      a.u_ticket[i] = 0;
+  if (threadIdx.x == 0) {  // the sources' position ranges in one flat index space
+    uint32_t run = 0;
+    for (uint32_t r = 0; r < c.world; ++r) {
+      s_off[r] = run;
+      run += min(*reinterpret_cast<const volatile uint32_t*>(&h->cnt_in[r]), c.cap);
     }
-    if (row == kNoRow) continue;  // table error (reported through the counters)
-    if (c.diag & 2) continue;
-    const float4* e = reinterpret_cast<const float4*>(d.emb) + (size_t)row * D4;
-    // the group's origins (<= world) in one parallel load, then each lane's
-    // part of the row (held in registers) goes to every requester
-    const uint32_t my_origin = g < cnt ? __ldg(a.origins + (size_t)slot * c.world + g) : 0u;
-    if (D4 <= 4 * kBucket) {
-      float4 v[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (g + j * kBucket < D4) v[j] = __ldg(e + g + j * kBucket);
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const uint32_t origin = k < kBucket ? __shfl_sync(gmask, my_origin, k, kBucket)
-                                            : __ldg(a.origins + (size_t)slot * c.world + k);
-        const uint32_t src = (c.diag & 1) ? c.rank : origin / c.cap, jj = origin - (origin / c.cap) * c.cap;
-        float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
-                      ((size_t)c.rank * c.cap + jj) * D4;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (g + j * kBucket < D4) dst[g + j * kBucket] = v[j];
-      }
-    } else {
-      for (uint32_t k = 0; k < cnt; ++k) {
-        const uint32_t origin = __ldg(a.origins + (size_t)slot * c.world + k);
-        const uint32_t src = origin / c.cap, jj = origin - src * c.cap;
-        float4* dst = reinterpret_cast<float4*>(c.peers[src] + c.off_emb) +
-                      ((size_t)c.rank * c.cap + jj) * D4;
-        for (uint32_t q = g; q < D4; q += kBucket) dst[q] = __ldg(e + q);
-      }
-    }
+    s_off[c.world] = run;
+    if (blockIdx.x == 0) *a.touched_clr = 0;  // the previous op's list is consumed
   }
   __syncthreads();
+  const uint32_t total = s_off[c.world];
+  const unsigned lane = lane_id();
+  const unsigned warp = threadIdx.x >> 5;
+  const unsigned g = lane & (kBucket - 1);
+  const unsigned gbase = lane & ~(kBucket - 1);
+  const unsigned gmask = 0xFFu << gbase;
+  const uint32_t D4 = d.dim >> 2;
+  const uint64_t* ids = reinterpret_cast<const uint64_t*>(c.peers[c.rank] + c.off_ids);
+  constexpr unsigned kGroupsPB = 256 / kBucket;
+  for (uint32_t base = blockIdx.x * kGroupsPB; base < total; base += gridDim.x * kGroupsPB) {
+    const uint32_t i = base + (threadIdx.x >> 3);
+    const bool valid = i < total;  // group-uniform
+    uint32_t src = 0, j = 0, row = kNoRow;
+    if (valid) {
+      while (src + 1 < c.world && s_off[src + 1] <= i) ++src;
+      j = i - s_off[src];
+      const uint64_t key = ids[(size_t)src * c.cap + j];
+      row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins, &s_reuse);
+    }
+    bool first = false;
+    if (valid && row != kNoRow && g == 0) {
+      const uint32_t k = atomicAdd(a.row_cnt + row, 1u);
+      if (k < c.world) a.row_orig[(size_t)row * c.world + k] = src * c.cap + j;
+      else c.trace[kTrError] = 2;  // a source sent an id twice
+      first = k == 0;
+    }
+    // each row's first origin appends it to the touched list (one atomic per block)
+    const unsigned fm = __ballot_sync(kFull, first);
+    if (lane == 0) s_w[warp] = __popc(fm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t run = 0;
+      for (uint32_t w = 0; w < 8; ++w) {
+        const uint32_t x = s_w[w];
+        s_w[w] = run;
+        run += x;
+      }
+      s_base = run ? atomicAdd(a.touched_cnt, run) : 0u;
+    }
+    __syncthreads();
+    if (first) a.touched[s_base + s_w[warp] + __popc(fm & lanemask_lt())] = row;
+    // the row to the requester that asked for it
+    if (valid && row != kNoRow && !(c.diag & 2)) {
+      const float4* e = reinterpret_cast<const float4*>(d.emb) + (size_t)row * D4;
+      const uint32_t dsrc = (c.diag & 1) ? c.rank : src;
+      float4* dst = reinterpret_cast<float4*>(c.peers[dsrc] + c.off_emb) + ((size_t)c.rank * c.cap + j) * D4;
+      for (uint32_t q = g; q < D4; q += kBucket) dst[q] = __ldg(e + q);
+    }
+    __syncthreads();  // s_w / s_base of the next round
+  }
   if (threadIdx.x == 0) {
     if (s_ins) atomicAdd(&td->c.inserted, s_ins);
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
   launch_epilogue(td, free_n0, fresh0, true, tick_now, a.mirror_out);
-  if (blockIdx.x == 0) {  // every source's flag was observed by k_own_dedup
-    const ArenaHdr* h = hdr_of(c, c.rank);
-    uint64_t tot = 0;
+  if (blockIdx.x == 0) {  // every source's flag was observed above
     for (uint32_t r = threadIdx.x; r < c.world; r += blockDim.x) c.trace[kTrEmbsSent + r] = h->cnt_in[r];
-    if (threadIdx.x == 0) {
-      for (uint32_t r = 0; r < c.world; ++r) tot += h->cnt_in[r];
-      c.trace[kTrReceived] = tot;  // two-stage: one vector back per received id
-      c.trace[kTrLookups] = nu;
-    }
+    if (threadIdx.x == 0) c.trace[kTrReceived] = total;  // two-stage: one vector back per received id
   }
   if (last_block_signal(c, 1, c.done + 1)) {
     raise_flags(c, 1, c.done + 1, *c.epoch);
-    if (threadIdx.x == 0) *a.clean.cnt = 0;  // every block cleaned: the cleaned set starts empty
+    if (threadIdx.x == 0) c.trace[kTrLookups] = *reinterpret_cast<volatile uint32_t*>(a.touched_cnt);
   }
 }
 
-// Raise flag `phase` at every peer (after the kernels that stored the data).
+// Owner update: per touched row (G lanes, NV float4 chunks each), its <= W
+// origins ranked into (source, position) order -- the stage-2 origin order
+// of exchange_sim.cpp:100-115 -- the requesters' sums at those positions of
+// grad_in added in that order, then the optimizer on the row
+// (sparse_update.cpp:49-75 arithmetic, opt_dev.cuh).  Resets row_cnt.
+struct OwnUpdateArgs {
+  TableDev* td;
+  uint32_t* row_cnt;
+  const uint32_t* row_orig;
+  const uint32_t* touched;
+  const uint32_t* touched_cnt;
+  const float* grad_in;  // [W * cap x D] the requesters' per-id sums (this op's parity)
+};
+
+template <int G, int NV>
+__global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, OwnUpdateArgs a, OptArgs o) {
+  WarpTrace wt_(c.tl, 14);
+  constexpr int PPT = (kMaxWorld + G - 1) / G;  // origin positions held per lane
+  __shared__ uint32_t order_s[(256 / G) * kMaxWorld];
+  const TableDesc d = a.td->d;
+  const uint32_t D4 = d.dim >> 2;
+  const uint32_t W = c.world;
+  const uint32_t lane = lane_id();
+  const uint32_t gl = lane & (G - 1);
+  const unsigned gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (lane & ~(G - 1));
+  uint32_t* order = order_s + (threadIdx.x / G) * kMaxWorld;
+  const uint32_t gid = blockIdx.x * (256 / G) + threadIdx.x / G;
+  const uint32_t ngroups = gridDim.x * (256 / G);
+  const uint32_t nu = *reinterpret_cast<const volatile uint32_t*>(a.touched_cnt);
+  const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grad_in);
+  float4* rw = reinterpret_cast<float4*>(d.emb);
+  float4* rv = reinterpret_cast<float4*>(d.s2);
+  float4* rm = reinterpret_cast<float4*>(d.s1);
+  for (uint32_t u = gid; u < nu; u += ngroups) {
+    const uint32_t row = __ldcg(a.touched + u);
+    // the origin count, the origin positions (speculatively, all W) and the
+    // row's state in one round trip
+    const uint32_t cnt = __ldcg(a.row_cnt + row);
+    uint32_t p[PPT], r[PPT];
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq) {
+      const uint32_t k = gl + jq * G;
+      p[jq] = k < W ? __ldcg(a.row_orig + (size_t)row * W + k) : kFull;
+      r[jq] = 0;
+    }
+    const size_t rbase = (size_t)row * D4;
+    float4 wv[NV], vv[NV], mv[NV];
+#pragma unroll
+    for (int jv = 0; jv < NV; ++jv) {
+      const uint32_t q = gl + jv * G;
+      wv[jv] = vv[jv] = mv[jv] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (q < D4) {
+        wv[jv] = rw[rbase + q];
+        vv[jv] = rv[rbase + q];
+        if (rm) mv[jv] = rm[rbase + q];
+      }
+    }
+    uint32_t st0 = 0;
+    if (gl == 0) st0 = d.step[row];
+    const uint32_t cc = min(cnt, W);
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq)
+      if (gl + jq * G >= cc) p[jq] = kFull;
+    // rank every held position against all cc positions of the row
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq) {
+      if ((uint32_t)(jq * G) >= cc) break;
+      const uint32_t lim = min((uint32_t)G, cc - (uint32_t)(jq * G));
+      for (uint32_t sl = 0; sl < lim; ++sl) {
+        const uint32_t qv = __shfl_sync(gmask, p[jq], sl, G);
+#pragma unroll
+        for (int j2 = 0; j2 < PPT; ++j2) r[j2] += qv < p[j2];
+      }
+    }
+#pragma unroll
+    for (int jq = 0; jq < PPT; ++jq)
+      if (gl + jq * G < cc) order[r[jq]] = p[jq];
+    __syncwarp(gmask);
+    // the sums in (source, position) order, B rows in flight
+    float4 acc[NV];
+#pragma unroll
+    for (int jv = 0; jv < NV; ++jv) acc[jv] = make_float4(0.f, 0.f, 0.f, 0.f);
+    constexpr int B = NV <= 2 ? 4 : 2;
+    uint32_t k = 0;
+    for (; k + B <= cc; k += B) {
+      float4 x[B][NV];
+#pragma unroll
+      for (int qb = 0; qb < B; ++qb)
+#pragma unroll
+        for (int jv = 0; jv < NV; ++jv) {
+          const uint32_t q = gl + jv * G;
+          x[qb][jv] = q < D4 ? __ldcg(g4 + (size_t)order[k + qb] * D4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int qb = 0; qb < B; ++qb)
+#pragma unroll
+        for (int jv = 0; jv < NV; ++jv) {
+          acc[jv].x += x[qb][jv].x;
+          acc[jv].y += x[qb][jv].y;
+          acc[jv].z += x[qb][jv].z;
+          acc[jv].w += x[qb][jv].w;
+        }
+    }
+    for (; k < cc; ++k) {
+#pragma unroll
+      for (int jv = 0; jv < NV; ++jv) {
+        const uint32_t q = gl + jv * G;
+        if (q >= D4) continue;
+        const float4 x = __ldcg(g4 + (size_t)order[k] * D4 + q);
+        acc[jv].x += x.x;
+        acc[jv].y += x.y;
+        acc[jv].z += x.z;
+        acc[jv].w += x.w;
+      }
+    }
+    __syncwarp(gmask);
+    uint32_t st = 0;
+    if (gl == 0) {
+      a.row_cnt[row] = 0;  // the row's origin list is consumed
+      st = st0 + 1;
+      d.step[row] = st;
+    }
+    st = __shfl_sync(gmask, st, 0, G);
+    double bc1 = 1.0, bc2 = 1.0;
+    if (o.kind == RS_OPT_ADAM) {
+      if (st < o.bc_len) {
+        bc1 = o.bc[st];
+        bc2 = o.bc[o.bc_len + st];
+      } else {
+        bc1 = 1.0 - pow(o.b1, (double)st);
+        bc2 = 1.0 - pow(o.b2, (double)st);
+      }
+    }
+#pragma unroll
+    for (int jv = 0; jv < NV; ++jv) {
+      const uint32_t q = gl + jv * G;
+      if (q >= D4) continue;
+      float* wp = reinterpret_cast<float*>(&wv[jv]);
+      float* vp = reinterpret_cast<float*>(&vv[jv]);
+      float* mp = reinterpret_cast<float*>(&mv[jv]);
+      const float* gp = reinterpret_cast<const float*>(&acc[jv]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (o.kind == RS_OPT_ADAM)
+          adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
+        else
+          adagrad_elem(wp[e], vp[e], gp[e], o);
+      }
+      rw[rbase + q] = wv[jv];
+      rv[rbase + q] = vv[jv];
+      if (rm) rm[rbase + q] = mv[jv];
+    }
+  }
+}
+
+// A forward-only op's origin lists, consumed without an update (the next op
+// starts from zero counts).
+__global__ void k_own_reset(uint32_t* row_cnt, const uint32_t* touched, const uint32_t* touched_cnt) {
+  const uint32_t nu = *touched_cnt;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x)
+    row_cnt[touched[u]] = 0;
+}
+
 // timeline stamp (RS_TRACE=1 only): the stream reached this point
 __global__ void k_tl_stamp(CommDev c, int slot) { trace_mark(c.tl, slot); }
 
@@ -329,7 +449,7 @@ struct DistGraph {
   rs_table* t;
   const void *ids, *grads, *out;
   uint64_t n;
-  int mirror, ru, ou, par, fu;
+  int mirror, ru, par, fu;
   const void* pbuf;
   double* csum;
   unsigned char opt[256];
@@ -359,10 +479,17 @@ struct rs_comm {
   unsigned int* done = nullptr;
   uint32_t* send_pos = nullptr;
   uint32_t* send_cnt = nullptr;
-  uint32_t* origins = nullptr;  // owner: [scratch slot][W] origin positions
+  // owner: row-indexed origin scratch (k_own_lookup / k_own_update), sized
+  // for the shard's row capacity and grown with it (zero between ops)
+  uint32_t* row_cnt = nullptr;    // [scr_rows]
+  uint32_t* row_orig = nullptr;   // [scr_rows * W]
+  uint64_t scr_rows = 0;
+  uint32_t* touched[2] = {nullptr, nullptr};  // per op parity: rows with an origin
+  uint32_t* touched_cnt = nullptr;            // [2]
+  bool pending_reset = false;  // a forward-only op left origin counts behind
+  int pending_par = 0;
   TableDev* view = nullptr;
   rs_workspace* ws_req = nullptr;
-  rs_workspace* ws_own = nullptr;
   StepSets last_sets{0, 0, 0};
   uint64_t last_n = 0;
   bool have_forward = false;
@@ -504,35 +631,24 @@ static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
 // caller) and the row stored into every requester that asked for it (KB')
 static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
                         TableCounters* mirror_out = nullptr, cudaEvent_t ev_dedup = nullptr) {
-  rs_workspace* wo = c->ws_own;
   const CommDev cd = comm_dev(c, ss.par, kOwner);
-  const uint64_t nflat = (uint64_t)c->world * c->cap;
-  const int ou = ss.ou;
   RS_TRY(prof_begin(c, kPhWaitIds, s));
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
+  carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
   RS_LAUNCH_CHECK("k_wait(ids)");
   RS_TRY(prof_end(c, kPhWaitIds, s));
-  RS_TRY(prof_begin(c, kPhOwnerTable, s));
-  k_own_dedup<<<dim3((unsigned)((c->cap + 255) / 256), c->world), 256, 0, s>>>(
-      cd, set_dev(wo, ou), c->origins, wo->unique);
-  RS_LAUNCH_CHECK("k_own_dedup");
   if (ev_dedup) RS_CUDA(cudaEventRecord(ev_dedup, s));
-  RS_TRY(prof_end(c, kPhOwnerTable, s));
   RS_TRY(prof_begin(c, kPhRespond, s));
-  OwnTableArgs a;
+  OwnLookupArgs a;
   a.td = t->dev;
-  a.use = set_dev(wo, ou);
-  a.clean = set_dev(wo, ou ^ 1);
-  a.origins = c->origins;
-  a.unique = wo->unique;
-  a.urow = wo->urow;
-  a.u_cnt = wo->u_cnt;
-  a.u_poff = wo->u_poff;
-  a.u_ntile = wo->u_ntile;
-  a.u_ticket = wo->u_ticket;
+  a.row_cnt = c->row_cnt;
+  a.row_orig = c->row_orig;
+  a.touched = c->touched[ss.par];
+  a.touched_cnt = c->touched_cnt + ss.par;
+  a.touched_clr = c->touched_cnt + (ss.par ^ 1);
   a.mirror_out = mirror_out;
-  k_own_table<<<grid_for(nflat, 32, 148 * 8), 256, 0, s>>>(cd, a);
-  RS_LAUNCH_CHECK("k_own_table");
+  static const unsigned grid = getenv("RS_OWN_GRID") ? (unsigned)atoi(getenv("RS_OWN_GRID")) : 148u * RS_OWN_MINB;
+  carve(k_own_lookup), k_own_lookup<<<grid, 256, 0, s>>>(cd, a);
+  RS_LAUNCH_CHECK("k_own_lookup");
   return prof_end(c, kPhRespond, s);
 }
 
@@ -541,7 +657,7 @@ static int req_gather(rs_comm* c, rs_table* t, uint64_t n, float* d_out, StepSet
                       cudaStream_t s) {
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhWaitEmbs, s));
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+  carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
   RS_LAUNCH_CHECK("k_wait(embs)");
   RS_TRY(prof_end(c, kPhWaitEmbs, s));
   RS_TRY(prof_begin(c, kPhGather, s));
@@ -577,7 +693,7 @@ static int req_reduce(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
     o.sync = signal_sync(c);  // the last finish block raises the gradient flags
     RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &o));
   } else {  // idle rank: the owners still wait for its (empty) gradients
-    k_signal<<<1, 64, 0, s>>>(cd, 2);
+    carve(k_signal), k_signal<<<1, 64, 0, s>>>(cd, 2);
     RS_LAUNCH_CHECK("k_signal(grads)");
   }
   RS_TRY(prof_end(c, kPhReqReduce, s));
@@ -592,7 +708,7 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
   rs_workspace* wr = c->ws_req;
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   RS_TRY(prof_begin(c, kPhWaitEmbs, s));
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+  carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
   RS_LAUNCH_CHECK("k_wait(embs)");
   RS_TRY(prof_end(c, kPhWaitEmbs, s));
   RS_TRY(prof_begin(c, kPhGather, s));
@@ -610,7 +726,7 @@ static int req_gather_reduce(rs_comm* c, rs_table* t, uint64_t n, float* d_out,
     f.sync = signal_sync(c);  // the last finish block raises the gradient flags
     RS_TRY(step_finish(wr, t, ss.ru, n, d_grads, nullptr, nullptr, s, &f));
   } else {
-    k_signal<<<1, 64, 0, s>>>(cd, 2);
+    carve(k_signal), k_signal<<<1, 64, 0, s>>>(cd, 2);
     RS_LAUNCH_CHECK("k_signal(grads)");
   }
   RS_TRY(prof_end(c, kPhGather, s));
@@ -649,7 +765,7 @@ static int req_reduce_fast(rs_comm* c, const float* d_grads, uint64_t n, StepSet
   RS_TRY(prof_begin(c, kPhReqReduce, s));
   RS_TRY(fast_dist_reduce(c->ws_req, c->view, c->dim, n, d_grads, ss.fu, s, c->ws_req->fork,
                           c->d_peer_grad[ss.par], (uint32_t)c->cap, (uint32_t)c->rank));
-  k_signal<<<1, 64, 0, s>>>(cd, 2);  // every branch joined: the sums are out
+  carve(k_signal), k_signal<<<1, 64, 0, s>>>(cd, 2);  // every branch joined: the sums are out
   RS_LAUNCH_CHECK("k_signal(grads)");
   return prof_end(c, kPhReqReduce, s);
 }
@@ -664,7 +780,7 @@ static int req_gather_fast(rs_comm* c, uint64_t n, float* d_out, StepSets ss, cu
   const CommDev cd = comm_dev(c, ss.par, kRequester);
   if (!spin) {
     RS_TRY(prof_begin(c, kPhWaitEmbs, s));
-    k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
+    carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 1);
     RS_LAUNCH_CHECK("k_wait(embs)");
     RS_TRY(prof_end(c, kPhWaitEmbs, s));
   }
@@ -677,27 +793,41 @@ static int req_gather_fast(rs_comm* c, uint64_t n, float* d_out, StepSets ss, cu
 // owner: per id sum over its origins in (source, position) order -- the
 // stage-2 origin order -- fused with the optimizer on the shard
 static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cudaStream_t s) {
-  rs_workspace* wo = c->ws_own;
   const CommDev cd = comm_dev(c, ss.par, kOwner);
-  const uint64_t nflat = (uint64_t)c->world * c->cap;
   RS_TRY(prof_begin(c, kPhWaitGrads, s));
-  k_wait<<<1, kMaxWorld, 0, s>>>(cd, 2);
+  carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 2);  // every requester's sums landed
   RS_LAUNCH_CHECK("k_wait(grads)");
   RS_TRY(prof_end(c, kPhWaitGrads, s));
   RS_TRY(prof_begin(c, kPhOwnerUpdate, s));
-  const float* grad_in = reinterpret_cast<const float*>(c->arena + c->off_grad[ss.par]);
-  rs_dist_opts oo;  // at most `world` origins per id: the CSR finish over the origin rows
-  oo.no_hot = true;
-  oo.csr_pos = c->origins;
-  oo.sync = wait_sync(c, c->own_sig_grad, kOwner);  // every requester's sums landed
-  oo.sync.tl = c->ws_req->fast.trace;
-  RS_TRY(step_finish(wo, t, ss.ou, nflat, grad_in, ob, nullptr, s, &oo));
+  OwnUpdateArgs a;
+  a.td = t->dev;
+  a.row_cnt = c->row_cnt;
+  a.row_orig = c->row_orig;
+  a.touched = c->touched[ss.par];
+  a.touched_cnt = c->touched_cnt + ss.par;
+  a.grad_in = reinterpret_cast<const float*>(c->arena + c->off_grad[ss.par]);
+  OptArgs o;
+  std::memcpy(&o, ob, sizeof(o));
+  const uint32_t D4 = c->dim / 4;
+  // G lanes x NV float4 per row; persistent grid (resident blocks)
+  static const unsigned gcap = getenv("RS_OWN_UGRID") ? (unsigned)atoi(getenv("RS_OWN_UGRID")) : 0u;
+#define RS_OU(GG, NN, MB)                                                                   \
+  {                                                                                         \
+    const unsigned grid = gcap ? gcap : 148u * (MB);                                        \
+    carve(k_own_update<GG, NN>), k_own_update<GG, NN><<<grid, 256, 0, s>>>(cd, a, o);       \
+  }
+  if (D4 <= 4) RS_OU(4, 1, 4)
+  else if (D4 <= 16) RS_OU(8, 2, 4)
+  else if (D4 <= 32) RS_OU(8, 4, 2)
+  else if (D4 <= 64) RS_OU(8, 8, 2)
+  else return fail(RS_ERR_CONFIG, "sharded step: embedding_dim > 256 unsupported");
+#undef RS_OU
+  RS_LAUNCH_CHECK("k_own_update");
   if (cd.tl) {
-    k_tl_stamp<<<1, 32, 0, s>>>(cd, 13);
+    carve(k_tl_stamp), k_tl_stamp<<<1, 32, 0, s>>>(cd, 13);
     RS_LAUNCH_CHECK("k_tl_stamp");
   }
-  RS_TRY(prof_end(c, kPhOwnerUpdate, s));
-  return RS_OK;
+  return prof_end(c, kPhOwnerUpdate, s);
 }
 
 static int check_call(rs_comm* c, rs_table* t, uint64_t n, const char* who) {
@@ -713,18 +843,39 @@ static int check_call(rs_comm* c, rs_table* t, uint64_t n, const char* who) {
 // host side of a step, outside any graph: shapes, capacity (may rehash or
 // grow the row pool on s), the partial-sum buffer
 static int prepare_step(rs_comm* c, rs_table* t, uint64_t n_reduce, cudaStream_t s) {
-  c->ws_req->last_tile = c->ws_own->last_tile = tile_tokens_for_dim(c->dim);
+  c->ws_req->last_tile = tile_tokens_for_dim(c->dim);
   // new keys at this owner <= ids received <= world * max_tokens (the peers'
   // batch sizes are not known here without a host round trip)
   RS_TRY(table_prepare(t, (uint64_t)c->world * c->cap, s));
   if (n_reduce) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n_reduce, s));
+  if (c->scr_rows < t->desc.row_cap) {  // the origin scratch follows the shard's row capacity
+    RS_CUDA(cudaDeviceSynchronize());     // (graphs in flight use the old one)
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->row_cnt) cudaFree(c->row_cnt);
+    if (c->row_orig) cudaFree(c->row_orig);
+    c->row_cnt = c->row_orig = nullptr;
+    c->scr_rows = 0;
+    const uint64_t rows = t->desc.row_cap;
+    if (cudaMalloc(&c->row_cnt, rows * 4) != cudaSuccess ||
+        cudaMalloc(&c->row_orig, rows * 4 * (uint64_t)c->world) != cudaSuccess)
+      return cuda_fail(cudaGetLastError(), "sharded step: origin scratch");
+    RS_CUDA(cudaMemset(c->row_cnt, 0, rows * 4));
+    c->scr_rows = rows;
+  }
+  if (c->pending_reset) {  // the last forward-only op's origin counts (before this op's lookup)
+    carve(k_own_reset), k_own_reset<<<grid_for((uint64_t)c->world * c->cap, 256, 148 * 4), 256, 0, s>>>(
+        c->row_cnt, c->touched[c->pending_par], c->touched_cnt + c->pending_par);
+    RS_LAUNCH_CHECK("k_own_reset");
+    c->pending_reset = false;
+  }
   return RS_OK;
 }
 // fast: the requester runs on the fast kernels (a step with gradients, n > 0)
 static int begin_step(rs_comm* c, bool fast, StepSets* out) {
   if (fast) RS_TRY(fast_prepare(c->ws_req));
   c->epoch++;
-  StepSets ss{c->ws_req->cur, c->ws_own->cur, (int)(c->epoch & 1)};
+  StepSets ss{c->ws_req->cur, 0, (int)(c->epoch & 1)};
   ss.fu = fast ? c->ws_req->fast.cur : -1;
   *out = ss;
   return RS_OK;
@@ -741,7 +892,6 @@ static void end_step(rs_comm* c, StepSets ss) {
   } else {
     c->ws_req->cur = ss.ru ^ 1;
   }
-  c->ws_own->cur = ss.ou ^ 1;
 }
 
 // The owner role runs on its own stream, concurrently with the requester
@@ -849,20 +999,15 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   v.d.row_cap = rows;
   RS_CUDA(cudaMemcpy(c->view, &v, sizeof(v), cudaMemcpyHostToDevice));
   int st = rs_workspace_create(max_tokens, &c->ws_req);
-  if (!st) st = rs_workspace_create(rows, &c->ws_own);
   if (st) {
     rs_comm_destroy(c);
     return st;
   }
-  const uint64_t oslots = (c->ws_own->S + 1) * (uint64_t)world;  // u_poff = slot * W is 32-bit
-  if (oslots > 0xFFFFFFFFull) {
-    rs_comm_destroy(c);
-    return fail(RS_ERR_CONFIG, "rs_comm_create: world * max_tokens too large for the origin rows");
-  }
-  if (cudaMalloc(&c->origins, oslots * 4) != cudaSuccess) {
+  if (cudaMalloc(&c->touched[0], rows * 4) != cudaSuccess || cudaMalloc(&c->touched[1], rows * 4) != cudaSuccess ||
+      cudaMalloc(&c->touched_cnt, 16) != cudaSuccess || cudaMemset(c->touched_cnt, 0, 16) != cudaSuccess) {
     cudaGetLastError();
     rs_comm_destroy(c);
-    return fail(RS_ERR_CUDA, "rs_comm_create: cudaMalloc of the origin rows failed");
+    return fail(RS_ERR_CUDA, "rs_comm_create: cudaMalloc of the touched-row lists failed");
   }
   if (const char* e = getenv("RS_NO_GRAPH")) c->use_graphs = e[0] == '0';
   if (const char* e = getenv("RS_DIST_GRAPH_FORK")) c->graph_fork = e[0] != '0';
@@ -978,8 +1123,9 @@ int rs_comm_destroy(rs_comm* c) {
   for (int r = 0; r < c->world; ++r)
     if (!c->local && r != c->rank && c->h_peers[r]) cudaIpcCloseMemHandle(c->h_peers[r]);
   void* ps[] = {c->arena, c->d_peers, c->d_peer_grad[0], c->d_peer_grad[1], c->trace, c->done,
-                c->send_pos, c->send_cnt, c->origins, c->view, c->d_epoch, c->d_sig_grad_ptrs,
-                c->d_sig_ids_ptrs, c->d_cnt_ptrs};
+                c->send_pos, c->send_cnt, c->view, c->d_epoch, c->d_sig_grad_ptrs,
+                c->d_sig_ids_ptrs, c->d_cnt_ptrs, c->row_cnt, c->row_orig, c->touched[0],
+                c->touched[1], c->touched_cnt};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& e : c->pev)
@@ -994,7 +1140,6 @@ int rs_comm_destroy(rs_comm* c) {
   if (c->ev_gjoin) cudaEventDestroy(c->ev_gjoin);
   if (c->ev_dedup) cudaEventDestroy(c->ev_dedup);
   rs_workspace_destroy(c->ws_req);
-  rs_workspace_destroy(c->ws_own);
   delete c;
   return RS_OK;
 }
@@ -1020,6 +1165,8 @@ int rs_dist_forward(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, 
   c->last_n = n;
   c->last_table = t;
   c->have_forward = true;
+  c->pending_reset = true;  // unless rs_dist_backward consumes the origins
+  c->pending_par = ss.par;
   return RS_OK;
 }
 
@@ -1041,6 +1188,7 @@ int rs_dist_backward(rs_comm* c, rs_table* t, const float* d_grads, uint64_t n,
   RS_TRY(join_owner(c, s, own));
   t->applies++;
   c->have_forward = false;
+  c->pending_reset = false;  // the update consumed the origins
   return prof_step_done(c);
 }
 
@@ -1122,7 +1270,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     DistGraph* hit = nullptr;
     for (auto& g : c->graphs)
       if (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n &&
-          g.mirror == mirror && g.ru == ss.ru && g.ou == ss.ou && g.par == ss.par && g.fu == ss.fu &&
+          g.mirror == mirror && g.ru == ss.ru && g.par == ss.par && g.fu == ss.fu &&
           g.pbuf == c->ws_req->pbuf && g.csum == c->csum_dst && std::memcmp(g.opt, ob, sizeof(ob)) == 0) {
         hit = &g;
         break;
@@ -1144,23 +1292,20 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
       e.n = n;
       e.mirror = mirror;
       e.ru = ss.ru;
-      e.ou = ss.ou;
       e.par = ss.par;
       e.fu = ss.fu;
       e.pbuf = c->ws_req->pbuf;
       e.csum = c->csum_dst;
       std::memcpy(e.opt, ob, sizeof(ob));
       // hot-id finish as a forked graph branch (RS_DIST_GRAPH_FORK=0: linear)
-      const bool f0 = c->ws_req->fork, f1 = c->ws_own->fork;
+      const bool f0 = c->ws_req->fork;
       c->ws_req->fork = c->ws_req->fork && c->graph_fork;
-      c->ws_own->fork = false;
       const uint64_t before = launches();
       RS_CUDA(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
       const int st = enqueue(c->cap_stream);
       cudaGraph_t g = nullptr;
       const cudaError_t ce = cudaStreamEndCapture(c->cap_stream, &g);
       c->ws_req->fork = f0;
-      c->ws_own->fork = f1;
       if (st) {
         if (g) cudaGraphDestroy(g);
         return st;
@@ -1207,7 +1352,7 @@ int rs_dist_step_checksum(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64
 // work enqueued after it starts only once every rank reached it.
 int rs_comm_barrier(rs_comm* c, void* stream) {
   if (!c) return fail(RS_ERR_CONFIG, "rs_comm_barrier: null comm");
-  k_barrier<<<1, kMaxWorld, 0, S(stream)>>>(comm_dev(c, 0, kRequester), c->d_bar_epoch);
+  carve(k_barrier), k_barrier<<<1, kMaxWorld, 0, S(stream)>>>(comm_dev(c, 0, kRequester), c->d_bar_epoch);
   RS_LAUNCH_CHECK("k_barrier");
   return RS_OK;
 }
@@ -1297,6 +1442,8 @@ int rs_dist_group_forward(rs_comm* const* cs, rs_table* const* ts, int world, co
     cs[r]->last_n = n[r];
     cs[r]->last_table = ts[r];
     cs[r]->have_forward = true;
+    cs[r]->pending_reset = true;
+    cs[r]->pending_par = ss[r].par;
   }
   return RS_OK;
 }
@@ -1318,6 +1465,7 @@ int rs_dist_group_backward(rs_comm* const* cs, rs_table* const* ts, int world, c
   for (int r = 0; r < world; ++r) {
     ts[r]->applies++;
     cs[r]->have_forward = false;
+    cs[r]->pending_reset = false;
   }
   return RS_OK;
 }

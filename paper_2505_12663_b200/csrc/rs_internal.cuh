@@ -8,6 +8,9 @@
 //  * embedding structure: SoA row pool (emb, opt_m, opt_v, step), rows never
 //    move when the key structure expands (embed_table.cpp:267-285).
 #pragma once
+#include <cstdlib>
+#include <unordered_set>
+#include <mutex>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -105,6 +108,30 @@ __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+// Uniform shared-memory carveout for every kernel of the step (host side).
+// Kernels whose launch configurations ask for different L1 / shared splits
+// cannot share an SM: a block of the second waits until the SM drained the
+// first's.  The step runs several latency-bound kernels side by side (the
+// fast step's branches, the sharded step's owner and requester roles).
+// RS_CARVEOUT=<percent> gives all of them the same split (experiment knob:
+// measured no faster than the driver's per-kernel choice at 50 / 75, slower
+// at 25 / 100 -- the default, -1, leaves the driver's choice).
+inline void carve_ptr(const void* k) {
+  static const int v = getenv("RS_CARVEOUT") ? atoi(getenv("RS_CARVEOUT")) : -1;
+  if (v < 0) return;
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.insert(k).second) {
+    (void)cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, v);
+    (void)cudaGetLastError();
+  }
+}
+template <typename... A>
+inline void carve(void (*k)(A...)) {
+  carve_ptr(reinterpret_cast<const void*>(k));
+}
+
 // Programmatic dependent launch: a kernel launched with launch_pdl may start
 // while its same-stream predecessor drains; pdl_wait() (first statement of
 // such a kernel, before any global access) blocks until the predecessor grid
@@ -144,6 +171,7 @@ bool debug_sync();  // RS_DEBUG_SYNC=1: synchronize after every launch (debuggin
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), unsigned g, unsigned b, size_t smem,
                               cudaStream_t s, Args... args) {
+  carve(k);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(g);
   cfg.blockDim = dim3(b);

@@ -1381,7 +1381,7 @@ static int launch_fdedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, in
   const uint32_t TT = ws->last_tile;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4 + 4 + 4);
-  k_fdedup<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, set_dev(ws, use), ws->slot_of, ws->unique,
+  carve(k_fdedup), k_fdedup<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, set_dev(ws, use), ws->slot_of, ws->unique,
                                   ws->ctr, d_n, ranks ? ws->tok_rank : nullptr);
   RS_LAUNCH_CHECK("k_fdedup");
   ws->tok_rank_ok = ranks;
@@ -1393,7 +1393,7 @@ static int fast_dedup_table(rs_workspace* ws, rs_table* t, const uint64_t* d_ids
                             int use, cudaStream_t s) {
   int st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true);
   if (st) return st;
-  k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
+  carve(k_ftable), k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(ftable_args(ws, t, use));
   RS_LAUNCH_CHECK("k_ftable");
   return RS_OK;
 }
@@ -1445,7 +1445,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     a.csum_ticket = ws->csum_ticket;
   }
   if (d_out && D % 4 != 0) {
-    k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, a.use, t->dev,
+    carve(k_gather_scalar), k_gather_scalar<<<grid_for(n, 8, 148 * 8), 256, 0, s>>>(ws->slot_of, a.use, t->dev,
                                                             (uint32_t)n, ws->inverse, d_out);
     RS_LAUNCH_CHECK("k_gather_scalar");
     if (!d_grads) {
@@ -1488,7 +1488,7 @@ static int launch_tile(rs_workspace* ws, rs_table* t, int use, uint64_t n, float
     bool kc2 = false;
 #define RS_HOT(V, C)                                                           \
   if (!kc2 && sh.vec == V && sh.ch == C) {                                     \
-    k_ftile<V, C, 1, kTileHot><<<hot_grid, TT, smem, hs>>>(a2);                \
+    carve(k_ftile<V, C, 1, kTileHot>), k_ftile<V, C, 1, kTileHot><<<hot_grid, TT, smem, hs>>>(a2);                \
     RS_LAUNCH_CHECK("k_ftile(hot)");                                           \
     kc2 = true;                                                                \
   }
@@ -1659,13 +1659,13 @@ static int forward_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids,
                            float* d_out, const float* d_grads, int use, cudaStream_t s) {
   int st;
   if (t->cfg.max_keys) {
-    k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
+    carve(k_clean), k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
     RS_LAUNCH_CHECK("k_clean");
     if ((st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true))) return st;
     FTableArgs a = ftable_args(ws, t, use);
     a.do_clean = false;
     a.do_table = false;
-    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
+    carve(k_ftable), k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
     RS_LAUNCH_CHECK("k_ftable(meta)");
     st = table_ensure_any(t, ws->unique, ws->set[use].cnt, n, ws->urow, ws->urow64,
                           ws->set[use].u_slot, ws->set[use].srow, s);
@@ -1687,7 +1687,7 @@ int step_ftable(rs_workspace* ws, rs_table* t, int use, uint64_t n_max, bool do_
   a.do_table = do_table;
   a.do_clean = do_clean;
   if (send) a.send = *send;
-  k_ftable<<<grid_for(n_max, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
+  carve(k_ftable), k_ftable<<<grid_for(n_max, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
   RS_LAUNCH_CHECK("k_ftable");
   return RS_OK;
 }
@@ -1763,7 +1763,7 @@ int rs_workspace_create(uint64_t max_tokens, rs_workspace** out) {
     return RS_ERR_CUDA;
   }
   for (int k = 0; k < 2; ++k) {
-    k_clear_all<<<grid_for(S_ + 1, 256, 148 * 16), 256>>>(set_dev(ws, k), S_ + 1);
+    carve(k_clear_all), k_clear_all<<<grid_for(S_ + 1, 256, 148 * 16), 256>>>(set_dev(ws, k), S_ + 1);
     count_launch();
   }
   cudaMemset(ws->scan_status, 0, ((N + kScanTile - 1) / kScanTile + 1) * 8);
@@ -1815,7 +1815,7 @@ int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_un
   const int use = ws->cur;
   const SetDev su = set_dev(ws, use), sc = set_dev(ws, use ^ 1);
   ws->have_forward = false;
-  k_clean<<<grid_for(n + 1, 256, 148 * 8), 256, 0, s>>>(sc);
+  carve(k_clean), k_clean<<<grid_for(n + 1, 256, 148 * 8), 256, 0, s>>>(sc);
   RS_LAUNCH_CHECK("k_clean");
   if (n == 0) {
     RS_CUDA(cudaMemsetAsync(ws->set[use].cnt, 0, 4, s));
@@ -1830,17 +1830,17 @@ int rs_dedup(rs_workspace* ws, const uint64_t* d_ids, uint64_t n, uint64_t* d_un
   const uint32_t TT = 256;
   const uint32_t ntiles = (uint32_t)((n + TT - 1) / TT);
   const size_t sm = (size_t)(2 * TT + 1) * (8 + 4 + 4);
-  k_dedup_tile_exact<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, su, ws->slot_of);
+  carve(k_dedup_tile_exact), k_dedup_tile_exact<<<ntiles, TT, sm, s>>>(d_ids, (uint32_t)n, su, ws->slot_of);
   RS_LAUNCH_CHECK("k_dedup_tile_exact");
   const uint32_t stiles = (uint32_t)((n + kScanTile - 1) / kScanTile);
-  k_dedup_compact<<<stiles, kScanThreads, 0, s>>>(d_ids, (uint32_t)n, ws->slot_of, su, ws->unique,
+  carve(k_dedup_compact), k_dedup_compact<<<stiles, kScanThreads, 0, s>>>(d_ids, (uint32_t)n, ws->slot_of, su, ws->unique,
                                                   ws->scan_status, ws->ctr, stiles, sc.cnt);
   RS_LAUNCH_CHECK("k_dedup_compact");
   if (d_inverse) {
-    k_inverse<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->slot_of, su, (uint32_t)n, d_inverse);
+    carve(k_inverse), k_inverse<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->slot_of, su, (uint32_t)n, d_inverse);
     RS_LAUNCH_CHECK("k_inverse");
   }
-  k_copy_unique<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->unique, su.cnt, d_unique, d_n_unique);
+  carve(k_copy_unique), k_copy_unique<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(ws->unique, su.cnt, d_unique, d_n_unique);
   RS_LAUNCH_CHECK("k_copy_unique");
   ws->last_set = use;
   ws->last_fast = false;
@@ -1927,14 +1927,14 @@ static int step_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, ui
   ws->pdl_now = false;
   if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
   if (t->cfg.max_keys) {  // bounded: dedup + metadata, then probe / evict / insert on the device
-    k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
+    carve(k_clean), k_clean<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(set_dev(ws, use ^ 1));
     RS_LAUNCH_CHECK("k_clean");
     if ((st = launch_fdedup(ws, d_ids, n, use, s, nullptr, true))) return st;
     if (ev) RS_CUDA(cudaEventRecord(ev[1], s));
     FTableArgs a = ftable_args(ws, t, use);
     a.do_clean = false;
     a.do_table = false;
-    k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
+    carve(k_ftable), k_ftable<<<grid_for(n, kGroups, 148 * 8), kGroups * kBucket, 0, s>>>(a);
     RS_LAUNCH_CHECK("k_ftable(meta)");
     if ((st = table_bounded_enqueue(t, ws->unique, ws->set[use].cnt, n, ws->urow, ws->urow64,
                                     ws->set[use].u_slot, ws->set[use].srow, s)))
@@ -2214,7 +2214,7 @@ int rs_apply_aggregated(rs_table* t, const uint64_t* d_keys, uint64_t n, const f
   const unsigned grid = grid_for(n, 8, 148 * 8);
 #define RS_SHAPE(V, C)                                                                   \
   if (sh.vec == V && sh.ch == C) {                                                       \
-    k_apply_sums<V, C><<<grid, 256, 0, s>>>(t->dev, rows, n, d_sums, o);                 \
+    carve(k_apply_sums<V, C>), k_apply_sums<V, C><<<grid, 256, 0, s>>>(t->dev, rows, n, d_sums, o);                 \
     RS_LAUNCH_CHECK("k_apply_sums");                                                     \
     RS_CUDA(cudaFreeAsync(rows, s));                                                     \
     t->applies++;                                                                        \

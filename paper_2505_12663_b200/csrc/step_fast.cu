@@ -1191,7 +1191,7 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   fa.urow64 = ws->urow64;
   if (send) fa.send = *send;
   if (do_ka) {
-    k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);  // an idle sharded rank still publishes its (empty) send
+    carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);  // an idle sharded rank still publishes its (empty) send
     RS_LAUNCH_CHECK("k_fa");
   }
   if (!do_reduce) return RS_OK;
@@ -1240,14 +1240,14 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
     if (fsm > 48 * 1024)                                                                     \
       RS_CUDA(cudaFuncSetAttribute(k_fhf<V, C, NWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                    (int)fsm));                                               \
-    k_fhf<V, C, NWV><<<fgrid, NWV * 32, fsm, q>>>(ff, o);                                    \
+    carve(k_fhf<V, C, NWV>), k_fhf<V, C, NWV><<<fgrid, NWV * 32, fsm, q>>>(ff, o);                                    \
   }
 #define RS_FH(V, C)                                                                        \
   if (shp.vec == V && shp.ch == C) {                                                       \
     if ((kTT / 32) * kRowStage * D * 4 > 48 * 1024)                                         \
       RS_CUDA(cudaFuncSetAttribute(k_fh<V, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                                    (int)((kTT / 32) * kRowStage * D * 4)));                  \
-    k_fh<V, C><<<ntiles, kTT, (kTT / 32) * kRowStage * D * 4, q>>>(h);                      \
+    carve(k_fh<V, C>), k_fh<V, C><<<ntiles, kTT, (kTT / 32) * kRowStage * D * 4, q>>>(h);                      \
     RS_LAUNCH_CHECK("k_fh");                                                               \
     RS_KF(V, C, 4) RS_KF(V, C, 8) RS_KF(V, C, 16)                                          \
     RS_LAUNCH_CHECK("k_fhf");                                                              \
@@ -1287,7 +1287,7 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
     ch.c_max = f.hot_min;
     const uint64_t max_heavy = n / (f.light_max + 1) + 1;
 #define RS_FC(GG, NVV, PM, MB, args, q, items)                                              \
-  k_fc<GG, NVV, PM, MB><<<grid_for(items, 256 / GG, cap_blocks), 256, 0, q>>>(args, o);
+  carve(k_fc<GG, NVV, PM, MB>), k_fc<GG, NVV, PM, MB><<<grid_for(items, 256 / GG, cap_blocks), 256, 0, q>>>(args, o);
     // a grid-stride grid: the heavy ids are ~1-2% of the unique ids
     static const uint64_t hcap = getenv("RS_FCH_ITEMS") ? (uint64_t)atoll(getenv("RS_FCH_ITEMS")) : 148ull * 16;
     const uint64_t hitems = std::min<uint64_t>(max_heavy, hcap);
@@ -1317,13 +1317,13 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   };
   auto checksum = [&](cudaStream_t q) -> int {
     if (!ws->csum_dst || peer) return RS_OK;
-    k_fcs<<<ntiles, kTT, 0, q>>>(f.tokcs, (uint32_t)n, ws->csum_dst, ws->csum_part, ws->csum_ticket);
+    carve(k_fcs), k_fcs<<<ntiles, kTT, 0, q>>>(f.tokcs, (uint32_t)n, ws->csum_dst, ws->csum_part, ws->csum_ticket);
     RS_LAUNCH_CHECK("k_fcs");
     return RS_OK;
   };
   int st;
   if (ev) {  // eager, serial: KA (+ clean) | KD | KH + KF | KS
-    k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
+    carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
                                                             td, mirror_out);
     RS_LAUNCH_CHECK("k_fclean");
     if ((st = csr(s, s))) return st;
@@ -1338,7 +1338,7 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   static const int skip = getenv("RS_FAST_SKIP") ? atoi(getenv("RS_FAST_SKIP")) : 0;
   if (skip != 1 && (st = hot(sh2))) return st;
   if (skip != 2 && (st = csr(sd, sd3))) return st;
-  k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
+  carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
                                                             td, mirror_out);
   RS_LAUNCH_CHECK("k_fclean");
   if (sd != s) {
@@ -1493,10 +1493,10 @@ int fast_dist_gather(rs_workspace* ws, const TableDev* view, uint32_t D, uint64_
   const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
   const uint32_t nb = grid ? std::min(grid, ntiles) : ntiles;
   const uint32_t D4 = D / 4;
-  if (D4 >= 32) k_fgd<32><<<nb, kTT, 0, s>>>(g);
-  else if (D4 >= 16) k_fgd<16><<<nb, kTT, 0, s>>>(g);
-  else if (D4 >= 8) k_fgd<8><<<nb, kTT, 0, s>>>(g);
-  else k_fgd<4><<<nb, kTT, 0, s>>>(g);
+  if (D4 >= 32) carve(k_fgd<32>), k_fgd<32><<<nb, kTT, 0, s>>>(g);
+  else if (D4 >= 16) carve(k_fgd<16>), k_fgd<16><<<nb, kTT, 0, s>>>(g);
+  else if (D4 >= 8) carve(k_fgd<8>), k_fgd<8><<<nb, kTT, 0, s>>>(g);
+  else carve(k_fgd<4>), k_fgd<4><<<nb, kTT, 0, s>>>(g);
   RS_LAUNCH_CHECK("k_fgd");
   return RS_OK;
 }
