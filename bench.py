@@ -753,6 +753,7 @@ def dist_timeline(st, one, flush, lib, P):
         t0 = t[0, :, 0][t[0, :, 1] > 0].min()
         if os.environ.get("RS_TRACE_DUMP") and k == 5:  # raw per-block spans of the last step (us)
             np.save(f"{os.environ['RS_TRACE_DUMP']}_rank{st.rank}.npy", np.where(t > 0, (t - t0) / 1e3, np.nan))
+            np.save(f"{os.environ['RS_TRACE_DUMP']}_rank{st.rank}_t0.npy", np.array([t0]))
         for i, name in enumerate(DIST_TRACE_NAMES):
             ok = t[i, :, 1] > 0
             if ok.any():

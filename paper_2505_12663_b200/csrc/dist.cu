@@ -165,6 +165,7 @@ struct OwnLookupArgs {
   uint32_t* touched_cnt;      // their count (this op's parity)
   uint32_t* touched_clr;      // the other parity's count, zeroed here
   TableCounters* mirror_out;  // host's pinned counter mirror (mapped), or null
+  bool bump;                  // no k_wait(ids) before: this kernel advances the owner epoch
 };
 
 __global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_lookup(CommDev c, OwnLookupArgs a) {
@@ -178,8 +179,10 @@ __global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_lookup(CommDev c, OwnL
   __shared__ uint32_t s_off[kMaxWorld + 1];
   __shared__ uint32_t s_w[8], s_base;
   __shared__ unsigned long long s_ins, s_reuse;
-  // every source's ids landed (k_wait passed: one cheap check per block)
-  if (threadIdx.x < c.world) spin_flag(&h->sig_ids[threadIdx.x], *c.epoch, c.trace + kTrError);
+  // every source's ids landed (after k_wait: one cheap check per block; with
+  // bump, the wait itself -- the last block then publishes the new epoch)
+  const unsigned long long ep = *c.epoch + (a.bump ? 1 : 0);
+  if (threadIdx.x < c.world) spin_flag(&h->sig_ids[threadIdx.x], ep, c.trace + kTrError);
   if (threadIdx.x == 0) {
     s_ins = 0;
     s_reuse = 0;
@@ -255,8 +258,11 @@ __global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_lookup(CommDev c, OwnL
     if (threadIdx.x == 0) c.trace[kTrReceived] = total;  // two-stage: one vector back per received id
   }
   if (last_block_signal(c, 1, c.done + 1)) {
-    raise_flags(c, 1, c.done + 1, *c.epoch);
-    if (threadIdx.x == 0) c.trace[kTrLookups] = *reinterpret_cast<volatile uint32_t*>(a.touched_cnt);
+    raise_flags(c, 1, c.done + 1, ep);
+    if (threadIdx.x == 0) {
+      c.trace[kTrLookups] = *reinterpret_cast<volatile uint32_t*>(a.touched_cnt);
+      if (a.bump) *c.epoch = ep;  // every block read the old value before arriving
+    }
   }
 }
 
@@ -274,10 +280,11 @@ struct OwnUpdateArgs {
   const float* grad_in;  // [W * cap x D] the requesters' per-id sums (this op's parity)
 };
 
-template <int G, int NV>
+// PPT: origin positions held per lane (W <= G * PPT); ADAM: o.kind (the
+// Adagrad build carries no first-moment state or bias corrections)
+template <int G, int NV, int PPT, bool ADAM>
 __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, OwnUpdateArgs a, OptArgs o) {
   WarpTrace wt_(c.tl, 14);
-  constexpr int PPT = (kMaxWorld + G - 1) / G;  // origin positions held per lane
   __shared__ uint32_t order_s[(256 / G) * kMaxWorld];
   const TableDesc d = a.td->d;
   const uint32_t D4 = d.dim >> 2;
@@ -292,7 +299,7 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
   const float4* __restrict__ g4 = reinterpret_cast<const float4*>(a.grad_in);
   float4* rw = reinterpret_cast<float4*>(d.emb);
   float4* rv = reinterpret_cast<float4*>(d.s2);
-  float4* rm = reinterpret_cast<float4*>(d.s1);
+  float4* rm = ADAM ? reinterpret_cast<float4*>(d.s1) : nullptr;
   for (uint32_t u = gid; u < nu; u += ngroups) {
     const uint32_t row = __ldcg(a.touched + u);
     // the origin count, the origin positions (speculatively, all W) and the
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
     float4 acc[NV];
 #pragma unroll
     for (int jv = 0; jv < NV; ++jv) acc[jv] = make_float4(0.f, 0.f, 0.f, 0.f);
-    constexpr int B = NV <= 2 ? 4 : 2;
+    constexpr int B = NV == 1 ? 4 : 2;  // (NV = 2 at B = 4 spills at 64 registers)
     uint32_t k = 0;
     for (; k + B <= cc; k += B) {
       float4 x[B][NV];
@@ -384,7 +391,7 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
     }
     st = __shfl_sync(gmask, st, 0, G);
     double bc1 = 1.0, bc2 = 1.0;
-    if (o.kind == RS_OPT_ADAM) {
+    if (ADAM) {
       if (st < o.bc_len) {
         bc1 = o.bc[st];
         bc2 = o.bc[o.bc_len + st];
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
       const float* gp = reinterpret_cast<const float*>(&acc[jv]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        if (o.kind == RS_OPT_ADAM)
+        if (ADAM)
           adam_elem(wp[e], mp[e], vp[e], gp[e], bc1, bc2, o);
         else
           adagrad_elem(wp[e], vp[e], gp[e], o);
@@ -511,6 +518,7 @@ struct rs_comm {
   cudaEvent_t ev_dedup = nullptr;        // owner dedup done (reduce_after_dedup)
   bool reduce_after_dedup = false;       // RS_DIST_REDUCE_AFTER=1
   bool host_prof = false;                // RS_HOST_PROF=1
+  bool lookup_spin = true;               // rs_dist_step: no k_wait(ids) (RS_DIST_LOOKUP_SPIN=0: with)
   double host_ns[5] = {0, 0, 0, 0, 0};
   uint64_t host_calls = 0;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_meta = nullptr, ev_gjoin = nullptr;
@@ -630,12 +638,18 @@ static int req_front(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n,
 // owner-unique id find-or-insert on the shard (capacity prepared by the
 // caller) and the row stored into every requester that asked for it (KB')
 static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
-                        TableCounters* mirror_out = nullptr, cudaEvent_t ev_dedup = nullptr) {
+                        TableCounters* mirror_out = nullptr, cudaEvent_t ev_dedup = nullptr,
+                        bool spin = false) {
   const CommDev cd = comm_dev(c, ss.par, kOwner);
-  RS_TRY(prof_begin(c, kPhWaitIds, s));
-  carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
-  RS_LAUNCH_CHECK("k_wait(ids)");
-  RS_TRY(prof_end(c, kPhWaitIds, s));
+  // spin: the lookup's blocks wait for the ids themselves (the caller
+  // ordered the owner stream after this rank's own id send, so they only
+  // wait for remote producers); else one waiter block first
+  if (!spin) {
+    RS_TRY(prof_begin(c, kPhWaitIds, s));
+    carve(k_wait), k_wait<<<1, kMaxWorld, 0, s>>>(cd, 0);
+    RS_LAUNCH_CHECK("k_wait(ids)");
+    RS_TRY(prof_end(c, kPhWaitIds, s));
+  }
   if (ev_dedup) RS_CUDA(cudaEventRecord(ev_dedup, s));
   RS_TRY(prof_begin(c, kPhRespond, s));
   OwnLookupArgs a;
@@ -646,6 +660,7 @@ static int owner_lookup(rs_comm* c, rs_table* t, StepSets ss, cudaStream_t s,
   a.touched_cnt = c->touched_cnt + ss.par;
   a.touched_clr = c->touched_cnt + (ss.par ^ 1);
   a.mirror_out = mirror_out;
+  a.bump = spin;
   static const unsigned grid = getenv("RS_OWN_GRID") ? (unsigned)atoi(getenv("RS_OWN_GRID")) : 148u * RS_OWN_MINB;
   carve(k_own_lookup), k_own_lookup<<<grid, 256, 0, s>>>(cd, a);
   RS_LAUNCH_CHECK("k_own_lookup");
@@ -814,9 +829,23 @@ static int owner_update(rs_comm* c, rs_table* t, const void* ob, StepSets ss, cu
 #define RS_OU(GG, NN, MB)                                                                   \
   {                                                                                         \
     const unsigned grid = gcap ? gcap : 148u * (MB);                                        \
-    carve(k_own_update<GG, NN>), k_own_update<GG, NN><<<grid, 256, 0, s>>>(cd, a, o);       \
+    const bool adam = o.kind == RS_OPT_ADAM;                                                \
+    if ((uint32_t)c->world <= (GG) && adam)                                                 \
+      carve(k_own_update<GG, NN, 1, true>), k_own_update<GG, NN, 1, true><<<grid, 256, 0, s>>>(cd, a, o); \
+    else if ((uint32_t)c->world <= (GG))                                                    \
+      carve(k_own_update<GG, NN, 1, false>), k_own_update<GG, NN, 1, false><<<grid, 256, 0, s>>>(cd, a, o); \
+    else if (adam)                                                                          \
+      carve(k_own_update<GG, NN, kMaxWorld / (GG), true>),                                  \
+          k_own_update<GG, NN, kMaxWorld / (GG), true><<<grid, 256, 0, s>>>(cd, a, o);      \
+    else                                                                                    \
+      carve(k_own_update<GG, NN, kMaxWorld / (GG), false>),                                 \
+          k_own_update<GG, NN, kMaxWorld / (GG), false><<<grid, 256, 0, s>>>(cd, a, o);     \
   }
+  // D <= 64: 4 lanes x 4 float4 per row (measured ~2 us faster at config 1
+  // than 8 x 2: twice the rows in flight); RS_OWN_G4=0 for 8 x 2
+  static const int g4 = getenv("RS_OWN_G4") ? atoi(getenv("RS_OWN_G4")) : 1;
   if (D4 <= 4) RS_OU(4, 1, 4)
+  else if (D4 <= 16 && g4) RS_OU(4, 4, 2)
   else if (D4 <= 16) RS_OU(8, 2, 4)
   else if (D4 <= 32) RS_OU(8, 4, 2)
   else if (D4 <= 64) RS_OU(8, 8, 2)
@@ -1032,6 +1061,7 @@ int rs_comm_create(int rank, int world, uint64_t max_tokens, uint32_t dim, rs_co
   RS_CUDA(cudaEventCreateWithFlags(&c->ev_dedup, cudaEventDisableTiming));
   if (const char* e = getenv("RS_DIST_REDUCE_AFTER")) c->reduce_after_dedup = e[0] == '1';
   if (const char* e = getenv("RS_HOST_PROF")) c->host_prof = e[0] == '1';
+  if (const char* e = getenv("RS_DIST_LOOKUP_SPIN")) c->lookup_spin = e[0] == '1';
   c->h_peers[rank] = c->arena;
   *out = c;
   return RS_OK;
@@ -1233,9 +1263,11 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     // requester on q: dedup, ids out, reduce + sums out, then the gather;
     // owner on its stream: stage 2, table + answer, then the update
     cudaStream_t own;
-    RS_TRY(fork_owner(c, q, &own));
+    // (the owner stream forks after the id send when the lookup spins)
+    if (!c->lookup_spin) RS_TRY(fork_owner(c, q, &own));
     if (fast) RS_TRY(req_front_fast(c, d_ids, n, ss, q));
     else RS_TRY(req_front(c, t, d_ids, n, ss, q));
+    if (c->lookup_spin) RS_TRY(fork_owner(c, q, &own));
     // the gather needs only the metadata (and the rows): it runs on its own
     // stream, concurrently with the segment-reduce of the same tokens
     RS_CUDA(cudaEventRecord(c->ev_meta, q));
@@ -1254,7 +1286,7 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     } else {
       if (fast) RS_TRY(req_reduce_fast(c, d_grads, n, ss, q));
       else RS_TRY(req_reduce(c, t, d_grads, n, ss, q));
-      RS_TRY(owner_lookup(c, t, ss, own, mo));
+      RS_TRY(owner_lookup(c, t, ss, own, mo, nullptr, c->lookup_spin));
     }
     if (!mo) RS_TRY(table_mirror_copy(t, mirror, own));
     RS_TRY(owner_update(c, t, ob, ss, own));
@@ -1380,6 +1412,11 @@ int rs_comm_phase_ms(rs_comm* c, double* ms, int n, uint64_t* count) {
 // the device timeline of this rank's last step (RS_TRACE=1): rs_workspace_trace of the requester workspace
 int rs_comm_timeline(rs_comm* c, uint64_t* out, uint64_t cap, uint64_t* n_out) {
   if (!c) return fail(RS_ERR_CONFIG, "rs_comm_timeline: null comm");
+  if (getenv("RS_EPOCH_DBG")) {
+    unsigned long long e[4];
+    RS_CUDA(cudaMemcpy(e, c->d_epoch, 32, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "rank %d epochs: requester %llu owner %llu host %llu\n", c->rank, e[0], e[2], c->epoch);
+  }
   return rs_workspace_trace(c->ws_req, out, cap, n_out);
 }
 
