@@ -704,7 +704,9 @@ def run_c3(args, cfg):
                       "l2": "flushed (512 MiB write) between timed steps"},
            "roofline": {"bound": "hbm", "kernel": "whole step", "achieved": ach, "peak": hbm, "unit": "GB/s",
                         "frac": ach / hbm, "traffic": None, "peak_source": how, "algorithmic_bytes_per_launch": byt},
-           "victim_selection": "device radix select over (tick, key) (evict.cu), no host round trip",
+           "victim_selection": "stamp log (evict.cu k_lg_*): the live records from the log head, no slot scan; "
+                               "device radix select over (tick, key) slot scan when the log is off (RS_EVICT_LOG=0)",
+           "step_ms": {"min": min(ms), "median": float(np.median(ms)), "max": max(ms)},
            "table_host_syncs_in_timed_region": int(syncs),
            "gpu_launches": int(launches), "clocks": clk.summary()}
     print(json.dumps(res), flush=True)

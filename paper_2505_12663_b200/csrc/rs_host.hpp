@@ -49,6 +49,17 @@ struct rs_table {
   uint64_t evict_cap = 0, victim_idx_cap = 0;
   uint64_t buf_gen = 0;  // bumps when a buffer baked into captured graphs is reallocated
   bool evict_tmin_valid = false;  // the device selection may start its tick window at its last min
+  // bounded tables: the stamp log (evict.cu; rs_internal.cuh LogRec)
+  rs::LogRec* d_log = nullptr;
+  rs::LogCtl* d_log_ctl = nullptr;
+  uint64_t log_cap = 0;           // records (power of two)
+  bool log_valid = false;         // the log lists every live entry (else: rebuilt before the next ensure)
+  uint64_t log_tail_ub = 0;       // host upper bound of the device tail
+  uint64_t log_head_lb = 0;       // host lower bound of the device head (last read)
+  uint32_t* d_lg_cnt = nullptr;   // per window block: live records
+  long long* d_lg_pre = nullptr;
+  uint64_t lg_nb = 0;             // window blocks allocated
+  uint64_t log_rebuilds = 0;
 };
 
 struct rs_graph_entry {
@@ -141,6 +152,7 @@ struct rs_workspace {
   cudaStream_t aux_stream = nullptr;  // forked branch of the step (reserved)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<rs_graph_entry> graphs;
+  std::vector<uint64_t> seen;  // bounded tables: step signatures run once eagerly (capture on the second)
   uint64_t graph_clock = 0;
   bool use_graphs = true;
   bool fork = true;  // run the hot-id finish concurrently on aux_stream
@@ -242,6 +254,9 @@ int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n
                         uint32_t* d_srow, cudaStream_t s);
 // evict.cu: device victim selection + removal (bounded ensure after the
 // probe: explicit_k == 0; explicit evict: explicit_k = k)
+int log_prepare(rs_table* t, uint64_t n_max, cudaStream_t s);  // bounded ensure: log room / rebuild
+rs::LogArgs log_args(rs_table* t, int probe);                     // (null rec: no log)
+void log_invalidate(rs_table* t);                                 // rebuilt before the next bounded ensure
 int evict_device(rs_table* t, const uint32_t* d_n, uint64_t n_host, uint64_t explicit_k,
                  cudaStream_t s);
 int evict_count(rs_table* t, uint64_t* out, cudaStream_t s);

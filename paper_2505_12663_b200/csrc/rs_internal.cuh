@@ -87,6 +87,30 @@ struct TableDev {
   TableCounters c;
 };
 
+// Bounded tables: the stamp log (evict.cu).  Every batch op of the bounded
+// ensure writes one record per key at log position base + (key index): the
+// entry it stamped (or inserted) with the op's tick, or a placeholder (slot
+// kNoLogSlot).  Ops are stream-ordered, so the log is tick-ordered; a record
+// is live while its slot still holds that key with that tick.
+constexpr uint32_t kNoLogSlot = 0xFFFFFFFFu;
+struct LogRec {
+  unsigned long long key;
+  uint32_t slot;  // slot index, capacity + {0, 1} for the sentinel keys, or kNoLogSlot
+  uint32_t tick;
+};
+struct LogCtl {
+  unsigned long long tail, head;  // positions (monotone; index = pos & mask)
+  unsigned long long op_base;     // base of the last probe op (the insert pass writes there too)
+  unsigned long long sorted_end;  // [0, sorted_end): rebuilt, (tick, key)-sorted
+};
+struct LogArgs {
+  LogRec* rec = nullptr;  // null: no log
+  LogCtl* ctl = nullptr;
+  uint64_t mask = 0;
+  uint64_t cap = 0;       // table key slots (the sentinels' virtual slots follow)
+  int probe = 0;          // 1: this launch opens the op (base = tail, advances tail)
+};
+
 enum : unsigned int {
   kErrRowPool = 1u,    // ran out of pre-sized rows (host bound violated)
   kErrTableFull = 2u,  // probe walked every bucket without a usable slot

@@ -2013,7 +2013,25 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
     const int e = fast_enqueue(ws, t, d_ids, n, d_grads, d_out, &o, use, q, ev, ws->fork, mo);
     return e ? e : (mo ? RS_OK : table_mirror_copy(t, mirror, q));
   };
-  if (ws->profiling || !ws->use_graphs) {
+  // Bounded tables (evict-heavy streams: batches rarely repeat) capture a
+  // step's graph only when its buffers / size come back: a one-off batch runs
+  // eagerly instead of paying a capture + instantiate
+  bool once = false;
+  if (t->cfg.max_keys && !ws->profiling && ws->use_graphs) {
+    const uint64_t sig = (uint64_t)(uintptr_t)d_ids * 0x9E3779B97F4A7C15ull ^ (uint64_t)(uintptr_t)d_grads * 31 ^
+                         (uint64_t)(uintptr_t)d_out * 131 ^ n * 0xC2B2AE3D27D4EB4Full ^ (uint64_t)(uintptr_t)t;
+    bool cached = false;
+    for (auto& g : ws->graphs)
+      cached = cached || (g.t == t && g.ids == d_ids && g.grads == d_grads && g.out == d_out && g.n == n);
+    if (!cached) {
+      once = std::find(ws->seen.begin(), ws->seen.end(), sig) == ws->seen.end();
+      if (once) {
+        if (ws->seen.size() >= 64) ws->seen.erase(ws->seen.begin());
+        ws->seen.push_back(sig);
+      }
+    }
+  }
+  if (ws->profiling || !ws->use_graphs || once) {
     // profiling runs the kernels one after another (no fork) so that every
     // phase's events bracket only its own kernels
     const bool f0 = ws->fork;

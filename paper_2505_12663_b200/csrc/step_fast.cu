@@ -445,6 +445,182 @@ struct FcArgs {
   uint32_t cap, rank;
 };
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// KD heavy, warp per id (D = 32 or 64): one warp per heavy id (light_max <
+// c <= 64 occurrences), EPL floats of the row per lane (float2 at D = 64:
+// half the registers per row in flight of k_fc's 16 lanes x float4, so 16
+// gradient rows are loaded per round trip instead of 4).  Positions ranked
+// into token order, rows summed in token order -- the same sequential f32
+// adds as k_fc, so the same bits -- then the forward rows and the optimizer.
+template <int EPL>
+__device__ __forceinline__ void ld_row(const float* p, float (&x)[EPL]) {
+  if (EPL == 2) {
+    const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+    x[0] = v.x;
+    x[EPL > 1 ? 1 : 0] = v.y;
+  } else {
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) x[e] = __ldg(p + e);
+  }
+}
+
+template <int EPL, int NWB>
+__global__ void __launch_bounds__(NWB * 32) k_fcb(FcArgs a, OptArgs o) {
+  WarpTrace wt_(a.sh.trace, 5);
+  __shared__ uint32_t s_order[NWB][kPosMax];
+  const TableDesc d = a.td->d;
+  const uint32_t D = d.dim;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t* order = s_order[warp];
+  const uint32_t nitems = *a.list_n;
+  const bool peer = a.peer_dst != nullptr;
+  const uint32_t e0 = lane * EPL;  // this lane's floats [e0, e0 + EPL)
+  const bool mine = e0 < D;
+  float* ew = d.emb;
+  float* ev = d.s2;
+  float* em = d.s1;
+  for (uint32_t it = blockIdx.x * NWB + warp; it < nitems; it += gridDim.x * NWB) {
+    const uint32_t gs = __ldg(a.list + it);
+    if (!RS_IDX_OK(gs < a.sh.n_slots, a.sh.ctr)) continue;
+    const uint2 cr = __ldcg(reinterpret_cast<const uint2*>(&a.use.rec[gs].cnt));
+    const uint32_t c = cr.x, row = cr.y;
+    const uint32_t uu = __ldcg(a.sh.uidx + gs);
+    uint32_t p0 = __ldcg(a.sh.pos + (size_t)gs * kPosMax + lane);
+    uint32_t p1 = __ldcg(a.sh.pos + (size_t)gs * kPosMax + 32 + lane);
+    if (row == kNoRow) continue;  // table error (reported through the counters)
+    if (c > a.c_max || c <= a.c_min) continue;  // (warp-uniform)
+    if (!RS_IDX_OK(c <= kPosMax && (peer || row < d.row_cap), a.sh.ctr)) continue;
+    // the row's state, issued before the sums
+    float w[EPL], v[EPL], m[EPL];
+    uint32_t st0 = 0;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) w[e] = v[e] = m[e] = 0.f;
+    if (!peer && mine) {
+      const size_t rb = (size_t)row * D + e0;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        w[e] = ew[rb + e];
+        v[e] = ev[rb + e];
+        if (em) m[e] = em[rb + e];
+      }
+    }
+    if (!peer && lane == 0) st0 = d.step[row];
+    if (lane >= c) p0 = kFull;
+    if (32 + lane >= c) p1 = kFull;
+    // rank every held position against all c positions: token order
+    uint32_t r0 = 0, r1 = 0;
+    const uint32_t c0 = min(c, 32u);
+    for (uint32_t sl = 0; sl < c0; ++sl) {
+      const uint32_t q = __shfl_sync(kFull, p0, sl);
+      r0 += q < p0;
+      r1 += q < p1;
+    }
+    for (uint32_t sl = 32; sl < c; ++sl) {
+      const uint32_t q = __shfl_sync(kFull, p1, sl - 32);
+      r0 += q < p0;
+      r1 += q < p1;
+    }
+    if (lane < c && RS_IDX_OK(r0 < c && p0 < a.n_tokens, a.sh.ctr)) order[r0] = p0;
+    if (32 + lane < c && RS_IDX_OK(r1 < c && p1 < a.n_tokens, a.sh.ctr)) order[r1] = p1;
+    __syncwarp();
+    // the forward: the pre-update row to each token
+    if (!(a.exp & 4) && !peer) {
+      for (uint32_t k = 0; k < c; ++k) {
+        float* dst = a.out + (size_t)order[k] * D + e0;
+        if (mine) {
+          if (EPL == 2)
+            __stcs(reinterpret_cast<float2*>(dst), make_float2(w[0], w[EPL > 1 ? 1 : 0]));
+          else
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) __stcs(dst + e, w[e]);
+        }
+      }
+      for (uint32_t k = lane; k < c; k += 32) a.inverse[order[k]] = (int32_t)uu;
+      if (a.tokcs) {  // the row sum in k_fc's tree: per float4 (x + y) + (z + w), then over the float4s
+        double rs = 0.0;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) rs += mine ? (double)w[e] : 0.0;  // EPL 2: x + y (or z + w)
+        if (EPL == 1) rs += __shfl_xor_sync(kFull, rs, 1);               // x + y
+        rs += __shfl_xor_sync(kFull, rs, EPL == 1 ? 2 : 1);              // (x + y) + (z + w)
+        for (uint32_t o2 = 16; o2 >= (EPL == 1 ? 4u : 2u); o2 >>= 1) rs += __shfl_xor_sync(kFull, rs, o2);
+        for (uint32_t k = lane; k < c; k += 32) a.tokcs[order[k]] = rs;
+      }
+    }
+    // the sums in token order, kB rows in flight
+    float acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    constexpr int kB = 16;
+    if (!(a.exp & 2) && mine) {
+      uint32_t k = 0;
+      for (; k + kB <= c; k += kB) {
+        float x[kB][EPL];
+#pragma unroll
+        for (int q = 0; q < kB; ++q) ld_row<EPL>(a.grads + (size_t)order[k + q] * D + e0, x[q]);
+#pragma unroll
+        for (int q = 0; q < kB; ++q)
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc[e] += x[q][e];
+      }
+      if (k < c) {  // the tail: all its rows in flight, then the adds in order
+        float x[kB][EPL];
+#pragma unroll
+        for (int q = 0; q < kB; ++q)
+          if (k + q < c) ld_row<EPL>(a.grads + (size_t)order[k + q] * D + e0, x[q]);
+#pragma unroll
+        for (int q = 0; q < kB; ++q)
+          if (k + q < c)
+#pragma unroll
+            for (int e = 0; e < EPL; ++e) acc[e] += x[q][e];
+      }
+    }
+    __syncwarp();
+    if (peer) {  // the id's sum to its owner's gradient receive buffer (NVLink store)
+      const uint32_t ow = row / a.cap, jj = row - ow * a.cap;
+      if (mine) {
+        float* dst = a.peer_dst[ow] + ((size_t)a.rank * a.cap + jj) * D + e0;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) dst[e] = acc[e];
+      }
+      continue;
+    }
+    uint32_t st = 0;
+    if (lane == 0) {
+      st = st0 + 1;
+      d.step[row] = st;
+    }
+    st = __shfl_sync(kFull, st, 0);
+    double bc1 = 1.0, bc2 = 1.0;
+    if (o.kind == RS_OPT_ADAM) {
+      if (st < o.bc_len) {
+        bc1 = o.bc[st];
+        bc2 = o.bc[o.bc_len + st];
+      } else {
+        bc1 = 1.0 - pow(o.b1, (double)st);
+        bc2 = 1.0 - pow(o.b2, (double)st);
+      }
+    }
+    if (mine) {
+      const size_t rb = (size_t)row * D + e0;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        if (a.exp & 1)
+          w[e] += acc[e];
+        else if (o.kind == RS_OPT_ADAM)
+          adam_elem(w[e], m[e], v[e], acc[e], bc1, bc2, o);
+        else
+          adagrad_elem(w[e], v[e], acc[e], o);
+        ew[rb + e] = w[e];
+        ev[rb + e] = v[e];
+        if (em) em[rb + e] = m[e];
+      }
+    }
+  }
+}
+
 #ifndef RS_FC_MINB
 #define RS_FC_MINB 5
 #endif
@@ -665,9 +841,6 @@ struct FhArgs {
 };
 
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 
 constexpr uint32_t kRowStage = 8;  // group rows per warp staged in smem (more: read from global)
 
@@ -1292,7 +1465,19 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
     static const uint64_t hcap = getenv("RS_FCH_ITEMS") ? (uint64_t)atoll(getenv("RS_FCH_ITEMS")) : 148ull * 16;
     const uint64_t hitems = std::min<uint64_t>(max_heavy, hcap);
     static const int hminb = getenv("RS_FC_HMINB") ? atoi(getenv("RS_FC_HMINB")) : 5;  // experiment knob
-    if (D4 == 4) { RS_FC(4, 1, 64, 5, ch, qh, hitems) }
+    // D = 32 / 64: the bulk-load heavy kernel (RS_FCB=0: k_fc)
+    static const bool fcb = !getenv("RS_FCB") || getenv("RS_FCB")[0] != '0';
+    constexpr int kNWB = 4;
+    if (fcb && (D4 == 8 || D4 == 16)) {
+      // a grid-stride grid: the heavy ids are ~1-2 % of the unique ids
+      static const unsigned gcap = getenv("RS_FCB_GRID") ? (unsigned)atoi(getenv("RS_FCB_GRID")) : 296u;
+      const unsigned g = grid_for(hitems, kNWB, gcap);
+      if (D4 == 16)
+        carve(k_fcb<2, kNWB>), k_fcb<2, kNWB><<<g, kNWB * 32, 0, qh>>>(ch, o);
+      else
+        carve(k_fcb<1, kNWB>), k_fcb<1, kNWB><<<g, kNWB * 32, 0, qh>>>(ch, o);
+    }
+    else if (D4 == 4) { RS_FC(4, 1, 64, 5, ch, qh, hitems) }
     else if (D4 == 8) { RS_FC(8, 1, 64, 5, ch, qh, hitems) }
     else if (D4 == 16 && hminb == 2) { RS_FC(16, 1, 64, 2, ch, qh, hitems) }
     else if (D4 == 16) { RS_FC(16, 1, 64, 5, ch, qh, hitems) }

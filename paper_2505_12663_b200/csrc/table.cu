@@ -34,8 +34,10 @@ __global__ void __launch_bounds__(kProbeThreads)
                    const uint32_t* __restrict__ d_n, uint32_t n_host,
                    const float* __restrict__ src, int mode, uint32_t* rows32, int64_t* rows64,
                    const uint32_t* __restrict__ uslot, uint32_t* srow, uint32_t* missing_list,
-                   const uint32_t* __restrict__ sel) {
+                   const uint32_t* __restrict__ sel, LogArgs lg = LogArgs{}) {
   const TableDesc d = td->d;
+  // the stamp log (bounded tables): this op's records at base + key index
+  const unsigned long long lbase = lg.rec ? (lg.probe ? lg.ctl->tail : lg.ctl->op_base) : 0ull;
   const unsigned long long free_n0 = td->c.free_n;
   const unsigned long long fresh0 = td->c.fresh_next;
   const uint32_t tick_now = td->c.tick + 1;
@@ -76,7 +78,13 @@ __global__ void __launch_bounds__(kProbeThreads)
             }
           }
         }
-        if (r != kNoRow) td->c.special_tick[sp] = tick_now;
+        bool logged = false;
+        if (r != kNoRow) {
+          const unsigned int old = atomicExch(&td->c.special_tick[sp], tick_now);
+          logged = old != tick_now || fresh;
+        }
+        if (lg.rec)
+          lg.rec[(lbase + i) & lg.mask] = LogRec{key, logged ? (uint32_t)(lg.cap + sp) : kNoLogSlot, tick_now};
         if (r == kNoRow && mode == 2 && missing_list) {
           const unsigned idx = atomicAdd(&td->c.missing, 1u);
           missing_list[idx] = (uint32_t)i;
@@ -97,7 +105,12 @@ __global__ void __launch_bounds__(kProbeThreads)
         if (p.found) {
           row = p.row == kNoRow ? wait_row(d.slots, p.slot) : p.row;
           if (g == 0 && new_row != kNoRow) return_row(td, free_n0, new_row);
-          if (g == 0 && p.tick != tick_now) d.slots[p.slot].tick = tick_now;
+          if (g == 0 && lg.rec) {  // one record per stamp: the tick CAS picks it
+            const bool won = p.tick != tick_now && atomicCAS(&d.slots[p.slot].tick, p.tick, tick_now) == p.tick;
+            lg.rec[(lbase + i) & lg.mask] = LogRec{key, won ? (uint32_t)p.slot : kNoLogSlot, tick_now};
+          } else if (g == 0 && p.tick != tick_now) {
+            d.slots[p.slot].tick = tick_now;
+          }
           if (mode == 1) {  // upsert: overwrite the embedding in place
             float* e = d.emb + (size_t)row * d.dim;
             for (uint32_t k = g; k < d.dim; k += kBucket) e[k] = srow_src[k];
@@ -109,17 +122,22 @@ __global__ void __launch_bounds__(kProbeThreads)
             const unsigned idx = atomicAdd(&td->c.missing, 1u);
             missing_list[idx] = (uint32_t)i;
           }
+          if (g == 0 && lg.rec) lg.rec[(lbase + i) & lg.mask] = LogRec{key, kNoLogSlot, tick_now};
           break;
         }
         if (p.ins == ~0ull) {
           if (g == 0) atomicOr(&td->c.error, kErrTableFull);
+          if (g == 0 && lg.rec) lg.rec[(lbase + i) & lg.mask] = LogRec{key, kNoLogSlot, tick_now};
           break;
         }
         if (new_row == kNoRow) {
           uint32_t r = 0;
           if (g == 0) r = alloc_row(td, free_n0, fresh0, d.row_cap);
           new_row = __shfl_sync(gmask, r, gbase);
-          if (new_row == kNoRow) break;
+          if (new_row == kNoRow) {
+            if (g == 0 && lg.rec) lg.rec[(lbase + i) & lg.mask] = LogRec{key, kNoLogSlot, tick_now};
+            break;
+          }
         }
         int ok = 0;
         if (g == 0) {
@@ -133,6 +151,7 @@ __global__ void __launch_bounds__(kProbeThreads)
           *reinterpret_cast<uint2*>(&d.slots[p.ins].row) = rt;
           atomicAdd(&s_ins, 1ull);
           if (p.ins_tomb) atomicAdd(&s_reuse, 1ull);
+          if (lg.rec) lg.rec[(lbase + i) & lg.mask] = LogRec{key, (uint32_t)p.ins, tick_now};
         }
         init_row(d, new_row, srow_src, g);
         row = new_row;
@@ -150,7 +169,9 @@ __global__ void __launch_bounds__(kProbeThreads)
     if (s_ins) atomicAdd(&td->c.inserted, s_ins);
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
-  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  // a probe launch opens the op in the log: its last block (every block has
+  // read the old tail) moves the tail past the op's n records
+  launch_epilogue(td, free_n0, fresh0, true, tick_now, nullptr, lg.rec && lg.probe ? lg.ctl : nullptr, n);
 }
 
 // find (no side effects) / lookup_batch (stamp hits, copy or zero rows)
@@ -473,6 +494,7 @@ int read_counters(rs_table* t, TableCounters* out, cudaStream_t s) {
 }
 
 int rehash_to(rs_table* t, uint64_t new_cap, cudaStream_t s) {
+  log_invalidate(t);  // slot indices change
   Slot* fresh = nullptr;
   RS_CUDA(cudaMallocAsync(&fresh, new_cap * sizeof(Slot), s));
   k_fill_slots<<<grid_for(new_cap, 256, 148 * 16), 256, 0, s>>>(fresh, new_cap);
@@ -652,7 +674,8 @@ int table_bounded_prepare(rs_table* t, uint64_t n_max, cudaStream_t s) {
   if (st) return st;
   if (t->missing_cap != cap0) t->buf_gen++;
   if ((st = table_prepare(t, n_max, s))) return st;
-  return evict_prepare(t, n_max);
+  if ((st = evict_prepare(t, n_max))) return st;
+  return log_prepare(t, n_max, s);
 }
 
 // Bounded ensure, device part: probe (stamp hits, list misses), the device
@@ -662,16 +685,21 @@ int table_bounded_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d
                           uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
                           uint32_t* d_srow, cudaStream_t s) {
   RS_CUDA(cudaMemsetAsync(&t->dev->c.missing, 0, sizeof(unsigned int), s));
+  // both passes write the op's stamp-log records (probe: hits + placeholders,
+  // insert: the misses' records over their placeholders)
   k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
       t->dev, d_keys, d_n, (uint32_t)n_max, nullptr, 2, d_rows32, d_rows64, d_uslot, d_srow,
-      t->d_missing, nullptr);
+      t->d_missing, nullptr, log_args(t, 1));
   RS_LAUNCH_CHECK("k_table_upsert(probe)");
   int st = evict_device(t, d_n, n_max, 0, s);
   if (st) return st;
   k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
       t->dev, d_keys, &t->dev->c.missing, (uint32_t)n_max, nullptr, 0, d_rows32, d_rows64, d_uslot,
-      d_srow, nullptr, t->d_missing);
+      d_srow, nullptr, t->d_missing, log_args(t, 0));
   RS_LAUNCH_CHECK("k_table_upsert(insert missing)");
+  // a big op (a fill) leaves one huge unsorted group: the next op rebuilds
+  // the log (tick, key)-sorted instead of selecting inside it every time
+  if (n_max > (1u << 18)) log_invalidate(t);
   return RS_OK;
 }
 
@@ -785,6 +813,9 @@ int rs_table_destroy(rs_table* t) {
   if (t->d_evict) cudaFree(t->d_evict);
   if (t->d_cand) cudaFree(t->d_cand);
   if (t->d_victim_idx) cudaFree(t->d_victim_idx);
+  void* lgp[] = {t->d_log, t->d_log_ctl, t->d_lg_cnt, t->d_lg_pre};
+  for (void* p : lgp)
+    if (p) cudaFree(p);
   for (auto& m : t->mirror) {
     if (m.pinned) cudaFreeHost(m.pinned);
     if (m.ev) cudaEventDestroy(m.ev);
@@ -863,6 +894,7 @@ int rs_table_lookup(rs_table* t, const uint64_t* d_keys, uint64_t n, float* d_ou
       t->dev, d_keys, n, nullptr, d_out, 1);
   RS_LAUNCH_CHECK("k_table_find(lookup)");
   t->host_tick++;
+  if (t->cfg.max_keys) log_invalidate(t);  // stamps without log records
   return RS_OK;
 }
 
@@ -1074,6 +1106,7 @@ int rs_table_export(rs_table* t, uint64_t max_entries, uint64_t* keys, float* em
 int rs_table_import(rs_table* t, uint64_t n, const uint64_t* keys, const float* emb,
                     const float* m, const float* v, const uint64_t* step, const uint64_t* ts) {
   if (t) t->evict_tmin_valid = false;  // imported ticks may lie below the last selection's min
+  if (t) log_invalidate(t);              // (and the stamp log does not list them)
   if (!t) return fail(RS_ERR_CONFIG, "rs_table_import: null table");
   if (n == 0) return RS_OK;
   const size_t D = t->desc.dim;

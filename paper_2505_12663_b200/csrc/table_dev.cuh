@@ -218,7 +218,8 @@ __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const Tab
 // pinned mirror (mapped memory), so no copy node follows the kernel.
 __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
                                                 unsigned long long fresh0, int bump_tick,
-                                                uint32_t tick_now, TableCounters* mirror_out = nullptr) {
+                                                uint32_t tick_now, TableCounters* mirror_out = nullptr,
+                                                LogCtl* log_open = nullptr, uint32_t log_n = 0) {
   __syncthreads();
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
@@ -253,6 +254,10 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     c.removed = 0;
     if (bump_tick == 1 || (bump_tick == 2 && any_removed)) c.tick = tick_now;
     c.blocks_done = 0;
+    if (log_open) {  // the stamp log: this op's records took [tail, tail + n)
+      log_open->op_base = log_open->tail;
+      log_open->tail += log_n;
+    }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (mirror_out) {
       *mirror_out = c;

@@ -397,6 +397,44 @@ def test_bounded_table_eviction_vs_oracle(cuda, oracle):
     _compare_contents(g, o, ("keys", "ts"))
 
 
+def test_evict_log_stream_vs_oracle(cuda, oracle):
+    # the stamp-log victim selection (evict.cu k_lg_*) over a config-3-like
+    # stream: a big fill (rebuilt into the (tick, key)-sorted region), then
+    # batches of resident + never-seen ids evicting the oldest, a remove, an
+    # explicit evict, the sentinel keys; no host sync between the batches
+    rng = np.random.default_rng(77)
+    dim, bound = 8, 6000
+    g = _gpu_table(1 << 14, dim, opt="adagrad", max_keys=bound)
+    o = Table(oracle, 1 << 14, dim, chunk_rows=4096)
+    fill = rng.choice(1 << 40, bound - 2, replace=False).astype(np.uint64)
+    fill = np.concatenate([fill, np.array([~np.uint64(0), ~np.uint64(0) - np.uint64(1)], np.uint64)])
+    tick = g.tick() + 1
+    g.ensure(fill)
+    oracle.table_ensure_batch(o.h, fill, len(fill), tick, bound, None)
+    fresh = np.uint64(1 << 50)
+    resident = fill.copy()
+    for b in range(40):
+        old = rng.choice(resident, 400)
+        new = fresh + np.arange(250, dtype=np.uint64)
+        fresh += np.uint64(250)
+        keys = np.unique(np.concatenate([old, new]))
+        rng.shuffle(keys)
+        tick = g.tick() + 1
+        g.ensure(keys)
+        oracle.table_ensure_batch(o.h, keys, len(keys), tick, bound, None)
+        resident = np.concatenate([resident, new])[-bound:]
+        if b == 12:
+            rm = rng.choice(keys, 30, replace=False)
+            g.remove(rm)
+            for k in rm:
+                oracle.table_remove(o.h, int(k))
+        if b == 20:
+            g.evict(500)
+            oracle.table_evict_oldest(o.h, 500)
+    assert g.occupied() == oracle.table_occupied(o.h)
+    _compare_contents(g, o, ("keys", "ts", "emb", "v", "step"))
+
+
 def test_ensure_duplicate_keys_in_one_batch(cuda, oracle):
     # ensure (embed_table.cpp:243-248) with every key repeated inside one batch:
     # one row per key, no row leaked, same contents as sequential ensures
