@@ -449,7 +449,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// KD heavy, warp per id (D = 32 or 64): one warp per heavy id (light_max <
+// KD heavy, warp per id (D = 32 or 64; RS_FCB=1): one warp per heavy id (light_max <
 // c <= 64 occurrences), EPL floats of the row per lane (float2 at D = 64:
 // half the registers per row in flight of k_fc's 16 lanes x float4, so 16
 // gradient rows are loaded per round trip instead of 4).  Positions ranked
@@ -1465,8 +1465,10 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
     static const uint64_t hcap = getenv("RS_FCH_ITEMS") ? (uint64_t)atoll(getenv("RS_FCH_ITEMS")) : 148ull * 16;
     const uint64_t hitems = std::min<uint64_t>(max_heavy, hcap);
     static const int hminb = getenv("RS_FC_HMINB") ? atoi(getenv("RS_FC_HMINB")) : 5;  // experiment knob
-    // D = 32 / 64: the bulk-load heavy kernel (RS_FCB=0: k_fc)
-    static const bool fcb = !getenv("RS_FCB") || getenv("RS_FCB")[0] != '0';
+    // RS_FCB=1 (D = 32 / 64): the warp-per-id heavy kernel k_fcb -- measured
+    // ~1-3 us slower per step at config 1 than k_fc (its blocks delay the
+    // light kernel's), kept for other shapes' experiments
+    static const bool fcb = getenv("RS_FCB") && getenv("RS_FCB")[0] == '1';
     constexpr int kNWB = 4;
     if (fcb && (D4 == 8 || D4 == 16)) {
       // a grid-stride grid: the heavy ids are ~1-2 % of the unique ids
