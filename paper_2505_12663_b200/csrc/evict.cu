@@ -569,6 +569,44 @@ __global__ void __launch_bounds__(1024) k_lg_pick(const TableDev* td, EvictState
   }
   const unsigned long long q = s_pos;
   if (q == ~0ull) return;  // (cannot happen)
+  if (q < lg.ctl->sorted_end) {
+    // [head, q] lies in the rebuilt, globally (tick, key)-sorted region: the
+    // victims are exactly its live records (q is the need-th) -- no group bounds
+    const uint32_t per2 = (nb + 1023) / 1024;
+    unsigned long long loc2 = 0;
+    for (uint32_t j = 0; j < per2; ++j) {
+      const uint32_t b = tid * per2 + j;
+      if (b < nb) loc2 += cnt[b];
+    }
+    part[tid] = loc2;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      const unsigned long long v = tid >= (uint32_t)o ? part[tid - o] : 0;
+      __syncthreads();
+      part[tid] += v;
+      __syncthreads();
+    }
+    long long run = (long long)(part[tid] - loc2);
+    for (uint32_t j = 0; j < per2; ++j) {
+      const uint32_t b = tid * per2 + j;
+      if (b >= nb) break;
+      pre[b] = run;
+      run += cnt[b];
+    }
+    if (tid == 0) {
+      st->lg_p0 = head;  // rank from the head: the first `need` live records
+      st->lg_p1 = q + 1;
+      st->lg_need2 = need;
+      st->lg_sorted = 1;
+      st->lg_mode = 1;
+      st->lg_attempt = (uint32_t)attempt;
+      st->t_star_found = 1;
+      st->active = 0;
+      st->lg_head = head;
+      lg.ctl->head = q + 1;
+    }
+    return;
+  }
   const uint32_t ts = lg.rec[q & lg.mask].tick;
   const unsigned long long p0 = lg_bound(lg, head, q + 1, ts, false);
   const unsigned long long p1 = lg_bound(lg, q, end, ts, true);
@@ -854,8 +892,8 @@ int evict_device(rs_table* t, const uint32_t* d_n, uint64_t n_host, uint64_t exp
     // an unsorted group's candidates: the key select
     k_ev_select_block<<<1, 1024, 0, s>>>(t->dev, st, cand[0], cand[1], t->d_victim_idx, cap);
     RS_LAUNCH_CHECK("k_ev_select_block");
-    k_ev_remove<<<grid_for(max_vict, 256, 148 * 4), 256, 0, s>>>(t->dev, st, t->d_victim_idx, cap,
-                                                                bound ? 1 : 0);
+    k_ev_remove<<<grid_for(max_vict, 256, 148), 256, 0, s>>>(t->dev, st, t->d_victim_idx, cap,
+                                                            bound ? 1 : 0);
     RS_LAUNCH_CHECK("k_ev_remove");
     return RS_OK;
   }

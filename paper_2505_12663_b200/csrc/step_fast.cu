@@ -151,6 +151,7 @@ struct FaArgs {
   uint64_t* unique;
   uint32_t* urow;
   int64_t* urow64;
+  int no_table = 0;  // bounded tables: dedup + metadata only (the bounded ensure follows, then k_fpatch)
 };
 
 // Sharded requester: the ids this tile claimed go to their owners
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   __shared__ uint32_t s_nnew, s_base;
   __shared__ unsigned long long s_ins, s_reuse;
   TableDev* td = a.td;
-  const bool sending = a.send.peers != nullptr;
+  const bool sending = a.send.peers != nullptr || a.no_table;  // (no table work in this kernel)
   const TableDesc d = sending ? TableDesc{} : td->d;
   const unsigned long long free_n0 = sending ? 0ull : td->c.free_n;
   const unsigned long long fresh0 = sending ? 0ull : td->c.fresh_next;
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     if (rank < kPosMax && RS_IDX_OK(gs < a.sh.n_slots, a.sh.ctr)) a.sh.pos[(size_t)gs * kPosMax + rank] = t;
   }
   __syncthreads();
+  if (a.no_table) return;
   if (sending) {  // the claimed ids to their owners (positions by block-local then global counters)
     fa_send(a, nnew, fid, fslot, fu);
     return;
@@ -1194,7 +1196,11 @@ Shape shape_of(uint32_t D) {
 }  // namespace
 
 // ---- host side ---------------------------------------------------------------
-bool fast_step_supported(const rs_table* t) { return !t->cfg.max_keys && fast_dim_supported(t->desc.dim); }
+bool fast_step_supported(const rs_table* t) {
+  // bounded tables too: KA without table work, then the bounded ensure (fast_enqueue); RS_FAST_BOUNDED=0: split kernels
+  static const bool bounded = !getenv("RS_FAST_BOUNDED") || getenv("RS_FAST_BOUNDED")[0] != '0';
+  return (bounded || !t->cfg.max_keys) && fast_dim_supported(t->desc.dim);
+}
 
 bool fast_dim_supported(uint32_t D) {
   if (D % 4) return false;
@@ -1539,9 +1545,47 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   return checksum(s);
 }
 
+// Bounded tables: the rows the bounded ensure found / inserted (urow) into
+// the set's records (the reduce kernels read rec.row).
+__global__ void k_fpatch(FSet use, const uint32_t* __restrict__ urow) {
+  const uint32_t nu = *use.cnt;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += gridDim.x * blockDim.x)
+    use.rec[use.u_slot[u]].row = urow[u];
+}
+
 int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t n, const float* d_grads,
                  float* d_out, const void* opt, int use, cudaStream_t s, cudaEvent_t* ev, bool fork,
                  TableCounters* mirror_out) {
+  if (t->cfg.max_keys) {
+    // bounded: KA's dedup + metadata, then the bounded ensure on its unique
+    // ids (probe + stamp-log victim selection + insert of the misses,
+    // table.cu / evict.cu), the rows into the records, then the reduce
+    FaArgs fa;
+    fa.ids = d_ids;
+    fa.n = (uint32_t)n;
+    fa.set = (uint32_t)use;
+    fa.use = fset(ws, use);
+    fa.clean = fset(ws, use ^ 1);
+    fa.sh = fshared(ws);
+    fa.td = t->dev;
+    fa.slot_of = ws->slot_of;
+    fa.unique = ws->unique;
+    fa.urow = ws->urow;
+    fa.urow64 = ws->urow64;
+    fa.no_table = 1;
+    const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
+    if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
+    carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);
+    RS_LAUNCH_CHECK("k_fa(no table)");
+    int st = table_bounded_enqueue(t, ws->unique, ws->fast.set[use].cnt, n, ws->urow, ws->urow64, nullptr,
+                                   nullptr, s);
+    if (st) return st;
+    carve(k_fpatch), k_fpatch<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(fa.use, ws->urow);
+    RS_LAUNCH_CHECK("k_fpatch");
+    return fast_launch(ws, t->dev, t->desc.emb, t->desc.dim, d_ids, n, d_grads, d_out,
+                       *static_cast<const OptArgs*>(opt), use, s, ev, fork, mirror_out, nullptr, nullptr, false,
+                       true);
+  }
   return fast_launch(ws, t->dev, t->desc.emb, t->desc.dim, d_ids, n, d_grads, d_out,
                      *static_cast<const OptArgs*>(opt), use, s, ev, fork, mirror_out, nullptr, nullptr, true, true);
 }
