@@ -1529,11 +1529,19 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   }
   // RS_FAST_SKIP (timing experiments only, wrong results): 1 = no hot branch, 2 = no CSR branch
   static const int skip = getenv("RS_FAST_SKIP") ? atoi(getenv("RS_FAST_SKIP")) : 0;
+  // the clean after the branches (RS_CLEAN_LAST=0: before them -- measured
+  // ~2 us slower at config 1: its blocks then delay the branches' first waves)
+  static const bool clean_last = !getenv("RS_CLEAN_LAST") || getenv("RS_CLEAN_LAST")[0] != '0';
+  auto clean = [&]() -> int {
+    carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(
+        fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace, td, mirror_out);
+    RS_LAUNCH_CHECK("k_fclean");
+    return RS_OK;
+  };
+  if (!clean_last && (st = clean())) return st;
   if (skip != 1 && (st = hot(sh2))) return st;
   if (skip != 2 && (st = csr(sd, sd3))) return st;
-  carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
-                                                            td, mirror_out);
-  RS_LAUNCH_CHECK("k_fclean");
+  if (clean_last && (st = clean())) return st;
   if (sd != s) {
     RS_CUDA(cudaEventRecord(f.ev_j1, sd));
     RS_CUDA(cudaStreamWaitEvent(s, f.ev_j1, 0));
