@@ -10,6 +10,9 @@
 // copy stream while step k computes (two device buffer sets, reuse ordered by
 // events), and only the 8-byte checksum travels back.
 #include <cuda_runtime.h>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 
 #include <algorithm>
 
@@ -168,12 +171,31 @@ int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* 
   if (!f || !ws || !t) return fail(RS_ERR_CONFIG, "rs_feeder_step: null handle");
   if (t->desc.dim != f->dim) return fail(RS_ERR_CONFIG, "rs_feeder_step: table dim != feeder dim");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  static const bool prof = getenv("RS_HOST_PROF") && getenv("RS_HOST_PROF")[0] == '1';
+  static double acc[4] = {0, 0, 0, 0};
+  static uint64_t calls = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  const auto t0 = now();
   int b = 0;
   int st = feeder_stage(f, h_ids, n, h_lengths, n_seq, first_sample_id, step, s, &b);
+  const auto t1 = now();
   bool direct = false;
   double* dst = checksum_dst(f, b, h_checksum, &direct);
   if (!st) st = rs_step_checksum(ws, t, f->ids[b], n, f->grads[b], f->out[b], opt, dst, stream);
+  const auto t2 = now();
   if (!st) st = feeder_finish(f, b, n, h_checksum, s, true, dst, direct);
+  if (prof) {  // host time by section (diagnostics): stage (incl. the staging-buffer wait), step, finish
+    const auto t3 = now();
+    acc[0] += us(t0, t1);
+    acc[1] += us(t1, t2);
+    acc[2] += us(t2, t3);
+    if (++calls % 16 == 0) {
+      fprintf(stderr, "rs_feeder_step host us/call: stage %.1f step %.1f finish %.1f\n", acc[0] / 16, acc[1] / 16,
+              acc[2] / 16);
+      acc[0] = acc[1] = acc[2] = 0;
+    }
+  }
   return st;
 }
 
