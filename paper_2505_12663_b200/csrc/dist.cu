@@ -1290,6 +1290,11 @@ int rs_dist_step(rs_comm* c, rs_table* t, const uint64_t* d_ids, uint64_t n, con
     }
     if (!mo) RS_TRY(table_mirror_copy(t, mirror, own));
     RS_TRY(owner_update(c, t, ob, ss, own));
+    static const bool gather_q = getenv("RS_DIST_GATHER_ON_Q") && getenv("RS_DIST_GATHER_ON_Q")[0] == '1';
+    if (fast && gather_q) {  // experiment: the gather after the reduce, on the requester's stream
+      RS_TRY(req_gather_fast(c, n, d_out, ss, q));
+      return join_owner(c, q, own);
+    }
     if (fast) RS_TRY(req_gather_fast(c, n, d_out, ss, c->gather_stream));
     else RS_TRY(req_gather(c, t, n, d_out, ss, c->gather_stream));
     RS_CUDA(cudaEventRecord(c->ev_gjoin, c->gather_stream));
