@@ -875,7 +875,7 @@ static int prepare_step(rs_comm* c, rs_table* t, uint64_t n_reduce, cudaStream_t
   c->ws_req->last_tile = tile_tokens_for_dim(c->dim);
   // new keys at this owner <= ids received <= world * max_tokens (the peers'
   // batch sizes are not known here without a host round trip)
-  RS_TRY(table_prepare(t, (uint64_t)c->world * c->cap, s));
+  RS_TRY(table_prepare(t, (uint64_t)c->world * c->cap, s, 8));
   if (n_reduce) RS_TRY(step_reduce_prepare(c->ws_req, c->dim, n_reduce, s));
   if (c->scr_rows < t->desc.row_cap) {  // the origin scratch follows the shard's row capacity
     RS_CUDA(cudaDeviceSynchronize());     // (graphs in flight use the old one)

@@ -30,6 +30,7 @@ struct rs_table {
   int mirror_next = 0;
   uint64_t requested_total = 0;  // Σ n over all insert/ensure batches
   uint64_t exact_occ = 0, exact_tomb = 0, exact_rows = 0, exact_requested = 0;
+  uint64_t ahead_n = 0;  // largest batch the headroom was sized for (table_prepare)
   // Adam bias-correction tables 1 - beta^step computed with the host libm
   // (bit-identical to sparse_update.cpp:25-26 on this host)
   double* d_bc = nullptr;        // [2 x bc_len]
@@ -247,7 +248,8 @@ inline unsigned long long graph_flags() {
   return off ? 0ull : (unsigned long long)cudaGraphInstantiateFlagUseNodePriority;
 }
 // table.cu
-int table_prepare(rs_table* t, uint64_t n, cudaStream_t s);  // room for n more keys
+int table_prepare(rs_table* t, uint64_t n, cudaStream_t s, int headroom = 0);  // room for n more keys
+                                                                               // (+ headroom batches' worth, steps)
 int table_after_op(rs_table* t, cudaStream_t s);             // enqueue counter mirror
 int table_ensure_device(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                         uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,

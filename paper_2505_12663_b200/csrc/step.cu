@@ -1997,7 +1997,7 @@ static int step_call(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint6
   if ((st = set_smem_attrs())) return st;
   // host side, outside the graph: capacity bound (may rehash / grow rows on s),
   // bounded tables also size the device victim selection
-  if ((st = t->cfg.max_keys ? table_bounded_prepare(t, n, s) : table_prepare(t, n, s))) return st;
+  if ((st = t->cfg.max_keys ? table_bounded_prepare(t, n, s) : table_prepare(t, n, s, 16))) return st;
   ws->last_tile = tile_tokens_for_dim(t->desc.dim);
   if ((st = reduce_prepare(ws, t->desc.dim, n, s))) return st;
   const int mirror = t->mirror_next;

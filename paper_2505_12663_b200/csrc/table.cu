@@ -534,9 +534,35 @@ static void refresh_from_mirror(rs_table* t) {
   (void)cudaGetLastError();
 }
 
-int table_prepare(rs_table* t, uint64_t n, cudaStream_t s) {
+int table_prepare(rs_table* t, uint64_t n, cudaStream_t s, int headroom) {
   refresh_from_mirror(t);
   const double lf = t->cfg.max_load_factor;
+  // training steps on unbounded tables (headroom > 0) keep room for that
+  // many more batches of the largest size seen: grown once (the first batch
+  // of a new size: one exact read), the in-flight bound below then rarely
+  // trips and waits
+  const uint64_t ahead = t->cfg.max_keys || headroom <= 0 ? 0 : std::min<uint64_t>(headroom * n, 1ull << 22);
+  if (ahead && n > t->ahead_n) {
+    TableCounters c;
+    int st = read_counters(t, &c, s);
+    if (st) return st;
+    t->ahead_n = n;
+    if ((double)(c.occupied + c.tombstones + n + ahead) > lf * (double)t->capacity) {
+      uint64_t nc = t->capacity;
+      while ((double)(c.occupied + n + ahead) > lf * (double)nc) nc <<= 1;
+      if (nc != t->capacity || c.tombstones) {
+        st = rehash_to(t, nc, s);
+        if (st) return st;
+      }
+    }
+    if (c.fresh_next + n + ahead > t->desc.row_cap) {
+      uint64_t want = std::max<uint64_t>(t->desc.row_cap * 2, c.fresh_next + n + ahead);
+      const uint64_t cr = std::max<uint32_t>(1, t->cfg.chunk_rows);
+      want = (want + cr - 1) / cr * cr;
+      st = alloc_rows(t, want, s);
+      if (st) return st;
+    }
+  }
   auto occ_ub = [&]() { return t->exact_occ + (t->requested_total - t->exact_requested); };
   auto rows_ub = [&]() { return t->exact_rows + (t->requested_total - t->exact_requested); };
   bool slots_ok = (double)(occ_ub() + t->exact_tomb + n) <= lf * (double)t->capacity;
