@@ -542,7 +542,11 @@ int table_prepare(rs_table* t, uint64_t n, cudaStream_t s, int headroom) {
   // of a new size: one exact read), the in-flight bound below then rarely
   // trips and waits
   const uint64_t ahead = t->cfg.max_keys || headroom <= 0 ? 0 : std::min<uint64_t>(headroom * n, 1ull << 22);
-  if (ahead && n > t->ahead_n) {
+  // (only while a regrowth is cheap: the row pool and the slots are copied
+  // when they grow, and at 100 M rows a copy would not fit beside the original)
+  const uint64_t pool_bytes = t->desc.row_cap * (uint64_t)t->desc.dim * 4 * (t->desc.s1 ? 3 : 2) +
+                              t->capacity * sizeof(Slot);
+  if (ahead && n > t->ahead_n && pool_bytes < (16ull << 30)) {
     TableCounters c;
     int st = read_counters(t, &c, s);
     if (st) return st;
@@ -555,8 +559,8 @@ int table_prepare(rs_table* t, uint64_t n, cudaStream_t s, int headroom) {
         if (st) return st;
       }
     }
-    if (c.fresh_next + n + ahead > t->desc.row_cap) {
-      uint64_t want = std::max<uint64_t>(t->desc.row_cap * 2, c.fresh_next + n + ahead);
+    if (c.fresh_next + n + ahead > t->desc.row_cap) {  // (exactly the headroom: pools can be huge)
+      uint64_t want = c.fresh_next + n + ahead;
       const uint64_t cr = std::max<uint32_t>(1, t->cfg.chunk_rows);
       want = (want + cr - 1) / cr * cr;
       st = alloc_rows(t, want, s);
