@@ -472,6 +472,7 @@ int alloc_rows(rs_table* t, uint64_t new_cap, cudaStream_t s) {
   d.free_stack = fs;
   d.row_cap = new_cap;
   RS_CUDA(cudaMemcpyAsync(&t->dev->d, &t->desc, sizeof(TableDesc), cudaMemcpyHostToDevice, s));
+  t->buf_gen++;  // captured steps that baked the row pointers in are stale
   return RS_OK;
 }
 
@@ -511,6 +512,7 @@ int rehash_to(rs_table* t, uint64_t new_cap, cudaStream_t s) {
   // tombstones are dropped by the rehash (embed_table.cpp:283)
   RS_CUDA(cudaMemsetAsync(&t->dev->c.tombstones, 0, sizeof(unsigned long long), s));
   t->exact_tomb = 0;
+  t->buf_gen++;
   return RS_OK;
 }
 
@@ -550,7 +552,7 @@ int table_prepare(rs_table* t, uint64_t n, cudaStream_t s, int headroom) {
     TableCounters c;
     int st = read_counters(t, &c, s);
     if (st) return st;
-    t->ahead_n = n;
+    t->ahead_n = n + n / 4;  // (batch sizes jitter: not one exact read per new maximum)
     if ((double)(c.occupied + c.tombstones + n + ahead) > lf * (double)t->capacity) {
       uint64_t nc = t->capacity;
       while ((double)(c.occupied + n + ahead) > lf * (double)nc) nc <<= 1;

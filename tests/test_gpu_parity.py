@@ -435,6 +435,42 @@ def test_evict_log_stream_vs_oracle(cuda, oracle):
     _compare_contents(g, o, ("keys", "ts", "emb", "v", "step"))
 
 
+def test_step_graphs_survive_row_pool_growth(cuda):
+    # the captured fast-step graphs bake the row pool's pointers in: a growth
+    # of the pool between replays (new keys of another batch) must re-capture
+    # them (buf_gen).  Same step sequence on a table that grows and on one
+    # sized up front: bit-identical contents and outputs.
+    rng = np.random.default_rng(91)
+    dim, vocab = 64, 4000
+    params = P.AdagradParams(lr=0.01, eps=1e-8)
+    tabs = [P.EmbedTable(P.TableConfig(capacity=1 << 16, embedding_dim=dim, optimizer="adagrad", chunk_rows=64,
+                                       initial_rows=r)) for r in (vocab + 64, 1 << 20)]
+    keys0 = np.arange(vocab, dtype=np.uint64)
+    for t in tabs:
+        t.insert(keys0, torch.zeros(vocab, dim))
+    batches = []
+    for b, nb in enumerate((800, 2000, 5000)):  # growing batches: the pool grows at each new size
+        ids = rng.integers(0, vocab, nb).astype(np.uint64)
+        ids[::5] = np.uint64(10**6 * (b + 1)) + np.arange(len(ids[::5]), dtype=np.uint64)  # new keys
+        ids[1::7] = np.uint64(7)  # a hot id: the hot-tile kernel reads the rows through the baked pointer
+        batches.append((P.as_keys(ids), W.pseudo_grads(torch.arange(len(ids)), b, dim)))
+    steps = [P.SparseStep(t, 5000, params) for t in tabs]
+    outs = [[], []]
+    for k, bi in enumerate((0, 0, 1, 0, 2, 1, 0, 2, 0)):  # replays of graphs captured before a growth
+        ids, g = batches[bi]
+        for j in range(2):
+            out = torch.empty((ids.numel(), dim), device="cuda")
+            steps[j].step(ids, g, out)
+            outs[j].append(out.clone())
+    torch.cuda.synchronize()
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
+    ea, eb = tabs[0].export(), tabs[1].export()
+    oa, ob = np.argsort(ea["keys"]), np.argsort(eb["keys"])
+    for f in ("keys", "emb", "v", "step"):
+        np.testing.assert_array_equal(ea[f][oa], eb[f][ob], err_msg=f)
+
+
 def test_ensure_duplicate_keys_in_one_batch(cuda, oracle):
     # ensure (embed_table.cpp:243-248) with every key repeated inside one batch:
     # one row per key, no row leaked, same contents as sequential ensures
