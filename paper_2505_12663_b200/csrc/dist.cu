@@ -217,6 +217,12 @@ __global__ void __launch_bounds__(256, RS_OWN_MINB) k_own_lookup(CommDev c, OwnL
       const uint64_t key = ids[(size_t)src * c.cap + j];
       row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins, &s_reuse);
     }
+#ifdef RS_BOUNDS
+    if (valid && row != kNoRow && row >= d.row_cap) {  // checked builds
+      if (g == 0) c.trace[kTrError] = 3;
+      row = kNoRow;
+    }
+#endif
     bool first = false;
     if (valid && row != kNoRow && g == 0) {
       const uint32_t k = atomicAdd(a.row_cnt + row, 1u);
@@ -302,6 +308,12 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
   float4* rm = ADAM ? reinterpret_cast<float4*>(d.s1) : nullptr;
   for (uint32_t u = gid; u < nu; u += ngroups) {
     const uint32_t row = __ldcg(a.touched + u);
+#ifdef RS_BOUNDS
+    if (row >= d.row_cap) {  // checked builds: a bad touched row fails the step (trace error)
+      if (gl == 0) c.trace[kTrError] = 3;
+      continue;
+    }
+#endif
     // the origin count, the origin positions (speculatively, all W) and the
     // row's state in one round trip
     const uint32_t cnt = __ldcg(a.row_cnt + row);
@@ -351,6 +363,16 @@ __global__ void __launch_bounds__(256, NV <= 2 ? 4 : 2) k_own_update(CommDev c, 
     for (int jv = 0; jv < NV; ++jv) acc[jv] = make_float4(0.f, 0.f, 0.f, 0.f);
     constexpr int B = NV == 1 ? 4 : 2;  // (NV = 2 at B = 4 spills at 64 registers)
     uint32_t k = 0;
+#ifdef RS_BOUNDS
+    {
+      bool bad = false;
+      for (uint32_t k2 = 0; k2 < cc; ++k2) bad |= order[k2] >= W * c.cap;
+      if (bad) {
+        if (gl == 0) c.trace[kTrError] = 3;
+        continue;
+      }
+    }
+#endif
     for (; k + B <= cc; k += B) {
       float4 x[B][NV];
 #pragma unroll
