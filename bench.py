@@ -497,7 +497,7 @@ def run_sharded(args, cfg):
 def e2e_sharded(args, cfg, batches, st, params, P, W):
     import torch
     import torch.distributed as dist
-    n = max(30, args.steps)  # ~0.15 ms per step: enough steps to average the host-fed pipeline
+    n = max(200, args.steps)  # ~0.15 ms per step: enough steps (~30 ms) to average the host-fed pipeline
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
     t, uniq, h2d, d2h = workload_e2e(batches, cfg["dim"], lambda f, hi, hl, k: f.dist_step(st, params, hi, hl, k),
                                      n, uniq_b, barrier=dist.barrier)
@@ -941,7 +941,7 @@ def host_batches(batches, dim, W):
 
 def e2e_pass(args, cfg, batches, step, P, W, rank):
     """Same metric through rs_step with host buffers (pipelined_e2e)."""
-    n = max(30, args.steps)  # ~0.1 ms per step: enough steps to average the host-fed pipeline
+    n = max(200, args.steps)  # ~0.1 ms per step: enough steps (~20 ms) to average the host-fed pipeline
     uniq_b = [int(np.unique(ids).size) for _, ids in batches]
     t, uniq, h2d, d2h = workload_e2e(batches, cfg["dim"], lambda f, hi, hl, k: f.step(step, hi, hl, k), n, uniq_b)
     tf, uf, hf, df = pipelined_e2e(host_batches(batches, cfg["dim"], W), cfg["dim"],
