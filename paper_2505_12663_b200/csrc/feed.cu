@@ -24,6 +24,7 @@ static constexpr uint64_t kChunkTok = 512;  // tokens per block of the gradient 
 
 struct rs_feeder {
   uint64_t max_tokens = 0, max_seqs = 0;
+  double wait_us = 0;  // RS_HOST_PROF: host time blocked on the staging buffer
   uint32_t dim = 0;
   cudaStream_t copy = nullptr;
   cudaEvent_t in_free[2] = {}, landed[2] = {};
@@ -98,7 +99,12 @@ static int feeder_stage(rs_feeder* f, const uint64_t* h_ids, uint64_t n, const u
   RS_CUDA(cudaStreamWaitEvent(f->copy, f->in_free[b], 0));
   // the loader's lengths -> token offsets (host, a few thousand adds); the
   // staging buffer of this set is free once its previous copy completed
-  RS_CUDA(cudaEventSynchronize(f->landed[b]));
+  {
+    static const bool prof = getenv("RS_HOST_PROF") && getenv("RS_HOST_PROF")[0] == '1';
+    const auto w0 = std::chrono::steady_clock::now();
+    RS_CUDA(cudaEventSynchronize(f->landed[b]));
+    if (prof) f->wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - w0).count();
+  }
   {  // validate before touching the pinned staging buffers
     uint64_t tot = 0, chunks = 0;
     for (uint64_t i = 0; i < n_seq; ++i) {
@@ -191,8 +197,9 @@ int rs_feeder_step(rs_feeder* f, rs_workspace* ws, rs_table* t, const uint64_t* 
     acc[1] += us(t1, t2);
     acc[2] += us(t2, t3);
     if (++calls % 16 == 0) {
-      fprintf(stderr, "rs_feeder_step host us/call: stage %.1f step %.1f finish %.1f\n", acc[0] / 16, acc[1] / 16,
-              acc[2] / 16);
+      fprintf(stderr, "rs_feeder_step host us/call: stage %.1f (of which waiting %.1f) step %.1f finish %.1f\n",
+              acc[0] / 16, f->wait_us / 16, acc[1] / 16, acc[2] / 16);
+      f->wait_us = 0;
       acc[0] = acc[1] = acc[2] = 0;
     }
   }
