@@ -265,6 +265,8 @@ int evict_count(rs_table* t, uint64_t* out, cudaStream_t s);
 int evict_prepare(rs_table* t, uint64_t max_victims);  // host: size the selection buffers
 // bounded ensure split for graph capture: host part, then enqueue-only part
 int table_bounded_prepare(rs_table* t, uint64_t n_max, cudaStream_t s);
+int table_bounded_evict_insert(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                               uint32_t* d_rows32, int64_t* d_rows64, cudaStream_t s);
 int table_bounded_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                           uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,
                           uint32_t* d_srow, cudaStream_t s);  // victims of the last selection (syncs)

@@ -152,6 +152,11 @@ struct FaArgs {
   uint32_t* urow;
   int64_t* urow64;
   int no_table = 0;  // bounded tables: dedup + metadata only (the bounded ensure follows, then k_fpatch)
+  // bounded tables, probe mode: the claiming tile probes its ids (stamp the
+  // hits, list the misses, one stamp-log record per unique id at base + u)
+  int probe_only = 0;
+  uint32_t* missing = nullptr;
+  LogArgs lg;
 };
 
 // Sharded requester: the ids this tile claimed go to their owners
@@ -330,6 +335,41 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   const unsigned g = lane & (kBucket - 1);
   const unsigned gbase = lane & ~(kBucket - 1);
   const unsigned gmask = 0xFFu << gbase;
+  if (a.probe_only) {  // bounded tables: probe only (the evict + the insert of the misses follow)
+    const unsigned long long lbase = a.lg.rec ? a.lg.ctl->tail : 0ull;
+    for (uint32_t k = tid >> 3; k < nnew; k += kTT / kBucket) {
+      const uint64_t key = fid[k];
+      const uint32_t u = fu[k];
+      uint32_t row = kNoRow, lslot = kNoLogSlot;
+      const int sp = key == kEmptyKey ? 0 : (key == kTombKey ? 1 : -1);
+      if (sp >= 0) {
+        if (g == 0) {
+          const uint32_t r = td->c.special_row[sp];
+          if (r != kNoRow) {
+            row = r;
+            if (atomicExch(&td->c.special_tick[sp], tick_now) != tick_now) lslot = (uint32_t)(a.lg.cap + sp);
+          }
+        }
+      } else {
+        const Probe p = probe_group<true>(d.slots, d.nb_mask, key, g, gbase, gmask);
+        if (p.found) {
+          row = p.row == kNoRow ? wait_row(d.slots, p.slot) : p.row;
+          if (g == 0 && p.tick != tick_now && atomicCAS(&d.slots[p.slot].tick, p.tick, tick_now) == p.tick)
+            lslot = (uint32_t)p.slot;
+        }
+      }
+      if (g == 0) {
+        if (row == kNoRow) a.missing[atomicAdd(&td->c.missing, 1u)] = u;
+        if (a.lg.rec) a.lg.rec[(lbase + u) & a.lg.mask] = LogRec{key, lslot, tick_now};
+        a.use.rec[fslot[k]].row = row;
+        a.urow[u] = row;
+        a.urow64[u] = row == kNoRow ? -1 : (int64_t)row;
+      }
+    }
+    // the op's records took [tail, tail + unique count): moved by the last block
+    launch_epilogue(td, free_n0, fresh0, true, tick_now, nullptr, a.lg.rec ? a.lg.ctl : nullptr, 0, a.use.cnt);
+    return;
+  }
   for (uint32_t k = tid >> 3; k < nnew; k += kTT / kBucket) {
     const uint64_t key = fid[k];
     const uint32_t row = find_or_insert_group(td, d, key, g, gbase, gmask, tick_now, free_n0, fresh0, &s_ins,
@@ -1580,13 +1620,25 @@ int fast_enqueue(rs_workspace* ws, rs_table* t, const uint64_t* d_ids, uint64_t 
     fa.unique = ws->unique;
     fa.urow = ws->urow;
     fa.urow64 = ws->urow64;
-    fa.no_table = 1;
+    static const bool ka_probe = !getenv("RS_BOUNDED_KA_PROBE") || getenv("RS_BOUNDED_KA_PROBE")[0] != '0';
     const uint32_t ntiles = (uint32_t)((n + kTT - 1) / kTT);
     if (ev) RS_CUDA(cudaEventRecord(ev[0], s));
-    carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);
-    RS_LAUNCH_CHECK("k_fa(no table)");
-    int st = table_bounded_enqueue(t, ws->unique, ws->fast.set[use].cnt, n, ws->urow, ws->urow64, nullptr,
-                                   nullptr, s);
+    int st = RS_OK;
+    if (ka_probe) {  // KA probes (stamp, log, misses), then the evict and the insert of the misses
+      fa.probe_only = 1;
+      fa.missing = t->d_missing;
+      fa.lg = log_args(t, 1);
+      RS_CUDA(cudaMemsetAsync(&t->dev->c.missing, 0, sizeof(unsigned int), s));
+      carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);
+      RS_LAUNCH_CHECK("k_fa(probe)");
+      st = table_bounded_evict_insert(t, ws->unique, ws->fast.set[use].cnt, n, ws->urow, ws->urow64, s);
+    } else {
+      fa.no_table = 1;
+      carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);
+      RS_LAUNCH_CHECK("k_fa(no table)");
+      st = table_bounded_enqueue(t, ws->unique, ws->fast.set[use].cnt, n, ws->urow, ws->urow64, nullptr,
+                                 nullptr, s);
+    }
     if (st) return st;
     carve(k_fpatch), k_fpatch<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(fa.use, ws->urow);
     RS_LAUNCH_CHECK("k_fpatch");

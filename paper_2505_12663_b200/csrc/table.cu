@@ -735,6 +735,20 @@ int table_bounded_enqueue(rs_table* t, const uint64_t* d_keys, const uint32_t* d
   return RS_OK;
 }
 
+// The bounded ensure after an external probe (the fast step's KA probed,
+// stamped and listed the misses in t->d_missing): victims, then the misses.
+int table_bounded_evict_insert(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
+                               uint32_t* d_rows32, int64_t* d_rows64, cudaStream_t s) {
+  int st = evict_device(t, d_n, n_max, 0, s);
+  if (st) return st;
+  k_table_upsert<<<grid_for(n_max, kGroupsPerBlock, 148 * 8), kProbeThreads, 0, s>>>(
+      t->dev, d_keys, &t->dev->c.missing, (uint32_t)n_max, nullptr, 0, d_rows32, d_rows64, nullptr, nullptr,
+      nullptr, t->d_missing, log_args(t, 0));
+  RS_LAUNCH_CHECK("k_table_upsert(insert missing)");
+  if (n_max > (1u << 18)) log_invalidate(t);
+  return RS_OK;
+}
+
 // ensure for any table; bounded tables probe, evict, then insert the misses.
 int table_ensure_any(rs_table* t, const uint64_t* d_keys, const uint32_t* d_n, uint64_t n_max,
                      uint32_t* d_rows32, int64_t* d_rows64, const uint32_t* d_uslot,

@@ -219,7 +219,8 @@ __device__ __forceinline__ uint32_t find_or_insert_group(TableDev* td, const Tab
 __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long free_n0,
                                                 unsigned long long fresh0, int bump_tick,
                                                 uint32_t tick_now, TableCounters* mirror_out = nullptr,
-                                                LogCtl* log_open = nullptr, uint32_t log_n = 0) {
+                                                LogCtl* log_open = nullptr, uint32_t log_n = 0,
+                                                const uint32_t* log_n_ptr = nullptr) {
   __syncthreads();
   __shared__ bool s_last;
   if (threadIdx.x == 0) {
@@ -256,7 +257,7 @@ __device__ __forceinline__ void launch_epilogue(TableDev* td, unsigned long long
     c.blocks_done = 0;
     if (log_open) {  // the stamp log: this op's records took [tail, tail + n)
       log_open->op_base = log_open->tail;
-      log_open->tail += log_n;
+      log_open->tail += log_n_ptr ? *log_n_ptr : log_n;  // (a device count: read by the last block)
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     if (mirror_out) {
