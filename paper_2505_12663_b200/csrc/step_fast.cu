@@ -157,6 +157,11 @@ struct FaArgs {
   int probe_only = 0;
   uint32_t* missing = nullptr;
   LogArgs lg;
+  // the previous step's set cleaned inside KA (no k_fclean): its slice per
+  // block, the last block (ctr[3] arrivals) zeroes its count; table mode also
+  // stores the counters into the host's mapped mirror from KA's epilogue
+  int clean_in_ka = 0;
+  TableCounters* mirror_out = nullptr;
 };
 
 // Sharded requester: the ids this tile claimed go to their owners
@@ -241,6 +246,23 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
   // blocks append to this set's (zeroed by the previous step), block 0 zeroes
   // the other one for the next step
   if (blockIdx.x == 0 && tid == 0) a.sh.ctr[5 + (a.set ^ 1)] = 0;
+  if (a.clean_in_ka) {  // the previous step's records back to empty (its dirty list), off every chain
+    const uint32_t prev = *a.clean.cnt;
+    for (uint32_t i = blockIdx.x * kTT + tid; i <= prev; i += gridDim.x * kTT) {
+      const uint64_t sl = i < prev ? a.clean.u_slot[i] : a.clean.spare;
+      a.clean.rec[sl] = Rec{kEmptyKey, 0u, kNoRow};
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      unsigned int* done = reinterpret_cast<unsigned int*>(a.sh.ctr + 3);
+      if (atomicAdd(done, 1u) == gridDim.x - 1) {  // every block read prev: the set starts empty
+        __threadfence();
+        *a.clean.cnt = 0;
+        *done = 0;
+      }
+    }
+  }
   for (uint32_t i = tid; i <= L; i += kTT) {
     lkey[i] = kEmptyKey;
     lnew[i] = 0;
@@ -385,7 +407,7 @@ __global__ void __launch_bounds__(kTT) k_fa(FaArgs a) {
     if (s_ins) atomicAdd(&td->c.inserted, s_ins);
     if (s_reuse) atomicAdd(&td->c.reused, s_reuse);
   }
-  launch_epilogue(td, free_n0, fresh0, true, tick_now);
+  launch_epilogue(td, free_n0, fresh0, true, tick_now, a.mirror_out);
   // (launch_epilogue's last block has folded the counters; every block ran it)
 }
 
@@ -1409,6 +1431,12 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   fa.urow = ws->urow;
   fa.urow64 = ws->urow64;
   if (send) fa.send = *send;
+  // RS_CLEAN_IN_KA=1: KA cleans the previous set instead of k_fclean (the
+  // single-GPU table step's counters then reach the mirror from KA's
+  // epilogue) -- measured no faster at config 1 / N = 4, e2e slower; off
+  static const bool clean_ka = getenv("RS_CLEAN_IN_KA") && getenv("RS_CLEAN_IN_KA")[0] == '1';
+  fa.clean_in_ka = clean_ka ? 1 : 0;
+  if (clean_ka && td && !send && !peer) fa.mirror_out = mirror_out;
   if (do_ka) {
     carve(k_fa), k_fa<<<std::max(ntiles, 1u), kTT, 0, s>>>(fa);  // an idle sharded rank still publishes its (empty) send
     RS_LAUNCH_CHECK("k_fa");
@@ -1554,11 +1582,19 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
     RS_LAUNCH_CHECK("k_fcs");
     return RS_OK;
   };
+  // (KA cleaned the set when it ran with clean_in_ka -- here, or as the
+  // sharded requester's front; the bounded step's KA did not)
+  const bool cleaned = clean_ka && (do_ka || peer);
+  auto clean = [&]() -> int {
+    if (cleaned) return RS_OK;
+    carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(
+        fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace, td, mirror_out);
+    RS_LAUNCH_CHECK("k_fclean");
+    return RS_OK;
+  };
   int st;
   if (ev) {  // eager, serial: KA (+ clean) | KD | KH + KF | KS
-    carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace,
-                                                            td, mirror_out);
-    RS_LAUNCH_CHECK("k_fclean");
+    if ((st = clean())) return st;
     if ((st = csr(s, s))) return st;
     RS_CUDA(cudaEventRecord(ev[2], s));
     if ((st = hot(s))) return st;
@@ -1572,12 +1608,7 @@ static int fast_launch(rs_workspace* ws, TableDev* td, const float* emb, uint32_
   // the clean after the branches (RS_CLEAN_LAST=0: before them -- measured
   // ~2 us slower at config 1: its blocks then delay the branches' first waves)
   static const bool clean_last = !getenv("RS_CLEAN_LAST") || getenv("RS_CLEAN_LAST")[0] != '0';
-  auto clean = [&]() -> int {
-    carve(k_fclean), k_fclean<<<grid_for(n + 1, 256, 148 * 2), 256, 0, s>>>(
-        fa.clean, reinterpret_cast<unsigned int*>(sh.ctr + 3), sh.trace, td, mirror_out);
-    RS_LAUNCH_CHECK("k_fclean");
-    return RS_OK;
-  };
+
   if (!clean_last && (st = clean())) return st;
   if (skip != 1 && (st = hot(sh2))) return st;
   if (skip != 2 && (st = csr(sd, sd3))) return st;
